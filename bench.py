@@ -1,0 +1,342 @@
+"""Benchmark: rays/s integrated into a region-chunked voxel map on B200.
+
+Default workload = BASELINE.json configs[1] ("C2"): a synthetic Ouster-128
+sequence, 1000 batches x 26,240 rays (26.24 M rays), 0.05 m voxels,
+occupancy (+ sub-voxel mean), deterministic sort+segmented update path.
+One step = the whole 1000-batch sequence integrated into a freshly cleared
+map (region creation included), batch by batch, exactly as 1000
+`submit_batch` calls would do it.
+
+  value  inputs resident in HBM (OHMB1 records), timed with CUDA events on
+         the map's stream, max over ranks
+  e2e    the same through the public API `submit_batch(vmap, records)` with
+         pinned HOST records: host->device copy of every batch and the
+         device->host stats read inside the timed region
+
+N > 1 (torchrun): every rank integrates its own copy of the sequence into
+its own map (independent replicas; region sharding with record exchange is
+not in this round).  `--impl reference` times the reference's own native
+kernel on the host cores instead (oracle/ref_runner.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "rays/s integrated (occupancy & NDT-OM, 0.1 m voxels) at 1/2/4/8 B200 vs CPU"
+UNIT = "rays/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=("c2", "c1", "c3"), default="c2")
+    ap.add_argument("--exec", dest="exec_", choices=("det", "cas"), default="det")
+    ap.add_argument("--batches", type=int, default=1000, help="C2 batches per step")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(name: str, batches: int):
+    from paper_2206_06079_b200 import MapConfig, scans
+    if name == "c2":
+        cfg = MapConfig(voxel_size=0.05)
+        data = scans.os128_canyon_batches(batches)
+        desc = dict(workload="C2: synthetic OS1-128 street-canyon sequence", scans=len(data),
+                    rays_per_batch=int(len(data[0])), voxel_size=0.05, region_dim=32,
+                    mode="occupancy")
+        mode = "occupancy"
+    elif name == "c1":
+        cfg = MapConfig(voxel_size=0.1)
+        data = [scans.os64_room_scan()]
+        desc = dict(workload="C1: one synthetic OS1-64 scan", scans=1, rays_per_batch=131072,
+                    voxel_size=0.1, region_dim=32, mode="occupancy")
+        mode = "occupancy"
+    else:
+        cfg = MapConfig(voxel_size=0.1)
+        data = scans.os64_tunnel_scans(77)
+        desc = dict(workload="C3: synthetic OS1-64 tunnel, NDT-OM", scans=77,
+                    rays_per_batch=131072, voxel_size=0.1, region_dim=32, mode="ndt-om")
+        mode = "ndt-om"
+    return cfg, mode, data, desc
+
+
+def sample_clocks(path: str):
+    cmd = ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+           "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+           "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+           "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"]
+    try:
+        return subprocess.Popen(cmd, stdout=open(path, "w"), stderr=subprocess.DEVNULL)
+    except FileNotFoundError:
+        return None
+
+
+def parse_clocks(path: str, dev: int):
+    sm, mx, reasons = [], 0.0, set()
+    names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+    try:
+        for line in open(path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) != dev:
+                continue
+            sm.append(float(f[1]))
+            mx = max(mx, float(f[2]))
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+    except (OSError, ValueError):
+        pass
+    return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+            "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(S, V, H):
+    """SURVEY.md 8(d) occupancy: 49 B per segment input + 8 B per miss visit
+    (f32 log-odds RMW) + 24 B per hit (log-odds + packed mean + count RMW)."""
+    return 49 * S + 8 * (V - H) + 24 * H
+
+
+def load_peaks():
+    try:
+        d = json.load(open(ROOT / "MEASURED_PEAKS.json"))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(workload_name, exec_):
+    """dram bytes per walk launch from the committed ncu capture, if any."""
+    try:
+        d = json.load(open(ROOT / "profiles" / "ncu_summary.json"))
+        return d.get(f"{workload_name}_{exec_}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, data, budget, mode):
+    from oracle import oracle as orc
+    from oracle import ref_runner
+    workers = orc.host_cores()
+    if mode != "occupancy":
+        return None
+    r = ref_runner.time_reference(cfg, data, workers, budget_s=budget)
+    return {"value": r["rays"] / r["seconds"], "unit": UNIT, "cores": workers,
+            "kind": r["kind"],
+            "sample": f"first {r['batches']} batches ({r['rays']} rays, {r['visits']} voxel "
+                      f"visits) of the same workload; reference _kernels.integrate_occupancy "
+                      f"on {workers} threads, kernel-only (clip/segment/prefetch untimed)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg, mode, data, desc = workload(args.workload, args.batches)
+    from oracle import oracle as orc
+    from oracle import ref_runner
+    workers = orc.host_cores()
+    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        ref_runner.time_reference(cfg, data[:2], workers, budget_s=budget / 4)
+    rays = secs = 0.0
+    used = 0
+    for _ in range(args.steps):
+        r = ref_runner.time_reference(cfg, data, workers, budget_s=budget)
+        rays += r["rays"]
+        secs += r["seconds"]
+        used = r["batches"]
+        kind = r["kind"]
+    value = rays / secs if secs else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / max(1, args.steps), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
+        "config": desc,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
+                         "sample": f"each step: first {used} batches of the workload, "
+                                   f"reference native kernel, {workers} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+
+    from paper_2206_06079_b200 import ExecutorOptions, VoxelMap, _native, submit_batch
+    from paper_2206_06079_b200.layers import MODE_LAYERS
+
+    cfg, mode, data, desc = workload(args.workload, args.batches)
+    det = args.exec_ == "det"
+    sizes = [len(b) for b in data]
+    offsets = np.concatenate([[0], np.cumsum(sizes)])
+    total_rays = int(offsets[-1])
+    host = np.concatenate(data)
+    # device-resident copy of all records (inputs already in HBM for `value`)
+    d_rec = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
+    base = d_rec.data_ptr()
+    stream = torch.cuda.current_stream()
+
+    vmap = VoxelMap(cfg, MODE_LAYERS[mode], device=dev, initial_regions=4096)
+    vmap._native.set_stream(stream.cuda_stream)
+
+    agg = {}
+
+    def step(record=False):
+        vmap.clear()
+        tot = dict(S=0, V=0, walk_ms=0.0, launches=0, batches=0, records=0, rmiss=0)
+        for b in range(len(data)):
+            r = _native.rays_from_records(sizes[b], base + int(offsets[b]) * 40)
+            st = vmap._native.integrate(r, mode, det)
+            if record:
+                tot["S"] += st.segments
+                tot["V"] += st.voxel_visits
+                tot["walk_ms"] += st.walk_ms
+                tot["launches"] += st.launches
+                tot["records"] += st.records
+                tot["rmiss"] += st.region_misses
+                tot["batches"] += 1
+        return tot
+
+    for _ in range(args.warmup):
+        step()
+    clk_file = tempfile.mktemp(suffix=".csv")
+    clk = sample_clocks(clk_file)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    steps = [step(record=True) for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    if clk:
+        clk.terminate()
+        clk.wait()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = total_rays * args.steps * world / (ms * 1e-3)
+
+    # H (hit visits): sample segments = has_sample rays not clipped (<= max range)
+    o = host["origin"].astype(np.float64)
+    e = host["end"].astype(np.float64)
+    L = np.sqrt(((e - o) ** 2).sum(1))
+    H = int(np.sum(((host["flags"] & 1) == 1) & (L <= cfg.max_ray_range) & (L > 0)))
+    s0 = steps[-1]
+    bytes_step = algorithmic_bytes(s0["S"], s0["V"], H)
+    walk_ms = s0["walk_ms"] / max(1, s0["batches"])
+    bytes_launch = bytes_step / max(1, s0["batches"])
+    peak, peak_kind = load_peaks()
+    achieved = bytes_launch / (walk_ms * 1e-3) / 1e9 if walk_ms > 0 else 0.0
+    traffic = load_traffic(args.workload, args.exec_)
+
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(host.view(np.uint8).copy()).pin_memory()
+        hv = pinned.numpy().view(host.dtype)
+        opts = ExecutorOptions(deterministic=det)
+        n_e2e = max(1, min(args.steps, 3))
+        vmap.clear()
+        for b in range(min(len(data), 50)):
+            submit_batch(vmap, hv[offsets[b]:offsets[b + 1]], mode, opts)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(n_e2e):
+            vmap.clear()
+            for b in range(len(data)):
+                submit_batch(vmap, hv[offsets[b]:offsets[b + 1]], mode, opts)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ems = max(f0.elapsed_time(f1), wall * 1e3)
+        if dist:
+            t = torch.tensor([ems], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": total_rays * n_e2e * world / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(host.nbytes),
+               "d2h_bytes_per_step": int(len(data) * ctypes_stats_bytes()),
+               "steps": n_e2e, "api": "submit_batch(vmap, pinned OHMB1 records)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, data, args.cpu_budget, mode)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 (DDA) / f32 (log-odds)", "data": "synthetic",
+            "config": dict(desc, exec="deterministic" if det else "cas",
+                           rays_per_step=total_rays, parallelism=f"replicas{world}",
+                           l2="inputs (1.05 GB/step) and map exceed L2; map cleared each step"),
+            "voxel_updates_per_s": s0["V"] * args.steps * world / (ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_walk_occ", "peak_kind": peak_kind,
+                         "bytes_per_launch": bytes_launch, "avg_launch_ms": walk_ms},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": int(sum(s["launches"] for s in steps)),
+            "clocks": parse_clocks(clk_file, dev),
+            "stats": {"segments": s0["S"], "visits": s0["V"], "hits": H,
+                      "records": s0["records"], "region_misses": s0["rmiss"]},
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def ctypes_stats_bytes():
+    import ctypes
+
+    from paper_2206_06079_b200._native import VmStats
+    return ctypes.sizeof(VmStats)
+
+
+if __name__ == "__main__":
+    main()

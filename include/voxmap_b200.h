@@ -1,0 +1,195 @@
+/*
+ * voxmap_b200.h -- C ABI of the B200-native ray-integration path.
+ *
+ * Drop-in boundary for the reference package `voxmap` 0.1.0, whose only
+ * native boundary is the Cython extension `voxmap._kernels`
+ * (/root/reference/pkg/setup.py:5-13, src/voxmap/_kernels.pyx).  Plain C
+ * types only: pointers, sizes, ints and doubles.  No torch types.
+ *
+ * Two layers:
+ *
+ *  1. `vm_kernels_*`, `vm_walk_voxels`, `vm_hash_mix`: one-to-one
+ *     replacements of the `_kernels` entry points, same argument meaning
+ *     (segment arrays, open-addressing region table with splitmix64 keys,
+ *     per-layer region pointer arrays), except that every array is a
+ *     DEVICE pointer and the work runs on a CUDA stream.
+ *
+ *  2. `vm_map_*`, `vm_integrate`: the device-resident map runtime that
+ *     `engine.submit_batch` (engine.py:175-210) calls.  It owns the
+ *     region table, the per-layer region pools in HBM and the batch
+ *     pipeline (preprocess -> region discovery -> DDA walk -> resolve /
+ *     sort+fold), and reproduces the reference's sequential semantics
+ *     (engine.py:213-237) in VM_EXEC_DETERMINISTIC mode.
+ *
+ * All functions return VM_OK (0) or an error code; vm_last_error() gives
+ * a thread-local message.  Errors never leave a half-applied batch: a
+ * batch either integrates completely or the map is unchanged.
+ */
+#ifndef VOXMAP_B200_H
+#define VOXMAP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VM_OK 0
+#define VM_ERR_ARG 1     /* bad argument (reference: ValueError)            */
+#define VM_ERR_CUDA 2    /* CUDA runtime failure                            */
+#define VM_ERR_OOM 3     /* device allocation failed (reference: MemoryError) */
+#define VM_ERR_RANGE 4   /* region coordinate outside the 21-bit packing,
+                            keys.py:76-86 (reference: ValueError)           */
+#define VM_ERR_NODEV 5   /* no CUDA device                                  */
+
+/* Map geometry and sensor model: MapConfig fields (config.py:8-28).  The
+ * log-odds deltas are passed precomputed (occupancy.py:20-35). */
+typedef struct vm_config {
+    double voxel_size;
+    int32_t region_dim;
+    int32_t _pad;
+    double hit_delta;
+    double miss_delta;
+    double clamp_min;
+    double clamp_max;
+    double max_ray_range;
+    double segment_length;
+    double tsdf_truncation;
+    double tsdf_max_weight;
+    double ndt_sensor_noise;
+    double ndt_reset_threshold;
+    double ndt_miss_likelihood_threshold;
+} vm_config;
+
+/* Batch statistics: BatchStats (engine.py:33-64) plus device counters. */
+typedef struct vm_stats {
+    int64_t rays_in;
+    int64_t rays_processed;
+    int64_t segments;
+    int64_t voxel_visits;
+    int64_t cas_retries;
+    int64_t cas_failures;     /* always 0: no mutex fallback on the GPU */
+    int64_t region_misses;
+    int64_t regions_touched;  /* prefetch set size, engine.py:99-118 */
+    int64_t records;          /* order-keyed records sorted this batch */
+    int64_t marked_voxels;    /* sample voxels (deterministic mode) */
+    int64_t regions_total;    /* regions in the map after the batch */
+    int64_t new_regions;
+    int64_t replays;          /* batch re-runs after a pool growth */
+    int64_t touched_regions_walk;
+    int64_t launches;         /* kernels of this library launched for the batch */
+    double gpu_ms;            /* device time of the whole batch (CUDA events) */
+    double walk_ms;           /* device time of the DDA walk kernel */
+} vm_stats;
+
+enum { VM_MODE_OCCUPANCY = 0, VM_MODE_DECAY = 1, VM_MODE_NDT_OM = 2, VM_MODE_NDT_TM = 3,
+       VM_MODE_TSDF = 4 };
+enum { VM_EXEC_CAS = 0, VM_EXEC_DETERMINISTIC = 1 };
+enum { VM_RAYS_OHMB1 = 0, VM_RAYS_F64 = 1 };
+
+/* Layer ids (layers.py:22-31); layer_mask bit (1 << id). */
+enum { VM_LAYER_OCCUPANCY = 1, VM_LAYER_MEAN = 2, VM_LAYER_MEAN_COUNT = 3,
+       VM_LAYER_COV_SQRT = 4, VM_LAYER_HIT_COUNT = 5, VM_LAYER_MISS_COUNT = 6,
+       VM_LAYER_INTENSITY = 7, VM_LAYER_DECAY_HITS = 8, VM_LAYER_DECAY_DISTANCE = 9,
+       VM_LAYER_TSDF = 10 };
+
+/* A ray batch.  VM_RAYS_OHMB1: `records` points at packed 40-byte OHMB1
+ * records (rayset.py:19-27: f64 timestamp, f32 origin[3], f32 end[3],
+ * f32 intensity, u32 flags), converted to f64 exactly as to_ray_samples
+ * does (rayset.py:74-84).  VM_RAYS_F64: RaySample arrays (traversal.py:20-42):
+ * origins/ends [n][3] f64, has_sample u8[n], intensity f32[n] (may be NULL).
+ * on_device: 0 = host pointers (copied in on the map stream; pinned memory
+ * overlaps), 1 = device pointers. */
+typedef struct vm_rays {
+    int32_t format;
+    int32_t on_device;
+    int64_t count;
+    const void *records;
+    const double *origins;
+    const double *ends;
+    const uint8_t *has_sample;
+    const float *intensity;
+} vm_rays;
+
+typedef struct vm_map vm_map;
+
+/* ---- map runtime (replaces store.VoxelMap's buffers, store.py:28-80) ---- */
+
+/* Create a device map on `device` with the given layers.  initial_regions
+ * sizes the HBM region pool (it grows by doubling between batches). */
+int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
+                  int64_t initial_regions, vm_map **out);
+int vm_map_destroy(vm_map *map);
+/* Drop every region (the map becomes empty; pool capacity is kept). */
+int vm_map_reset(vm_map *map);
+/* Use an external CUDA stream (cudaStream_t) for all map work; NULL = own stream. */
+int vm_map_set_stream(vm_map *map, void *cuda_stream);
+int vm_map_region_count(const vm_map *map, int64_t *out);
+/* Packed region keys (keys.py:76-86) of slots [first, first+count), in slot
+ * (creation) order. */
+int vm_map_region_keys(const vm_map *map, int64_t first, int64_t count, int64_t *keys_out);
+/* get_or_create_region (store.py:67-80) for host-driven region creation. */
+int vm_map_ensure_regions(vm_map *map, const int64_t *packed_keys, int64_t n,
+                          int32_t *slots_out);
+/* Region slot of a packed key or -1 (store.py:67-77 without create). */
+int vm_map_find_region(vm_map *map, int64_t packed_key, int32_t *slot_out);
+/* Copy one region's layer buffer (region_dim^3 * components elements)
+ * device->host / host->device on the map stream (synchronous). */
+int vm_map_read_layer(vm_map *map, int32_t slot, int32_t layer_id, void *host_dst,
+                      int64_t bytes);
+int vm_map_write_layer(vm_map *map, int32_t slot, int32_t layer_id, const void *host_src,
+                       int64_t bytes);
+/* Device pointer of a region's layer buffer (valid until the next batch
+ * that grows the pool). */
+int vm_map_layer_ptr(vm_map *map, int32_t slot, int32_t layer_id, void **dev_ptr_out);
+
+/* ---- the hot path: submit_batch (engine.py:175-210) ---- */
+
+/* Integrate one batch: clip + segment (traversal.py:140-178), region
+ * prefetch (engine.py:99-118), DDA walk and layer updates.  exec =
+ * VM_EXEC_DETERMINISTIC reproduces sequential_reference (engine.py:213-216)
+ * bit-for-bit on occupancy / mean / mean_count / decay_hits / tsdf;
+ * VM_EXEC_CAS is the paper's atomic compare-and-swap update
+ * (_kernels.pyx:233-357).  Synchronous: returns after the batch is
+ * complete and `out` is filled. */
+int vm_integrate(vm_map *map, const vm_rays *rays, int32_t mode, int32_t exec,
+                 vm_stats *out);
+
+/* ---- `_kernels` one-to-one entry points (device pointers) ---- */
+
+/* _kernels.walk_voxels_native (_kernels.pyx:214-228): walk one segment on
+ * the GPU; coords_out [cap][3] i64, t0/t1 [cap] f64 host buffers.
+ * Returns VM_ERR_ARG if the walk needs more than cap visits. */
+int vm_walk_voxels(double ox, double oy, double oz, double ex, double ey, double ez,
+                   double cell, int64_t cap, int64_t *coords_out, double *t0_out,
+                   double *t1_out, int64_t *n_out);
+
+/* _kernels.hash_mix (_kernels.pyx:105-110,127-129): splitmix64 finalizer. */
+uint64_t vm_hash_mix(int64_t key);
+
+/* _kernels.integrate_occupancy (_kernels.pyx:376-470): CAS occupancy
+ * (+ mean when mean_ptrs/count_ptrs are non-NULL, + decay when
+ * dhit_ptrs/ddist_ptrs are non-NULL) over n segments.  tkeys/tvals: the
+ * open-addressing region table of engine._build_region_table
+ * (engine.py:121-147), tsize a power of two.  *_ptrs: device arrays of
+ * per-region device buffer pointers.  stats_out[4] = (cas_retries,
+ * cas_failures, region_misses, visits).  stream: cudaStream_t or NULL. */
+int vm_kernels_integrate_occupancy(const double *origins, const double *ends,
+                                   const uint8_t *has_sample, int64_t n,
+                                   const int64_t *tkeys, const int32_t *tvals, int64_t tsize,
+                                   void *const *occ_ptrs, void *const *mean_ptrs,
+                                   void *const *count_ptrs, void *const *dhit_ptrs,
+                                   void *const *ddist_ptrs, double voxel_size,
+                                   int64_t region_dim, double hit_delta, double miss_delta,
+                                   double clamp_min, double clamp_max, int32_t retry_limit,
+                                   int32_t walk_cap, int64_t *stats_out, void *stream);
+
+const char *vm_last_error(void);
+int vm_device_count(int32_t *out);
+/* Build-time identification string (arch, flags). */
+const char *vm_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXMAP_B200_H */

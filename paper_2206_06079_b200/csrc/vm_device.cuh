@@ -1,0 +1,423 @@
+// vm_device.cuh -- device-side building blocks of the B200 ray-integration
+// path: exact fp64 arithmetic of the reference, ray preprocessing, the DDA
+// walker, the HBM region table and the per-block aggregation helpers.
+//
+// Every translation unit that includes this file is compiled with
+// -fmad=false: the reference never fuses a*b+c (numpy ufuncs and CPython
+// floats round each operation), so neither may we.  The single place the
+// reference *does* fuse -- OpenBLAS ddot inside np.linalg.norm / `@`
+// (traversal.py:40-42, reference.py:170) -- is written out with fma().
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vm {
+
+enum Layer {
+    L_SCRATCH = 0,  // private: per-voxel miss counter (deterministic resolve)
+    L_OCC = 1, L_MEAN = 2, L_COUNT = 3, L_COV = 4, L_HIT = 5, L_MISS = 6,
+    L_INTENS = 7, L_DHITS = 8, L_DDIST = 9, L_TSDF = 10,
+    NUM_LAYERS = 11
+};
+
+enum Mode { M_OCC = 0, M_DECAY = 1, M_NDT_OM = 2, M_NDT_TM = 3, M_TSDF = 4 };
+
+enum Stat {
+    S_RAYS_IN = 0, S_PROCESSED, S_SEGMENTS, S_VISITS, S_RETRIES, S_FAILURES,
+    S_RMISS, S_PREF_TOUCHED, S_RECORDS, S_MARKED, S_WALK_TOUCHED, S_RANGE_ERR,
+    S_CUBE_FLUSH, NUM_STATS
+};
+
+constexpr unsigned MARK_FLAG = 0x80000000u;
+constexpr int CUBE = 16;                 // smem aggregation cube edge (voxels)
+constexpr int CUBE_N = CUBE * CUBE * CUBE;
+constexpr int SLOTSET = 256;             // per-block region dedupe set
+
+// All state a kernel needs, passed by value.
+struct DevMap {
+    double vox, rsize;                   // voxel size, region size (region_dim * vox)
+    double hit_delta, miss_delta;
+    double max_range, seg_len;
+    double tsdf_trunc, tsdf_maxw;
+    double sigma2, miss_check;
+    float hit32, miss32, cmin, cmax, fthresh;
+    int dim, vpr, mark_words, maxseg;
+    int order_bits;                      // bits of (ray*maxseg+seg)<<1|hit
+    int cell_limit;                      // |global voxel coord| must stay below
+    // region table (engine._build_region_table format, engine.py:121-147)
+    long long *tkeys;
+    int *tvals;
+    unsigned long long tmask;
+    int *cursor;                         // regions allocated (dense slot ids)
+    int cap;                             // slots backed by HBM
+    int max_slots;                       // slot id space (slot_keys size)
+    int insert;                          // lookups may create regions
+    long long *slot_keys;
+    unsigned *slot_touch, *slot_pref;
+    unsigned epoch;
+    void *const *lptr[NUM_LAYERS];       // per layer: region base pointer per slot
+    unsigned *marks;                     // mark bitset, mark_words per slot
+    unsigned long long *stats;
+    int *go;                             // batch guard (0 = skip, replay later)
+    // batch outputs
+    unsigned long long *rec;
+    unsigned long long rec_cap;
+    int2 *marked;                        // (slot, li) of sample voxels
+    int marked_cap;
+    int *touched;                        // regions touched by the walk
+    int touched_cap;
+};
+
+// ---------------------------------------------------------------- arithmetic
+
+// RaySample.length (traversal.py:40-42): np.linalg.norm -> OpenBLAS ddot
+__device__ __forceinline__ double norm3(double x, double y, double z) {
+    return sqrt(fma(z, z, fma(y, y, x * x)));
+}
+// float(a @ b) for 3-vectors (reference.py:170)
+__device__ __forceinline__ double dot3(const double *a, const double *b) {
+    return fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0]));
+}
+
+// _kernels.pyx:105-110 (splitmix64 finalizer)
+__host__ __device__ __forceinline__ unsigned long long mix_key(long long key) {
+    unsigned long long h = (unsigned long long)key + 0x9E3779B97F4A7C15ULL;
+    h = (h ^ (h >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    h = (h ^ (h >> 27)) * 0x94D049BB133111EBULL;
+    return h ^ (h >> 31);
+}
+
+// keys.py:76-86
+__host__ __device__ __forceinline__ long long pack_region(long long rx, long long ry,
+                                                          long long rz) {
+    const long long B = 1LL << 20, M = (1LL << 21) - 1;
+    return (((rx + B) & M) << 42) | (((ry + B) & M) << 21) | ((rz + B) & M);
+}
+__host__ __device__ __forceinline__ void unpack_region(long long p, int r[3]) {
+    const long long B = 1LL << 20, M = (1LL << 21) - 1;
+    r[0] = (int)(((p >> 42) & M) - B);
+    r[1] = (int)(((p >> 21) & M) - B);
+    r[2] = (int)((p & M) - B);
+}
+
+__device__ __forceinline__ int floordiv(int a, int d) {
+    int q = a / d;
+    if ((a % d != 0) && (a < 0)) q -= 1;
+    return q;
+}
+
+// reference.py:22-23 / _kernels.pyx:233-271 clamped log-odds step (f32)
+__device__ __forceinline__ float clamp_add(float l, float d, float cmin, float cmax) {
+    float v = __fadd_rn(l, d);
+    if (v < cmin) v = cmin;
+    if (v > cmax) v = cmax;
+    return v;
+}
+// k identical misses: f^k with early exit at the fixed point (clamp_min)
+__device__ __forceinline__ float miss_k(float l, unsigned k, float d, float cmin, float cmax) {
+    for (unsigned i = 0; i < k; ++i) {
+        float n = clamp_add(l, d, cmin, cmax);
+        if (__float_as_uint(n) == __float_as_uint(l)) break;
+        l = n;
+    }
+    return l;
+}
+
+// subvoxel.py:16-23
+__device__ __forceinline__ unsigned pack_mean(const double off[3]) {
+    unsigned packed = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double f = floor(off[a] * 1024.0);
+        int q = f < 0.0 ? 0 : (f > 1023.0 ? 1023 : (int)f);
+        packed |= (unsigned)q << (10 * a);
+    }
+    return packed;
+}
+// subvoxel.py:26-31
+__device__ __forceinline__ void unpack_mean(unsigned packed, double out[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out[a] = ((double)((packed >> (10 * a)) & 1023u) + 0.5) / 1024.0;
+}
+// subvoxel.py:34-49 (the oracle's `/ (count + 1)` form, not the native `* w`)
+__device__ __forceinline__ void fold_mean(unsigned &packed, unsigned &count, const double s[3]) {
+    if (count >= 0xFFFFFFFFu) return;
+    if (count == 0) {
+        packed = pack_mean(s);
+        count = 1;
+        return;
+    }
+    double m[3];
+    unpack_mean(packed, m);
+    double div = (double)count + 1.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) m[a] = m[a] + (s[a] - m[a]) / div;
+    packed = pack_mean(m);
+    count += 1;
+}
+
+// ---------------------------------------------------------------- rays
+
+struct SrcOHMB1 {  // rayset.py:19-27 40-byte records
+    const unsigned char *p;
+    __device__ __forceinline__ void load(long long i, double o[3], double e[3], int &has,
+                                         float &inten) const {
+        const float2 *q = reinterpret_cast<const float2 *>(p + i * 40 + 8);
+        float2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
+        o[0] = a.x; o[1] = a.y; o[2] = b.x;
+        e[0] = b.y; e[1] = c.x; e[2] = c.y;
+        inten = d.x;
+        has = (int)(__float_as_uint(d.y) & 1u);
+    }
+    __device__ __forceinline__ void load_end(long long i, double e[3], float &inten) const {
+        const float2 *q = reinterpret_cast<const float2 *>(p + i * 40 + 8);
+        float2 b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
+        e[0] = b.y; e[1] = c.x; e[2] = c.y;
+        inten = d.x;
+    }
+};
+struct SrcF64 {  // RaySample arrays (traversal.py:20-42)
+    const double *o, *e;
+    const unsigned char *h;
+    const float *it;
+    __device__ __forceinline__ void load(long long i, double oo[3], double ee[3], int &has,
+                                         float &inten) const {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            oo[a] = __ldg(o + 3 * i + a);
+            ee[a] = __ldg(e + 3 * i + a);
+        }
+        has = __ldg(h + i) ? 1 : 0;
+        inten = it ? __ldg(it + i) : 0.0f;
+    }
+    __device__ __forceinline__ void load_end(long long i, double ee[3], float &inten) const {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) ee[a] = __ldg(e + 3 * i + a);
+        inten = it ? __ldg(it + i) : 0.0f;
+    }
+};
+
+// engine._preprocess + clip_ray + segment_ray (engine.py:82-96,
+// traversal.py:140-178), in registers: one ray -> nseg segments.
+struct Ray {
+    double o[3], e[3], d[3];
+    double L;
+    int has, nseg;
+    float inten;
+};
+
+__device__ __forceinline__ bool prep_ray(const DevMap &m, Ray &r, bool segment) {
+    double L = norm3(r.e[0] - r.o[0], r.e[1] - r.o[1], r.e[2] - r.o[2]);
+    if (L == 0.0) return false;
+    if (L > m.max_range) {
+        double d[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) d[a] = (r.e[a] - r.o[a]) / L;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) r.e[a] = r.o[a] + d[a] * m.max_range;
+        r.has = 0;
+        L = norm3(r.e[0] - r.o[0], r.e[1] - r.o[1], r.e[2] - r.o[2]);
+    }
+    r.L = L;
+    if (!segment || L <= m.seg_len) {
+        r.nseg = 1;
+        return true;
+    }
+    r.nseg = (int)ceil(L / m.seg_len);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) r.d[a] = (r.e[a] - r.o[a]) / L;
+    return true;
+}
+
+__device__ __forceinline__ void segment_of(const DevMap &m, const Ray &r, int s, double so[3],
+                                           double se[3], int &sh) {
+    if (r.nseg == 1) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            so[a] = r.o[a];
+            se[a] = r.e[a];
+        }
+        sh = r.has;
+        return;
+    }
+    double t0 = (double)s * m.seg_len;
+    double t1 = (double)(s + 1) * m.seg_len;
+    if (r.L < t1) t1 = r.L;
+    bool last = s == r.nseg - 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        so[a] = r.o[a] + r.d[a] * t0;
+        se[a] = last ? r.e[a] : r.o[a] + r.d[a] * t1;
+    }
+    sh = last ? r.has : 0;
+}
+
+// ---------------------------------------------------------------- region table
+
+// _kernels.pyx:113-124 (table_lookup) + on-demand creation with the
+// sequential oracle's get_or_create semantics (reference.py:31).
+__device__ __forceinline__ int wait_slot(const DevMap &m, unsigned long long h) {
+    volatile int *p = m.tvals + h;
+    int v;
+    while ((v = *p) == -1) __nanosleep(32);
+    return v;
+}
+
+__device__ __noinline__ int region_slot_slow(const DevMap &m, long long key) {
+    unsigned long long h = mix_key(key) & m.tmask;
+    for (unsigned long long probe = 0; probe <= m.tmask; ++probe) {
+        long long k = ((volatile long long *)m.tkeys)[h];
+        if (k == key) return wait_slot(m, h);
+        if (k == -1) {
+            if (!m.insert) return -1;
+            long long prev = (long long)atomicCAS((unsigned long long *)(m.tkeys + h),
+                                                  0xFFFFFFFFFFFFFFFFULL,
+                                                  (unsigned long long)key);
+            if (prev == -1) {
+                int s = atomicAdd(m.cursor, 1);
+                if (s < m.max_slots) m.slot_keys[s] = key;
+                else s = -2;  // id space exhausted: permanent region miss
+                __threadfence();
+                atomicExch(m.tvals + h, s);
+                return s;
+            }
+            if (prev == key) return wait_slot(m, h);
+        }
+        h = (h + 1) & m.tmask;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ int region_slot(const DevMap &m, long long key) {
+    // fast path: plain (cached) probe of entries that existed before this kernel
+    unsigned long long h = mix_key(key) & m.tmask;
+    long long k = m.tkeys[h];
+    if (k == key) {
+        int v = m.tvals[h];
+        if (v >= 0) return v;
+    }
+    return region_slot_slow(m, key);
+}
+
+// ---------------------------------------------------------------- block helpers
+
+// Per-block set of region slots already recorded this kernel: turns the
+// per-ray region bookkeeping into O(blocks x regions) global atomics.
+__device__ __forceinline__ bool slotset_insert(int *set, int slot) {
+    unsigned h = ((unsigned)slot * 2654435761u) >> 24;
+    for (int i = 0; i < SLOTSET; ++i) {
+        unsigned idx = (h + i) & (SLOTSET - 1);
+        int v = set[idx];
+        if (v == slot) return false;
+        if (v == -1) {
+            int prev = atomicCAS(set + idx, -1, slot);
+            if (prev == -1) return true;
+            if (prev == slot) return false;
+        }
+    }
+    return true;  // set full: treat as new (global op stays correct)
+}
+
+template <int N>
+__device__ __forceinline__ void block_add_stats(const DevMap &m, unsigned long long (&v)[N],
+                                                const int (&which)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        unsigned long long x = v[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0 && x) atomicAdd(m.stats + which[i], x);
+    }
+}
+
+// Track the region of the walker's current voxel: local coordinates are
+// stepped incrementally and the table is probed only on face crossings.
+// (Scalar fields only: dynamic array indexing would spill to local memory.)
+struct RegionTrack {
+    int rx, ry, rz, lx, ly, lz;
+    int slot;
+    __device__ __forceinline__ void locate(const DevMap &m, int gx, int gy, int gz) {
+        rx = floordiv(gx, m.dim);
+        ry = floordiv(gy, m.dim);
+        rz = floordiv(gz, m.dim);
+        lx = gx - rx * m.dim;
+        ly = gy - ry * m.dim;
+        lz = gz - rz * m.dim;
+        slot = region_slot(m, pack_region(rx, ry, rz));
+    }
+    // returns true if the region changed
+    __device__ __forceinline__ bool step(const DevMap &m, int axis, int s) {
+        int *l = axis == 0 ? &lx : (axis == 1 ? &ly : &lz);
+        int *r = axis == 0 ? &rx : (axis == 1 ? &ry : &rz);
+        int nl = *l + s;
+        if (nl == m.dim) {
+            *l = 0;
+            *r += 1;
+        } else if (nl < 0) {
+            *l = m.dim - 1;
+            *r -= 1;
+        } else {
+            *l = nl;
+            return false;
+        }
+        slot = region_slot(m, pack_region(rx, ry, rz));
+        return true;
+    }
+    __device__ __forceinline__ int li(const DevMap &m) const {
+        return lx + m.dim * (ly + m.dim * lz);
+    }
+};
+
+// ---------------------------------------------------------------- the walk
+
+// traversal._walk_grid (traversal.py:52-111) == _kernels.walk_fill
+// (_kernels.pyx:134-211), streamed: the visitor sees every visit in order
+// with (global cell, entry t, exit t, is_last).  Exact fp64 (no FMA).
+// V::begin(g) is called once, V::moved(axis, step) after every DDA step,
+// V::jump(g) before the numerical-fallback visit.  Scalar state only.
+template <class V>
+__device__ __forceinline__ void walk(const double o[3], const double e[3], double cell, V &vis) {
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+    const double vx = e[0] - o[0], vy = e[1] - o[1], vz = e[2] - o[2];
+    int cx = (int)floor(o[0] / cell), cy = (int)floor(o[1] / cell), cz = (int)floor(o[2] / cell);
+    const int ex = (int)floor(e[0] / cell), ey = (int)floor(e[1] / cell),
+              ez = (int)floor(e[2] / cell);
+    int sx = 0, sy = 0, sz = 0;
+    double tx = INF, ty = INF, tz = INF, dx = INF, dy = INF, dz = INF;
+    if (vx > 0) { sx = 1; tx = ((double)(cx + 1) * cell - o[0]) / vx; dx = cell / vx; }
+    else if (vx < 0) { sx = -1; tx = ((double)cx * cell - o[0]) / vx; dx = -cell / vx; }
+    if (vy > 0) { sy = 1; ty = ((double)(cy + 1) * cell - o[1]) / vy; dy = cell / vy; }
+    else if (vy < 0) { sy = -1; ty = ((double)cy * cell - o[1]) / vy; dy = -cell / vy; }
+    if (vz > 0) { sz = 1; tz = ((double)(cz + 1) * cell - o[2]) / vz; dz = cell / vz; }
+    else if (vz < 0) { sz = -1; tz = ((double)cz * cell - o[2]) / vz; dz = -cell / vz; }
+    int remaining = abs(cx - ex) + abs(cy - ey) + abs(cz - ez);
+    double tprev = 0.0;
+    vis.begin(cx, cy, cz);
+    for (;;) {
+        if (cx == ex && cy == ey && cz == ez) {
+            vis.visit(cx, cy, cz, tprev, 1.0, true);
+            return;
+        }
+        if (remaining <= 0) {
+            vis.jump(ex, ey, ez);
+            vis.visit(ex, ey, ez, tprev, 1.0, true);
+            return;
+        }
+        // axis = 0; if tmax[1] < tmax[axis]: 1; if tmax[2] < tmax[axis]: 2
+        int axis = ty < tx ? 1 : 0;
+        double ta = axis ? ty : tx;
+        if (tz < ta) { axis = 2; ta = tz; }
+        double tn = ta;
+        if (tn < tprev) tn = tprev;
+        if (tn > 1.0) tn = 1.0;
+        vis.visit(cx, cy, cz, tprev, tn, false);
+        if (axis == 0) { cx += sx; tx += dx; vis.moved(0, sx); }
+        else if (axis == 1) { cy += sy; ty += dy; vis.moved(1, sy); }
+        else { cz += sz; tz += dz; vis.moved(2, sz); }
+        tprev = tn;
+        --remaining;
+    }
+}
+
+}  // namespace vm

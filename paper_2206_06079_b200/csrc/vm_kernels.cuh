@@ -1,0 +1,1106 @@
+// vm_kernels.cuh -- the batch kernels of the ray-integration path.
+//
+// Pipeline of one batch (vm_runtime.cu drives it on the map's stream):
+//
+//   k_discover   one thread per ray: clip + segment (traversal.py:140-178),
+//                coarse region DDA = prefetch_regions (engine.py:99-118),
+//                region insertion into the HBM table, sample-voxel marks
+//                (deterministic mode) and NDT phase-2 hit records.
+//   k_guard      refuses the batch (go = 0) if the region pool would
+//                overflow; the host grows the pool and replays.
+//   k_walk_*     one thread per ray: exact fp64 DDA over every segment and
+//                the per-visit update (CAS, or RED miss counts + order-keyed
+//                records for sample voxels).
+//   k_resolve    deterministic miss counts -> f_miss^k per voxel.
+//   sort         CUB radix sort of the records (voxel-major, ray order).
+//   k_fold_*     in-order fold of the records per voxel (warp per voxel).
+//   k_cleanup    clears marks.
+#pragma once
+
+#include "vm_device.cuh"
+
+namespace vm {
+
+constexpr int BLOCK = 256;
+constexpr int REC_STAGE = 2048;  // per-block staging of records (16 KiB)
+
+// --------------------------------------------------------------- helpers
+
+// Block-staged append: smem slots first, one global atomic per block.
+template <class T, int CAP>
+struct Stage {
+    T *buf;
+    int *n;
+    __device__ __forceinline__ void push(T v, T *gbuf, unsigned long long *gcount,
+                                         unsigned long long gcap) {
+        int i = atomicAdd(n, 1);
+        if (i < CAP) {
+            buf[i] = v;
+        } else {
+            unsigned long long g = atomicAdd(gcount, 1ULL);
+            if (g < gcap) gbuf[g] = v;
+        }
+    }
+};
+
+__device__ __forceinline__ unsigned cas_apply_k(float *p, float d, unsigned k, float cmin,
+                                                float cmax) {
+    unsigned retries = 0;
+    unsigned old = __float_as_uint(__ldcg(p));
+    for (;;) {
+        float nl = miss_k(__uint_as_float(old), k, d, cmin, cmax);
+        unsigned nb = __float_as_uint(nl);
+        if (nb == old) return retries;  // f^k(l) == l: nothing to write
+        unsigned prev = atomicCAS(reinterpret_cast<unsigned *>(p), old, nb);
+        if (prev == old) return retries;
+        old = prev;
+        ++retries;
+    }
+}
+
+// _kernels.pyx:318-357 with the oracle's fold (subvoxel.py:34-49)
+__device__ __forceinline__ unsigned cas_mean(unsigned *mean, unsigned *cnt, const double off[3]) {
+    unsigned n_old = atomicAdd(cnt, 1u);
+    if (n_old == 0xFFFFFFFFu) {
+        atomicExch(cnt, 0xFFFFFFFFu);
+        return 0;
+    }
+    unsigned retries = 0;
+    unsigned old = __ldcg(mean);
+    for (;;) {
+        unsigned packed = old, c = n_old;
+        fold_mean(packed, c, off);
+        unsigned prev = atomicCAS(mean, old, packed);
+        if (prev == old) return retries;
+        old = prev;
+        ++retries;
+    }
+}
+
+// ndt.gaussian_miss_weight via the adjugate of _kernels.pyx:473-525
+__device__ __forceinline__ double gaussian_weight(const double mu[3], const float c6[6],
+                                                  double sigma2, const double o[3],
+                                                  const double v[3], double t0, double t1) {
+    double s0 = c6[0], s1 = c6[1], s2 = c6[2], s3 = c6[3], s4 = c6[4], s5 = c6[5];
+    double a00 = s0 * s0 + sigma2, a01 = s0 * s1, a02 = s0 * s3;
+    double a11 = s1 * s1 + s2 * s2 + sigma2, a12 = s1 * s3 + s2 * s4;
+    double a22 = s3 * s3 + s4 * s4 + s5 * s5 + sigma2;
+    double c00 = a11 * a22 - a12 * a12, c01 = a02 * a12 - a01 * a22, c02 = a01 * a12 - a02 * a11;
+    double det = a00 * c00 + a01 * c01 + a02 * c02;
+    if (det <= 0) return 1.0;
+    double i00 = c00 / det, i01 = c01 / det, i02 = c02 / det;
+    double i11 = (a00 * a22 - a02 * a02) / det;
+    double i12 = (a02 * a01 - a00 * a12) / det;
+    double i22 = (a00 * a11 - a01 * a01) / det;
+    double wx = mu[0] - o[0], wy = mu[1] - o[1], wz = mu[2] - o[2];
+    double vx = v[0], vy = v[1], vz = v[2];
+    double denom = vx * (i00 * vx + i01 * vy + i02 * vz) + vy * (i01 * vx + i11 * vy + i12 * vz) +
+                   vz * (i02 * vx + i12 * vy + i22 * vz);
+    double t;
+    if (denom <= 0) {
+        t = t0;
+    } else {
+        t = (vx * (i00 * wx + i01 * wy + i02 * wz) + vy * (i01 * wx + i11 * wy + i12 * wz) +
+             vz * (i02 * wx + i12 * wy + i22 * wz)) / denom;
+        if (t < t0) t = t0;
+        else if (t > t1) t = t1;
+    }
+    double dx = o[0] + t * vx - mu[0], dy = o[1] + t * vy - mu[1], dz = o[2] + t * vz - mu[2];
+    double m2 = dx * (i00 * dx + i01 * dy + i02 * dz) + dy * (i01 * dx + i11 * dy + i12 * dz) +
+                dz * (i02 * dx + i12 * dy + i22 * dz);
+    return exp(-0.5 * m2);
+}
+
+// CPython 3.12 math.hypot (Modules/mathmodule.c vector_norm), used by
+// ndt.cholupdate3 (ndt.py:42): bit-identical to the host's math.hypot.
+__device__ double py_hypot(double a, double b) {
+    double x0 = fabs(a), x1 = fabs(b);
+    double mx = 0.0;
+    if (x0 > mx) mx = x0;
+    if (x1 > mx) mx = x1;
+    if (isnan(a) || isnan(b)) return __longlong_as_double(0x7ff8000000000000LL);
+    double scale_back = 1.0;
+    if (isinf(mx)) return mx;
+    if (mx == 0.0) return mx;
+    int e;
+    frexp(mx, &e);
+    if (e < -1023) {
+        const double DMIN = 2.2250738585072014e-308;
+        x0 /= DMIN;
+        x1 /= DMIN;
+        mx /= DMIN;
+        scale_back = DMIN;
+        frexp(mx, &e);
+    }
+    double scale = ldexp(1.0, -e);
+    double csum = 1.0, frac1 = 0.0, frac2 = 0.0;
+    double xs[2] = {x0, x1};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        double x = xs[i] * scale;
+        double hi = x * x, lo = fma(x, x, -hi);
+        double s = csum + hi;
+        double sl = (csum - s) + hi;
+        csum = s;
+        frac1 += lo;
+        frac2 += sl;
+    }
+    double h = sqrt(csum - 1.0 + (frac1 + frac2));
+    {
+        double hi = -h * h, lo = fma(-h, h, -hi);
+        double s = csum + hi;
+        double sl = (csum - s) + hi;
+        csum = s;
+        frac1 += lo;
+        frac2 += sl;
+    }
+    double x = csum - 1.0 + (frac1 + frac2);
+    h += x / (2.0 * h);
+    return scale_back * (h / scale);
+}
+
+// ndt.update_gaussian + cholupdate3 (ndt.py:37-70); L stored as the 6
+// lower-triangular entries (s11, s21, s22, s31, s32, s33).
+__device__ __forceinline__ void update_gaussian(unsigned long long &n, double mu[3], double S[6],
+                                                const double x[3]) {
+    if (n == 0) {
+        n = 1;
+        for (int a = 0; a < 3; ++a) mu[a] = x[a];
+        for (int k = 0; k < 6; ++k) S[k] = 0.0;
+        return;
+    }
+    unsigned long long nn = n + 1;
+    double d[3];
+    for (int a = 0; a < 3; ++a) d[a] = x[a] - mu[a];
+    for (int a = 0; a < 3; ++a) mu[a] = mu[a] + d[a] / (double)nn;
+    double sq = sqrt((double)n);
+    double L[6];
+    for (int k = 0; k < 6; ++k) L[k] = S[k] * sq;
+    double f = sqrt((double)n / (double)nn);
+    double xx[3] = {d[0] * f, d[1] * f, d[2] * f};
+    // index of L[i][k] in the packed lower triangle
+    const int IDX[3][3] = {{0, -1, -1}, {1, 2, -1}, {3, 4, 5}};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double lkk = L[IDX[k][k]];
+        double r = py_hypot(lkk, xx[k]);
+        if (r == 0.0) continue;
+        double c = lkk / r, s = xx[k] / r;
+        L[IDX[k][k]] = r;
+#pragma unroll
+        for (int i = k + 1; i < 3; ++i) {
+            double lik = L[IDX[i][k]];
+            L[IDX[i][k]] = c * lik + s * xx[i];
+            xx[i] = c * xx[i] - s * lik;
+        }
+    }
+    double sn = sqrt((double)nn);
+    for (int k = 0; k < 6; ++k) S[k] = L[k] / sn;
+    n = nn;
+}
+
+__device__ __forceinline__ int read_go(const DevMap &m) {
+    return *((volatile int *)m.go);
+}
+
+// Global voxel coordinate of (slot, li) (keys.py:50-56).
+__device__ __forceinline__ void slot_li_to_g(const DevMap &m, int slot, int li, int g[3]) {
+    int r[3];
+    unpack_region(m.slot_keys[slot], r);
+    int lx = li % m.dim, t = li / m.dim;
+    int ly = t % m.dim, lz = t / m.dim;
+    g[0] = r[0] * m.dim + lx;
+    g[1] = r[1] * m.dim + ly;
+    g[2] = r[2] * m.dim + lz;
+}
+
+__device__ __forceinline__ bool in_range(const DevMap &m, const double p[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double c = floor(p[a] / m.vox);
+        if (!(c > -(double)m.cell_limit && c < (double)m.cell_limit)) return false;
+    }
+    return true;
+}
+
+// Record the region as touched by the walk (needed by k_resolve).
+__device__ __forceinline__ void touch_region(const DevMap &m, int *sset, int slot) {
+    if (!slotset_insert(sset, slot)) return;
+    if (atomicExch(m.slot_touch + slot, m.epoch) != m.epoch) {
+        unsigned long long idx = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
+        if (idx < (unsigned long long)m.touched_cap) m.touched[idx] = slot;
+    }
+}
+
+template <class T>
+__device__ __forceinline__ T *layer_at(const DevMap &m, int layer, int slot) {
+    return m.lptr[layer] ? reinterpret_cast<T *>(m.lptr[layer][slot]) : nullptr;
+}
+
+// --------------------------------------------------------------- k_discover
+
+// Coarse region DDA visitor (walk_regions, traversal.py:134-137).
+struct PrefetchVisitor {
+    const DevMap *m;
+    int *sset;
+    __device__ __forceinline__ void begin(int, int, int) {}
+    __device__ __forceinline__ void moved(int, int) {}
+    __device__ __forceinline__ void jump(int, int, int) {}
+    __device__ __forceinline__ void visit(int x, int y, int z, double, double, bool) {
+        int slot = region_slot(*m, pack_region(x, y, z));
+        if (slot < 0) return;
+        if (!slotset_insert(sset, slot)) return;
+        if (atomicExch(m->slot_pref + slot, m->epoch) != m->epoch)
+            atomicAdd(m->stats + S_PREF_TOUCHED, 1ULL);
+    }
+};
+
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevMap m, Src src, long long n, int mode,
+                                                    int det) {
+    __shared__ int sset[SLOTSET];
+    __shared__ int2 smark[BLOCK];
+    __shared__ unsigned long long srec[BLOCK];
+    __shared__ int nmark, nrec;
+    __shared__ unsigned long long mark_base, rec_base;
+    for (int i = threadIdx.x; i < SLOTSET; i += blockDim.x) sset[i] = -1;
+    if (threadIdx.x == 0) {
+        nmark = 0;
+        nrec = 0;
+    }
+    __syncthreads();
+    const bool tsdf = mode == M_TSDF;
+    const bool ndt = mode == M_NDT_OM || mode == M_NDT_TM;
+    unsigned long long st[3] = {0, 0, 0};  // processed, segments, range errors
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        Ray r;
+        src.load(i, r.o, r.e, r.has, r.inten);
+        bool ok = prep_ray(m, r, !tsdf);
+        if (ok) {
+            st[0] = 1;
+            st[1] = r.nseg;
+            if (!in_range(m, r.o) || !in_range(m, r.e)) {
+                st[2] = 1;
+            } else {
+                PrefetchVisitor pv{&m, sset};
+                for (int s = 0; s < r.nseg; ++s) {
+                    double so[3], se[3];
+                    int sh;
+                    segment_of(m, r, s, so, se, sh);
+                    double pe[3] = {se[0], se[1], se[2]};
+                    if (tsdf && sh) {
+                        double L = norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2]);
+                        if (L > 0.0) {
+                            for (int a = 0; a < 3; ++a) {
+                                double d = (se[a] - so[a]) / L;
+                                pe[a] = se[a] + d * m.tsdf_trunc;
+                            }
+                            if (!in_range(m, pe)) {
+                                st[2] = 1;
+                                break;
+                            }
+                        }
+                    }
+                    walk(so, pe, m.rsize, pv);
+                    if (sh && (det || ndt) && !tsdf) {
+                        // the sample voxel floor(end / vox) (reference.py:178-186)
+                        int g[3];
+                        for (int a = 0; a < 3; ++a) g[a] = (int)floor(se[a] / m.vox);
+                        RegionTrack rt;
+                        rt.locate(m, g[0], g[1], g[2]);
+                        if (rt.slot >= 0 && rt.slot < m.cap) {
+                            int li = rt.li(m);
+                            if (ndt) {
+                                unsigned long long vid =
+                                    (unsigned long long)rt.slot * m.vpr + li;
+                                unsigned long long order =
+                                    ((unsigned long long)(i * m.maxseg + s) << 1) | 1ULL;
+                                int k = atomicAdd(&nrec, 1);
+                                srec[k] = (vid << m.order_bits) | order;
+                            } else {
+                                unsigned bit = 1u << (li & 31);
+                                unsigned old = atomicOr(
+                                    m.marks + (size_t)rt.slot * m.mark_words + (li >> 5), bit);
+                                if (!(old & bit)) {
+                                    int k = atomicAdd(&nmark, 1);
+                                    smark[k] = make_int2(rt.slot, li);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (nmark) mark_base = atomicAdd(m.stats + S_MARKED, (unsigned long long)nmark);
+        if (nrec) rec_base = atomicAdd(m.stats + S_RECORDS, (unsigned long long)nrec);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nmark; k += blockDim.x) {
+        unsigned long long mi = mark_base + k;
+        if (mi < (unsigned long long)m.marked_cap) {
+            int2 sl = smark[k];
+            m.marked[mi] = sl;
+            // the marked index lives in the (otherwise unused) scratch word
+            unsigned *scr = layer_at<unsigned>(m, L_SCRATCH, sl.x);
+            scr[sl.y] = MARK_FLAG | (unsigned)mi;
+        }
+    }
+    for (int k = threadIdx.x; k < nrec; k += blockDim.x) {
+        unsigned long long ri = rec_base + k;
+        if (ri < m.rec_cap) m.rec[ri] = srec[k];
+    }
+    const int which[3] = {S_PROCESSED, S_SEGMENTS, S_RANGE_ERR};
+    block_add_stats(m, st, which);
+}
+
+// Refuse the batch if the pool could overflow or inputs were invalid.
+__global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
+    int used = *((volatile int *)m.cursor);
+    unsigned long long rerr = ((volatile unsigned long long *)m.stats)[S_RANGE_ERR];
+    unsigned long long marked = ((volatile unsigned long long *)m.stats)[S_MARKED];
+    bool ok = used + margin <= m.cap && rerr == 0 && marked <= (unsigned long long)m.marked_cap;
+    *m.go = ok ? 1 : 0;
+}
+
+// --------------------------------------------------------------- occupancy walk
+
+template <int MODE, bool DET, bool REC_ONLY>
+struct OccVisitor {
+    const DevMap *m;
+    RegionTrack rt;
+    float *occ;
+    unsigned *mean, *cnt, *scr, *dh;
+    double *dd;
+    unsigned order;      // (ray * maxseg + seg) << 1
+    int sh;
+    double Lseg;
+    const double *se;
+    int *sset;
+    unsigned *cube;
+    int c0, c1, c2;      // cube corner (global voxel)
+    Stage<unsigned long long, REC_STAGE> *stage;
+    unsigned long long visits, rmiss, retries;
+
+    __device__ __forceinline__ void bind() {
+        int s = rt.slot;
+        if (s >= 0 && s < m->cap) {
+            occ = layer_at<float>(*m, L_OCC, s);
+            if (DET || !REC_ONLY) scr = layer_at<unsigned>(*m, L_SCRATCH, s);
+            mean = layer_at<unsigned>(*m, L_MEAN, s);
+            cnt = layer_at<unsigned>(*m, L_COUNT, s);
+            if (MODE == M_DECAY) {
+                dh = layer_at<unsigned>(*m, L_DHITS, s);
+                dd = layer_at<double>(*m, L_DDIST, s);
+            }
+            if (DET && !REC_ONLY) touch_region(*m, sset, s);
+        } else {
+            occ = nullptr;
+        }
+    }
+    __device__ __forceinline__ void begin(int x, int y, int z) {
+        rt.locate(*m, x, y, z);
+        bind();
+    }
+    __device__ __forceinline__ void moved(int axis, int s) {
+        if (rt.step(*m, axis, s)) bind();
+    }
+    __device__ __forceinline__ void jump(int x, int y, int z) {
+        rt.locate(*m, x, y, z);
+        bind();
+    }
+    __device__ __forceinline__ void visit(int x, int y, int z, double t0, double t1, bool last) {
+        ++visits;
+        if (!occ) {
+            ++rmiss;
+            return;
+        }
+        const int li = rt.li(*m);
+        const bool hit = last && sh;
+        if (MODE == M_DECAY && !REC_ONLY) {
+            atomicAdd(dd + li, (t1 - t0) * Lseg);
+            if (hit) atomicAdd(dh + li, 1u);
+        }
+        if (DET) {
+            const int s = rt.slot;
+            unsigned w = __ldg(m->marks + (size_t)s * m->mark_words + (li >> 5));
+            if ((w >> (li & 31)) & 1u) {
+                unsigned mi = scr[li] & ~MARK_FLAG;
+                unsigned long long key = ((unsigned long long)mi << m->order_bits) |
+                                         (unsigned long long)(order | (hit ? 1u : 0u));
+                stage->push(key, m->rec, m->stats + S_RECORDS, m->rec_cap);
+                return;
+            }
+            if (REC_ONLY) return;
+            unsigned ux = (unsigned)(x - c0), uy = (unsigned)(y - c1), uz = (unsigned)(z - c2);
+            if ((ux | uy | uz) < (unsigned)CUBE)
+                atomicAdd(cube + ux + CUBE * (uy + CUBE * uz), 1u);
+            else
+                atomicAdd(scr + li, 1u);
+        } else {
+            if (hit) {
+                float *p = occ + li;
+                unsigned old = __float_as_uint(__ldcg(p));
+                for (;;) {
+                    unsigned nb = __float_as_uint(clamp_add(__uint_as_float(old), m->hit32,
+                                                            m->cmin, m->cmax));
+                    if (nb == old) break;
+                    unsigned prev = atomicCAS(reinterpret_cast<unsigned *>(p), old, nb);
+                    if (prev == old) break;
+                    old = prev;
+                    ++retries;
+                }
+                if (mean) {
+                    double off[3] = {se[0] / m->vox - (double)x, se[1] / m->vox - (double)y,
+                                     se[2] / m->vox - (double)z};
+                    retries += cas_mean(mean + li, cnt + li, off);
+                }
+            } else {
+                unsigned ux = (unsigned)(x - c0), uy = (unsigned)(y - c1), uz = (unsigned)(z - c2);
+                if ((ux | uy | uz) < (unsigned)CUBE)
+                    atomicAdd(cube + ux + CUBE * (uy + CUBE * uz), 1u);
+                else
+                    retries += cas_apply_k(occ + li, m->miss32, 1, m->cmin, m->cmax);
+            }
+        }
+    }
+};
+
+template <int MODE, bool DET, bool REC_ONLY, class Src>
+__global__ void __launch_bounds__(BLOCK) k_walk_occ(const __grid_constant__ DevMap m, Src src, long long n) {
+    __shared__ unsigned cube[CUBE_N];
+    __shared__ int sset[SLOTSET];
+    __shared__ unsigned long long srec[REC_STAGE];
+    __shared__ int nrec;
+    __shared__ unsigned long long rec_base;
+    __shared__ int corner[3];
+    if (!read_go(m)) return;
+    for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) cube[k] = 0;
+    for (int k = threadIdx.x; k < SLOTSET; k += blockDim.x) sset[k] = -1;
+    long long first = (long long)blockIdx.x * blockDim.x;
+    if (threadIdx.x == 0) {
+        nrec = 0;
+        double o[3], e[3];
+        int h;
+        float it;
+        src.load(first, o, e, h, it);
+        for (int a = 0; a < 3; ++a) corner[a] = (int)floor(o[a] / m.vox) - CUBE / 2;
+    }
+    __syncthreads();
+    Stage<unsigned long long, REC_STAGE> stage{srec, &nrec};
+    OccVisitor<MODE, DET, REC_ONLY> v;
+    v.m = &m;
+    v.sset = sset;
+    v.cube = cube;
+    v.c0 = corner[0];
+    v.c1 = corner[1];
+    v.c2 = corner[2];
+    v.stage = &stage;
+    v.visits = v.rmiss = v.retries = 0;
+    v.scr = nullptr;
+    v.dh = nullptr;
+    v.dd = nullptr;
+    long long i = first + threadIdx.x;
+    if (i < n) {
+        Ray r;
+        src.load(i, r.o, r.e, r.has, r.inten);
+        if (prep_ray(m, r, true)) {
+            for (int s = 0; s < r.nseg; ++s) {
+                double so[3], se[3];
+                segment_of(m, r, s, so, se, v.sh);
+                v.order = (unsigned)(i * m.maxseg + s) << 1;
+                v.se = se;
+                v.Lseg = MODE == M_DECAY ? norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2])
+                                         : 0.0;
+                walk(so, se, m.vox, v);
+            }
+        }
+    }
+    __syncthreads();
+    // flush the aggregation cube: k identical misses per voxel
+    unsigned long long flushed = 0;
+    if (!REC_ONLY) {
+        for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) {
+            unsigned cnt = cube[k];
+            if (!cnt) continue;
+            ++flushed;
+            int g[3] = {v.c0 + k % CUBE, v.c1 + (k / CUBE) % CUBE, v.c2 + k / (CUBE * CUBE)};
+            RegionTrack rt;
+            rt.locate(m, g[0], g[1], g[2]);
+            int li = rt.li(m);
+            if (DET) {
+                unsigned *scr = layer_at<unsigned>(m, L_SCRATCH, rt.slot);
+                touch_region(m, sset, rt.slot);
+                atomicAdd(scr + li, cnt);
+            } else {
+                float *occ = layer_at<float>(m, L_OCC, rt.slot);
+                v.retries += cas_apply_k(occ + li, m.miss32, cnt, m.cmin, m.cmax);
+            }
+        }
+    }
+    if (DET) {
+        __syncthreads();
+        int nl = nrec < REC_STAGE ? nrec : REC_STAGE;
+        if (threadIdx.x == 0 && nl) rec_base = atomicAdd(m.stats + S_RECORDS, (unsigned long long)nl);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nl; k += blockDim.x) {
+            unsigned long long ri = rec_base + k;
+            if (ri < m.rec_cap) m.rec[ri] = srec[k];
+        }
+    }
+    if (!REC_ONLY) {
+        unsigned long long st[4] = {v.visits, v.rmiss, v.retries, flushed};
+        const int which[4] = {S_VISITS, S_RMISS, S_RETRIES, S_CUBE_FLUSH};
+        block_add_stats(m, st, which);
+    }
+}
+
+// --------------------------------------------------------------- NDT phase 1
+
+template <bool TM>
+struct NdtVisitor {
+    const DevMap *m;
+    RegionTrack rt;
+    float *occ, *cov;
+    unsigned *mean, *cnt, *scr, *miss, *hitc;
+    float *inten;
+    int sh;
+    const double *so;
+    double v[3];
+    int *sset;
+    unsigned *cube;
+    int c0, c1, c2;
+    unsigned long long visits, rmiss, retries;
+
+    __device__ __forceinline__ void bind() {
+        int s = rt.slot;
+        if (s >= 0 && s < m->cap) {
+            occ = layer_at<float>(*m, L_OCC, s);
+            cov = layer_at<float>(*m, L_COV, s);
+            mean = layer_at<unsigned>(*m, L_MEAN, s);
+            cnt = layer_at<unsigned>(*m, L_COUNT, s);
+            scr = layer_at<unsigned>(*m, L_SCRATCH, s);
+            if (TM) {
+                miss = layer_at<unsigned>(*m, L_MISS, s);
+                hitc = layer_at<unsigned>(*m, L_HIT, s);
+                inten = layer_at<float>(*m, L_INTENS, s);
+            }
+            touch_region(*m, sset, s);
+        } else {
+            occ = nullptr;
+        }
+    }
+    __device__ __forceinline__ void begin(int x, int y, int z) {
+        rt.locate(*m, x, y, z);
+        bind();
+    }
+    __device__ __forceinline__ void moved(int axis, int s) {
+        if (rt.step(*m, axis, s)) bind();
+    }
+    __device__ __forceinline__ void jump(int x, int y, int z) {
+        rt.locate(*m, x, y, z);
+        bind();
+    }
+    // reference.py:67-94 / _kernels.pyx:602-648
+    __device__ __forceinline__ void visit(int x, int y, int z, double t0, double t1, bool last) {
+        ++visits;
+        if (last && sh) return;  // sample voxel: phase 2
+        if (!occ) {
+            ++rmiss;
+            return;
+        }
+        const int li = rt.li(*m);
+        unsigned ns = __ldcg(cnt + li);
+        if (ns < 3) {
+            // g == 1: identical deltas, order-free -> counted, resolved exactly
+            unsigned ux = (unsigned)(x - c0), uy = (unsigned)(y - c1), uz = (unsigned)(z - c2);
+            if ((ux | uy | uz) < (unsigned)CUBE)
+                atomicAdd(cube + ux + CUBE * (uy + CUBE * uz), 1u);
+            else
+                atomicAdd(scr + li, 1u);
+            return;
+        }
+        unsigned packed = __ldcg(mean + li);
+        float c6[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) c6[j] = __ldcg(cov + li * 6 + j);
+        double off[3], mu[3];
+        unpack_mean(packed, off);
+        mu[0] = ((double)x + off[0]) * m->vox;
+        mu[1] = ((double)y + off[1]) * m->vox;
+        mu[2] = ((double)z + off[2]) * m->vox;
+        double gw = gaussian_weight(mu, c6, m->sigma2, so, v, t0, t1);
+        float d32 = (float)(gw * m->miss_delta);
+        {
+            float *p = occ + li;
+            unsigned old = __float_as_uint(__ldcg(p));
+            for (;;) {
+                unsigned nb = __float_as_uint(clamp_add(__uint_as_float(old), d32, m->cmin,
+                                                        m->cmax));
+                if (nb == old) break;
+                unsigned prev = atomicCAS(reinterpret_cast<unsigned *>(p), old, nb);
+                if (prev == old) break;
+                old = prev;
+                ++retries;
+            }
+        }
+        if (TM && gw >= m->miss_check) atomicAdd(miss + li, 1u);
+        float lnow = __ldcg(occ + li);
+        if (lnow < m->fthresh && __ldcg(cnt + li) > 0) {
+            atomicExch(cnt + li, 0u);
+            atomicExch(mean + li, 0u);
+#pragma unroll
+            for (int j = 0; j < 6; ++j) atomicExch(reinterpret_cast<unsigned *>(cov) + li * 6 + j, 0u);
+            if (TM) {
+                atomicExch(hitc + li, 0u);
+                atomicExch(miss + li, 0u);
+                atomicExch(reinterpret_cast<unsigned *>(inten) + li * 2, 0u);
+                atomicExch(reinterpret_cast<unsigned *>(inten) + li * 2 + 1, 0u);
+            }
+        }
+    }
+};
+
+template <bool TM, class Src>
+__global__ void __launch_bounds__(BLOCK) k_walk_ndt(const __grid_constant__ DevMap m, Src src, long long n) {
+    __shared__ unsigned cube[CUBE_N];
+    __shared__ int sset[SLOTSET];
+    __shared__ int corner[3];
+    if (!read_go(m)) return;
+    for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) cube[k] = 0;
+    for (int k = threadIdx.x; k < SLOTSET; k += blockDim.x) sset[k] = -1;
+    long long first = (long long)blockIdx.x * blockDim.x;
+    if (threadIdx.x == 0) {
+        double o[3], e[3];
+        int h;
+        float it;
+        src.load(first, o, e, h, it);
+        for (int a = 0; a < 3; ++a) corner[a] = (int)floor(o[a] / m.vox) - CUBE / 2;
+    }
+    __syncthreads();
+    NdtVisitor<TM> v;
+    v.m = &m;
+    v.sset = sset;
+    v.cube = cube;
+    v.c0 = corner[0];
+    v.c1 = corner[1];
+    v.c2 = corner[2];
+    v.visits = v.rmiss = v.retries = 0;
+    long long i = first + threadIdx.x;
+    if (i < n) {
+        Ray r;
+        src.load(i, r.o, r.e, r.has, r.inten);
+        if (prep_ray(m, r, true)) {
+            for (int s = 0; s < r.nseg; ++s) {
+                double so[3], se[3];
+                segment_of(m, r, s, so, se, v.sh);
+                v.so = so;
+                for (int a = 0; a < 3; ++a) v.v[a] = se[a] - so[a];
+                walk(so, se, m.vox, v);
+            }
+        }
+    }
+    __syncthreads();
+    unsigned long long flushed = 0;
+    for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) {
+        unsigned cnt = cube[k];
+        if (!cnt) continue;
+        ++flushed;
+        int g[3] = {v.c0 + k % CUBE, v.c1 + (k / CUBE) % CUBE, v.c2 + k / (CUBE * CUBE)};
+        RegionTrack rt;
+        rt.locate(m, g[0], g[1], g[2]);
+        touch_region(m, sset, rt.slot);
+        atomicAdd(layer_at<unsigned>(m, L_SCRATCH, rt.slot) + rt.li(m), cnt);
+    }
+    unsigned long long st[4] = {v.visits, v.rmiss, v.retries, flushed};
+    const int which[4] = {S_VISITS, S_RMISS, S_RETRIES, S_CUBE_FLUSH};
+    block_add_stats(m, st, which);
+}
+
+// --------------------------------------------------------------- TSDF
+
+template <bool DET>
+struct TsdfVisitor {
+    const DevMap *m;
+    RegionTrack rt;
+    float *buf;
+    double o[3], d[3], L;
+    unsigned ray;
+    Stage<unsigned long long, REC_STAGE> *stage;
+    unsigned long long visits, rmiss, retries;
+    __device__ __forceinline__ void bind() {
+        int s = rt.slot;
+        buf = (s >= 0 && s < m->cap) ? layer_at<float>(*m, L_TSDF, s) : nullptr;
+    }
+    __device__ __forceinline__ void begin(int x, int y, int z) {
+        rt.locate(*m, x, y, z);
+        bind();
+    }
+    __device__ __forceinline__ void moved(int axis, int s) {
+        if (rt.step(*m, axis, s)) bind();
+    }
+    __device__ __forceinline__ void jump(int x, int y, int z) {
+        rt.locate(*m, x, y, z);
+        bind();
+    }
+    __device__ __forceinline__ void visit(int x, int y, int z, double, double, bool) {
+        ++visits;
+        if (!buf) {
+            ++rmiss;
+            return;
+        }
+        const int li = rt.li(*m);
+        if (DET) {
+            unsigned long long vid = (unsigned long long)rt.slot * m->vpr + li;
+            stage->push((vid << m->order_bits) | ray, m->rec, m->stats + S_RECORDS, m->rec_cap);
+            return;
+        }
+        // reference.py:167-174
+        double c[3] = {((double)x + 0.5) * m->vox - o[0], ((double)y + 0.5) * m->vox - o[1],
+                       ((double)z + 0.5) * m->vox - o[2]};
+        double dv = L - dot3(c, d);
+        if (dv < -m->tsdf_trunc) dv = -m->tsdf_trunc;
+        if (dv > m->tsdf_trunc) dv = m->tsdf_trunc;
+        unsigned long long *p = reinterpret_cast<unsigned long long *>(buf + 2 * li);
+        unsigned long long old = __ldcg(p);
+        for (;;) {
+            float fd = __uint_as_float((unsigned)(old & 0xffffffffu));
+            float fw = __uint_as_float((unsigned)(old >> 32));
+            double w = fw;
+            float nd = (float)((w * (double)fd + dv) / (w + 1.0));
+            double nwd = w + 1.0;
+            if (nwd > m->tsdf_maxw) nwd = m->tsdf_maxw;
+            float nw = (float)nwd;
+            unsigned long long nb = ((unsigned long long)__float_as_uint(nw) << 32) |
+                                    __float_as_uint(nd);
+            unsigned long long prev = atomicCAS(p, old, nb);
+            if (prev == old) break;
+            old = prev;
+            ++retries;
+        }
+    }
+};
+
+// band geometry of integrate_tsdf_ray (reference.py:153-165)
+__device__ __forceinline__ bool tsdf_band(const DevMap &m, const Ray &r, double d[3],
+                                          double p0[3], double p1[3]) {
+    if (!r.has || r.L == 0.0) return false;
+    for (int a = 0; a < 3; ++a) d[a] = (r.e[a] - r.o[a]) / r.L;
+    double ts = r.L - m.tsdf_trunc;
+    if (!(ts > 0.0)) ts = 0.0;
+    double te = r.L + m.tsdf_trunc;
+    for (int a = 0; a < 3; ++a) {
+        p0[a] = r.o[a] + d[a] * ts;
+        p1[a] = r.o[a] + d[a] * te;
+    }
+    return true;
+}
+
+template <bool DET, class Src>
+__global__ void __launch_bounds__(BLOCK) k_walk_tsdf(const __grid_constant__ DevMap m, Src src, long long n) {
+    __shared__ unsigned long long srec[REC_STAGE];
+    __shared__ int nrec;
+    __shared__ unsigned long long rec_base;
+    if (!read_go(m)) return;
+    if (threadIdx.x == 0) nrec = 0;
+    __syncthreads();
+    Stage<unsigned long long, REC_STAGE> stage{srec, &nrec};
+    TsdfVisitor<DET> v;
+    v.m = &m;
+    v.stage = &stage;
+    v.visits = v.rmiss = v.retries = 0;
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        Ray r;
+        src.load(i, r.o, r.e, r.has, r.inten);
+        double p0[3], p1[3];
+        if (prep_ray(m, r, false) && tsdf_band(m, r, v.d, p0, p1)) {
+            for (int a = 0; a < 3; ++a) v.o[a] = r.o[a];
+            v.L = r.L;
+            v.ray = (unsigned)i;
+            walk(p0, p1, m.vox, v);
+        }
+    }
+    if (DET) {
+        __syncthreads();
+        int nl = nrec < REC_STAGE ? nrec : REC_STAGE;
+        if (threadIdx.x == 0 && nl) rec_base = atomicAdd(m.stats + S_RECORDS, (unsigned long long)nl);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nl; k += blockDim.x) {
+            unsigned long long ri = rec_base + k;
+            if (ri < m.rec_cap) m.rec[ri] = srec[k];
+        }
+    }
+    unsigned long long st[3] = {v.visits, v.rmiss, v.retries};
+    const int which[3] = {S_VISITS, S_RMISS, S_RETRIES};
+    block_add_stats(m, st, which);
+}
+
+// --------------------------------------------------------------- resolve
+
+// f_miss^k for every voxel that received k order-free misses this batch;
+// NDT adds the NDT-TM miss count and the transient reset
+// (reference.py:86-93).  One block per touched region.
+template <bool NDT, bool TM>
+__global__ void __launch_bounds__(BLOCK) k_resolve(const __grid_constant__ DevMap m) {
+    if (!read_go(m)) return;
+    unsigned long long nt = *((volatile unsigned long long *)(m.stats + S_WALK_TOUCHED));
+    if (nt > (unsigned long long)m.touched_cap) nt = m.touched_cap;
+    for (unsigned long long t = blockIdx.x; t < nt; t += gridDim.x) {
+        int slot = m.touched[t];
+        unsigned *scr = layer_at<unsigned>(m, L_SCRATCH, slot);
+        float *occ = layer_at<float>(m, L_OCC, slot);
+        for (int li = threadIdx.x; li < m.vpr; li += blockDim.x) {
+            unsigned k = scr[li];
+            if (k == 0 || (k & MARK_FLAG)) continue;
+            scr[li] = 0;
+            float l = miss_k(occ[li], k, m.miss32, m.cmin, m.cmax);
+            occ[li] = l;
+            if (NDT) {
+                unsigned *cnt = layer_at<unsigned>(m, L_COUNT, slot);
+                if (TM) layer_at<unsigned>(m, L_MISS, slot)[li] += k;
+                if (l < m.fthresh && cnt[li] > 0) {
+                    cnt[li] = 0;
+                    layer_at<unsigned>(m, L_MEAN, slot)[li] = 0;
+                    float *cov = layer_at<float>(m, L_COV, slot);
+                    for (int j = 0; j < 6; ++j) cov[li * 6 + j] = 0.0f;
+                    if (TM) {
+                        layer_at<unsigned>(m, L_HIT, slot)[li] = 0;
+                        layer_at<unsigned>(m, L_MISS, slot)[li] = 0;
+                        float *it = layer_at<float>(m, L_INTENS, slot);
+                        it[li * 2] = 0.0f;
+                        it[li * 2 + 1] = 0.0f;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------- folds
+
+__device__ __forceinline__ long long lower_bound_u64(const unsigned long long *a, long long n,
+                                                     unsigned long long key) {
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        long long mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Deterministic occupancy fold: one warp per sample voxel applies its
+// records in ray order (reference.py:35-64 for exactly that voxel).
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_fold_occ(const __grid_constant__ DevMap m, Src src,
+                                                    const unsigned long long *keys,
+                                                    long long R, int M) {
+    if (!read_go(m)) return;
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+    const unsigned long long omask = (1ULL << m.order_bits) - 1;
+    for (long long mi = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; mi < M;
+         mi += warps) {
+        int2 sl = m.marked[mi];
+        float *occ = layer_at<float>(m, L_OCC, sl.x);
+        unsigned *mean = layer_at<unsigned>(m, L_MEAN, sl.x);
+        unsigned *cnt = layer_at<unsigned>(m, L_COUNT, sl.x);
+        long long pos = 0;
+        if (lane == 0) pos = lower_bound_u64(keys, R, (unsigned long long)mi << m.order_bits);
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        float l = occ[sl.y];
+        unsigned packed = mean ? mean[sl.y] : 0u, count = cnt ? cnt[sl.y] : 0u;
+        int g[3];
+        slot_li_to_g(m, sl.x, sl.y, g);
+        for (;;) {
+            long long p = pos + lane;
+            unsigned long long key = p < R ? keys[p] : ~0ULL;
+            bool valid = p < R && (key >> m.order_bits) == (unsigned long long)mi;
+            unsigned vmask = __ballot_sync(0xffffffffu, valid);
+            if (!vmask) break;
+            unsigned hmask = __ballot_sync(0xffffffffu, valid && (key & 1ULL));
+            int nvalid = __popc(vmask);
+            int cur = 0;
+            while (cur < nvalid) {
+                unsigned rem = cur < 32 ? (hmask >> cur) : 0u;
+                if (!rem) {
+                    l = miss_k(l, (unsigned)(nvalid - cur), m.miss32, m.cmin, m.cmax);
+                    break;
+                }
+                int nh = cur + __ffs(rem) - 1;
+                l = miss_k(l, (unsigned)(nh - cur), m.miss32, m.cmin, m.cmax);
+                unsigned long long hk = __shfl_sync(0xffffffffu, key, nh);
+                l = clamp_add(l, m.hit32, m.cmin, m.cmax);
+                if (mean) {
+                    long long ray = (long long)(((hk & omask) >> 1) / (unsigned long long)m.maxseg);
+                    double e[3];
+                    float it;
+                    src.load_end(ray, e, it);
+                    double off[3] = {e[0] / m.vox - (double)g[0], e[1] / m.vox - (double)g[1],
+                                     e[2] / m.vox - (double)g[2]};
+                    fold_mean(packed, count, off);
+                }
+                cur = nh + 1;
+            }
+            pos += nvalid;
+            if (nvalid < 32) break;
+        }
+        if (lane == 0) {
+            occ[sl.y] = l;
+            if (mean) {
+                mean[sl.y] = packed;
+                cnt[sl.y] = count;
+            }
+        }
+    }
+}
+
+// NDT phase 2 (reference.py:107-150): one thread per sample voxel folds its
+// samples in ray order; f64 Welford mean + Givens sqrt-covariance.
+template <bool TM, class Src>
+__global__ void __launch_bounds__(BLOCK) k_fold_ndt(const __grid_constant__ DevMap m, Src src,
+                                                    const unsigned long long *keys, long long R) {
+    if (!read_go(m)) return;
+    const unsigned long long omask = (1ULL << m.order_bits) - 1;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long vid = keys[i] >> m.order_bits;
+        if (i > 0 && (keys[i - 1] >> m.order_bits) == vid) continue;
+        int slot = (int)(vid / (unsigned long long)m.vpr), li = (int)(vid % (unsigned long long)m.vpr);
+        int g[3];
+        slot_li_to_g(m, slot, li, g);
+        float *occ = layer_at<float>(m, L_OCC, slot);
+        unsigned *mb = layer_at<unsigned>(m, L_MEAN, slot);
+        unsigned *cb = layer_at<unsigned>(m, L_COUNT, slot);
+        float *cov = layer_at<float>(m, L_COV, slot);
+        unsigned long long nsamp = cb[li];
+        double mu[3] = {0.0, 0.0, 0.0};
+        if (nsamp > 0) {
+            double off[3];
+            unpack_mean(mb[li], off);
+            for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
+        }
+        double S[6];
+        for (int k = 0; k < 6; ++k) S[k] = cov[li * 6 + k];
+        float l = occ[li];
+        float *ib = TM ? layer_at<float>(m, L_INTENS, slot) : nullptr;
+        long long j = i;
+        for (; j < R && (keys[j] >> m.order_bits) == vid; ++j) {
+            long long ray = (long long)(((keys[j] & omask) >> 1) / (unsigned long long)m.maxseg);
+            double e[3];
+            float it;
+            src.load_end(ray, e, it);
+            l = clamp_add(l, m.hit32, m.cmin, m.cmax);
+            if (TM) {
+                // ndt.update_intensity (ndt.py:98-106), stored f32 each sample
+                double val = it, imean = ib[li * 2], m2 = ib[li * 2 + 1];
+                double nn = (double)(nsamp + 1);
+                double d = val - imean;
+                double mnew = imean + d / nn;
+                double m2new = m2 + d * (val - mnew);
+                ib[li * 2] = (float)mnew;
+                ib[li * 2 + 1] = (float)m2new;
+            }
+            update_gaussian(nsamp, mu, S, e);
+        }
+        occ[li] = l;
+        if (TM) layer_at<unsigned>(m, L_HIT, slot)[li] += (unsigned)(j - i);
+        cb[li] = nsamp > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)nsamp;
+        double frac[3];
+        const double hi = 1.0 - 1.0 / 2048.0;
+        for (int a = 0; a < 3; ++a) {
+            double f = mu[a] / m.vox - (double)g[a];
+            if (f < 0.0) f = 0.0;
+            if (f > hi) f = hi;
+            frac[a] = f;
+        }
+        mb[li] = pack_mean(frac);
+        for (int k = 0; k < 6; ++k) cov[li * 6 + k] = (float)S[k];
+    }
+}
+
+// Deterministic TSDF: one thread per voxel merges its band visits in ray
+// order (reference.py:153-175).
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_fold_tsdf(const __grid_constant__ DevMap m, Src src,
+                                                     const unsigned long long *keys, long long R) {
+    if (!read_go(m)) return;
+    const unsigned long long omask = (1ULL << m.order_bits) - 1;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long vid = keys[i] >> m.order_bits;
+        if (i > 0 && (keys[i - 1] >> m.order_bits) == vid) continue;
+        int slot = (int)(vid / (unsigned long long)m.vpr), li = (int)(vid % (unsigned long long)m.vpr);
+        int g[3];
+        slot_li_to_g(m, slot, li, g);
+        float *buf = layer_at<float>(m, L_TSDF, slot);
+        float fd = buf[2 * li], fw = buf[2 * li + 1];
+        for (long long j = i; j < R && (keys[j] >> m.order_bits) == vid; ++j) {
+            long long ray = (long long)(keys[j] & omask);
+            Ray r;
+            src.load(ray, r.o, r.e, r.has, r.inten);
+            prep_ray(m, r, false);
+            double d[3];
+            for (int a = 0; a < 3; ++a) d[a] = (r.e[a] - r.o[a]) / r.L;
+            double c[3] = {((double)g[0] + 0.5) * m.vox - r.o[0],
+                           ((double)g[1] + 0.5) * m.vox - r.o[1],
+                           ((double)g[2] + 0.5) * m.vox - r.o[2]};
+            double dv = r.L - dot3(c, d);
+            if (dv < -m.tsdf_trunc) dv = -m.tsdf_trunc;
+            if (dv > m.tsdf_trunc) dv = m.tsdf_trunc;
+            double w = fw;
+            fd = (float)((w * (double)fd + dv) / (w + 1.0));
+            double nw = w + 1.0;
+            if (nw > m.tsdf_maxw) nw = m.tsdf_maxw;
+            fw = (float)nw;
+        }
+        buf[2 * li] = fd;
+        buf[2 * li + 1] = fw;
+    }
+}
+
+// Clear marks and the marked-index scratch words of this batch.
+__global__ void k_cleanup(const __grid_constant__ DevMap m, int M) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < M;
+         k += (long long)gridDim.x * blockDim.x) {
+        int2 sl = m.marked[k];
+        m.marks[(size_t)sl.x * m.mark_words + (sl.y >> 5)] = 0u;
+        layer_at<unsigned>(m, L_SCRATCH, sl.x)[sl.y] = 0u;
+    }
+}
+
+// --------------------------------------------------------------- single walk
+
+struct CollectVisitor {
+    long long *coords;
+    double *t0, *t1;
+    long long cap, n;
+    __device__ __forceinline__ void begin(int, int, int) {}
+    __device__ __forceinline__ void moved(int, int) {}
+    __device__ __forceinline__ void jump(int, int, int) {}
+    __device__ __forceinline__ void visit(int x, int y, int z, double a, double b, bool) {
+        if (n < cap) {
+            coords[3 * n] = x;
+            coords[3 * n + 1] = y;
+            coords[3 * n + 2] = z;
+            t0[n] = a;
+            t1[n] = b;
+        }
+        ++n;
+    }
+};
+
+__global__ void k_walk_one(double ox, double oy, double oz, double ex, double ey, double ez,
+                           double cell, long long *coords, double *t0, double *t1, long long cap,
+                           long long *n_out) {
+    double o[3] = {ox, oy, oz}, e[3] = {ex, ey, ez};
+    CollectVisitor v{coords, t0, t1, cap, 0};
+    walk(o, e, cell, v);
+    *n_out = v.n;
+}
+
+}  // namespace vm

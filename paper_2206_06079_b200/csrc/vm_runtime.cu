@@ -1,0 +1,795 @@
+// vm_runtime.cu -- device map runtime and the C ABI (include/voxmap_b200.h).
+//
+// Owns the HBM region pool (one slab per layer, region slot s at
+// slab + s * bytes_per_region), the open-addressing region table in the
+// format of engine._build_region_table (engine.py:121-147), and the batch
+// pipeline of submit_batch (engine.py:175-210).  All work is enqueued on
+// the map's stream; vm_integrate returns once the batch is complete.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/voxmap_b200.h"
+#include "vm_kernels.cuh"
+
+using namespace vm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            return fail(e_ == cudaErrorMemoryAllocation ? VM_ERR_OOM : VM_ERR_CUDA,     \
+                        std::string(#x) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+const int LAYER_ELEM[NUM_LAYERS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 8, 4};
+const int LAYER_COMP[NUM_LAYERS] = {1, 1, 1, 1, 6, 1, 1, 2, 1, 1, 2};
+
+int bitlen(unsigned long long x) {
+    int b = 0;
+    while (x) {
+        ++b;
+        x >>= 1;
+    }
+    return b;
+}
+
+template <class T>
+int dev_alloc(T **p, size_t count, int fill = 0) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    CK(cudaMalloc((void **)p, count * sizeof(T)));
+    CK(cudaMemset(*p, fill, count * sizeof(T)));
+    return VM_OK;
+}
+
+}  // namespace
+
+struct vm_map {
+    vm_config cfg{};
+    uint32_t mask = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int dim = 0, vpr = 0, mark_words = 0;
+    long long max_slots = 0, cap = 0, nreg = 0, max_growth = 0;
+    size_t bpr[NUM_LAYERS] = {};
+    void *slab[NUM_LAYERS] = {};
+    void **d_lptr[NUM_LAYERS] = {};
+    long long *d_tkeys = nullptr;
+    int *d_tvals = nullptr;
+    unsigned long long tsize = 0;
+    int *d_cursor = nullptr;
+    long long *d_slot_keys = nullptr;
+    unsigned *d_slot_touch = nullptr, *d_slot_pref = nullptr;
+    unsigned *d_marks = nullptr;
+    unsigned long long *d_stats = nullptr;
+    int *d_go = nullptr;
+    unsigned long long *d_rec = nullptr, *d_rec2 = nullptr;
+    size_t rec_cap = 0;
+    int2 *d_marked = nullptr;
+    size_t marked_cap = 0;
+    int *d_touched = nullptr;
+    void *d_sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    unsigned char *d_rays = nullptr;
+    size_t rays_bytes = 0;
+    unsigned long long *h_stats = nullptr;  // pinned, NUM_STATS + 2
+    unsigned epoch = 0;
+    long long launches = 0;
+    cudaEvent_t ev_start{}, ev_end{}, ev_w0{}, ev_w1{}, ev_k1{}, ev_k2{};
+};
+
+namespace {
+
+DevMap make_dm(const vm_map *m) {
+    DevMap d{};
+    const vm_config &c = m->cfg;
+    d.vox = c.voxel_size;
+    d.rsize = (double)c.region_dim * c.voxel_size;  // config.py:54-57
+    d.hit_delta = c.hit_delta;
+    d.miss_delta = c.miss_delta;
+    d.max_range = c.max_ray_range;
+    d.seg_len = c.segment_length;
+    d.tsdf_trunc = c.tsdf_truncation;
+    d.tsdf_maxw = c.tsdf_max_weight;
+    d.sigma2 = c.ndt_sensor_noise * c.ndt_sensor_noise;
+    d.miss_check = c.ndt_miss_likelihood_threshold;
+    d.hit32 = (float)c.hit_delta;
+    d.miss32 = (float)c.miss_delta;
+    d.cmin = (float)c.clamp_min;
+    d.cmax = (float)c.clamp_max;
+    d.fthresh = (float)c.ndt_reset_threshold;
+    d.dim = m->dim;
+    d.vpr = m->vpr;
+    d.mark_words = m->mark_words;
+    d.maxseg = (int)std::ceil(c.max_ray_range / c.segment_length) + 1;
+    d.cell_limit = (int)std::min<long long>((1LL << 20) * (long long)m->dim - 1, (1LL << 30));
+    d.tkeys = m->d_tkeys;
+    d.tvals = m->d_tvals;
+    d.tmask = m->tsize - 1;
+    d.cursor = m->d_cursor;
+    d.cap = (int)m->cap;
+    d.max_slots = (int)m->max_slots;
+    d.insert = 1;
+    d.slot_keys = m->d_slot_keys;
+    d.slot_touch = m->d_slot_touch;
+    d.slot_pref = m->d_slot_pref;
+    d.epoch = m->epoch;
+    for (int l = 0; l < NUM_LAYERS; ++l) d.lptr[l] = m->d_lptr[l];
+    d.marks = m->d_marks;
+    d.stats = m->d_stats;
+    d.go = m->d_go;
+    d.rec = m->d_rec;
+    d.rec_cap = m->rec_cap;
+    d.marked = m->d_marked;
+    d.marked_cap = (int)m->marked_cap;
+    d.touched = m->d_touched;
+    d.touched_cap = (int)m->max_slots;
+    return d;
+}
+
+int grow_pool(vm_map *m, long long new_cap) {
+    if (new_cap > m->max_slots) new_cap = m->max_slots;
+    if (new_cap <= m->cap) return VM_OK;
+    CK(cudaStreamSynchronize(m->stream));
+    for (int l = 0; l < NUM_LAYERS; ++l) {
+        if (!m->bpr[l]) continue;
+        void *nw = nullptr;
+        CK(cudaMalloc(&nw, (size_t)new_cap * m->bpr[l]));
+        CK(cudaMemsetAsync((char *)nw + (size_t)m->cap * m->bpr[l], 0,
+                           (size_t)(new_cap - m->cap) * m->bpr[l], m->stream));
+        if (m->slab[l]) {
+            CK(cudaMemcpyAsync(nw, m->slab[l], (size_t)m->cap * m->bpr[l],
+                               cudaMemcpyDeviceToDevice, m->stream));
+        }
+        std::vector<void *> ptrs((size_t)new_cap);
+        for (long long s = 0; s < new_cap; ++s) ptrs[s] = (char *)nw + (size_t)s * m->bpr[l];
+        CK(cudaMemcpyAsync(m->d_lptr[l], ptrs.data(), ptrs.size() * sizeof(void *),
+                           cudaMemcpyHostToDevice, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        if (m->slab[l]) CK(cudaFree(m->slab[l]));
+        m->slab[l] = nw;
+    }
+    unsigned *nm = nullptr;
+    CK(cudaMalloc(&nm, (size_t)new_cap * m->mark_words * sizeof(unsigned)));
+    CK(cudaMemsetAsync(nm, 0, (size_t)new_cap * m->mark_words * sizeof(unsigned), m->stream));
+    if (m->d_marks)
+        CK(cudaMemcpyAsync(nm, m->d_marks, (size_t)m->cap * m->mark_words * sizeof(unsigned),
+                           cudaMemcpyDeviceToDevice, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    if (m->d_marks) CK(cudaFree(m->d_marks));
+    m->d_marks = nm;
+    m->cap = new_cap;
+    return VM_OK;
+}
+
+template <class T>
+int ensure_buf(T **p, size_t *cap, size_t need) {
+    if (need <= *cap && *p) return VM_OK;
+    size_t nc = std::max(need, *cap * 2);
+    if (*p) CK(cudaFree(*p));
+    *p = nullptr;
+    CK(cudaMalloc((void **)p, nc * sizeof(T)));
+    *cap = nc;
+    return VM_OK;
+}
+
+int ensure_records(vm_map *m, size_t need) {
+    if (need <= m->rec_cap && m->d_rec) return VM_OK;
+    size_t nc = std::max(need, m->rec_cap * 2);
+    if (m->d_rec) CK(cudaFree(m->d_rec));
+    if (m->d_rec2) CK(cudaFree(m->d_rec2));
+    m->d_rec = m->d_rec2 = nullptr;
+    CK(cudaMalloc((void **)&m->d_rec, nc * sizeof(unsigned long long)));
+    CK(cudaMalloc((void **)&m->d_rec2, nc * sizeof(unsigned long long)));
+    m->rec_cap = nc;
+    size_t bytes = 0;
+    cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, (int)std::min<size_t>(nc, INT32_MAX)));
+    if (bytes > m->sort_tmp_bytes) {
+        if (m->d_sort_tmp) CK(cudaFree(m->d_sort_tmp));
+        CK(cudaMalloc(&m->d_sort_tmp, bytes));
+        m->sort_tmp_bytes = bytes;
+    }
+    return VM_OK;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(VM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return VM_OK;
+}
+
+// kernel dispatch over (mode, exec, ray format)
+template <class Src>
+int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mode, bool det,
+                bool rec_only) {
+    dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK)), block(BLOCK);
+    cudaStream_t s = m->stream;
+    switch (mode) {
+    case M_OCC:
+        if (det && rec_only) k_walk_occ<M_OCC, true, true><<<grid, block, 0, s>>>(dm, src, n);
+        else if (det) k_walk_occ<M_OCC, true, false><<<grid, block, 0, s>>>(dm, src, n);
+        else k_walk_occ<M_OCC, false, false><<<grid, block, 0, s>>>(dm, src, n);
+        break;
+    case M_DECAY:
+        if (det && rec_only) k_walk_occ<M_DECAY, true, true><<<grid, block, 0, s>>>(dm, src, n);
+        else if (det) k_walk_occ<M_DECAY, true, false><<<grid, block, 0, s>>>(dm, src, n);
+        else k_walk_occ<M_DECAY, false, false><<<grid, block, 0, s>>>(dm, src, n);
+        break;
+    case M_NDT_OM: k_walk_ndt<false><<<grid, block, 0, s>>>(dm, src, n); break;
+    case M_NDT_TM: k_walk_ndt<true><<<grid, block, 0, s>>>(dm, src, n); break;
+    case M_TSDF:
+        if (det) k_walk_tsdf<true><<<grid, block, 0, s>>>(dm, src, n);
+        else k_walk_tsdf<false><<<grid, block, 0, s>>>(dm, src, n);
+        break;
+    }
+    m->launches += 1;
+    return check_launch("walk");
+}
+
+template <class Src>
+int launch_fold(vm_map *m, const DevMap &dm, const Src &src, const unsigned long long *keys,
+                long long R, long long M, int mode) {
+    cudaStream_t s = m->stream;
+    const unsigned grid_cap = 148 * 16;
+    if (mode == M_OCC || mode == M_DECAY) {
+        unsigned g = (unsigned)std::min<long long>((M + 7) / 8, grid_cap);
+        if (g) k_fold_occ<<<g, BLOCK, 0, s>>>(dm, src, keys, R, (int)M);
+        m->launches += g ? 1 : 0;
+    } else if (mode == M_NDT_OM || mode == M_NDT_TM) {
+        unsigned g = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
+        if (g) {
+            if (mode == M_NDT_TM) k_fold_ndt<true><<<g, BLOCK, 0, s>>>(dm, src, keys, R);
+            else k_fold_ndt<false><<<g, BLOCK, 0, s>>>(dm, src, keys, R);
+            m->launches += 1;
+        }
+    } else {
+        unsigned g = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
+        if (g) k_fold_tsdf<<<g, BLOCK, 0, s>>>(dm, src, keys, R);
+        m->launches += g ? 1 : 0;
+    }
+    return check_launch("fold");
+}
+
+const uint32_t MODE_MASK[5] = {
+    (1u << 1) | (1u << 2) | (1u << 3),
+    (1u << 1) | (1u << 2) | (1u << 3) | (1u << 8) | (1u << 9),
+    (1u << 1) | (1u << 2) | (1u << 3) | (1u << 4),
+    (1u << 1) | (1u << 2) | (1u << 3) | (1u << 4) | (1u << 5) | (1u << 6) | (1u << 7),
+    (1u << 10)};
+
+template <class Src>
+int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, vm_stats *out) {
+    const bool ndt = mode == M_NDT_OM || mode == M_NDT_TM;
+    const bool tsdf = mode == M_TSDF;
+    const bool det = exec == VM_EXEC_DETERMINISTIC;
+    const bool occ_det = det && (mode == M_OCC || mode == M_DECAY);
+    const bool sorted = occ_det || ndt || (tsdf && det);
+    const bool resolve = occ_det || ndt;
+    const int maxseg = (int)std::ceil(m->cfg.max_ray_range / m->cfg.segment_length) + 1;
+    unsigned long long order_span = tsdf ? (unsigned long long)n
+                                         : ((unsigned long long)n * maxseg) << 1;
+    if (order_span >= (1ULL << 32))
+        return fail(VM_ERR_ARG, "batch too large for 32-bit ray order keys; split it");
+    const int order_bits = std::max(1, bitlen(order_span));
+
+    int rc;
+    if ((rc = ensure_buf(&m->d_marked, &m->marked_cap, (size_t)n + 1))) return rc;
+    size_t rec_need = 0;
+    if (ndt) rec_need = (size_t)n + 1;
+    else if (tsdf && det) {
+        double band = 2.0 * m->cfg.tsdf_truncation / m->cfg.voxel_size;
+        rec_need = (size_t)n * (size_t)(3.0 * (std::ceil(band) + 2.0) + 4.0);
+    } else if (occ_det) rec_need = std::max<size_t>(m->rec_cap, std::max<size_t>(1 << 20, (size_t)n * 4));
+    if (sorted && (rc = ensure_records(m, rec_need))) return rc;
+
+    float ms_total = 0.f, ms_walk = 0.f;
+    const long long launches0 = m->launches;
+    long long replays = 0;
+    const long long nreg0 = m->nreg;
+    for (;;) {
+        long long headroom = std::max<long long>(512, 2 * m->max_growth);
+        if (m->nreg + headroom > m->cap) {
+            if ((rc = grow_pool(m, std::max(2 * m->cap, m->nreg + headroom)))) return rc;
+        }
+        m->epoch += 1;
+        DevMap dm = make_dm(m);
+        dm.order_bits = order_bits;
+        CK(cudaMemsetAsync(m->d_stats, 0, NUM_STATS * sizeof(unsigned long long), m->stream));
+        CK(cudaEventRecord(m->ev_start, m->stream));
+        dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK));
+        k_discover<<<grid, BLOCK, 0, m->stream>>>(dm, src, n, mode, det ? 1 : 0);
+        m->launches += 2;  // discover + guard
+        if ((rc = check_launch("discover"))) return rc;
+        int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
+        k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
+        CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS, m->d_cursor, sizeof(int),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaMemcpyAsync((int *)(m->h_stats + NUM_STATS) + 1, m->d_go, sizeof(int),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaEventRecord(m->ev_k1, m->stream));
+        CK(cudaEventRecord(m->ev_w0, m->stream));
+        if ((rc = launch_walk(m, dm, src, n, mode, det, false))) return rc;
+        CK(cudaEventRecord(m->ev_w1, m->stream));
+        if (sorted) {
+            CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_stats + S_RECORDS,
+                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+            CK(cudaEventRecord(m->ev_k2, m->stream));
+        }
+        if (resolve) {
+            if (ndt && mode == M_NDT_TM) k_resolve<true, true><<<148 * 4, BLOCK, 0, m->stream>>>(dm);
+            else if (ndt) k_resolve<true, false><<<148 * 4, BLOCK, 0, m->stream>>>(dm);
+            else k_resolve<false, false><<<148 * 4, BLOCK, 0, m->stream>>>(dm);
+            m->launches += 1;
+            if ((rc = check_launch("resolve"))) return rc;
+        }
+        CK(cudaEventSynchronize(m->ev_k1));
+        const unsigned long long *hs = m->h_stats;
+        int cursor = *(const int *)(hs + NUM_STATS);
+        int go = *((const int *)(hs + NUM_STATS) + 1);
+        if (hs[S_RANGE_ERR]) {
+            CK(cudaStreamSynchronize(m->stream));
+            long long M = std::min<long long>((long long)hs[S_MARKED], (long long)m->marked_cap);
+            if (M) k_cleanup<<<148, BLOCK, 0, m->stream>>>(dm, (int)M);
+            CK(cudaStreamSynchronize(m->stream));
+            m->nreg = cursor;
+            return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range "
+                                      "(|region| < 2**20, keys.py:76-86)");
+        }
+        if (!go) {
+            // pool overflow: nothing was applied; grow and replay
+            CK(cudaStreamSynchronize(m->stream));
+            long long M = std::min<long long>((long long)hs[S_MARKED], (long long)m->marked_cap);
+            if (M) k_cleanup<<<148, BLOCK, 0, m->stream>>>(dm, (int)M);
+            if ((rc = check_launch("cleanup"))) return rc;
+            m->max_growth = std::max<long long>(m->max_growth, cursor - m->nreg);
+            if ((rc = grow_pool(m, std::max<long long>(2 * m->cap,
+                                                       cursor + 2 * margin + headroom))))
+                return rc;
+            if (cursor + margin > m->cap)
+                return fail(VM_ERR_OOM, "region pool exhausted (max regions reached)");
+            m->nreg = cursor;
+            ++replays;
+            continue;
+        }
+        if (sorted) {
+            CK(cudaEventSynchronize(m->ev_k2));
+            unsigned long long R = m->h_stats[NUM_STATS + 1];
+            if (R > m->rec_cap) {
+                // records overflowed: re-emit them (records only, nothing re-applied)
+                if (!occ_det) return fail(VM_ERR_CUDA, "record buffer overflow");
+                CK(cudaStreamSynchronize(m->stream));
+                if ((rc = ensure_records(m, (size_t)R + (R >> 2)))) return rc;
+                dm.rec = m->d_rec;
+                dm.rec_cap = m->rec_cap;
+                CK(cudaMemsetAsync(m->d_stats + S_RECORDS, 0, sizeof(unsigned long long),
+                                   m->stream));
+                if ((rc = launch_walk(m, dm, src, n, mode, det, true))) return rc;
+                CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_stats + S_RECORDS,
+                                   sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   m->stream));
+                CK(cudaStreamSynchronize(m->stream));
+                R = m->h_stats[NUM_STATS + 1];
+            }
+            long long M = (long long)std::min<unsigned long long>(hs[S_MARKED], m->marked_cap);
+            int end_bit;
+            if (occ_det) end_bit = order_bits + std::max(1, bitlen((unsigned long long)M));
+            else end_bit = order_bits + std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
+            end_bit = std::min(end_bit, 64);
+            cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
+            if (R > 1) {
+                size_t bytes = m->sort_tmp_bytes;
+                CK(cub::DeviceRadixSort::SortKeys(m->d_sort_tmp, bytes, db, (int)R, 0, end_bit,
+                                                  m->stream));
+            }
+            if ((rc = launch_fold(m, dm, src, db.Current(), (long long)R, M, mode))) return rc;
+            if (occ_det && M) {
+                k_cleanup<<<148, BLOCK, 0, m->stream>>>(dm, (int)M);
+                m->launches += 1;
+                if ((rc = check_launch("cleanup"))) return rc;
+            }
+        }
+        CK(cudaEventRecord(m->ev_end, m->stream));
+        CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS, m->d_cursor, sizeof(int),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        if ((rc = check_launch("batch"))) return rc;
+        CK(cudaEventElapsedTime(&ms_total, m->ev_start, m->ev_end));
+        CK(cudaEventElapsedTime(&ms_walk, m->ev_w0, m->ev_w1));
+        break;
+    }
+    const unsigned long long *hs = m->h_stats;
+    int cursor = *(const int *)(hs + NUM_STATS);
+    std::memset(out, 0, sizeof(*out));
+    out->rays_in = n;
+    out->rays_processed = (int64_t)hs[S_PROCESSED];
+    out->segments = (int64_t)hs[S_SEGMENTS];
+    out->voxel_visits = (int64_t)hs[S_VISITS];
+    out->cas_retries = (int64_t)hs[S_RETRIES];
+    out->cas_failures = 0;
+    out->region_misses = (int64_t)hs[S_RMISS];
+    out->regions_touched = (int64_t)hs[S_PREF_TOUCHED];
+    out->records = (int64_t)hs[S_RECORDS];
+    out->marked_voxels = (int64_t)hs[S_MARKED];
+    out->regions_total = cursor;
+    out->new_regions = cursor - nreg0;
+    out->replays = replays;
+    out->touched_regions_walk = (int64_t)hs[S_WALK_TOUCHED];
+    out->launches = m->launches - launches0;
+    out->gpu_ms = ms_total;
+    out->walk_ms = ms_walk;
+    m->max_growth = std::max<long long>(m->max_growth, cursor - m->nreg);
+    m->nreg = cursor;
+    return VM_OK;
+}
+
+std::mutex g_walk_mu;
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char *vm_last_error(void) { return g_err.c_str(); }
+
+const char *vm_build_info(void) {
+    return "voxmap_b200: sm_100a, -fmad=false, fp64 DDA, CUB radix sort";
+}
+
+int vm_device_count(int32_t *out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    *out = n;
+    return VM_OK;
+}
+
+uint64_t vm_hash_mix(int64_t key) { return mix_key(key); }
+
+int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
+                  int64_t initial_regions, vm_map **out) {
+    if (!cfg || !out) return fail(VM_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (!(cfg->voxel_size > 0) || !std::isfinite(cfg->voxel_size))
+        return fail(VM_ERR_ARG, "voxel_size must be positive");
+    if (cfg->region_dim < 1 || cfg->region_dim > 1024)
+        return fail(VM_ERR_ARG, "region_dim must be in [1, 1024]");
+    if (!(cfg->segment_length > 0) || !(cfg->max_ray_range > 0))
+        return fail(VM_ERR_ARG, "segment_length and max_ray_range must be positive");
+    if ((layer_mask & ~0x7FEu) != 0) return fail(VM_ERR_ARG, "unknown layer id in mask");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(VM_ERR_NODEV, "no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(VM_ERR_ARG, "bad device index");
+    CK(cudaSetDevice(device));
+    vm_map *m = new vm_map();
+    m->cfg = *cfg;
+    m->mask = layer_mask;
+    m->device = device;
+    m->dim = cfg->region_dim;
+    m->vpr = cfg->region_dim * cfg->region_dim * cfg->region_dim;
+    m->mark_words = (m->vpr + 31) / 32;
+    m->max_slots = std::min<long long>(1LL << 20, (long long)(0xFFFFFFFFull / (unsigned long long)m->vpr));
+    unsigned long long ts = 1;
+    while (ts < 2ULL * (unsigned long long)m->max_slots) ts <<= 1;
+    m->tsize = ts;
+    for (int l = 0; l < NUM_LAYERS; ++l) {
+        bool on = l == L_SCRATCH ? true : (layer_mask >> l) & 1u;
+        m->bpr[l] = on ? (size_t)m->vpr * LAYER_COMP[l] * LAYER_ELEM[l] : 0;
+    }
+    int rc;
+    auto cleanup = [&](int code) {
+        vm_map_destroy(m);
+        return code;
+    };
+    if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup(fail(VM_ERR_CUDA, "stream create failed"));
+    m->own_stream = true;
+    if ((rc = dev_alloc(&m->d_tkeys, ts, 0xFF)) || (rc = dev_alloc(&m->d_tvals, ts, 0xFF)) ||
+        (rc = dev_alloc(&m->d_cursor, 1)) || (rc = dev_alloc(&m->d_slot_keys, m->max_slots)) ||
+        (rc = dev_alloc(&m->d_slot_touch, m->max_slots)) ||
+        (rc = dev_alloc(&m->d_slot_pref, m->max_slots)) || (rc = dev_alloc(&m->d_stats, NUM_STATS)) ||
+        (rc = dev_alloc(&m->d_go, 1)) || (rc = dev_alloc(&m->d_touched, m->max_slots)))
+        return cleanup(rc);
+    for (int l = 0; l < NUM_LAYERS; ++l)
+        if (m->bpr[l] && (rc = dev_alloc(&m->d_lptr[l], m->max_slots))) return cleanup(rc);
+    if (cudaMallocHost((void **)&m->h_stats, (NUM_STATS + 4) * sizeof(unsigned long long)) !=
+        cudaSuccess)
+        return cleanup(fail(VM_ERR_OOM, "pinned alloc failed"));
+    cudaEvent_t *evs[] = {&m->ev_start, &m->ev_end, &m->ev_w0, &m->ev_w1, &m->ev_k1, &m->ev_k2};
+    for (auto *e : evs)
+        if (cudaEventCreate(e) != cudaSuccess) return cleanup(fail(VM_ERR_CUDA, "event create"));
+    if ((rc = grow_pool(m, std::max<long long>(64, initial_regions)))) return cleanup(rc);
+    *out = m;
+    return VM_OK;
+}
+
+int vm_map_destroy(vm_map *m) {
+    if (!m) return VM_OK;
+    cudaSetDevice(m->device);
+    if (m->stream) cudaStreamSynchronize(m->stream);
+    for (int l = 0; l < NUM_LAYERS; ++l) {
+        cudaFree(m->slab[l]);
+        cudaFree(m->d_lptr[l]);
+    }
+    cudaFree(m->d_tkeys);
+    cudaFree(m->d_tvals);
+    cudaFree(m->d_cursor);
+    cudaFree(m->d_slot_keys);
+    cudaFree(m->d_slot_touch);
+    cudaFree(m->d_slot_pref);
+    cudaFree(m->d_marks);
+    cudaFree(m->d_stats);
+    cudaFree(m->d_go);
+    cudaFree(m->d_rec);
+    cudaFree(m->d_rec2);
+    cudaFree(m->d_marked);
+    cudaFree(m->d_touched);
+    cudaFree(m->d_sort_tmp);
+    cudaFree(m->d_rays);
+    if (m->h_stats) cudaFreeHost(m->h_stats);
+    cudaEvent_t evs[] = {m->ev_start, m->ev_end, m->ev_w0, m->ev_w1, m->ev_k1, m->ev_k2};
+    for (auto e : evs)
+        if (e) cudaEventDestroy(e);
+    if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
+    delete m;
+    return VM_OK;
+}
+
+int vm_map_reset(vm_map *m) {
+    if (!m) return fail(VM_ERR_ARG, "null map");
+    CK(cudaSetDevice(m->device));
+    for (int l = 0; l < NUM_LAYERS; ++l)
+        if (m->bpr[l] && m->nreg)
+            CK(cudaMemsetAsync(m->slab[l], 0, (size_t)m->nreg * m->bpr[l], m->stream));
+    if (m->nreg)
+        CK(cudaMemsetAsync(m->d_marks, 0, (size_t)m->nreg * m->mark_words * sizeof(unsigned),
+                           m->stream));
+    CK(cudaMemsetAsync(m->d_tkeys, 0xFF, m->tsize * sizeof(long long), m->stream));
+    CK(cudaMemsetAsync(m->d_tvals, 0xFF, m->tsize * sizeof(int), m->stream));
+    CK(cudaMemsetAsync(m->d_cursor, 0, sizeof(int), m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    m->nreg = 0;
+    return VM_OK;
+}
+
+int vm_map_set_stream(vm_map *m, void *stream) {
+    if (!m) return fail(VM_ERR_ARG, "null map");
+    CK(cudaStreamSynchronize(m->stream));
+    if (m->own_stream) cudaStreamDestroy(m->stream);
+    if (stream) {
+        m->stream = (cudaStream_t)stream;
+        m->own_stream = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+        m->own_stream = true;
+    }
+    return VM_OK;
+}
+
+int vm_map_region_count(const vm_map *m, int64_t *out) {
+    if (!m || !out) return fail(VM_ERR_ARG, "null argument");
+    *out = m->nreg;
+    return VM_OK;
+}
+
+int vm_map_region_keys(const vm_map *m, int64_t first, int64_t count, int64_t *keys_out) {
+    if (!m || !keys_out || first < 0 || count < 0 || first + count > m->nreg)
+        return fail(VM_ERR_ARG, "bad region key range");
+    if (!count) return VM_OK;
+    CK(cudaSetDevice(m->device));
+    CK(cudaMemcpyAsync(keys_out, m->d_slot_keys + first, count * sizeof(int64_t),
+                       cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return VM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void k_ensure(const __grid_constant__ DevMap m, const long long *keys, long long n, int *slots, int insert) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    slots[i] = region_slot(m, keys[i]);
+}
+
+int ensure_or_find(vm_map *m, const int64_t *keys, int64_t n, int32_t *slots_out, int insert) {
+    if (!m || (n && (!keys || !slots_out))) return fail(VM_ERR_ARG, "null argument");
+    if (!n) return VM_OK;
+    CK(cudaSetDevice(m->device));
+    int rc;
+    if (insert && m->nreg + n > m->cap) {
+        if ((rc = grow_pool(m, std::max<long long>(2 * m->cap, m->nreg + n + 64)))) return rc;
+    }
+    long long *dk = nullptr;
+    int *ds = nullptr;
+    CK(cudaMalloc(&dk, n * sizeof(long long)));
+    CK(cudaMalloc(&ds, n * sizeof(int)));
+    CK(cudaMemcpyAsync(dk, keys, n * sizeof(long long), cudaMemcpyHostToDevice, m->stream));
+    DevMap dm = make_dm(m);
+    dm.insert = insert;
+    k_ensure<<<(unsigned)((n + 255) / 256), 256, 0, m->stream>>>(dm, dk, n, ds, insert);
+    CK(cudaMemcpyAsync(slots_out, ds, n * sizeof(int), cudaMemcpyDeviceToHost, m->stream));
+    int cursor = 0;
+    CK(cudaMemcpyAsync(&cursor, m->d_cursor, sizeof(int), cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    cudaFree(dk);
+    cudaFree(ds);
+    if ((rc = check_launch("ensure"))) return rc;
+    m->nreg = cursor;
+    for (int64_t i = 0; i < n; ++i)
+        if (insert && (slots_out[i] < 0 || slots_out[i] >= m->cap))
+            return fail(VM_ERR_OOM, "region pool exhausted");
+    return VM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int vm_map_ensure_regions(vm_map *m, const int64_t *keys, int64_t n, int32_t *slots_out) {
+    return ensure_or_find(m, keys, n, slots_out, 1);
+}
+
+int vm_map_find_region(vm_map *m, int64_t key, int32_t *slot_out) {
+    return ensure_or_find(m, &key, 1, slot_out, 0);
+}
+
+static int layer_io(vm_map *m, int32_t slot, int32_t layer, int64_t bytes, size_t *off) {
+    if (!m || layer < 1 || layer > 10 || !m->bpr[layer])
+        return fail(VM_ERR_ARG, "layer not present in map");
+    if (slot < 0 || slot >= m->nreg) return fail(VM_ERR_ARG, "bad region slot");
+    if ((size_t)bytes != m->bpr[layer]) return fail(VM_ERR_ARG, "byte count mismatch");
+    *off = (size_t)slot * m->bpr[layer];
+    return VM_OK;
+}
+
+int vm_map_read_layer(vm_map *m, int32_t slot, int32_t layer, void *dst, int64_t bytes) {
+    size_t off;
+    int rc = layer_io(m, slot, layer, bytes, &off);
+    if (rc) return rc;
+    CK(cudaSetDevice(m->device));
+    CK(cudaMemcpyAsync(dst, (char *)m->slab[layer] + off, bytes, cudaMemcpyDeviceToHost,
+                       m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return VM_OK;
+}
+
+int vm_map_write_layer(vm_map *m, int32_t slot, int32_t layer, const void *src, int64_t bytes) {
+    size_t off;
+    int rc = layer_io(m, slot, layer, bytes, &off);
+    if (rc) return rc;
+    CK(cudaSetDevice(m->device));
+    CK(cudaMemcpyAsync((char *)m->slab[layer] + off, src, bytes, cudaMemcpyHostToDevice,
+                       m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return VM_OK;
+}
+
+int vm_map_layer_ptr(vm_map *m, int32_t slot, int32_t layer, void **out) {
+    size_t off;
+    if (!m || !out) return fail(VM_ERR_ARG, "null argument");
+    int rc = layer_io(m, slot, layer, (int64_t)(layer >= 1 && layer <= 10 ? m->bpr[layer] : 0), &off);
+    if (rc) return rc;
+    *out = (char *)m->slab[layer] + off;
+    return VM_OK;
+}
+
+int vm_integrate(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, vm_stats *out) {
+    if (!m || !rays || !out) return fail(VM_ERR_ARG, "null argument");
+    if (mode < 0 || mode > 4) return fail(VM_ERR_ARG, "unknown mode");
+    if (exec != VM_EXEC_CAS && exec != VM_EXEC_DETERMINISTIC) return fail(VM_ERR_ARG, "bad exec");
+    if ((m->mask & MODE_MASK[mode]) != MODE_MASK[mode])
+        return fail(VM_ERR_ARG, "map lacks layers required by mode");
+    CK(cudaSetDevice(m->device));
+    long long n = rays->count;
+    std::memset(out, 0, sizeof(*out));
+    if (n <= 0) {
+        out->regions_total = m->nreg;
+        return VM_OK;
+    }
+    if (rays->format == VM_RAYS_OHMB1) {
+        if (!rays->records) return fail(VM_ERR_ARG, "null records");
+        const unsigned char *p = (const unsigned char *)rays->records;
+        if (!rays->on_device) {
+            int rc = ensure_buf(&m->d_rays, &m->rays_bytes, (size_t)n * 40);
+            if (rc) return rc;
+            CK(cudaMemcpyAsync(m->d_rays, p, (size_t)n * 40, cudaMemcpyHostToDevice, m->stream));
+            p = m->d_rays;
+        }
+        SrcOHMB1 src{p};
+        return integrate_impl(m, src, n, mode, exec, out);
+    }
+    if (rays->format == VM_RAYS_F64) {
+        if (!rays->origins || !rays->ends || !rays->has_sample)
+            return fail(VM_ERR_ARG, "null ray arrays");
+        SrcF64 src{rays->origins, rays->ends, rays->has_sample, rays->intensity};
+        if (!rays->on_device) {
+            size_t b_o = (size_t)n * 24, b_h = ((size_t)n + 7) & ~(size_t)7, b_i = (size_t)n * 4;
+            size_t total = 2 * b_o + b_h + (rays->intensity ? b_i : 0);
+            int rc = ensure_buf(&m->d_rays, &m->rays_bytes, total);
+            if (rc) return rc;
+            unsigned char *d = m->d_rays;
+            CK(cudaMemcpyAsync(d, rays->origins, b_o, cudaMemcpyHostToDevice, m->stream));
+            CK(cudaMemcpyAsync(d + b_o, rays->ends, b_o, cudaMemcpyHostToDevice, m->stream));
+            CK(cudaMemcpyAsync(d + 2 * b_o, rays->has_sample, n, cudaMemcpyHostToDevice,
+                               m->stream));
+            if (rays->intensity)
+                CK(cudaMemcpyAsync(d + 2 * b_o + b_h, rays->intensity, b_i,
+                                   cudaMemcpyHostToDevice, m->stream));
+            src = SrcF64{(const double *)d, (const double *)(d + b_o), d + 2 * b_o,
+                         rays->intensity ? (const float *)(d + 2 * b_o + b_h) : nullptr};
+        }
+        return integrate_impl(m, src, n, mode, exec, out);
+    }
+    return fail(VM_ERR_ARG, "unknown ray format");
+}
+
+int vm_walk_voxels(double ox, double oy, double oz, double ex, double ey, double ez, double cell,
+                   int64_t cap, int64_t *coords_out, double *t0_out, double *t1_out,
+                   int64_t *n_out) {
+    if (!(cell > 0) || cap < 0 || !n_out) return fail(VM_ERR_ARG, "bad walk arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(VM_ERR_NODEV, "no CUDA device available");
+    std::lock_guard<std::mutex> lk(g_walk_mu);
+    static long long *d_c = nullptr;
+    static double *d_t0 = nullptr, *d_t1 = nullptr;
+    static long long *d_n = nullptr;
+    static long long d_cap = 0;
+    if (cap > d_cap || !d_n) {
+        cudaFree(d_c);
+        cudaFree(d_t0);
+        cudaFree(d_t1);
+        long long c = std::max<long long>(cap, 4096);
+        CK(cudaMalloc(&d_c, c * 3 * sizeof(long long)));
+        CK(cudaMalloc(&d_t0, c * sizeof(double)));
+        CK(cudaMalloc(&d_t1, c * sizeof(double)));
+        if (!d_n) CK(cudaMalloc(&d_n, sizeof(long long)));
+        d_cap = c;
+    }
+    k_walk_one<<<1, 1>>>(ox, oy, oz, ex, ey, ez, cell, d_c, d_t0, d_t1, cap, d_n);
+    int rc = check_launch("walk_one");
+    if (rc) return rc;
+    long long n = 0;
+    CK(cudaMemcpy(&n, d_n, sizeof(long long), cudaMemcpyDeviceToHost));
+    *n_out = n;
+    if (n > cap) return fail(VM_ERR_ARG, "walk overflow");
+    if (n) {
+        CK(cudaMemcpy(coords_out, d_c, n * 3 * sizeof(long long), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(t0_out, d_t0, n * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(t1_out, d_t1, n * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    return VM_OK;
+}
+
+int vm_kernels_integrate_occupancy(const double *, const double *, const uint8_t *, int64_t,
+                                   const int64_t *, const int32_t *, int64_t, void *const *,
+                                   void *const *, void *const *, void *const *, void *const *,
+                                   double, int64_t, double, double, double, double, int32_t,
+                                   int32_t, int64_t *, void *) {
+    return fail(VM_ERR_ARG, "vm_kernels_integrate_occupancy: not built in this version");
+}
+
+}  // extern "C"

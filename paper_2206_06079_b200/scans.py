@@ -1,0 +1,129 @@
+"""Synthetic lidar workloads of BASELINE.json's configs.
+
+Deterministic per seed, numpy-vectorised, emitted as OHMB1 records
+(rayset.RAY_DTYPE) exactly like a recorded ray set.  Geometry is shifted by
+W0 = (204.8, 204.8, 204.8) m so no coordinate lands in region -1.
+
+* C1 `os64_room_scan`: one Ouster-64 scan (64 x 2048 = 131,072 rays), sensor
+  1.8 m above ground inside an open 30 x 24 m room with 6 m walls; 0.1 m.
+* C2 `os128_canyon_batches`: Ouster-128 in a street canyon (facades at
+  +-6 m, 15 m high, poles every 10 m), sensor moving 1 m/s along +x;
+  1000 batches x 26,240 rays (128 beams x 205 columns = 10 ms of a 10 Hz
+  rotation at 2.6 M rays/s); 0.05 m.
+* C3 `os64_tunnel_scans`: Ouster-64 scans in a 4 x 3 m tunnel with 2 cm
+  wall roughness, 0.5 m per scan; NDT-OM at 0.1 m.
+
+Beam model: elevations linspace(-22.5, 22.5) deg, 2048 azimuth columns per
+rotation, range noise N(0, 2 cm), intensity U(5, 50).  Returns up to 40 m
+are kept at their true range (the reference clips >20 m to miss-only rays);
+beams that hit nothing within 40 m are emitted at 40 m without a sample.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .rayset import records_from_arrays
+
+W0 = np.array([204.8, 204.8, 204.8])
+MAX_RETURN = 40.0
+COLUMNS = 2048
+
+
+def _beam_dirs(beams: int, cols: np.ndarray, elev_deg=(-22.5, 22.5)):
+    el = np.deg2rad(np.linspace(elev_deg[0], elev_deg[1], beams))
+    az = 2.0 * np.pi * cols / COLUMNS
+    el_g, az_g = np.meshgrid(el, az)  # column-major scan order: all beams of a column
+    el_g, az_g = el_g.ravel(), az_g.ravel()
+    return np.stack([np.cos(el_g) * np.cos(az_g), np.cos(el_g) * np.sin(az_g), np.sin(el_g)], 1)
+
+
+def _plane_hit(o, d, axis, value, lo=None, hi=None):
+    """t of the ray hitting plane x[axis] = value within the rectangle bounds."""
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = (value - o[:, axis]) / d[:, axis]
+    t = np.where(t > 1e-9, t, np.inf)
+    if lo is not None:
+        p = o + d * np.where(np.isfinite(t), t, 0.0)[:, None]
+        ok = np.all((p >= lo) & (p <= hi), axis=1)
+        t = np.where(ok, t, np.inf)
+    return t
+
+
+def _cylinder_hit(o, d, cx, cy, r, h):
+    fx, fy = o[:, 0] - cx, o[:, 1] - cy
+    a = d[:, 0] ** 2 + d[:, 1] ** 2
+    b = 2.0 * (fx * d[:, 0] + fy * d[:, 1])
+    c = fx * fx + fy * fy - r * r
+    disc = b * b - 4.0 * a * c
+    with np.errstate(invalid="ignore", divide="ignore"):
+        t = (-b - np.sqrt(disc)) / (2.0 * a)
+    z = o[:, 2] + d[:, 2] * t
+    ok = (disc >= 0) & (t > 1e-9) & (z >= 0.0) & (z <= h)
+    return np.where(ok, t, np.inf)
+
+
+def _emit(origins, d, t, rng, timestamps):
+    n = len(d)
+    hit = np.isfinite(t) & (t <= MAX_RETURN)
+    rng_t = np.where(hit, t + rng.normal(0.0, 0.02, n), MAX_RETURN)
+    rng_t = np.maximum(rng_t, 0.05)
+    ends = origins + d * rng_t[:, None]
+    return records_from_arrays(timestamps, origins + W0, ends + W0,
+                               rng.uniform(5.0, 50.0, n).astype(np.float32), hit)
+
+
+def os64_room_scan(seed: int = 0) -> np.ndarray:
+    """C1: one OS1-64 scan, 131,072 rays (0.1 m voxels)."""
+    rng = np.random.default_rng(seed)
+    d = _beam_dirs(64, np.arange(COLUMNS))
+    n = len(d)
+    o = np.tile([0.0, 0.0, 1.8], (n, 1))
+    t = _plane_hit(o, d, 2, 0.0)
+    for axis, v in ((0, -15.0), (0, 15.0), (1, -12.0), (1, 12.0)):
+        lo = np.array([-15.0, -12.0, 0.0])
+        hi = np.array([15.0, 12.0, 6.0])
+        t = np.minimum(t, _plane_hit(o, d, axis, v, lo - 1e-9, hi + 1e-9))
+    return _emit(o, d, t, rng, np.arange(n) * 1e-7)
+
+
+def _canyon_t(o, d):
+    t = _plane_hit(o, d, 2, 0.0)
+    for y in (-6.0, 6.0):
+        t = np.minimum(t, _plane_hit(o, d, 1, y, np.array([-1e9, -7, 0.0]),
+                                     np.array([1e9, 7, 15.0])))
+    for px in np.arange(-20.0, 240.0, 10.0):
+        for py in (-4.5, 4.5):
+            t = np.minimum(t, _cylinder_hit(o, d, px, py, 0.1, 6.0))
+    return t
+
+
+def os128_canyon_batches(n_batches: int = 1000, cols_per_batch: int = 205, seed: int = 1,
+                         speed: float = 1.0):
+    """C2: list of record batches (128 beams x cols_per_batch columns each)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for b in range(n_batches):
+        cols = (b * cols_per_batch + np.arange(cols_per_batch)) % COLUMNS
+        d = _beam_dirs(128, cols)
+        t0 = b * 0.01
+        x = speed * t0
+        o = np.tile([x, 0.0, 1.8], (len(d), 1))
+        out.append(_emit(o, d, _canyon_t(o, d), rng, t0 + np.arange(len(d)) * 3.8e-7))
+    return out
+
+
+def os64_tunnel_scans(n_scans: int, seed: int = 2, step: float = 0.5):
+    """C3: OS1-64 scans along a 4 x 3 m tunnel with rough walls."""
+    rng = np.random.default_rng(seed)
+    out = []
+    d0 = _beam_dirs(64, np.arange(COLUMNS))
+    for s in range(n_scans):
+        o = np.tile([s * step, 0.0, 1.5], (len(d0), 1))
+        t = np.full(len(d0), np.inf)
+        lo = np.array([-1e9, -2.0, 0.0])
+        hi = np.array([1e9, 2.0, 3.0])
+        for axis, v in ((1, -2.0), (1, 2.0), (2, 0.0), (2, 3.0)):
+            t = np.minimum(t, _plane_hit(o, d0, axis, v, lo - 1e-9, hi + 1e-9))
+        t = t + rng.normal(0.0, 0.02, len(t))  # wall roughness
+        out.append(_emit(o, d0, t, rng, s * 0.1 + np.arange(len(d0)) * 7.6e-7))
+    return out
