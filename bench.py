@@ -57,10 +57,13 @@ def workload(name: str, batches: int):
     from paper_2206_06079_b200 import MapConfig, scans
     if name == "c2":
         cfg = MapConfig(voxel_size=0.05)
-        data = scans.os128_canyon_batches(batches)
-        desc = dict(workload="C2: synthetic OS1-128 street-canyon sequence", scans=len(data),
-                    rays_per_batch=int(len(data[0])), voxel_size=0.05, region_dim=32,
-                    mode="occupancy")
+        scan_list = scans.os128_canyon_batches(batches)
+        # replayed in the reference CLI's 0.1 s batches (cli.py:31,70-94)
+        data = scans.batch_by_period(np.concatenate(scan_list))
+        desc = dict(workload="C2: synthetic OS1-128 street-canyon sequence", scans=len(scan_list),
+                    rays_per_scan=int(len(scan_list[0])), batches=len(data),
+                    batch_period_s=scans.BATCH_PERIOD, rays_per_batch=int(len(data[0])),
+                    voxel_size=0.05, region_dim=32, mode="occupancy")
         mode = "occupancy"
     elif name == "c1":
         cfg = MapConfig(voxel_size=0.1)
@@ -217,7 +220,8 @@ def main():
 
     def step(record=False):
         vmap.clear()
-        tot = dict(S=0, V=0, walk_ms=0.0, launches=0, batches=0, records=0, rmiss=0)
+        tot = dict(S=0, V=0, walk_ms=0.0, launches=0, batches=0, records=0, rmiss=0,
+                   discover_ms=0.0, resolve_ms=0.0, sort_ms=0.0, fold_ms=0.0, gpu_ms=0.0)
         for b in range(len(data)):
             r = _native.rays_from_records(sizes[b], base + int(offsets[b]) * 40)
             st = vmap._native.integrate(r, mode, det)
@@ -229,6 +233,8 @@ def main():
                 tot["records"] += st.records
                 tot["rmiss"] += st.region_misses
                 tot["batches"] += 1
+                for k in ("discover_ms", "resolve_ms", "sort_ms", "fold_ms", "gpu_ms"):
+                    tot[k] += getattr(st, k)
         return tot
 
     for _ in range(args.warmup):
@@ -325,6 +331,8 @@ def main():
             "clocks": parse_clocks(clk_file, dev),
             "stats": {"segments": s0["S"], "visits": s0["V"], "hits": H,
                       "records": s0["records"], "region_misses": s0["rmiss"]},
+            "stages_ms_per_step": {k: round(s0[k], 4) for k in (
+                "discover_ms", "walk_ms", "resolve_ms", "sort_ms", "fold_ms", "gpu_ms")},
         }
         print(json.dumps(line), flush=True)
     if dist:

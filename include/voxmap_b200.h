@@ -80,6 +80,10 @@ typedef struct vm_stats {
     int64_t launches;         /* kernels of this library launched for the batch */
     double gpu_ms;            /* device time of the whole batch (CUDA events) */
     double walk_ms;           /* device time of the DDA walk kernel */
+    double discover_ms;       /* preprocess + region discovery (+ dense grid) */
+    double resolve_ms;        /* order-free miss counts -> log-odds */
+    double sort_ms;           /* record sort */
+    double fold_ms;           /* in-order record fold + cleanup */
 } vm_stats;
 
 enum { VM_MODE_OCCUPANCY = 0, VM_MODE_DECAY = 1, VM_MODE_NDT_OM = 2, VM_MODE_NDT_TM = 3,

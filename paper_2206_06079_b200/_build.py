@@ -56,7 +56,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         print(" ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{res.stderr[-4000:]}")
+        errs = "\n".join(l for l in res.stderr.splitlines()
+                          if "error" in l or "warning" in l) or res.stderr[-4000:]
+        raise RuntimeError(f"nvcc failed:\n{errs[-6000:]}")
     if verbose:
         print(res.stderr, file=sys.stderr)
     os.replace(tmp, LIB)

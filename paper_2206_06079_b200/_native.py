@@ -52,7 +52,9 @@ class VmStats(ctypes.Structure):
         "rays_in", "rays_processed", "segments", "voxel_visits", "cas_retries", "cas_failures",
         "region_misses", "regions_touched", "records", "marked_voxels", "regions_total",
         "new_regions", "replays", "touched_regions_walk", "launches")] + [
-        ("gpu_ms", ctypes.c_double), ("walk_ms", ctypes.c_double)]
+        ("gpu_ms", ctypes.c_double), ("walk_ms", ctypes.c_double),
+        ("discover_ms", ctypes.c_double), ("resolve_ms", ctypes.c_double),
+        ("sort_ms", ctypes.c_double), ("fold_ms", ctypes.c_double)]
 
 
 class VmRays(ctypes.Structure):

@@ -9,6 +9,7 @@
 // (traversal.py:40-42, reference.py:170) -- is written out with fma().
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -26,13 +27,29 @@ enum Mode { M_OCC = 0, M_DECAY = 1, M_NDT_OM = 2, M_NDT_TM = 3, M_TSDF = 4 };
 enum Stat {
     S_RAYS_IN = 0, S_PROCESSED, S_SEGMENTS, S_VISITS, S_RETRIES, S_FAILURES,
     S_RMISS, S_PREF_TOUCHED, S_RECORDS, S_MARKED, S_WALK_TOUCHED, S_RANGE_ERR,
-    S_CUBE_FLUSH, NUM_STATS
+    S_CUBE_FLUSH, S_SEGDESC, S_WORK, S_RGRID, NUM_STATS
 };
 
 constexpr unsigned MARK_FLAG = 0x80000000u;
 constexpr int CUBE = 16;                 // smem aggregation cube edge (voxels)
 constexpr int CUBE_N = CUBE * CUBE * CUBE;
 constexpr int SLOTSET = 256;             // per-block region dedupe set
+
+// One preprocessed segment with its DDA initial state (k_discover writes
+// it, the persistent walk consumes it): 96 bytes, 16-byte aligned.
+struct __align__(16) SegDesc {
+    double t[3];       // t_max per axis at the start cell (traversal.py:70-78)
+    double d[3];       // t_delta per axis
+    int c[3];          // start cell
+    int e[3];          // end cell
+    unsigned order;    // (ray * maxseg + seg) << 1 ; 0xFFFFFFFF = empty
+    unsigned flags;    // bit0 has_sample(last visit is a hit), bits 1-6 step codes
+    int slot0;         // region slot of the start cell
+    unsigned local0;   // start cell's local coords: lx | ly << 10 | lz << 20
+    double L;          // segment length (RaySample.length), for decay
+    int r0[3];         // start cell's region coords
+    int pad;
+};
 
 // All state a kernel needs, passed by value.
 struct DevMap {
@@ -58,6 +75,16 @@ struct DevMap {
     unsigned epoch;
     void *const *lptr[NUM_LAYERS];       // per layer: region base pointer per slot
     unsigned *marks;                     // mark bitset, mark_words per slot
+    unsigned long long *bmask;           // per slot: 4x4x4 brick summary of marks
+    int brick_shift;                     // log2(dim) - 2 when dim is a power of 2 >= 4, else -1
+    char *slab[NUM_LAYERS];              // pool slabs: region s at slab + s * bpr
+    unsigned long long bpr[NUM_LAYERS];  // bytes per region per layer
+    int *rgrid;                          // dense region-slot grid over the batch bbox
+    int *rbox;                           // [6]: min xyz, max xyz (regions) of the batch
+    int rg_max;                          // capacity of rgrid (cells)
+    SegDesc *segs;                       // preprocessed segments of the batch
+    unsigned long long seg_cap;
+    unsigned long long *work;            // persistent-walk work counter
     unsigned long long *stats;
     int *go;                             // batch guard (0 = skip, replay later)
     // batch outputs
@@ -105,6 +132,14 @@ __device__ __forceinline__ int floordiv(int a, int d) {
     int q = a / d;
     if ((a % d != 0) && (a < 0)) q -= 1;
     return q;
+}
+
+// Fire-and-forget reductions (REDG): no return value, no scoreboard wait.
+__device__ __forceinline__ void red_add(unsigned *p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(double *p, double v) {
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 // reference.py:22-23 / _kernels.pyx:233-271 clamped log-odds step (f32)
@@ -370,6 +405,36 @@ struct RegionTrack {
 };
 
 // ---------------------------------------------------------------- the walk
+
+// DDA initial state of traversal._walk_grid (traversal.py:58-78) into a
+// descriptor (everything the persistent walk needs to start the segment).
+__device__ __forceinline__ void dda_init(const double o[3], const double e[3], double cell,
+                                         SegDesc &sd) {
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+    unsigned codes = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double v = e[a] - o[a];
+        const int c = (int)floor(o[a] / cell);
+        sd.c[a] = c;
+        sd.e[a] = (int)floor(e[a] / cell);
+        double t = INF, d = INF;
+        unsigned code = 1;  // step + 1
+        if (v > 0) {
+            code = 2;
+            t = ((double)(c + 1) * cell - o[a]) / v;
+            d = cell / v;
+        } else if (v < 0) {
+            code = 0;
+            t = ((double)c * cell - o[a]) / v;
+            d = -cell / v;
+        }
+        sd.t[a] = t;
+        sd.d[a] = d;
+        codes |= code << (2 * a);
+    }
+    sd.flags = codes << 1;
+}
 
 // traversal._walk_grid (traversal.py:52-111) == _kernels.walk_fill
 // (_kernels.pyx:134-211), streamed: the visitor sees every visit in order

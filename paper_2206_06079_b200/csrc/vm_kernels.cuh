@@ -243,21 +243,28 @@ __device__ __forceinline__ T *layer_at(const DevMap &m, int layer, int slot) {
 struct PrefetchVisitor {
     const DevMap *m;
     int *sset;
+    int lo[3], hi[3];
     __device__ __forceinline__ void begin(int, int, int) {}
     __device__ __forceinline__ void moved(int, int) {}
     __device__ __forceinline__ void jump(int, int, int) {}
     __device__ __forceinline__ void visit(int x, int y, int z, double, double, bool) {
+        lo[0] = min(lo[0], x); lo[1] = min(lo[1], y); lo[2] = min(lo[2], z);
+        hi[0] = max(hi[0], x); hi[1] = max(hi[1], y); hi[2] = max(hi[2], z);
         int slot = region_slot(*m, pack_region(x, y, z));
         if (slot < 0) return;
         if (!slotset_insert(sset, slot)) return;
         if (atomicExch(m->slot_pref + slot, m->epoch) != m->epoch)
             atomicAdd(m->stats + S_PREF_TOUCHED, 1ULL);
+        if (slot < m->cap && atomicExch(m->slot_touch + slot, m->epoch) != m->epoch) {
+            unsigned long long t = atomicAdd(m->stats + S_WALK_TOUCHED, 1ULL);
+            if (t < (unsigned long long)m->touched_cap) m->touched[t] = slot;
+        }
     }
 };
 
 template <class Src>
-__global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevMap m, Src src, long long n, int mode,
-                                                    int det) {
+__global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevMap m, Src src,
+                                                    long long n, int mode, int det, int emit) {
     __shared__ int sset[SLOTSET];
     __shared__ int2 smark[BLOCK];
     __shared__ unsigned long long srec[BLOCK];
@@ -271,62 +278,104 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     __syncthreads();
     const bool tsdf = mode == M_TSDF;
     const bool ndt = mode == M_NDT_OM || mode == M_NDT_TM;
+    const int lane = threadIdx.x & 31;
     unsigned long long st[3] = {0, 0, 0};  // processed, segments, range errors
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    Ray r;
+    bool ok = false;
     if (i < n) {
-        Ray r;
         src.load(i, r.o, r.e, r.has, r.inten);
-        bool ok = prep_ray(m, r, !tsdf);
+        ok = prep_ray(m, r, !tsdf);
         if (ok) {
             st[0] = 1;
             st[1] = r.nseg;
             if (!in_range(m, r.o) || !in_range(m, r.e)) {
                 st[2] = 1;
-            } else {
-                PrefetchVisitor pv{&m, sset};
-                for (int s = 0; s < r.nseg; ++s) {
-                    double so[3], se[3];
-                    int sh;
-                    segment_of(m, r, s, so, se, sh);
-                    double pe[3] = {se[0], se[1], se[2]};
-                    if (tsdf && sh) {
-                        double L = norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2]);
-                        if (L > 0.0) {
-                            for (int a = 0; a < 3; ++a) {
-                                double d = (se[a] - so[a]) / L;
-                                pe[a] = se[a] + d * m.tsdf_trunc;
-                            }
-                            if (!in_range(m, pe)) {
-                                st[2] = 1;
-                                break;
-                            }
-                        }
+                ok = false;
+            }
+        }
+    }
+    // warp-aggregated allocation of segment descriptors
+    unsigned long long dbase = 0;
+    if (emit) {
+        unsigned k = ok ? (unsigned)r.nseg : 0u, incl = k;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 0 && total) base = atomicAdd(m.stats + S_SEGDESC, (unsigned long long)total);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        dbase = base + (incl - k);
+    }
+    PrefetchVisitor pv{&m, sset, {INT_MAX, INT_MAX, INT_MAX}, {INT_MIN, INT_MIN, INT_MIN}};
+    if (ok) {
+        for (int s = 0; s < r.nseg; ++s) {
+            double so[3], se[3];
+            int sh;
+            segment_of(m, r, s, so, se, sh);
+            double pe[3] = {se[0], se[1], se[2]};
+            if (tsdf && sh) {
+                double L = norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2]);
+                if (L > 0.0) {
+                    for (int a = 0; a < 3; ++a) {
+                        double d = (se[a] - so[a]) / L;
+                        pe[a] = se[a] + d * m.tsdf_trunc;
                     }
-                    walk(so, pe, m.rsize, pv);
-                    if (sh && (det || ndt) && !tsdf) {
-                        // the sample voxel floor(end / vox) (reference.py:178-186)
-                        int g[3];
-                        for (int a = 0; a < 3; ++a) g[a] = (int)floor(se[a] / m.vox);
-                        RegionTrack rt;
-                        rt.locate(m, g[0], g[1], g[2]);
-                        if (rt.slot >= 0 && rt.slot < m.cap) {
-                            int li = rt.li(m);
-                            if (ndt) {
-                                unsigned long long vid =
-                                    (unsigned long long)rt.slot * m.vpr + li;
-                                unsigned long long order =
-                                    ((unsigned long long)(i * m.maxseg + s) << 1) | 1ULL;
-                                int k = atomicAdd(&nrec, 1);
-                                srec[k] = (vid << m.order_bits) | order;
-                            } else {
-                                unsigned bit = 1u << (li & 31);
-                                unsigned old = atomicOr(
-                                    m.marks + (size_t)rt.slot * m.mark_words + (li >> 5), bit);
-                                if (!(old & bit)) {
-                                    int k = atomicAdd(&nmark, 1);
-                                    smark[k] = make_int2(rt.slot, li);
-                                }
-                            }
+                    if (!in_range(m, pe)) {
+                        st[2] = 1;
+                        break;
+                    }
+                }
+            }
+            walk(so, pe, m.rsize, pv);
+            if (emit && dbase + s < m.seg_cap) {
+                SegDesc sd;
+                dda_init(so, se, m.vox, sd);
+                sd.order = (unsigned)(i * m.maxseg + s) << 1;
+                sd.flags |= sh ? 1u : 0u;
+                RegionTrack rt;
+                rt.locate(m, sd.c[0], sd.c[1], sd.c[2]);
+                sd.slot0 = rt.slot;
+                sd.local0 = (unsigned)rt.lx | ((unsigned)rt.ly << 10) | ((unsigned)rt.lz << 20);
+                sd.r0[0] = rt.rx;
+                sd.r0[1] = rt.ry;
+                sd.r0[2] = rt.rz;
+                sd.pad = 0;
+                sd.L = norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2]);
+                const uint4 *src4 = reinterpret_cast<const uint4 *>(&sd);
+                uint4 *dst4 = reinterpret_cast<uint4 *>(m.segs + dbase + s);
+#pragma unroll
+                for (int q = 0; q < 7; ++q) dst4[q] = src4[q];
+            }
+            if (sh && (det || ndt) && !tsdf) {
+                // the sample voxel floor(end / vox) (reference.py:178-186)
+                int g[3];
+                for (int a = 0; a < 3; ++a) g[a] = (int)floor(se[a] / m.vox);
+                RegionTrack rt;
+                rt.locate(m, g[0], g[1], g[2]);
+                if (rt.slot >= 0 && rt.slot < m.cap) {
+                    int li = rt.li(m);
+                    if (ndt) {
+                        unsigned long long vid = (unsigned long long)rt.slot * m.vpr + li;
+                        unsigned long long order =
+                            ((unsigned long long)(i * m.maxseg + s) << 1) | 1ULL;
+                        int k = atomicAdd(&nrec, 1);
+                        srec[k] = (vid << m.order_bits) | order;
+                    } else {
+                        unsigned bit = 1u << (li & 31);
+                        unsigned old = atomicOr(
+                            m.marks + (size_t)rt.slot * m.mark_words + (li >> 5), bit);
+                        if (!(old & bit)) {
+                            int k = atomicAdd(&nmark, 1);
+                            smark[k] = make_int2(rt.slot, li);
+                            const int bsh = m.brick_shift;
+                            const int b = bsh >= 0 ? ((rt.lx >> bsh) | ((rt.ly >> bsh) << 2) |
+                                                      ((rt.lz >> (bsh + 1)) << 4))
+                                                   : 0;
+                            atomicOr(m.bmask + rt.slot, bsh >= 0 ? (1ULL << b) : 0xFFFFFFFFULL);
                         }
                     }
                 }
@@ -355,6 +404,46 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     }
     const int which[3] = {S_PROCESSED, S_SEGMENTS, S_RANGE_ERR};
     block_add_stats(m, st, which);
+    // batch bounding box of prefetched regions (+1 margin for walk-entered ones)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int lo = pv.lo[a], hi = pv.hi[a];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if ((threadIdx.x & 31) == 0 && lo <= hi) {
+            atomicMin(m.rbox + a, lo - 1);
+            atomicMax(m.rbox + 3 + a, hi + 1);
+        }
+    }
+}
+
+// Dense region-slot grid over the batch bbox (walk lookups become one
+// shared-memory load).  Cells of absent regions hold -1.
+__global__ void k_rgrid(const __grid_constant__ DevMap m) {
+    if (!read_go(m)) return;
+    const int *b = m.rbox;
+    const long long nx = (long long)b[3] - b[0] + 1, ny = (long long)b[4] - b[1] + 1,
+                    nz = (long long)b[5] - b[2] + 1;
+    if (nx <= 0 || ny <= 0 || nz <= 0 || nx * ny * nz > m.rg_max) return;
+    const long long total = nx * ny * nz;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / (nx * ny));
+        long long key = pack_region(b[0] + x, b[1] + y, b[2] + z);
+        unsigned long long h = mix_key(key) & m.tmask;
+        int slot = -1;
+        for (unsigned long long p = 0; p <= m.tmask; ++p) {
+            long long k = m.tkeys[h];
+            if (k == key) { slot = m.tvals[h]; break; }
+            if (k == -1) break;
+            h = (h + 1) & m.tmask;
+        }
+        m.rgrid[i] = slot;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch((unsigned long long *)(m.stats + S_RGRID), 1ULL);
 }
 
 // Refuse the batch if the pool could overflow or inputs were invalid.
@@ -362,200 +451,10 @@ __global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
     int used = *((volatile int *)m.cursor);
     unsigned long long rerr = ((volatile unsigned long long *)m.stats)[S_RANGE_ERR];
     unsigned long long marked = ((volatile unsigned long long *)m.stats)[S_MARKED];
-    bool ok = used + margin <= m.cap && rerr == 0 && marked <= (unsigned long long)m.marked_cap;
+    unsigned long long nseg = ((volatile unsigned long long *)m.stats)[S_SEGDESC];
+    bool ok = used + margin <= m.cap && rerr == 0 && marked <= (unsigned long long)m.marked_cap &&
+              nseg <= m.seg_cap;
     *m.go = ok ? 1 : 0;
-}
-
-// --------------------------------------------------------------- occupancy walk
-
-template <int MODE, bool DET, bool REC_ONLY>
-struct OccVisitor {
-    const DevMap *m;
-    RegionTrack rt;
-    float *occ;
-    unsigned *mean, *cnt, *scr, *dh;
-    double *dd;
-    unsigned order;      // (ray * maxseg + seg) << 1
-    int sh;
-    double Lseg;
-    const double *se;
-    int *sset;
-    unsigned *cube;
-    int c0, c1, c2;      // cube corner (global voxel)
-    Stage<unsigned long long, REC_STAGE> *stage;
-    unsigned long long visits, rmiss, retries;
-
-    __device__ __forceinline__ void bind() {
-        int s = rt.slot;
-        if (s >= 0 && s < m->cap) {
-            occ = layer_at<float>(*m, L_OCC, s);
-            if (DET || !REC_ONLY) scr = layer_at<unsigned>(*m, L_SCRATCH, s);
-            mean = layer_at<unsigned>(*m, L_MEAN, s);
-            cnt = layer_at<unsigned>(*m, L_COUNT, s);
-            if (MODE == M_DECAY) {
-                dh = layer_at<unsigned>(*m, L_DHITS, s);
-                dd = layer_at<double>(*m, L_DDIST, s);
-            }
-            if (DET && !REC_ONLY) touch_region(*m, sset, s);
-        } else {
-            occ = nullptr;
-        }
-    }
-    __device__ __forceinline__ void begin(int x, int y, int z) {
-        rt.locate(*m, x, y, z);
-        bind();
-    }
-    __device__ __forceinline__ void moved(int axis, int s) {
-        if (rt.step(*m, axis, s)) bind();
-    }
-    __device__ __forceinline__ void jump(int x, int y, int z) {
-        rt.locate(*m, x, y, z);
-        bind();
-    }
-    __device__ __forceinline__ void visit(int x, int y, int z, double t0, double t1, bool last) {
-        ++visits;
-        if (!occ) {
-            ++rmiss;
-            return;
-        }
-        const int li = rt.li(*m);
-        const bool hit = last && sh;
-        if (MODE == M_DECAY && !REC_ONLY) {
-            atomicAdd(dd + li, (t1 - t0) * Lseg);
-            if (hit) atomicAdd(dh + li, 1u);
-        }
-        if (DET) {
-            const int s = rt.slot;
-            unsigned w = __ldg(m->marks + (size_t)s * m->mark_words + (li >> 5));
-            if ((w >> (li & 31)) & 1u) {
-                unsigned mi = scr[li] & ~MARK_FLAG;
-                unsigned long long key = ((unsigned long long)mi << m->order_bits) |
-                                         (unsigned long long)(order | (hit ? 1u : 0u));
-                stage->push(key, m->rec, m->stats + S_RECORDS, m->rec_cap);
-                return;
-            }
-            if (REC_ONLY) return;
-            unsigned ux = (unsigned)(x - c0), uy = (unsigned)(y - c1), uz = (unsigned)(z - c2);
-            if ((ux | uy | uz) < (unsigned)CUBE)
-                atomicAdd(cube + ux + CUBE * (uy + CUBE * uz), 1u);
-            else
-                atomicAdd(scr + li, 1u);
-        } else {
-            if (hit) {
-                float *p = occ + li;
-                unsigned old = __float_as_uint(__ldcg(p));
-                for (;;) {
-                    unsigned nb = __float_as_uint(clamp_add(__uint_as_float(old), m->hit32,
-                                                            m->cmin, m->cmax));
-                    if (nb == old) break;
-                    unsigned prev = atomicCAS(reinterpret_cast<unsigned *>(p), old, nb);
-                    if (prev == old) break;
-                    old = prev;
-                    ++retries;
-                }
-                if (mean) {
-                    double off[3] = {se[0] / m->vox - (double)x, se[1] / m->vox - (double)y,
-                                     se[2] / m->vox - (double)z};
-                    retries += cas_mean(mean + li, cnt + li, off);
-                }
-            } else {
-                unsigned ux = (unsigned)(x - c0), uy = (unsigned)(y - c1), uz = (unsigned)(z - c2);
-                if ((ux | uy | uz) < (unsigned)CUBE)
-                    atomicAdd(cube + ux + CUBE * (uy + CUBE * uz), 1u);
-                else
-                    retries += cas_apply_k(occ + li, m->miss32, 1, m->cmin, m->cmax);
-            }
-        }
-    }
-};
-
-template <int MODE, bool DET, bool REC_ONLY, class Src>
-__global__ void __launch_bounds__(BLOCK) k_walk_occ(const __grid_constant__ DevMap m, Src src, long long n) {
-    __shared__ unsigned cube[CUBE_N];
-    __shared__ int sset[SLOTSET];
-    __shared__ unsigned long long srec[REC_STAGE];
-    __shared__ int nrec;
-    __shared__ unsigned long long rec_base;
-    __shared__ int corner[3];
-    if (!read_go(m)) return;
-    for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) cube[k] = 0;
-    for (int k = threadIdx.x; k < SLOTSET; k += blockDim.x) sset[k] = -1;
-    long long first = (long long)blockIdx.x * blockDim.x;
-    if (threadIdx.x == 0) {
-        nrec = 0;
-        double o[3], e[3];
-        int h;
-        float it;
-        src.load(first, o, e, h, it);
-        for (int a = 0; a < 3; ++a) corner[a] = (int)floor(o[a] / m.vox) - CUBE / 2;
-    }
-    __syncthreads();
-    Stage<unsigned long long, REC_STAGE> stage{srec, &nrec};
-    OccVisitor<MODE, DET, REC_ONLY> v;
-    v.m = &m;
-    v.sset = sset;
-    v.cube = cube;
-    v.c0 = corner[0];
-    v.c1 = corner[1];
-    v.c2 = corner[2];
-    v.stage = &stage;
-    v.visits = v.rmiss = v.retries = 0;
-    v.scr = nullptr;
-    v.dh = nullptr;
-    v.dd = nullptr;
-    long long i = first + threadIdx.x;
-    if (i < n) {
-        Ray r;
-        src.load(i, r.o, r.e, r.has, r.inten);
-        if (prep_ray(m, r, true)) {
-            for (int s = 0; s < r.nseg; ++s) {
-                double so[3], se[3];
-                segment_of(m, r, s, so, se, v.sh);
-                v.order = (unsigned)(i * m.maxseg + s) << 1;
-                v.se = se;
-                v.Lseg = MODE == M_DECAY ? norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2])
-                                         : 0.0;
-                walk(so, se, m.vox, v);
-            }
-        }
-    }
-    __syncthreads();
-    // flush the aggregation cube: k identical misses per voxel
-    unsigned long long flushed = 0;
-    if (!REC_ONLY) {
-        for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) {
-            unsigned cnt = cube[k];
-            if (!cnt) continue;
-            ++flushed;
-            int g[3] = {v.c0 + k % CUBE, v.c1 + (k / CUBE) % CUBE, v.c2 + k / (CUBE * CUBE)};
-            RegionTrack rt;
-            rt.locate(m, g[0], g[1], g[2]);
-            int li = rt.li(m);
-            if (DET) {
-                unsigned *scr = layer_at<unsigned>(m, L_SCRATCH, rt.slot);
-                touch_region(m, sset, rt.slot);
-                atomicAdd(scr + li, cnt);
-            } else {
-                float *occ = layer_at<float>(m, L_OCC, rt.slot);
-                v.retries += cas_apply_k(occ + li, m.miss32, cnt, m.cmin, m.cmax);
-            }
-        }
-    }
-    if (DET) {
-        __syncthreads();
-        int nl = nrec < REC_STAGE ? nrec : REC_STAGE;
-        if (threadIdx.x == 0 && nl) rec_base = atomicAdd(m.stats + S_RECORDS, (unsigned long long)nl);
-        __syncthreads();
-        for (int k = threadIdx.x; k < nl; k += blockDim.x) {
-            unsigned long long ri = rec_base + k;
-            if (ri < m.rec_cap) m.rec[ri] = srec[k];
-        }
-    }
-    if (!REC_ONLY) {
-        unsigned long long st[4] = {v.visits, v.rmiss, v.retries, flushed};
-        const int which[4] = {S_VISITS, S_RMISS, S_RETRIES, S_CUBE_FLUSH};
-        block_add_stats(m, st, which);
-    }
 }
 
 // --------------------------------------------------------------- NDT phase 1
@@ -844,39 +743,123 @@ __global__ void __launch_bounds__(BLOCK) k_walk_tsdf(const __grid_constant__ Dev
 // f_miss^k for every voxel that received k order-free misses this batch;
 // NDT adds the NDT-TM miss count and the transient reset
 // (reference.py:86-93).  One block per touched region.
+// Resolve region `slot`, voxels [v0, v1): f_miss^k per counted voxel.
+template <bool NDT, bool TM>
+__device__ __forceinline__ void resolve_range(const DevMap &m, int slot, int v0, int v1) {
+    unsigned *scr = reinterpret_cast<unsigned *>(m.slab[L_SCRATCH] + (size_t)slot * m.bpr[L_SCRATCH]);
+    float *occ = reinterpret_cast<float *>(m.slab[L_OCC] + (size_t)slot * m.bpr[L_OCC]);
+    if (!NDT && ((v0 | v1) & 3) == 0) {
+        // 8 independent 16-byte loads in flight per thread
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(scr);
+        for (int q0 = (v0 >> 2) + threadIdx.x; q0 < (v1 >> 2); q0 += 8 * blockDim.x) {
+            uint4 w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * blockDim.x;
+                w[u] = q < (v1 >> 2) ? __ldcs(s4 + q) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (!(w[u].x | w[u].y | w[u].z | w[u].w)) continue;
+                const int q = q0 + u * blockDim.x;
+                unsigned ks[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+                bool clear = false;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (ks[j] == 0 || (ks[j] & MARK_FLAG)) continue;
+                    clear = true;
+                    occ[4 * q + j] = miss_k(occ[4 * q + j], ks[j], m.miss32, m.cmin, m.cmax);
+                    ks[j] = 0;
+                }
+                if (clear) reinterpret_cast<uint4 *>(scr)[q] = make_uint4(ks[0], ks[1], ks[2], ks[3]);
+            }
+        }
+        return;
+    }
+    for (int li = v0 + threadIdx.x; li < v1; li += blockDim.x) {
+        const unsigned k = scr[li];
+        if (k == 0 || (k & MARK_FLAG)) continue;
+        scr[li] = 0;
+        float l = occ[li];
+        if (!NDT) {
+            occ[li] = miss_k(l, k, m.miss32, m.cmin, m.cmax);
+            continue;
+        }
+        // NDT phase 1, g == 1 (reference.py:86-93): each miss is followed by
+        // the TM miss count and the transient reset check; with identical
+        // deltas the reset fires at the first miss j with l < threshold.
+        unsigned *cnt = layer_at<unsigned>(m, L_COUNT, slot);
+        unsigned j = 0;
+        if (cnt[li] > 0) {
+            for (unsigned i = 1; i <= k; ++i) {
+                const float nl = clamp_add(l, m.miss32, m.cmin, m.cmax);
+                const bool same = __float_as_uint(nl) == __float_as_uint(l);
+                l = nl;
+                if (l < m.fthresh) {
+                    j = i;
+                    break;
+                }
+                if (same) break;  // fixed point above the threshold: never resets
+            }
+        }
+        if (j) {
+            l = miss_k(l, k - j, m.miss32, m.cmin, m.cmax);
+            cnt[li] = 0;
+            layer_at<unsigned>(m, L_MEAN, slot)[li] = 0;
+            float *cov = layer_at<float>(m, L_COV, slot);
+            for (int q = 0; q < 6; ++q) cov[li * 6 + q] = 0.0f;
+            if (TM) {
+                layer_at<unsigned>(m, L_HIT, slot)[li] = 0;
+                layer_at<unsigned>(m, L_MISS, slot)[li] = k - j;
+                float *it = layer_at<float>(m, L_INTENS, slot);
+                it[li * 2] = 0.0f;
+                it[li * 2 + 1] = 0.0f;
+            }
+        } else {
+            l = miss_k(occ[li], k, m.miss32, m.cmin, m.cmax);
+            if (TM) layer_at<unsigned>(m, L_MISS, slot)[li] += k;
+        }
+        occ[li] = l;
+    }
+}
+
+// Resolve the order-free miss counts of every region the walk touched:
+// the dense-grid regions plus touched-list regions outside the grid.
+// Work item = (region, tile of RES_TILE voxels).
+constexpr int RES_TILE = 8192;
+
 template <bool NDT, bool TM>
 __global__ void __launch_bounds__(BLOCK) k_resolve(const __grid_constant__ DevMap m) {
     if (!read_go(m)) return;
     unsigned long long nt = *((volatile unsigned long long *)(m.stats + S_WALK_TOUCHED));
     if (nt > (unsigned long long)m.touched_cap) nt = m.touched_cap;
-    for (unsigned long long t = blockIdx.x; t < nt; t += gridDim.x) {
-        int slot = m.touched[t];
-        unsigned *scr = layer_at<unsigned>(m, L_SCRATCH, slot);
-        float *occ = layer_at<float>(m, L_OCC, slot);
-        for (int li = threadIdx.x; li < m.vpr; li += blockDim.x) {
-            unsigned k = scr[li];
-            if (k == 0 || (k & MARK_FLAG)) continue;
-            scr[li] = 0;
-            float l = miss_k(occ[li], k, m.miss32, m.cmin, m.cmax);
-            occ[li] = l;
-            if (NDT) {
-                unsigned *cnt = layer_at<unsigned>(m, L_COUNT, slot);
-                if (TM) layer_at<unsigned>(m, L_MISS, slot)[li] += k;
-                if (l < m.fthresh && cnt[li] > 0) {
-                    cnt[li] = 0;
-                    layer_at<unsigned>(m, L_MEAN, slot)[li] = 0;
-                    float *cov = layer_at<float>(m, L_COV, slot);
-                    for (int j = 0; j < 6; ++j) cov[li * 6 + j] = 0.0f;
-                    if (TM) {
-                        layer_at<unsigned>(m, L_HIT, slot)[li] = 0;
-                        layer_at<unsigned>(m, L_MISS, slot)[li] = 0;
-                        float *it = layer_at<float>(m, L_INTENS, slot);
-                        it[li * 2] = 0.0f;
-                        it[li * 2 + 1] = 0.0f;
-                    }
-                }
+    const bool grid = *((volatile unsigned long long *)(m.stats + S_RGRID)) != 0;
+    const int *b = m.rbox;
+    const long long gx = grid ? b[3] - b[0] + 1 : 0, gy = grid ? b[4] - b[1] + 1 : 0,
+                    gz = grid ? b[5] - b[2] + 1 : 0;
+    const unsigned long long ncell = (unsigned long long)(gx * gy * gz);
+    const int tiles = (m.vpr + RES_TILE - 1) / RES_TILE;
+    for (unsigned long long w = blockIdx.x; w < (ncell + nt) * tiles; w += gridDim.x) {
+        const unsigned long long t = w / tiles;
+        const int tile = (int)(w % tiles);
+        int slot;
+        if (t < ncell) {
+            slot = m.rgrid[t];
+            if (slot < 0 || slot >= m.cap) continue;
+        } else {
+            slot = m.touched[t - ncell];
+            if (grid) {
+                int r[3];
+                unpack_region(m.slot_keys[slot], r);
+                const long long ux = r[0] - b[0], uy = r[1] - b[1], uz = r[2] - b[2];
+                if (ux >= 0 && ux < gx && uy >= 0 && uy < gy && uz >= 0 && uz < gz &&
+                    m.rgrid[ux + gx * (uy + gy * uz)] == slot)
+                    continue;  // already covered by its grid cell
             }
         }
+        const int v0 = tile * RES_TILE;
+        const int v1 = min(m.vpr, v0 + RES_TILE);
+        resolve_range<NDT, TM>(m, slot, v0, v1);
     }
 }
 
@@ -1070,6 +1053,7 @@ __global__ void k_cleanup(const __grid_constant__ DevMap m, int M) {
         int2 sl = m.marked[k];
         m.marks[(size_t)sl.x * m.mark_words + (sl.y >> 5)] = 0u;
         layer_at<unsigned>(m, L_SCRATCH, sl.x)[sl.y] = 0u;
+        m.bmask[sl.x] = 0ULL;
     }
 }
 

@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/voxmap_b200.h"
-#include "vm_kernels.cuh"
+#include "vm_walk.cuh"
 
 using namespace vm;
 
@@ -78,6 +78,13 @@ struct vm_map {
     long long *d_slot_keys = nullptr;
     unsigned *d_slot_touch = nullptr, *d_slot_pref = nullptr;
     unsigned *d_marks = nullptr;
+    unsigned long long *d_bmask = nullptr;
+    SegDesc *d_segs = nullptr;
+    size_t seg_cap = 0;
+    unsigned long long *d_work = nullptr;
+    int *d_rgrid = nullptr;
+    int *d_rbox = nullptr;
+    int num_sms = 148;
     unsigned long long *d_stats = nullptr;
     int *d_go = nullptr;
     unsigned long long *d_rec = nullptr, *d_rec2 = nullptr;
@@ -92,7 +99,7 @@ struct vm_map {
     unsigned long long *h_stats = nullptr;  // pinned, NUM_STATS + 2
     unsigned epoch = 0;
     long long launches = 0;
-    cudaEvent_t ev_start{}, ev_end{}, ev_w0{}, ev_w1{}, ev_k1{}, ev_k2{};
+    cudaEvent_t ev_start{}, ev_end{}, ev_w0{}, ev_w1{}, ev_k1{}, ev_k2{}, ev_res{}, ev_sort{};
 };
 
 namespace {
@@ -131,8 +138,27 @@ DevMap make_dm(const vm_map *m) {
     d.slot_touch = m->d_slot_touch;
     d.slot_pref = m->d_slot_pref;
     d.epoch = m->epoch;
-    for (int l = 0; l < NUM_LAYERS; ++l) d.lptr[l] = m->d_lptr[l];
+    for (int l = 0; l < NUM_LAYERS; ++l) {
+        d.lptr[l] = m->d_lptr[l];
+        d.slab[l] = (char *)m->slab[l];
+        d.bpr[l] = m->bpr[l];
+    }
     d.marks = m->d_marks;
+    d.bmask = m->d_bmask;
+    {
+        int bs = -1;
+        if (m->dim >= 4 && (m->dim & (m->dim - 1)) == 0) {
+            bs = 0;
+            while ((1 << (bs + 2)) < m->dim) ++bs;
+        }
+        d.brick_shift = bs;
+    }
+    d.rgrid = m->d_rgrid;
+    d.rbox = m->d_rbox;
+    d.rg_max = RG_MAX;
+    d.segs = m->d_segs;
+    d.seg_cap = m->seg_cap;
+    d.work = m->d_work;
     d.stats = m->d_stats;
     d.go = m->d_go;
     d.rec = m->d_rec;
@@ -216,22 +242,41 @@ int check_launch(const char *what) {
     return VM_OK;
 }
 
+template <int MODE, bool DET, bool REC_ONLY, class Src>
+void launch_w3(dim3 grid, size_t smem, cudaStream_t s, const DevMap &dm, const Src &src) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_walk<MODE, DET, REC_ONLY, Src>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    k_walk<MODE, DET, REC_ONLY, Src><<<grid, BLOCK, smem, s>>>(dm, src);
+}
+
 // kernel dispatch over (mode, exec, ray format)
 template <class Src>
 int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mode, bool det,
                 bool rec_only) {
     dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK)), block(BLOCK);
     cudaStream_t s = m->stream;
+    // persistent grid: 2 resident blocks per SM, never more than the work needs
+    dim3 pgrid((unsigned)std::max<long long>(
+        1, std::min<long long>(2LL * m->num_sms, (n * 3 + BLOCK - 1) / BLOCK)));
+    if (mode == M_OCC || mode == M_DECAY) {
+        cudaError_t e = cudaMemsetAsync(m->d_work, 0, sizeof(unsigned long long), s);
+        if (e != cudaSuccess) return fail(VM_ERR_CUDA, cudaGetErrorString(e));
+    }
+    const size_t smem = sizeof(WalkSmem);
     switch (mode) {
     case M_OCC:
-        if (det && rec_only) k_walk_occ<M_OCC, true, true><<<grid, block, 0, s>>>(dm, src, n);
-        else if (det) k_walk_occ<M_OCC, true, false><<<grid, block, 0, s>>>(dm, src, n);
-        else k_walk_occ<M_OCC, false, false><<<grid, block, 0, s>>>(dm, src, n);
+        if (det && rec_only) launch_w3<M_OCC, true, true>(pgrid, smem, s, dm, src);
+        else if (det) launch_w3<M_OCC, true, false>(pgrid, smem, s, dm, src);
+        else launch_w3<M_OCC, false, false>(pgrid, smem, s, dm, src);
         break;
     case M_DECAY:
-        if (det && rec_only) k_walk_occ<M_DECAY, true, true><<<grid, block, 0, s>>>(dm, src, n);
-        else if (det) k_walk_occ<M_DECAY, true, false><<<grid, block, 0, s>>>(dm, src, n);
-        else k_walk_occ<M_DECAY, false, false><<<grid, block, 0, s>>>(dm, src, n);
+        if (det && rec_only) launch_w3<M_DECAY, true, true>(pgrid, smem, s, dm, src);
+        else if (det) launch_w3<M_DECAY, true, false>(pgrid, smem, s, dm, src);
+        else launch_w3<M_DECAY, false, false>(pgrid, smem, s, dm, src);
         break;
     case M_NDT_OM: k_walk_ndt<false><<<grid, block, 0, s>>>(dm, src, n); break;
     case M_NDT_TM: k_walk_ndt<true><<<grid, block, 0, s>>>(dm, src, n); break;
@@ -292,6 +337,8 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
 
     int rc;
     if ((rc = ensure_buf(&m->d_marked, &m->marked_cap, (size_t)n + 1))) return rc;
+    const bool emit = mode == M_OCC || mode == M_DECAY;
+    if (emit && (rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * maxseg + 1))) return rc;
     size_t rec_need = 0;
     if (ndt) rec_need = (size_t)n + 1;
     else if (tsdf && det) {
@@ -300,7 +347,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     } else if (occ_det) rec_need = std::max<size_t>(m->rec_cap, std::max<size_t>(1 << 20, (size_t)n * 4));
     if (sorted && (rc = ensure_records(m, rec_need))) return rc;
 
-    float ms_total = 0.f, ms_walk = 0.f;
+    float ms_total = 0.f, ms_walk = 0.f, ms_disc = 0.f, ms_res = 0.f, ms_sort = 0.f, ms_fold = 0.f;
     const long long launches0 = m->launches;
     long long replays = 0;
     const long long nreg0 = m->nreg;
@@ -313,13 +360,22 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         DevMap dm = make_dm(m);
         dm.order_bits = order_bits;
         CK(cudaMemsetAsync(m->d_stats, 0, NUM_STATS * sizeof(unsigned long long), m->stream));
+        {
+            static const int box_init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
+            CK(cudaMemcpyAsync(m->d_rbox, box_init, sizeof(box_init), cudaMemcpyHostToDevice,
+                               m->stream));
+        }
         CK(cudaEventRecord(m->ev_start, m->stream));
         dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK));
-        k_discover<<<grid, BLOCK, 0, m->stream>>>(dm, src, n, mode, det ? 1 : 0);
+        k_discover<<<grid, BLOCK, 0, m->stream>>>(dm, src, n, mode, det ? 1 : 0, emit ? 1 : 0);
         m->launches += 2;  // discover + guard
         if ((rc = check_launch("discover"))) return rc;
         int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
         k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
+        if (emit) {
+            k_rgrid<<<16, BLOCK, 0, m->stream>>>(dm);
+            m->launches += 1;
+        }
         CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, m->stream));
         CK(cudaMemcpyAsync(m->h_stats + NUM_STATS, m->d_cursor, sizeof(int),
@@ -336,12 +392,13 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             CK(cudaEventRecord(m->ev_k2, m->stream));
         }
         if (resolve) {
-            if (ndt && mode == M_NDT_TM) k_resolve<true, true><<<148 * 4, BLOCK, 0, m->stream>>>(dm);
-            else if (ndt) k_resolve<true, false><<<148 * 4, BLOCK, 0, m->stream>>>(dm);
-            else k_resolve<false, false><<<148 * 4, BLOCK, 0, m->stream>>>(dm);
+            if (ndt && mode == M_NDT_TM) k_resolve<true, true><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
+            else if (ndt) k_resolve<true, false><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
+            else k_resolve<false, false><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
             m->launches += 1;
             if ((rc = check_launch("resolve"))) return rc;
         }
+        CK(cudaEventRecord(m->ev_res, m->stream));
         CK(cudaEventSynchronize(m->ev_k1));
         const unsigned long long *hs = m->h_stats;
         int cursor = *(const int *)(hs + NUM_STATS);
@@ -401,6 +458,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 CK(cub::DeviceRadixSort::SortKeys(m->d_sort_tmp, bytes, db, (int)R, 0, end_bit,
                                                   m->stream));
             }
+            CK(cudaEventRecord(m->ev_sort, m->stream));
             if ((rc = launch_fold(m, dm, src, db.Current(), (long long)R, M, mode))) return rc;
             if (occ_det && M) {
                 k_cleanup<<<148, BLOCK, 0, m->stream>>>(dm, (int)M);
@@ -417,6 +475,12 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         if ((rc = check_launch("batch"))) return rc;
         CK(cudaEventElapsedTime(&ms_total, m->ev_start, m->ev_end));
         CK(cudaEventElapsedTime(&ms_walk, m->ev_w0, m->ev_w1));
+        CK(cudaEventElapsedTime(&ms_disc, m->ev_start, m->ev_w0));
+        CK(cudaEventElapsedTime(&ms_res, m->ev_w1, m->ev_res));
+        if (sorted) {
+            CK(cudaEventElapsedTime(&ms_sort, m->ev_res, m->ev_sort));
+            CK(cudaEventElapsedTime(&ms_fold, m->ev_sort, m->ev_end));
+        }
         break;
     }
     const unsigned long long *hs = m->h_stats;
@@ -439,6 +503,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     out->launches = m->launches - launches0;
     out->gpu_ms = ms_total;
     out->walk_ms = ms_walk;
+    out->discover_ms = ms_disc;
+    out->resolve_ms = ms_res;
+    out->sort_ms = ms_sort;
+    out->fold_ms = ms_fold;
     m->max_growth = std::max<long long>(m->max_growth, cursor - m->nreg);
     m->nreg = cursor;
     return VM_OK;
@@ -511,16 +579,23 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         (rc = dev_alloc(&m->d_cursor, 1)) || (rc = dev_alloc(&m->d_slot_keys, m->max_slots)) ||
         (rc = dev_alloc(&m->d_slot_touch, m->max_slots)) ||
         (rc = dev_alloc(&m->d_slot_pref, m->max_slots)) || (rc = dev_alloc(&m->d_stats, NUM_STATS)) ||
-        (rc = dev_alloc(&m->d_go, 1)) || (rc = dev_alloc(&m->d_touched, m->max_slots)))
+        (rc = dev_alloc(&m->d_go, 1)) || (rc = dev_alloc(&m->d_touched, m->max_slots)) ||
+        (rc = dev_alloc(&m->d_bmask, m->max_slots)) || (rc = dev_alloc(&m->d_work, 1)) ||
+        (rc = dev_alloc(&m->d_rgrid, RG_MAX)) || (rc = dev_alloc(&m->d_rbox, 6)))
         return cleanup(rc);
     for (int l = 0; l < NUM_LAYERS; ++l)
         if (m->bpr[l] && (rc = dev_alloc(&m->d_lptr[l], m->max_slots))) return cleanup(rc);
     if (cudaMallocHost((void **)&m->h_stats, (NUM_STATS + 4) * sizeof(unsigned long long)) !=
         cudaSuccess)
         return cleanup(fail(VM_ERR_OOM, "pinned alloc failed"));
-    cudaEvent_t *evs[] = {&m->ev_start, &m->ev_end, &m->ev_w0, &m->ev_w1, &m->ev_k1, &m->ev_k2};
+    cudaEvent_t *evs[] = {&m->ev_start, &m->ev_end, &m->ev_w0, &m->ev_w1,
+                          &m->ev_k1,    &m->ev_k2,  &m->ev_res, &m->ev_sort};
     for (auto *e : evs)
         if (cudaEventCreate(e) != cudaSuccess) return cleanup(fail(VM_ERR_CUDA, "event create"));
+    {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) m->num_sms = prop.multiProcessorCount;
+    }
     if ((rc = grow_pool(m, std::max<long long>(64, initial_regions)))) return cleanup(rc);
     *out = m;
     return VM_OK;
@@ -541,6 +616,11 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_slot_touch);
     cudaFree(m->d_slot_pref);
     cudaFree(m->d_marks);
+    cudaFree(m->d_bmask);
+    cudaFree(m->d_segs);
+    cudaFree(m->d_work);
+    cudaFree(m->d_rgrid);
+    cudaFree(m->d_rbox);
     cudaFree(m->d_stats);
     cudaFree(m->d_go);
     cudaFree(m->d_rec);
@@ -550,7 +630,8 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_sort_tmp);
     cudaFree(m->d_rays);
     if (m->h_stats) cudaFreeHost(m->h_stats);
-    cudaEvent_t evs[] = {m->ev_start, m->ev_end, m->ev_w0, m->ev_w1, m->ev_k1, m->ev_k2};
+    cudaEvent_t evs[] = {m->ev_start, m->ev_end, m->ev_w0,  m->ev_w1,
+                         m->ev_k1,    m->ev_k2,  m->ev_res, m->ev_sort};
     for (auto e : evs)
         if (e) cudaEventDestroy(e);
     if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
@@ -570,6 +651,7 @@ int vm_map_reset(vm_map *m) {
     CK(cudaMemsetAsync(m->d_tkeys, 0xFF, m->tsize * sizeof(long long), m->stream));
     CK(cudaMemsetAsync(m->d_tvals, 0xFF, m->tsize * sizeof(int), m->stream));
     CK(cudaMemsetAsync(m->d_cursor, 0, sizeof(int), m->stream));
+    CK(cudaMemsetAsync(m->d_bmask, 0, m->max_slots * sizeof(unsigned long long), m->stream));
     CK(cudaStreamSynchronize(m->stream));
     m->nreg = 0;
     return VM_OK;

@@ -112,6 +112,28 @@ def os128_canyon_batches(n_batches: int = 1000, cols_per_batch: int = 205, seed:
     return out
 
 
+BATCH_PERIOD = 0.1  # the reference CLI's batch period (cli.py:31)
+
+
+def batch_by_period(records: np.ndarray, period: float = BATCH_PERIOD) -> list[np.ndarray]:
+    """Cut a timestamp-ordered record stream into `period`-second batches, as
+    the reference CLI's _load_batches does (cli.py:70-94)."""
+    if len(records) == 0:
+        return []
+    ts = records["timestamp"]
+    t0 = ts[0]
+    edges = np.searchsorted(ts, t0 + period * np.arange(
+        1, int(np.ceil((ts[-1] - t0) / period)) + 2))
+    out, start = [], 0
+    for edge in edges:
+        if edge > start:
+            out.append(records[start:edge])
+            start = edge
+        if start >= len(records):
+            break
+    return out
+
+
 def os64_tunnel_scans(n_scans: int, seed: int = 2, step: float = 0.5):
     """C3: OS1-64 scans along a 4 x 3 m tunnel with rough walls."""
     rng = np.random.default_rng(seed)
