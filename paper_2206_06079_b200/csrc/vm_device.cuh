@@ -80,6 +80,7 @@ struct DevMap {
     char *slab[NUM_LAYERS];              // pool slabs: region s at slab + s * bpr
     unsigned long long bpr[NUM_LAYERS];  // bytes per region per layer
     int *rgrid;                          // dense region-slot grid over the batch bbox
+    unsigned *ztouch;                    // per grid cell: z-planes holding miss counts
     int *rbox;                           // [6]: min xyz, max xyz (regions) of the batch
     int rg_max;                          // capacity of rgrid (cells)
     SegDesc *segs;                       // preprocessed segments of the batch
@@ -137,6 +138,9 @@ __device__ __forceinline__ int floordiv(int a, int d) {
 // Fire-and-forget reductions (REDG): no return value, no scoreboard wait.
 __device__ __forceinline__ void red_add(unsigned *p, unsigned v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_or(unsigned *p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void red_add(double *p, double v) {
     asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");

@@ -239,9 +239,54 @@ __device__ __forceinline__ T *layer_at(const DevMap &m, int layer, int slot) {
 
 // --------------------------------------------------------------- k_discover
 
+// Per-block direct-mapped cache region -> slot, keyed by coordinates relative
+// to a block anchor (13 bits per axis) so key + slot fit one 64-bit word.
+constexpr int KCACHE = 1024;
+struct KeyCache {
+    unsigned long long *e;
+    int ax, ay, az;
+    // entry: bit 63 valid | bits 21..59 relative coords (13 bits each) | bits 0..20 slot + 2
+    __device__ __forceinline__ bool rel(int rx, int ry, int rz, unsigned long long &tag,
+                                        unsigned &idx) const {
+        const unsigned ux = (unsigned)(rx - ax), uy = (unsigned)(ry - ay), uz = (unsigned)(rz - az);
+        if ((ux | uy | uz) >= (1u << 13)) return false;
+        tag = (unsigned long long)ux | ((unsigned long long)uy << 13) | ((unsigned long long)uz << 26);
+        idx = (ux * 73856093u ^ uy * 19349663u ^ uz * 83492791u) & (KCACHE - 1);
+        return true;
+    }
+    // slot, or -3 on a miss (-1/-2 are valid cached answers: absent / exhausted)
+    __device__ __forceinline__ int find(int rx, int ry, int rz) const {
+        unsigned long long tag;
+        unsigned idx;
+        if (!rel(rx, ry, rz, tag, idx)) return -3;
+        const unsigned long long v = e[idx];
+        if ((v >> 63) && ((v >> 21) & ((1ULL << 39) - 1)) == tag) return (int)(v & 0x1FFFFFu) - 2;
+        return -3;
+    }
+    __device__ __forceinline__ void put(int rx, int ry, int rz, int slot) const {
+        unsigned long long tag;
+        unsigned idx;
+        if (!rel(rx, ry, rz, tag, idx) || slot < -2 || slot >= (1 << 21) - 2) return;
+        e[idx] = (1ULL << 63) | (tag << 21) | (unsigned long long)(slot + 2);
+    }
+};
+
+__device__ __forceinline__ int cached_slot(const DevMap &m, const KeyCache &kc, int rx, int ry,
+                                           int rz, bool *fresh) {
+    int slot = kc.find(rx, ry, rz);
+    *fresh = false;
+    if (slot == -3) {
+        slot = region_slot(m, pack_region(rx, ry, rz));
+        kc.put(rx, ry, rz, slot);
+        *fresh = true;
+    }
+    return slot;
+}
+
 // Coarse region DDA visitor (walk_regions, traversal.py:134-137).
 struct PrefetchVisitor {
     const DevMap *m;
+    const KeyCache *kc;
     int *sset;
     int lo[3], hi[3];
     __device__ __forceinline__ void begin(int, int, int) {}
@@ -250,9 +295,10 @@ struct PrefetchVisitor {
     __device__ __forceinline__ void visit(int x, int y, int z, double, double, bool) {
         lo[0] = min(lo[0], x); lo[1] = min(lo[1], y); lo[2] = min(lo[2], z);
         hi[0] = max(hi[0], x); hi[1] = max(hi[1], y); hi[2] = max(hi[2], z);
-        int slot = region_slot(*m, pack_region(x, y, z));
-        if (slot < 0) return;
-        if (!slotset_insert(sset, slot)) return;
+        bool fresh;
+        const int slot = cached_slot(*m, *kc, x, y, z, &fresh);
+        if (slot < 0 || !fresh) return;
+        if (!slotset_insert(sset, slot)) return;  // first sight of the region in this block only
         if (atomicExch(m->slot_pref + slot, m->epoch) != m->epoch)
             atomicAdd(m->stats + S_PREF_TOUCHED, 1ULL);
         if (slot < m->cap && atomicExch(m->slot_touch + slot, m->epoch) != m->epoch) {
@@ -265,17 +311,30 @@ struct PrefetchVisitor {
 template <class Src>
 __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevMap m, Src src,
                                                     long long n, int mode, int det, int emit) {
+    __shared__ unsigned long long kcache[KCACHE];
     __shared__ int sset[SLOTSET];
     __shared__ int2 smark[BLOCK];
     __shared__ unsigned long long srec[BLOCK];
     __shared__ int nmark, nrec;
     __shared__ unsigned long long mark_base, rec_base;
+    __shared__ int anchor[3];
+    for (int i = threadIdx.x; i < KCACHE; i += blockDim.x) kcache[i] = 0ULL;
     for (int i = threadIdx.x; i < SLOTSET; i += blockDim.x) sset[i] = -1;
     if (threadIdx.x == 0) {
         nmark = 0;
         nrec = 0;
+        const long long i0 = (long long)blockIdx.x * blockDim.x;
+        double o0[3], e0[3];
+        int h0;
+        float it0;
+        src.load(i0 < n ? i0 : 0, o0, e0, h0, it0);
+        for (int a = 0; a < 3; ++a) {
+            const double c = floor(o0[a] / m.rsize);
+            anchor[a] = (c > -1e9 && c < 1e9 ? (int)c : 0) - (1 << 12);
+        }
     }
     __syncthreads();
+    const KeyCache kc{kcache, anchor[0], anchor[1], anchor[2]};
     const bool tsdf = mode == M_TSDF;
     const bool ndt = mode == M_NDT_OM || mode == M_NDT_TM;
     const int lane = threadIdx.x & 31;
@@ -310,7 +369,7 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
         base = __shfl_sync(0xffffffffu, base, 0);
         dbase = base + (incl - k);
     }
-    PrefetchVisitor pv{&m, sset, {INT_MAX, INT_MAX, INT_MAX}, {INT_MIN, INT_MIN, INT_MIN}};
+    PrefetchVisitor pv{&m, &kc, sset, {INT_MAX, INT_MAX, INT_MAX}, {INT_MIN, INT_MIN, INT_MIN}};
     if (ok) {
         for (int s = 0; s < r.nseg; ++s) {
             double so[3], se[3];
@@ -337,7 +396,14 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                 sd.order = (unsigned)(i * m.maxseg + s) << 1;
                 sd.flags |= sh ? 1u : 0u;
                 RegionTrack rt;
-                rt.locate(m, sd.c[0], sd.c[1], sd.c[2]);
+                rt.rx = floordiv(sd.c[0], m.dim);
+                rt.ry = floordiv(sd.c[1], m.dim);
+                rt.rz = floordiv(sd.c[2], m.dim);
+                rt.lx = sd.c[0] - rt.rx * m.dim;
+                rt.ly = sd.c[1] - rt.ry * m.dim;
+                rt.lz = sd.c[2] - rt.rz * m.dim;
+                bool fresh;
+                rt.slot = cached_slot(m, kc, rt.rx, rt.ry, rt.rz, &fresh);
                 sd.slot0 = rt.slot;
                 sd.local0 = (unsigned)rt.lx | ((unsigned)rt.ly << 10) | ((unsigned)rt.lz << 20);
                 sd.r0[0] = rt.rx;
@@ -355,7 +421,14 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                 int g[3];
                 for (int a = 0; a < 3; ++a) g[a] = (int)floor(se[a] / m.vox);
                 RegionTrack rt;
-                rt.locate(m, g[0], g[1], g[2]);
+                rt.rx = floordiv(g[0], m.dim);
+                rt.ry = floordiv(g[1], m.dim);
+                rt.rz = floordiv(g[2], m.dim);
+                rt.lx = g[0] - rt.rx * m.dim;
+                rt.ly = g[1] - rt.ry * m.dim;
+                rt.lz = g[2] - rt.rz * m.dim;
+                bool fresh;
+                rt.slot = cached_slot(m, kc, rt.rx, rt.ry, rt.rz, &fresh);
                 if (rt.slot >= 0 && rt.slot < m.cap) {
                     int li = rt.li(m);
                     if (ndt) {
@@ -854,7 +927,7 @@ __global__ void __launch_bounds__(BLOCK) k_resolve(const __grid_constant__ DevMa
                 const long long ux = r[0] - b[0], uy = r[1] - b[1], uz = r[2] - b[2];
                 if (ux >= 0 && ux < gx && uy >= 0 && uy < gy && uz >= 0 && uz < gz &&
                     m.rgrid[ux + gx * (uy + gy * uz)] == slot)
-                    continue;  // already covered by its grid cell
+                    continue;  // covered by its grid cell
             }
         }
         const int v0 = tile * RES_TILE;
@@ -876,61 +949,134 @@ __device__ __forceinline__ long long lower_bound_u64(const unsigned long long *a
     return lo;
 }
 
-// Deterministic occupancy fold: one warp per sample voxel applies its
-// records in ray order (reference.py:35-64 for exactly that voxel).
+// Run starts of the sorted occupancy records: start[mi] = first record of
+// sample voxel mi (every sample voxel owns at least its own hit record).
+__global__ void k_heads(const __grid_constant__ DevMap m, const unsigned long long *keys,
+                        long long R, int *start) {
+    if (!read_go(m)) return;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long mi = keys[i] >> m.order_bits;
+        if (i == 0 || (keys[i - 1] >> m.order_bits) != mi) start[mi] = (int)i;
+    }
+}
+
+// Apply one sample voxel's records [s, e) in ray order (reference.py:35-64
+// restricted to that voxel): misses between hits collapse to f_miss^k.
+template <class Src>
+__device__ __forceinline__ void fold_voxel_serial(const DevMap &m, const Src &src,
+                                                  const unsigned long long *keys, int s, int e,
+                                                  int2 sl) {
+    const unsigned long long omask = (1ULL << m.order_bits) - 1;
+    float *occ = layer_at<float>(m, L_OCC, sl.x);
+    unsigned *mean = layer_at<unsigned>(m, L_MEAN, sl.x);
+    unsigned *cnt = layer_at<unsigned>(m, L_COUNT, sl.x);
+    float l = occ[sl.y];
+    unsigned packed = mean ? mean[sl.y] : 0u, count = cnt ? cnt[sl.y] : 0u;
+    int g[3];
+    slot_li_to_g(m, sl.x, sl.y, g);
+    unsigned misses = 0;
+    for (int i = s; i < e; ++i) {
+        const unsigned long long k = keys[i];
+        if (!(k & 1ULL)) {
+            ++misses;
+            continue;
+        }
+        l = miss_k(l, misses, m.miss32, m.cmin, m.cmax);
+        misses = 0;
+        l = clamp_add(l, m.hit32, m.cmin, m.cmax);
+        if (mean) {
+            const long long ray = (long long)(((k & omask) >> 1) / (unsigned long long)m.maxseg);
+            double ep[3];
+            float it;
+            src.load_end(ray, ep, it);
+            const double off[3] = {ep[0] / m.vox - (double)g[0], ep[1] / m.vox - (double)g[1],
+                                   ep[2] / m.vox - (double)g[2]};
+            fold_mean(packed, count, off);
+        }
+    }
+    l = miss_k(l, misses, m.miss32, m.cmin, m.cmax);
+    occ[sl.y] = l;
+    if (mean) {
+        mean[sl.y] = packed;
+        cnt[sl.y] = count;
+    }
+}
+
+constexpr int FOLD_SERIAL_MAX = 64;
+
+// One thread per sample voxel; voxels with long record runs are handed to
+// k_fold_occ_big (one warp each).
 template <class Src>
 __global__ void __launch_bounds__(BLOCK) k_fold_occ(const __grid_constant__ DevMap m, Src src,
-                                                    const unsigned long long *keys,
-                                                    long long R, int M) {
+                                                    const unsigned long long *keys, long long R,
+                                                    int M, const int *start, int *big,
+                                                    unsigned long long *nbig) {
+    if (!read_go(m)) return;
+    for (long long mi = (long long)blockIdx.x * blockDim.x + threadIdx.x; mi < M;
+         mi += (long long)gridDim.x * blockDim.x) {
+        const int s = start[mi];
+        const int e = mi + 1 < M ? start[mi + 1] : (int)R;
+        if (e - s > FOLD_SERIAL_MAX) {
+            big[atomicAdd(nbig, 1ULL)] = (int)mi;
+            continue;
+        }
+        fold_voxel_serial(m, src, keys, s, e, m.marked[mi]);
+    }
+}
+
+// Long runs: one warp scans 32 records at a time; misses between hits are
+// counted with ballots and applied as f_miss^k.
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_fold_occ_big(const __grid_constant__ DevMap m, Src src,
+                                                        const unsigned long long *keys, long long R,
+                                                        int M, const int *start, const int *big,
+                                                        const unsigned long long *nbig) {
     if (!read_go(m)) return;
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x / 32);
     const unsigned long long omask = (1ULL << m.order_bits) - 1;
-    for (long long mi = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; mi < M;
-         mi += warps) {
-        int2 sl = m.marked[mi];
+    const long long nb = (long long)*nbig;
+    for (long long w = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < nb;
+         w += warps) {
+        const int mi = big[w];
+        const int2 sl = m.marked[mi];
+        const int s = start[mi];
+        const int e = mi + 1 < M ? start[mi + 1] : (int)R;
         float *occ = layer_at<float>(m, L_OCC, sl.x);
         unsigned *mean = layer_at<unsigned>(m, L_MEAN, sl.x);
         unsigned *cnt = layer_at<unsigned>(m, L_COUNT, sl.x);
-        long long pos = 0;
-        if (lane == 0) pos = lower_bound_u64(keys, R, (unsigned long long)mi << m.order_bits);
-        pos = __shfl_sync(0xffffffffu, pos, 0);
         float l = occ[sl.y];
         unsigned packed = mean ? mean[sl.y] : 0u, count = cnt ? cnt[sl.y] : 0u;
         int g[3];
         slot_li_to_g(m, sl.x, sl.y, g);
-        for (;;) {
-            long long p = pos + lane;
-            unsigned long long key = p < R ? keys[p] : ~0ULL;
-            bool valid = p < R && (key >> m.order_bits) == (unsigned long long)mi;
-            unsigned vmask = __ballot_sync(0xffffffffu, valid);
-            if (!vmask) break;
-            unsigned hmask = __ballot_sync(0xffffffffu, valid && (key & 1ULL));
-            int nvalid = __popc(vmask);
+        for (int pos = s; pos < e; pos += 32) {
+            const int p = pos + lane;
+            const unsigned long long key = p < e ? keys[p] : 0ULL;
+            const unsigned hmask = __ballot_sync(0xffffffffu, p < e && (key & 1ULL));
+            const int nvalid = min(32, e - pos);
             int cur = 0;
             while (cur < nvalid) {
-                unsigned rem = cur < 32 ? (hmask >> cur) : 0u;
+                const unsigned rem = hmask >> cur;
                 if (!rem) {
                     l = miss_k(l, (unsigned)(nvalid - cur), m.miss32, m.cmin, m.cmax);
                     break;
                 }
-                int nh = cur + __ffs(rem) - 1;
+                const int nh = cur + __ffs(rem) - 1;
                 l = miss_k(l, (unsigned)(nh - cur), m.miss32, m.cmin, m.cmax);
-                unsigned long long hk = __shfl_sync(0xffffffffu, key, nh);
+                const unsigned long long hk = __shfl_sync(0xffffffffu, key, nh);
                 l = clamp_add(l, m.hit32, m.cmin, m.cmax);
                 if (mean) {
-                    long long ray = (long long)(((hk & omask) >> 1) / (unsigned long long)m.maxseg);
-                    double e[3];
+                    const long long ray = (long long)(((hk & omask) >> 1) / (unsigned long long)m.maxseg);
+                    double ep[3];
                     float it;
-                    src.load_end(ray, e, it);
-                    double off[3] = {e[0] / m.vox - (double)g[0], e[1] / m.vox - (double)g[1],
-                                     e[2] / m.vox - (double)g[2]};
+                    src.load_end(ray, ep, it);
+                    const double off[3] = {ep[0] / m.vox - (double)g[0], ep[1] / m.vox - (double)g[1],
+                                           ep[2] / m.vox - (double)g[2]};
                     fold_mean(packed, count, off);
                 }
                 cur = nh + 1;
             }
-            pos += nvalid;
-            if (nvalid < 32) break;
         }
         if (lane == 0) {
             occ[sl.y] = l;

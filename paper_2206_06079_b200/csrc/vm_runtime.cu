@@ -83,7 +83,11 @@ struct vm_map {
     size_t seg_cap = 0;
     unsigned long long *d_work = nullptr;
     int *d_rgrid = nullptr;
+    unsigned *d_ztouch = nullptr;
     int *d_rbox = nullptr;
+    int *d_start = nullptr, *d_big = nullptr;
+    size_t start_cap = 0, big_cap = 0;
+    unsigned long long *d_nbig = nullptr;
     int num_sms = 148;
     unsigned long long *d_stats = nullptr;
     int *d_go = nullptr;
@@ -154,6 +158,7 @@ DevMap make_dm(const vm_map *m) {
         d.brick_shift = bs;
     }
     d.rgrid = m->d_rgrid;
+    d.ztouch = m->d_ztouch;
     d.rbox = m->d_rbox;
     d.rg_max = RG_MAX;
     d.segs = m->d_segs;
@@ -295,9 +300,21 @@ int launch_fold(vm_map *m, const DevMap &dm, const Src &src, const unsigned long
     cudaStream_t s = m->stream;
     const unsigned grid_cap = 148 * 16;
     if (mode == M_OCC || mode == M_DECAY) {
-        unsigned g = (unsigned)std::min<long long>((M + 7) / 8, grid_cap);
-        if (g) k_fold_occ<<<g, BLOCK, 0, s>>>(dm, src, keys, R, (int)M);
-        m->launches += g ? 1 : 0;
+        if (M > 0) {
+            int rc = ensure_buf(&m->d_start, &m->start_cap, (size_t)M + 1);
+            if (rc) return rc;
+            rc = ensure_buf(&m->d_big, &m->big_cap, (size_t)M + 1);
+            if (rc) return rc;
+            cudaMemsetAsync(m->d_nbig, 0, sizeof(unsigned long long), s);
+            unsigned gh = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
+            k_heads<<<gh, BLOCK, 0, s>>>(dm, keys, R, m->d_start);
+            unsigned g = (unsigned)std::min<long long>((M + BLOCK - 1) / BLOCK, grid_cap);
+            k_fold_occ<<<g, BLOCK, 0, s>>>(dm, src, keys, R, (int)M, m->d_start, m->d_big,
+                                           m->d_nbig);
+            k_fold_occ_big<<<m->num_sms * 2, BLOCK, 0, s>>>(dm, src, keys, R, (int)M, m->d_start,
+                                                            m->d_big, m->d_nbig);
+            m->launches += 3;
+        }
     } else if (mode == M_NDT_OM || mode == M_NDT_TM) {
         unsigned g = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
         if (g) {
@@ -364,6 +381,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             static const int box_init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
             CK(cudaMemcpyAsync(m->d_rbox, box_init, sizeof(box_init), cudaMemcpyHostToDevice,
                                m->stream));
+            CK(cudaMemsetAsync(m->d_ztouch, 0, RG_MAX * sizeof(unsigned), m->stream));
         }
         CK(cudaEventRecord(m->ev_start, m->stream));
         dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK));
@@ -581,7 +599,9 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         (rc = dev_alloc(&m->d_slot_pref, m->max_slots)) || (rc = dev_alloc(&m->d_stats, NUM_STATS)) ||
         (rc = dev_alloc(&m->d_go, 1)) || (rc = dev_alloc(&m->d_touched, m->max_slots)) ||
         (rc = dev_alloc(&m->d_bmask, m->max_slots)) || (rc = dev_alloc(&m->d_work, 1)) ||
-        (rc = dev_alloc(&m->d_rgrid, RG_MAX)) || (rc = dev_alloc(&m->d_rbox, 6)))
+        (rc = dev_alloc(&m->d_rgrid, RG_MAX)) || (rc = dev_alloc(&m->d_rbox, 6)) ||
+        (rc = dev_alloc(&m->d_ztouch, RG_MAX)) ||
+        (rc = dev_alloc(&m->d_nbig, 1)))
         return cleanup(rc);
     for (int l = 0; l < NUM_LAYERS; ++l)
         if (m->bpr[l] && (rc = dev_alloc(&m->d_lptr[l], m->max_slots))) return cleanup(rc);
@@ -620,6 +640,10 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_segs);
     cudaFree(m->d_work);
     cudaFree(m->d_rgrid);
+    cudaFree(m->d_ztouch);
+    cudaFree(m->d_start);
+    cudaFree(m->d_big);
+    cudaFree(m->d_nbig);
     cudaFree(m->d_rbox);
     cudaFree(m->d_stats);
     cudaFree(m->d_go);

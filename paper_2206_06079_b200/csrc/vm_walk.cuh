@@ -33,6 +33,7 @@ namespace vm {
 
 constexpr int WK_STAGE = 3072;  // staged records per block (24 KiB)
 constexpr int RG_MAX = 4096;    // dense region grid cells held in smem (32 KiB)
+constexpr int WK_INNER = 8;     // DDA steps between warp-level work bookkeeping
 
 struct WalkSmem {
     unsigned cube[CUBE_N];
@@ -117,18 +118,37 @@ __global__ void __launch_bounds__(BLOCK, 2) k_walk(const __grid_constant__ DevMa
     // segment state
     double tx = 0, ty = 0, tz = 0, dx = 0, dy = 0, dz = 0, tprev = 0, L = 0;
     int cx = 0, cy = 0, cz = 0, ex = 0, ey = 0, ez = 0, remaining = 0;
-    int lx = 0, ly = 0, lz = 0, rx = 0, ry = 0, rz = 0, slot = -1;
+    int lx = 0, ly = 0, lz = 0, rx = 0, ry = 0, rz = 0;
     unsigned codes = 0, order = 0, bm = 0;
+    int cube_left = 0;          // steps the segment may still spend in the smem cube
     bool active = false;
-    // pipelined visit (issued loads, finished next iteration)
+    // current region: base pointers (null when the region is unavailable)
+    unsigned *scr_r = nullptr;
+    float *occ_r = nullptr;
+    const unsigned *mk_r = nullptr;
+    int slot = -1;
+    // pipelined visit (issued loads, finished next step)
     bool pend = false;
-    unsigned long long p_vidx = 0;
-    unsigned p_key = 0, p_w1 = 0, p_w2 = 0;
-    int p_cube = -1, p_li = 0;
+    unsigned *p_scr = nullptr;  // counter word (det) / log-odds word (cas)
+    unsigned p_key = 0, p_w1 = 0, p_w2 = 0, p_bit = 0;
+    int p_cube = -1;
     // prefetch + warp work pool
     bool pf_valid = false, exhausted = false;
     unsigned long long pool_next = 0, pool_end = 0;
     SegDesc *my_pf = &sm.pf[threadIdx.x];
+
+    auto set_region = [&](unsigned long long e) {
+        slot = (int)(unsigned)e;
+        bm = (unsigned)(e >> 32);
+        if ((unsigned)slot < (unsigned)cap) {
+            const unsigned long long base = (unsigned long long)slot * vpr;
+            scr_r = scr_base + base;
+            occ_r = occ_base + base;
+            mk_r = m.marks + (size_t)slot * m.mark_words;
+        } else {
+            scr_r = nullptr;
+        }
+    };
 
     for (;;) {
         // ---- claim work for lanes without a prefetched descriptor ----
@@ -166,158 +186,170 @@ __global__ void __launch_bounds__(BLOCK, 2) k_walk(const __grid_constant__ DevMa
             pool_next += __popc(served_mask);
             need &= ~served_mask;
         }
-        // ---- idle lanes start their prefetched segment ----
-        if (!active && pf_valid) {
-            __pipeline_wait_prior(0);
-            const SegDesc &d = *my_pf;
-            tx = d.t[0]; ty = d.t[1]; tz = d.t[2];
-            dx = d.d[0]; dy = d.d[1]; dz = d.d[2];
-            cx = d.c[0]; cy = d.c[1]; cz = d.c[2];
-            ex = d.e[0]; ey = d.e[1]; ez = d.e[2];
-            codes = d.flags;
-            order = d.order;
-            L = d.L;
-            lx = (int)(d.local0 & 1023u);
-            ly = (int)((d.local0 >> 10) & 1023u);
-            lz = (int)(d.local0 >> 20);
-            rx = d.r0[0]; ry = d.r0[1]; rz = d.r0[2];
-            tprev = 0.0;
-            remaining = abs(cx - ex) + abs(cy - ey) + abs(cz - ez);
-            const unsigned long long e = region_entry(m, sm, gv, rx, ry, rz);
-            slot = (int)(unsigned)e;
-            bm = (unsigned)(e >> 32);
-            pf_valid = false;
-            active = true;
-        }
         if (!__any_sync(0xffffffffu, active || pf_valid || !exhausted || pend)) break;
 
-        // ---- finish the visit pipelined from the previous iteration ----
-        if (pend) {
-            pend = false;
-            if (DET) {
-                if ((p_w1 >> (p_li & 31)) & 1u) {
-                    const unsigned long long key =
-                        ((unsigned long long)(p_w2 & ~MARK_FLAG) << m.order_bits) | p_key;
-                    const int k = atomicAdd(&sm.nrec, 1);
-                    if (k < WK_STAGE) {
-                        sm.rec[k] = key;
-                    } else {
-                        const unsigned long long g = atomicAdd(m.stats + S_RECORDS, 1ULL);
-                        if (g < m.rec_cap) m.rec[g] = key;
+        // ---- up to WK_INNER steps without warp-level bookkeeping ----
+#pragma unroll 1
+        for (int inner = 0; inner < WK_INNER; ++inner) {
+            // idle lanes start their prefetched segment
+            if (!active && pf_valid) {
+                __pipeline_wait_prior(0);
+                const SegDesc &d = *my_pf;
+                tx = d.t[0]; ty = d.t[1]; tz = d.t[2];
+                dx = d.d[0]; dy = d.d[1]; dz = d.d[2];
+                cx = d.c[0]; cy = d.c[1]; cz = d.c[2];
+                ex = d.e[0]; ey = d.e[1]; ez = d.e[2];
+                codes = d.flags;
+                order = d.order;
+                L = d.L;
+                lx = (int)(d.local0 & 1023u);
+                ly = (int)((d.local0 >> 10) & 1023u);
+                lz = (int)(d.local0 >> 20);
+                rx = d.r0[0]; ry = d.r0[1]; rz = d.r0[2];
+                tprev = 0.0;
+                remaining = abs(cx - ex) + abs(cy - ey) + abs(cz - ez);
+                set_region(region_entry(m, sm, gv, rx, ry, rz));
+                // a straight segment leaves the (convex) cube within 3*CUBE steps
+                // and never re-enters it
+                const unsigned ux = (unsigned)(cx - c0), uy = (unsigned)(cy - c1),
+                               uz = (unsigned)(cz - c2);
+                cube_left = (ux | uy | uz) < (unsigned)CUBE ? 3 * CUBE : 0;
+                pf_valid = false;
+                active = true;
+            }
+            // finish the visit pipelined from the previous step
+            if (pend) {
+                pend = false;
+                if (DET) {
+                    if (p_w1 & p_bit) {
+                        const unsigned long long key =
+                            ((unsigned long long)(p_w2 & ~MARK_FLAG) << m.order_bits) | p_key;
+                        const int k = atomicAdd(&sm.nrec, 1);
+                        if (k < WK_STAGE) {
+                            sm.rec[k] = key;
+                        } else {
+                            const unsigned long long g = atomicAdd(m.stats + S_RECORDS, 1ULL);
+                            if (g < m.rec_cap) m.rec[g] = key;
+                        }
+                    } else if (!REC_ONLY) {
+                        if (p_cube >= 0) atomicAdd(sm.cube + p_cube, 1u);
+                        else red_add(p_scr, 1u);
                     }
-                } else if (!REC_ONLY) {
-                    if (p_cube >= 0) atomicAdd(sm.cube + p_cube, 1u);
-                    else red_add(scr_base + p_vidx, 1u);
-                }
-            } else {
-                unsigned old = p_w1;
-                for (;;) {
-                    const unsigned nb =
-                        __float_as_uint(clamp_add(__uint_as_float(old), m.miss32, m.cmin, m.cmax));
-                    if (nb == old) break;
-                    const unsigned prev =
-                        atomicCAS(reinterpret_cast<unsigned *>(occ_base + p_vidx), old, nb);
-                    if (prev == old) break;
-                    old = prev;
-                    ++retries;
+                } else {
+                    unsigned old = p_w1;
+                    for (;;) {
+                        const unsigned nb = __float_as_uint(
+                            clamp_add(__uint_as_float(old), m.miss32, m.cmin, m.cmax));
+                        if (nb == old) break;
+                        const unsigned prev = atomicCAS(p_scr, old, nb);
+                        if (prev == old) break;
+                        old = prev;
+                        ++retries;
+                    }
                 }
             }
-        }
-        if (!active) continue;
+            if (!active) continue;
 
-        // ---- one DDA step = one voxel visit ----
-        bool last = remaining == 0;
-        if (last && !(cx == ex && cy == ey && cz == ez)) {
-            // numerical fallback: the walk jumps to the end cell (traversal.py:88-92)
-            cx = ex;
-            cy = ey;
-            cz = ez;
-            rx = floordiv(cx, dim);
-            ry = floordiv(cy, dim);
-            rz = floordiv(cz, dim);
-            lx = cx - rx * dim;
-            ly = cy - ry * dim;
-            lz = cz - rz * dim;
-            const unsigned long long e = region_entry(m, sm, gv, rx, ry, rz);
-            slot = (int)(unsigned)e;
-            bm = (unsigned)(e >> 32);
-        }
-        // axis = 0; if tmax[1] < tmax[axis]: 1; if tmax[2] < tmax[axis]: 2
-        const bool py = ty < tx;
-        const double ta = py ? ty : tx;
-        const bool pz = tz < ta;
-        double t1 = 1.0;
-        if (MODE == M_DECAY && !last) {
-            t1 = pz ? tz : ta;
-            if (t1 < tprev) t1 = tprev;
-            if (t1 > 1.0) t1 = 1.0;
-        }
-        ++visits;
-        if ((unsigned)slot >= (unsigned)cap) {
-            ++rmiss;
-        } else {
-            const int li = lx + dim * (ly + dim * lz);
-            const unsigned long long vidx = (unsigned long long)slot * vpr + (unsigned)li;
-            const bool hit = last && (codes & 1u);
-            if (MODE == M_DECAY && !REC_ONLY) {
-                red_add(reinterpret_cast<double *>(m.slab[L_DDIST]) + vidx, (t1 - tprev) * L);
-                if (hit) red_add(reinterpret_cast<unsigned *>(m.slab[L_DHITS]) + vidx, 1u);
+            // ---- one DDA step = one voxel visit ----
+            const bool last = remaining == 0;
+            if (last && !(cx == ex && cy == ey && cz == ez)) {
+                // numerical fallback: the walk jumps to the end cell (traversal.py:88-92)
+                cx = ex;
+                cy = ey;
+                cz = ez;
+                rx = floordiv(cx, dim);
+                ry = floordiv(cy, dim);
+                rz = floordiv(cz, dim);
+                lx = cx - rx * dim;
+                ly = cy - ry * dim;
+                lz = cz - rz * dim;
+                set_region(region_entry(m, sm, gv, rx, ry, rz));
+                cube_left = 1;
             }
-            const unsigned ux = (unsigned)(cx - c0), uy = (unsigned)(cy - c1),
-                           uz = (unsigned)(cz - c2);
-            const int cube = (ux | uy | uz) < (unsigned)CUBE ? (int)(ux + CUBE * (uy + CUBE * uz)) : -1;
-            if (DET) {
-                const int b = bs >= 0 ? brick32(lx, ly, lz, bs) : 0;
-                if ((bm >> b) & 1u) {
-                    pend = true;
-                    p_vidx = vidx;
-                    p_li = li;
-                    p_key = order | (hit ? 1u : 0u);
-                    p_cube = cube;
-                    p_w1 = __ldg(m.marks + (size_t)slot * m.mark_words + ((unsigned)li >> 5));
-                    p_w2 = __ldcg(scr_base + vidx);
-                } else if (!REC_ONLY) {
-                    if (cube >= 0) atomicAdd(sm.cube + cube, 1u);
-                    else red_add(scr_base + vidx, 1u);
-                }
-            } else if (hit) {
-                float *p = occ_base + vidx;
-                unsigned old = __float_as_uint(__ldcg(p));
-                for (;;) {
-                    const unsigned nb =
-                        __float_as_uint(clamp_add(__uint_as_float(old), m.hit32, m.cmin, m.cmax));
-                    if (nb == old) break;
-                    const unsigned prev = atomicCAS(reinterpret_cast<unsigned *>(p), old, nb);
-                    if (prev == old) break;
-                    old = prev;
-                    ++retries;
-                }
-                if (m.slab[L_MEAN]) {
-                    // a hit ends a has_sample segment: its end is the ray end
-                    double e[3];
-                    float it;
-                    src.load_end((long long)((order >> 1) / (unsigned)m.maxseg), e, it);
-                    const double off[3] = {e[0] / m.vox - (double)cx, e[1] / m.vox - (double)cy,
-                                           e[2] / m.vox - (double)cz};
-                    retries += cas_mean(reinterpret_cast<unsigned *>(m.slab[L_MEAN]) + vidx,
-                                        reinterpret_cast<unsigned *>(m.slab[L_COUNT]) + vidx, off);
-                }
-            } else if (cube >= 0) {
-                atomicAdd(sm.cube + cube, 1u);
+            // axis = 0; if tmax[1] < tmax[axis]: 1; if tmax[2] < tmax[axis]: 2
+            const bool py = ty < tx;
+            const double ta = py ? ty : tx;
+            const bool pz = tz < ta;
+            double t1 = 1.0;
+            if (MODE == M_DECAY && !last) {
+                t1 = pz ? tz : ta;
+                if (t1 < tprev) t1 = tprev;
+                if (t1 > 1.0) t1 = 1.0;
+            }
+            ++visits;
+            if (!scr_r) {
+                ++rmiss;
             } else {
-                pend = true;
-                p_vidx = vidx;
-                p_w1 = __float_as_uint(__ldcg(occ_base + vidx));
+                const int li = lx + dim * (ly + dim * lz);
+                const bool hit = last && (codes & 1u);
+                if (MODE == M_DECAY && !REC_ONLY) {
+                    const unsigned long long vidx = (unsigned long long)slot * vpr + (unsigned)li;
+                    red_add(reinterpret_cast<double *>(m.slab[L_DDIST]) + vidx, (t1 - tprev) * L);
+                    if (hit) red_add(reinterpret_cast<unsigned *>(m.slab[L_DHITS]) + vidx, 1u);
+                }
+                int cube = -1;
+                if (cube_left > 0) {
+                    const unsigned ux = (unsigned)(cx - c0), uy = (unsigned)(cy - c1),
+                                   uz = (unsigned)(cz - c2);
+                    if ((ux | uy | uz) < (unsigned)CUBE) {
+                        cube = (int)(ux + CUBE * (uy + CUBE * uz));
+                        --cube_left;
+                    } else {
+                        cube_left = 0;  // left the cube for good
+                    }
+                }
+                if (DET) {
+                    const int b = bs >= 0 ? brick32(lx, ly, lz, bs) : 0;
+                    if ((bm >> b) & 1u) {
+                        pend = true;
+                        p_scr = scr_r + li;
+                        p_bit = 1u << (li & 31);
+                        p_key = order | (hit ? 1u : 0u);
+                        p_cube = cube;
+                        p_w1 = __ldg(mk_r + ((unsigned)li >> 5));
+                        p_w2 = __ldcg(scr_r + li);
+                    } else if (!REC_ONLY) {
+                        if (cube >= 0) atomicAdd(sm.cube + cube, 1u);
+                        else red_add(scr_r + li, 1u);
+                    }
+                } else if (hit) {
+                    float *p = occ_r + li;
+                    unsigned old = __float_as_uint(__ldcg(p));
+                    for (;;) {
+                        const unsigned nb = __float_as_uint(
+                            clamp_add(__uint_as_float(old), m.hit32, m.cmin, m.cmax));
+                        if (nb == old) break;
+                        const unsigned prev = atomicCAS(reinterpret_cast<unsigned *>(p), old, nb);
+                        if (prev == old) break;
+                        old = prev;
+                        ++retries;
+                    }
+                    if (m.slab[L_MEAN]) {
+                        // a hit ends a has_sample segment: its end is the ray end
+                        double e[3];
+                        float it;
+                        src.load_end((long long)((order >> 1) / (unsigned)m.maxseg), e, it);
+                        const double off[3] = {e[0] / m.vox - (double)cx, e[1] / m.vox - (double)cy,
+                                               e[2] / m.vox - (double)cz};
+                        const unsigned long long vidx = (unsigned long long)slot * vpr + (unsigned)li;
+                        retries += cas_mean(reinterpret_cast<unsigned *>(m.slab[L_MEAN]) + vidx,
+                                            reinterpret_cast<unsigned *>(m.slab[L_COUNT]) + vidx, off);
+                    }
+                } else if (cube >= 0) {
+                    atomicAdd(sm.cube + cube, 1u);
+                } else {
+                    pend = true;
+                    p_scr = reinterpret_cast<unsigned *>(occ_r + li);
+                    p_w1 = __float_as_uint(__ldcg(occ_r + li));
+                }
             }
-        }
-        if (last) {
-            active = false;
-            continue;
-        }
-        // ---- advance (t_max[axis] += t_delta[axis]), branch-free ----
-        tprev = t1;
-        --remaining;
-        {
+            if (last) {
+                active = false;
+                continue;
+            }
+            // ---- advance (t_max[axis] += t_delta[axis]), branch-free ----
+            tprev = t1;
+            --remaining;
             const bool ax = !py && !pz, ay = py && !pz;
             const int shift = pz ? 5 : (py ? 3 : 1);
             const int st = (int)((codes >> shift) & 3u) - 1;
@@ -338,9 +370,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_walk(const __grid_constant__ DevMa
                 if (ax) { lx = wrapped; rx += st; }
                 if (ay) { ly = wrapped; ry += st; }
                 if (pz) { lz = wrapped; rz += st; }
-                const unsigned long long e = region_entry(m, sm, gv, rx, ry, rz);
-                slot = (int)(unsigned)e;
-                bm = (unsigned)(e >> 32);
+                set_region(region_entry(m, sm, gv, rx, ry, rz));
             }
         }
     }

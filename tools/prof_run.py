@@ -17,7 +17,8 @@ a = ap.parse_args()
 if a.workload == "c1":
     cfg, mode, data = MapConfig(), "occupancy", [scans.os64_room_scan()] * a.batches
 elif a.workload == "c2":
-    cfg, mode, data = MapConfig(voxel_size=0.05), "occupancy", scans.os128_canyon_batches(a.batches)
+    cfg, mode = MapConfig(voxel_size=0.05), "occupancy"
+    data = scans.batch_by_period(np.concatenate(scans.os128_canyon_batches(a.batches)))
 else:
     cfg, mode, data = MapConfig(), "ndt-om", scans.os64_tunnel_scans(a.batches)
 vm = VoxelMap(cfg, MODE_LAYERS[mode], initial_regions=4096)
