@@ -259,3 +259,24 @@ def walk_voxels_native(ox, oy, oz, ex, ey, ez, cell):
 def hash_mix(key: int) -> int:
     """_kernels.hash_mix (_kernels.pyx:127-129)."""
     return int(lib().vm_hash_mix(int(key)))
+
+
+def kernels_integrate_occupancy(origins, ends, has_sample, n, tkeys, tvals, tsize, occ_ptrs,
+                                mean_ptrs, count_ptrs, dhit_ptrs, ddist_ptrs, voxel_size,
+                                region_dim, hit_delta, miss_delta, clamp_min, clamp_max,
+                                retry_limit, walk_cap, stream=0):
+    """_kernels.integrate_occupancy (_kernels.pyx:376-470) on the GPU.
+
+    Every array argument is a DEVICE pointer (int); pass 0 for an absent
+    mean/count or decay pointer array, like the reference's empty arrays
+    (_kernels.pyx:393-394).  Returns (cas_retries, cas_failures,
+    region_misses, visits)."""
+    st = (ctypes.c_int64 * 4)()
+    P = ctypes.c_void_p
+    check(lib().vm_kernels_integrate_occupancy(
+        P(origins), P(ends), P(has_sample), int(n), P(tkeys), P(tvals), int(tsize), P(occ_ptrs),
+        P(mean_ptrs or 0), P(count_ptrs or 0), P(dhit_ptrs or 0), P(ddist_ptrs or 0),
+        float(voxel_size), int(region_dim), float(hit_delta), float(miss_delta),
+        float(clamp_min), float(clamp_max), int(retry_limit), int(walk_cap),
+        ctypes.cast(st, P), P(stream or 0)), "vm_kernels_integrate_occupancy")
+    return tuple(int(x) for x in st)

@@ -90,6 +90,7 @@ struct DevMap {
     int *go;                             // batch guard (0 = skip, replay later)
     // batch outputs
     unsigned long long *rec;
+    unsigned *recval;                    // per-record value (NDT deterministic phase 1)
     unsigned long long rec_cap;
     int2 *marked;                        // (slot, li) of sample voxels
     int marked_cap;

@@ -310,7 +310,8 @@ struct PrefetchVisitor {
 
 template <class Src>
 __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevMap m, Src src,
-                                                    long long n, int mode, int det, int emit) {
+                                                    long long n, int mode, int det, int emit,
+                                                    int count_stats = 1) {
     __shared__ unsigned long long kcache[KCACHE];
     __shared__ int sset[SLOTSET];
     __shared__ int2 smark[BLOCK];
@@ -436,7 +437,8 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                         unsigned long long order =
                             ((unsigned long long)(i * m.maxseg + s) << 1) | 1ULL;
                         int k = atomicAdd(&nrec, 1);
-                        srec[k] = (vid << m.order_bits) | order;
+                        // phase bit 1: after every phase-1 record of the voxel
+                        srec[k] = (vid << (m.order_bits + 1)) | (1ULL << m.order_bits) | order;
                     } else {
                         unsigned bit = 1u << (li & 31);
                         unsigned old = atomicOr(
@@ -473,10 +475,13 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     }
     for (int k = threadIdx.x; k < nrec; k += blockDim.x) {
         unsigned long long ri = rec_base + k;
-        if (ri < m.rec_cap) m.rec[ri] = srec[k];
+        if (ri < m.rec_cap) {
+            m.rec[ri] = srec[k];
+            if (m.recval) m.recval[ri] = 0u;
+        }
     }
     const int which[3] = {S_PROCESSED, S_SEGMENTS, S_RANGE_ERR};
-    block_add_stats(m, st, which);
+    if (count_stats) block_add_stats(m, st, which);
     // batch bounding box of prefetched regions (+1 margin for walk-entered ones)
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -532,7 +537,19 @@ __global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
 
 // --------------------------------------------------------------- NDT phase 1
 
-template <bool TM>
+// Deterministic NDT phase 1: a miss on a Gaussian voxel (count >= 3 at the
+// start of the batch; the walk never resets in this mode) becomes a record
+// (voxel | phase 0 | ray order) -> value = |fl32(g * miss_delta)| bits with
+// bit 31 = (g >= miss-likelihood threshold), folded in ray order by
+// k_fold_ndt together with the reset (reference.py:67-94).
+struct NdtRecStage {
+    unsigned long long *key;
+    unsigned *val;
+    int *n;
+};
+constexpr int NDT_STAGE = 1536;
+
+template <bool TM, bool DET = false, bool REC_ONLY = false>
 struct NdtVisitor {
     const DevMap *m;
     RegionTrack rt;
@@ -545,6 +562,8 @@ struct NdtVisitor {
     int *sset;
     unsigned *cube;
     int c0, c1, c2;
+    unsigned order;
+    NdtRecStage st;
     unsigned long long visits, rmiss, retries;
 
     __device__ __forceinline__ void bind() {
@@ -587,6 +606,7 @@ struct NdtVisitor {
         const int li = rt.li(*m);
         unsigned ns = __ldcg(cnt + li);
         if (ns < 3) {
+            if (REC_ONLY) return;
             // g == 1: identical deltas, order-free -> counted, resolved exactly
             unsigned ux = (unsigned)(x - c0), uy = (unsigned)(y - c1), uz = (unsigned)(z - c2);
             if ((ux | uy | uz) < (unsigned)CUBE)
@@ -606,6 +626,24 @@ struct NdtVisitor {
         mu[2] = ((double)z + off[2]) * m->vox;
         double gw = gaussian_weight(mu, c6, m->sigma2, so, v, t0, t1);
         float d32 = (float)(gw * m->miss_delta);
+        if (DET) {
+            const unsigned long long vid = (unsigned long long)rt.slot * m->vpr + li;
+            const unsigned val = (__float_as_uint(d32) & 0x7FFFFFFFu) |
+                                 (gw >= m->miss_check ? 0x80000000u : 0u);
+            const unsigned long long key = (vid << (m->order_bits + 1)) | order;
+            const int k = atomicAdd(st.n, 1);
+            if (k < NDT_STAGE) {
+                st.key[k] = key;
+                st.val[k] = val;
+            } else {
+                const unsigned long long g = atomicAdd(m->stats + S_RECORDS, 1ULL);
+                if (g < m->rec_cap) {
+                    m->rec[g] = key;
+                    m->recval[g] = val;
+                }
+            }
+            return;
+        }
         {
             float *p = occ + li;
             unsigned old = __float_as_uint(__ldcg(p));
@@ -636,11 +674,15 @@ struct NdtVisitor {
     }
 };
 
-template <bool TM, class Src>
+template <bool TM, bool DET, bool REC_ONLY, class Src>
 __global__ void __launch_bounds__(BLOCK) k_walk_ndt(const __grid_constant__ DevMap m, Src src, long long n) {
     __shared__ unsigned cube[CUBE_N];
     __shared__ int sset[SLOTSET];
     __shared__ int corner[3];
+    __shared__ unsigned long long skey[DET ? NDT_STAGE : 1];
+    __shared__ unsigned sval[DET ? NDT_STAGE : 1];
+    __shared__ int nrec;
+    __shared__ unsigned long long rec_base;
     if (!read_go(m)) return;
     for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) cube[k] = 0;
     for (int k = threadIdx.x; k < SLOTSET; k += blockDim.x) sset[k] = -1;
@@ -651,15 +693,17 @@ __global__ void __launch_bounds__(BLOCK) k_walk_ndt(const __grid_constant__ DevM
         float it;
         src.load(first, o, e, h, it);
         for (int a = 0; a < 3; ++a) corner[a] = (int)floor(o[a] / m.vox) - CUBE / 2;
+        nrec = 0;
     }
     __syncthreads();
-    NdtVisitor<TM> v;
+    NdtVisitor<TM, DET, REC_ONLY> v;
     v.m = &m;
     v.sset = sset;
     v.cube = cube;
     v.c0 = corner[0];
     v.c1 = corner[1];
     v.c2 = corner[2];
+    v.st = NdtRecStage{skey, sval, &nrec};
     v.visits = v.rmiss = v.retries = 0;
     long long i = first + threadIdx.x;
     if (i < n) {
@@ -670,12 +714,26 @@ __global__ void __launch_bounds__(BLOCK) k_walk_ndt(const __grid_constant__ DevM
                 double so[3], se[3];
                 segment_of(m, r, s, so, se, v.sh);
                 v.so = so;
+                v.order = (unsigned)(i * m.maxseg + s) << 1;
                 for (int a = 0; a < 3; ++a) v.v[a] = se[a] - so[a];
                 walk(so, se, m.vox, v);
             }
         }
     }
     __syncthreads();
+    if (DET) {
+        const int nl = nrec < NDT_STAGE ? nrec : NDT_STAGE;
+        if (threadIdx.x == 0 && nl) rec_base = atomicAdd(m.stats + S_RECORDS, (unsigned long long)nl);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nl; k += blockDim.x) {
+            const unsigned long long ri = rec_base + k;
+            if (ri < m.rec_cap) {
+                m.rec[ri] = skey[k];
+                m.recval[ri] = sval[k];
+            }
+        }
+    }
+    if (REC_ONLY) return;
     unsigned long long flushed = 0;
     for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) {
         unsigned cnt = cube[k];
@@ -1088,17 +1146,25 @@ __global__ void __launch_bounds__(BLOCK) k_fold_occ_big(const __grid_constant__ 
     }
 }
 
-// NDT phase 2 (reference.py:107-150): one thread per sample voxel folds its
-// samples in ray order; f64 Welford mean + Givens sqrt-covariance.
+// NDT in ray order, one thread per voxel run of the sorted records
+// (key = voxel | phase | ray order):
+//  * phase 0 (deterministic mode only): the phase-1 misses of a Gaussian
+//    voxel with their weights, including the transient reset and the TM miss
+//    count (reference.py:67-94; after a reset the voxel has < 3 samples, so
+//    the remaining misses use g = 1);
+//  * phase 1: NDT phase 2 (reference.py:107-150): the voxel's samples in ray
+//    order, f64 Welford mean + Givens sqrt-covariance.
 template <bool TM, class Src>
 __global__ void __launch_bounds__(BLOCK) k_fold_ndt(const __grid_constant__ DevMap m, Src src,
-                                                    const unsigned long long *keys, long long R) {
+                                                    const unsigned long long *keys,
+                                                    const unsigned *vals, long long R) {
     if (!read_go(m)) return;
     const unsigned long long omask = (1ULL << m.order_bits) - 1;
+    const int vshift = m.order_bits + 1;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
          i += (long long)gridDim.x * blockDim.x) {
-        unsigned long long vid = keys[i] >> m.order_bits;
-        if (i > 0 && (keys[i - 1] >> m.order_bits) == vid) continue;
+        unsigned long long vid = keys[i] >> vshift;
+        if (i > 0 && (keys[i - 1] >> vshift) == vid) continue;
         int slot = (int)(vid / (unsigned long long)m.vpr), li = (int)(vid % (unsigned long long)m.vpr);
         int g[3];
         slot_li_to_g(m, slot, li, g);
@@ -1106,49 +1172,79 @@ __global__ void __launch_bounds__(BLOCK) k_fold_ndt(const __grid_constant__ DevM
         unsigned *mb = layer_at<unsigned>(m, L_MEAN, slot);
         unsigned *cb = layer_at<unsigned>(m, L_COUNT, slot);
         float *cov = layer_at<float>(m, L_COV, slot);
-        unsigned long long nsamp = cb[li];
-        double mu[3] = {0.0, 0.0, 0.0};
-        if (nsamp > 0) {
-            double off[3];
-            unpack_mean(mb[li], off);
-            for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
-        }
-        double S[6];
-        for (int k = 0; k < 6; ++k) S[k] = cov[li * 6 + k];
-        float l = occ[li];
         float *ib = TM ? layer_at<float>(m, L_INTENS, slot) : nullptr;
+        unsigned *hb = TM ? layer_at<unsigned>(m, L_HIT, slot) : nullptr;
+        unsigned *missb = TM ? layer_at<unsigned>(m, L_MISS, slot) : nullptr;
+        float l = occ[li];
         long long j = i;
-        for (; j < R && (keys[j] >> m.order_bits) == vid; ++j) {
-            long long ray = (long long)(((keys[j] & omask) >> 1) / (unsigned long long)m.maxseg);
-            double e[3];
-            float it;
-            src.load_end(ray, e, it);
-            l = clamp_add(l, m.hit32, m.cmin, m.cmax);
-            if (TM) {
-                // ndt.update_intensity (ndt.py:98-106), stored f32 each sample
-                double val = it, imean = ib[li * 2], m2 = ib[li * 2 + 1];
-                double nn = (double)(nsamp + 1);
-                double d = val - imean;
-                double mnew = imean + d / nn;
-                double m2new = m2 + d * (val - mnew);
-                ib[li * 2] = (float)mnew;
-                ib[li * 2 + 1] = (float)m2new;
+        // ---- phase-1 records (deterministic mode) ----
+        bool reset = false;
+        unsigned miss_add = 0;
+        for (; j < R && (keys[j] >> vshift) == vid && !((keys[j] >> m.order_bits) & 1ULL); ++j) {
+            const unsigned v = vals[j];
+            const float d = reset ? m.miss32 : -__uint_as_float(v & 0x7FFFFFFFu);
+            l = clamp_add(l, d, m.cmin, m.cmax);
+            if (TM && (reset || (v >> 31))) ++miss_add;
+            if (!reset && l < m.fthresh && cb[li] > 0) {
+                reset = true;
+                miss_add = 0;
+                cb[li] = 0;
+                mb[li] = 0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) cov[li * 6 + k] = 0.0f;
+                if (TM) {
+                    hb[li] = 0;
+                    missb[li] = 0;
+                    ib[li * 2] = 0.0f;
+                    ib[li * 2 + 1] = 0.0f;
+                }
             }
-            update_gaussian(nsamp, mu, S, e);
+        }
+        if (TM && miss_add) missb[li] += miss_add;
+        if (j == i || (j < R && (keys[j] >> vshift) == vid)) {
+            // ---- phase-2 samples ----
+            unsigned long long nsamp = cb[li];
+            double mu[3] = {0.0, 0.0, 0.0};
+            if (nsamp > 0) {
+                double off[3];
+                unpack_mean(mb[li], off);
+                for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
+            }
+            double S[6];
+            for (int k = 0; k < 6; ++k) S[k] = cov[li * 6 + k];
+            const long long h0 = j;
+            for (; j < R && (keys[j] >> vshift) == vid; ++j) {
+                long long ray = (long long)(((keys[j] & omask) >> 1) / (unsigned long long)m.maxseg);
+                double e[3];
+                float it;
+                src.load_end(ray, e, it);
+                l = clamp_add(l, m.hit32, m.cmin, m.cmax);
+                if (TM) {
+                    // ndt.update_intensity (ndt.py:98-106), stored f32 each sample
+                    double val = it, imean = ib[li * 2], m2 = ib[li * 2 + 1];
+                    double nn = (double)(nsamp + 1);
+                    double d = val - imean;
+                    double mnew = imean + d / nn;
+                    double m2new = m2 + d * (val - mnew);
+                    ib[li * 2] = (float)mnew;
+                    ib[li * 2 + 1] = (float)m2new;
+                }
+                update_gaussian(nsamp, mu, S, e);
+            }
+            if (TM) hb[li] += (unsigned)(j - h0);
+            cb[li] = nsamp > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)nsamp;
+            double frac[3];
+            const double hi = 1.0 - 1.0 / 2048.0;
+            for (int a = 0; a < 3; ++a) {
+                double f = mu[a] / m.vox - (double)g[a];
+                if (f < 0.0) f = 0.0;
+                if (f > hi) f = hi;
+                frac[a] = f;
+            }
+            mb[li] = pack_mean(frac);
+            for (int k = 0; k < 6; ++k) cov[li * 6 + k] = (float)S[k];
         }
         occ[li] = l;
-        if (TM) layer_at<unsigned>(m, L_HIT, slot)[li] += (unsigned)(j - i);
-        cb[li] = nsamp > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)nsamp;
-        double frac[3];
-        const double hi = 1.0 - 1.0 / 2048.0;
-        for (int a = 0; a < 3; ++a) {
-            double f = mu[a] / m.vox - (double)g[a];
-            if (f < 0.0) f = 0.0;
-            if (f > hi) f = hi;
-            frac[a] = f;
-        }
-        mb[li] = pack_mean(frac);
-        for (int k = 0; k < 6; ++k) cov[li * 6 + k] = (float)S[k];
     }
 }
 

@@ -17,6 +17,7 @@
 
 #include "../../include/voxmap_b200.h"
 #include "vm_walk.cuh"
+#include "vm_compat.cuh"
 
 using namespace vm;
 
@@ -92,6 +93,7 @@ struct vm_map {
     unsigned long long *d_stats = nullptr;
     int *d_go = nullptr;
     unsigned long long *d_rec = nullptr, *d_rec2 = nullptr;
+    unsigned *d_val = nullptr, *d_val2 = nullptr;
     size_t rec_cap = 0;
     int2 *d_marked = nullptr;
     size_t marked_cap = 0;
@@ -167,6 +169,7 @@ DevMap make_dm(const vm_map *m) {
     d.stats = m->d_stats;
     d.go = m->d_go;
     d.rec = m->d_rec;
+    d.recval = m->d_val;
     d.rec_cap = m->rec_cap;
     d.marked = m->d_marked;
     d.marked_cap = (int)m->marked_cap;
@@ -226,13 +229,21 @@ int ensure_records(vm_map *m, size_t need) {
     size_t nc = std::max(need, m->rec_cap * 2);
     if (m->d_rec) CK(cudaFree(m->d_rec));
     if (m->d_rec2) CK(cudaFree(m->d_rec2));
+    if (m->d_val) CK(cudaFree(m->d_val));
+    if (m->d_val2) CK(cudaFree(m->d_val2));
     m->d_rec = m->d_rec2 = nullptr;
+    m->d_val = m->d_val2 = nullptr;
     CK(cudaMalloc((void **)&m->d_rec, nc * sizeof(unsigned long long)));
     CK(cudaMalloc((void **)&m->d_rec2, nc * sizeof(unsigned long long)));
+    CK(cudaMalloc((void **)&m->d_val, nc * sizeof(unsigned)));
+    CK(cudaMalloc((void **)&m->d_val2, nc * sizeof(unsigned)));
     m->rec_cap = nc;
-    size_t bytes = 0;
+    size_t bytes = 0, bytes2 = 0;
     cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
+    cub::DoubleBuffer<unsigned> dv(m->d_val, m->d_val2);
     CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, (int)std::min<size_t>(nc, INT32_MAX)));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes2, db, dv, (int)std::min<size_t>(nc, INT32_MAX)));
+    bytes = std::max(bytes, bytes2);
     if (bytes > m->sort_tmp_bytes) {
         if (m->d_sort_tmp) CK(cudaFree(m->d_sort_tmp));
         CK(cudaMalloc(&m->d_sort_tmp, bytes));
@@ -283,8 +294,16 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
         else if (det) launch_w3<M_DECAY, true, false>(pgrid, smem, s, dm, src);
         else launch_w3<M_DECAY, false, false>(pgrid, smem, s, dm, src);
         break;
-    case M_NDT_OM: k_walk_ndt<false><<<grid, block, 0, s>>>(dm, src, n); break;
-    case M_NDT_TM: k_walk_ndt<true><<<grid, block, 0, s>>>(dm, src, n); break;
+    case M_NDT_OM:
+        if (det && rec_only) k_walk_ndt<false, true, true><<<grid, block, 0, s>>>(dm, src, n);
+        else if (det) k_walk_ndt<false, true, false><<<grid, block, 0, s>>>(dm, src, n);
+        else k_walk_ndt<false, false, false><<<grid, block, 0, s>>>(dm, src, n);
+        break;
+    case M_NDT_TM:
+        if (det && rec_only) k_walk_ndt<true, true, true><<<grid, block, 0, s>>>(dm, src, n);
+        else if (det) k_walk_ndt<true, true, false><<<grid, block, 0, s>>>(dm, src, n);
+        else k_walk_ndt<true, false, false><<<grid, block, 0, s>>>(dm, src, n);
+        break;
     case M_TSDF:
         if (det) k_walk_tsdf<true><<<grid, block, 0, s>>>(dm, src, n);
         else k_walk_tsdf<false><<<grid, block, 0, s>>>(dm, src, n);
@@ -296,7 +315,7 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
 
 template <class Src>
 int launch_fold(vm_map *m, const DevMap &dm, const Src &src, const unsigned long long *keys,
-                long long R, long long M, int mode) {
+                const unsigned *vals, long long R, long long M, int mode) {
     cudaStream_t s = m->stream;
     const unsigned grid_cap = 148 * 16;
     if (mode == M_OCC || mode == M_DECAY) {
@@ -318,8 +337,8 @@ int launch_fold(vm_map *m, const DevMap &dm, const Src &src, const unsigned long
     } else if (mode == M_NDT_OM || mode == M_NDT_TM) {
         unsigned g = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
         if (g) {
-            if (mode == M_NDT_TM) k_fold_ndt<true><<<g, BLOCK, 0, s>>>(dm, src, keys, R);
-            else k_fold_ndt<false><<<g, BLOCK, 0, s>>>(dm, src, keys, R);
+            if (mode == M_NDT_TM) k_fold_ndt<true><<<g, BLOCK, 0, s>>>(dm, src, keys, vals, R);
+            else k_fold_ndt<false><<<g, BLOCK, 0, s>>>(dm, src, keys, vals, R);
             m->launches += 1;
         }
     } else {
@@ -357,7 +376,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     const bool emit = mode == M_OCC || mode == M_DECAY;
     if (emit && (rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * maxseg + 1))) return rc;
     size_t rec_need = 0;
-    if (ndt) rec_need = (size_t)n + 1;
+    if (ndt) rec_need = std::max<size_t>(m->rec_cap, (size_t)n * (det ? 8 : 1) + 1);
     else if (tsdf && det) {
         double band = 2.0 * m->cfg.tsdf_truncation / m->cfg.voxel_size;
         rec_need = (size_t)n * (size_t)(3.0 * (std::ceil(band) + 2.0) + 4.0);
@@ -451,13 +470,21 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             unsigned long long R = m->h_stats[NUM_STATS + 1];
             if (R > m->rec_cap) {
                 // records overflowed: re-emit them (records only, nothing re-applied)
-                if (!occ_det) return fail(VM_ERR_CUDA, "record buffer overflow");
+                if (!occ_det && !(ndt && det)) return fail(VM_ERR_CUDA, "record buffer overflow");
                 CK(cudaStreamSynchronize(m->stream));
                 if ((rc = ensure_records(m, (size_t)R + (R >> 2)))) return rc;
                 dm.rec = m->d_rec;
+                dm.recval = m->d_val;
                 dm.rec_cap = m->rec_cap;
                 CK(cudaMemsetAsync(m->d_stats + S_RECORDS, 0, sizeof(unsigned long long),
                                    m->stream));
+                if (ndt) {
+                    // the phase-2 hit records come from k_discover: re-emit them
+                    // with a records-only discover pass (no descriptors, no marks)
+                    dim3 g2((unsigned)((n + BLOCK - 1) / BLOCK));
+                    k_discover<<<g2, BLOCK, 0, m->stream>>>(dm, src, n, mode, 1, 0, 0);
+                    m->launches += 1;
+                }
                 if ((rc = launch_walk(m, dm, src, n, mode, det, true))) return rc;
                 CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_stats + S_RECORDS,
                                    sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -468,16 +495,23 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             long long M = (long long)std::min<unsigned long long>(hs[S_MARKED], m->marked_cap);
             int end_bit;
             if (occ_det) end_bit = order_bits + std::max(1, bitlen((unsigned long long)M));
-            else end_bit = order_bits + std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
+            else end_bit = order_bits + (ndt ? 1 : 0) +
+                           std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
             end_bit = std::min(end_bit, 64);
             cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
+            cub::DoubleBuffer<unsigned> dv(m->d_val, m->d_val2);
             if (R > 1) {
                 size_t bytes = m->sort_tmp_bytes;
-                CK(cub::DeviceRadixSort::SortKeys(m->d_sort_tmp, bytes, db, (int)R, 0, end_bit,
-                                                  m->stream));
+                if (ndt)
+                    CK(cub::DeviceRadixSort::SortPairs(m->d_sort_tmp, bytes, db, dv, (int)R, 0,
+                                                       end_bit, m->stream));
+                else
+                    CK(cub::DeviceRadixSort::SortKeys(m->d_sort_tmp, bytes, db, (int)R, 0,
+                                                      end_bit, m->stream));
             }
             CK(cudaEventRecord(m->ev_sort, m->stream));
-            if ((rc = launch_fold(m, dm, src, db.Current(), (long long)R, M, mode))) return rc;
+            if ((rc = launch_fold(m, dm, src, db.Current(), dv.Current(), (long long)R, M, mode)))
+                return rc;
             if (occ_det && M) {
                 k_cleanup<<<148, BLOCK, 0, m->stream>>>(dm, (int)M);
                 m->launches += 1;
@@ -649,6 +683,8 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_go);
     cudaFree(m->d_rec);
     cudaFree(m->d_rec2);
+    cudaFree(m->d_val);
+    cudaFree(m->d_val2);
     cudaFree(m->d_marked);
     cudaFree(m->d_touched);
     cudaFree(m->d_sort_tmp);
@@ -890,12 +926,70 @@ int vm_walk_voxels(double ox, double oy, double oz, double ex, double ey, double
     return VM_OK;
 }
 
-int vm_kernels_integrate_occupancy(const double *, const double *, const uint8_t *, int64_t,
-                                   const int64_t *, const int32_t *, int64_t, void *const *,
-                                   void *const *, void *const *, void *const *, void *const *,
-                                   double, int64_t, double, double, double, double, int32_t,
-                                   int32_t, int64_t *, void *) {
-    return fail(VM_ERR_ARG, "vm_kernels_integrate_occupancy: not built in this version");
+int vm_kernels_integrate_occupancy(const double *origins, const double *ends,
+                                   const uint8_t *has_sample, int64_t n, const int64_t *tkeys,
+                                   const int32_t *tvals, int64_t tsize, void *const *occ_ptrs,
+                                   void *const *mean_ptrs, void *const *count_ptrs,
+                                   void *const *dhit_ptrs, void *const *ddist_ptrs,
+                                   double voxel_size, int64_t region_dim, double hit_delta,
+                                   double miss_delta, double clamp_min, double clamp_max,
+                                   int32_t retry_limit, int32_t walk_cap, int64_t *stats_out,
+                                   void *stream) {
+    (void)retry_limit;  // no mutex fallback on the GPU: retries are only counted
+    if (!stats_out) return fail(VM_ERR_ARG, "null stats_out");
+    std::memset(stats_out, 0, 4 * sizeof(int64_t));
+    if (n < 0 || tsize <= 0 || (tsize & (tsize - 1)) != 0)
+        return fail(VM_ERR_ARG, "n must be >= 0 and tsize a power of two");
+    if (!(voxel_size > 0) || region_dim < 1 || region_dim > 1024)
+        return fail(VM_ERR_ARG, "bad voxel_size / region_dim");
+    if ((mean_ptrs == nullptr) != (count_ptrs == nullptr) ||
+        (dhit_ptrs == nullptr) != (ddist_ptrs == nullptr))
+        return fail(VM_ERR_ARG, "mean/count and decay pointer arrays come in pairs");
+    if (n == 0) return VM_OK;
+    if (!origins || !ends || !has_sample || !tkeys || !tvals || !occ_ptrs)
+        return fail(VM_ERR_ARG, "null device array");
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *d_st = nullptr;
+    CK(cudaMallocAsync((void **)&d_st, 4 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(d_st, 0, 4 * sizeof(unsigned long long), s));
+    CompatArgs a{};
+    a.o = origins;
+    a.e = ends;
+    a.has = has_sample;
+    a.n = n;
+    a.tkeys = (const long long *)tkeys;
+    a.tvals = tvals;
+    a.tmask = (unsigned long long)tsize - 1;
+    a.occ = occ_ptrs;
+    a.mean = mean_ptrs;
+    a.cnt = count_ptrs;
+    a.dhit = dhit_ptrs;
+    a.ddist = ddist_ptrs;
+    a.vox = voxel_size;
+    a.dim = (int)region_dim;
+    a.hit = (float)hit_delta;
+    a.miss = (float)miss_delta;
+    a.cmin = (float)clamp_min;
+    a.cmax = (float)clamp_max;
+    a.walk_cap = walk_cap;
+    a.stats = d_st;
+    int sms = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const unsigned grid = (unsigned)std::max<long long>(
+        1, std::min<long long>((n + BLOCK - 1) / BLOCK, (long long)sms * 8));
+    k_compat_occupancy<<<grid, BLOCK, 0, s>>>(a);
+    int rc = check_launch("compat_occupancy");
+    if (rc) return rc;
+    unsigned long long h[4];
+    CK(cudaMemcpyAsync(h, d_st, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(d_st, s));
+    CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < 4; ++i) stats_out[i] = (int64_t)h[i];
+    return VM_OK;
 }
 
 }  // extern "C"
