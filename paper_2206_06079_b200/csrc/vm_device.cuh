@@ -27,29 +27,30 @@ enum Mode { M_OCC = 0, M_DECAY = 1, M_NDT_OM = 2, M_NDT_TM = 3, M_TSDF = 4 };
 enum Stat {
     S_RAYS_IN = 0, S_PROCESSED, S_SEGMENTS, S_VISITS, S_RETRIES, S_FAILURES,
     S_RMISS, S_PREF_TOUCHED, S_RECORDS, S_MARKED, S_WALK_TOUCHED, S_RANGE_ERR,
-    S_CUBE_FLUSH, S_SEGDESC, S_WORK, S_RGRID, NUM_STATS
+    S_CUBE_FLUSH, S_SEGDESC, S_WORK, S_RGRID, S_SEGDESC2, NUM_STATS
 };
 
 constexpr unsigned MARK_FLAG = 0x80000000u;
 constexpr int CUBE = 16;                 // smem aggregation cube edge (voxels)
 constexpr int CUBE_N = CUBE * CUBE * CUBE;
 constexpr int SLOTSET = 256;             // per-block region dedupe set
+constexpr int RG_MAX = 1 << 16;          // dense per-batch region grid cells (HBM, L1-cached)
 
 // One preprocessed segment with its DDA initial state (k_discover writes
 // it, the persistent walk consumes it): 96 bytes, 16-byte aligned.
 struct __align__(16) SegDesc {
     double t[3];       // t_max per axis at the start cell (traversal.py:70-78)
     double d[3];       // t_delta per axis
-    int c[3];          // start cell
-    int e[3];          // end cell
-    unsigned order;    // (ray * maxseg + seg) << 1 ; 0xFFFFFFFF = empty
-    unsigned flags;    // bit0 has_sample(last visit is a hit), bits 1-6 step codes
-    int slot0;         // region slot of the start cell
-    unsigned local0;   // start cell's local coords: lx | ly << 10 | lz << 20
+    long long rkey;    // packed region key of the start cell (keys.py:76-86)
     double L;          // segment length (RaySample.length), for decay
-    int r0[3];         // start cell's region coords
-    int pad;
+    unsigned order;    // (ray * maxseg + seg) << 1
+    unsigned flags;    // bit0 has_sample (last visit is a hit), bits 1-6 step + 1 per axis
+    unsigned rem;      // Manhattan distance start cell -> end cell
+    unsigned lp0;      // start cell local coords, biased: (lx+1) | (ly+1) << 10 | (lz+1) << 20
+    int slot0;         // region slot of the start cell
+    int e[3];          // end cell (global)
 };
+static_assert(sizeof(SegDesc) == 96, "SegDesc layout");
 
 // All state a kernel needs, passed by value.
 struct DevMap {
@@ -59,7 +60,7 @@ struct DevMap {
     double tsdf_trunc, tsdf_maxw;
     double sigma2, miss_check;
     float hit32, miss32, cmin, cmax, fthresh;
-    int dim, vpr, mark_words, maxseg;
+    int dim, vpr, maxseg;
     int order_bits;                      // bits of (ray*maxseg+seg)<<1|hit
     int cell_limit;                      // |global voxel coord| must stay below
     // region table (engine._build_region_table format, engine.py:121-147)
@@ -74,13 +75,11 @@ struct DevMap {
     unsigned *slot_touch, *slot_pref;
     unsigned epoch;
     void *const *lptr[NUM_LAYERS];       // per layer: region base pointer per slot
-    unsigned *marks;                     // mark bitset, mark_words per slot
-    unsigned long long *bmask;           // per slot: 4x4x4 brick summary of marks
-    int brick_shift;                     // log2(dim) - 2 when dim is a power of 2 >= 4, else -1
     char *slab[NUM_LAYERS];              // pool slabs: region s at slab + s * bpr
     unsigned long long bpr[NUM_LAYERS];  // bytes per region per layer
     int *rgrid;                          // dense region-slot grid over the batch bbox
-    unsigned *ztouch;                    // per grid cell: z-planes holding miss counts
+    unsigned *bmask;                     // per slot: brick summary of the batch's sample voxels
+    int brick_shift;                     // log2(dim) - 2 for power-of-two dims >= 4, else -1
     int *rbox;                           // [6]: min xyz, max xyz (regions) of the batch
     int rg_max;                          // capacity of rgrid (cells)
     SegDesc *segs;                       // preprocessed segments of the batch
@@ -92,8 +91,6 @@ struct DevMap {
     unsigned long long *rec;
     unsigned *recval;                    // per-record value (NDT deterministic phase 1)
     unsigned long long rec_cap;
-    int2 *marked;                        // (slot, li) of sample voxels
-    int marked_cap;
     int *touched;                        // regions touched by the walk
     int touched_cap;
 };
@@ -329,6 +326,18 @@ __device__ __noinline__ int region_slot_slow(const DevMap &m, long long key) {
     return -1;
 }
 
+// Lookup only (never creates): slot or -1.
+__device__ __noinline__ int region_find(const DevMap &m, long long key) {
+    unsigned long long h = mix_key(key) & m.tmask;
+    for (unsigned long long probe = 0; probe <= m.tmask; ++probe) {
+        const long long k = ((volatile long long *)m.tkeys)[h];
+        if (k == key) return wait_slot(m, h);
+        if (k == -1) return -1;
+        h = (h + 1) & m.tmask;
+    }
+    return -1;
+}
+
 __device__ __forceinline__ int region_slot(const DevMap &m, long long key) {
     // fast path: plain (cached) probe of entries that existed before this kernel
     unsigned long long h = mix_key(key) & m.tmask;
@@ -413,25 +422,27 @@ struct RegionTrack {
 
 // DDA initial state of traversal._walk_grid (traversal.py:58-78) into a
 // descriptor (everything the persistent walk needs to start the segment).
+// Returns the start cell in c[].
 __device__ __forceinline__ void dda_init(const double o[3], const double e[3], double cell,
-                                         SegDesc &sd) {
+                                         SegDesc &sd, int c[3]) {
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
     unsigned codes = 0;
+    int rem = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const double v = e[a] - o[a];
-        const int c = (int)floor(o[a] / cell);
-        sd.c[a] = c;
+        c[a] = (int)floor(o[a] / cell);
         sd.e[a] = (int)floor(e[a] / cell);
+        rem += abs(sd.e[a] - c[a]);
         double t = INF, d = INF;
         unsigned code = 1;  // step + 1
         if (v > 0) {
             code = 2;
-            t = ((double)(c + 1) * cell - o[a]) / v;
+            t = ((double)(c[a] + 1) * cell - o[a]) / v;
             d = cell / v;
         } else if (v < 0) {
             code = 0;
-            t = ((double)c * cell - o[a]) / v;
+            t = ((double)c[a] * cell - o[a]) / v;
             d = -cell / v;
         }
         sd.t[a] = t;
@@ -439,6 +450,7 @@ __device__ __forceinline__ void dda_init(const double o[3], const double e[3], d
         codes |= code << (2 * a);
     }
     sd.flags = codes << 1;
+    sd.rem = (unsigned)rem;
 }
 
 // traversal._walk_grid (traversal.py:52-111) == _kernels.walk_fill

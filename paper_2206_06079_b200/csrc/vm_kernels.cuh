@@ -13,8 +13,8 @@
 //                records for sample voxels).
 //   k_resolve    deterministic miss counts -> f_miss^k per voxel.
 //   sort         CUB radix sort of the records (voxel-major, ray order).
-//   k_fold_*     in-order fold of the records per voxel (warp per voxel).
-//   k_cleanup    clears marks.
+//   k_fold_*     in-order fold of the records per voxel (warp per long run);
+//                clears the sample voxels' MARK'ed scratch words.
 #pragma once
 
 #include "vm_device.cuh"
@@ -314,15 +314,13 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                                                     int count_stats = 1) {
     __shared__ unsigned long long kcache[KCACHE];
     __shared__ int sset[SLOTSET];
-    __shared__ int2 smark[BLOCK];
     __shared__ unsigned long long srec[BLOCK];
-    __shared__ int nmark, nrec;
-    __shared__ unsigned long long mark_base, rec_base;
+    __shared__ int nrec;
+    __shared__ unsigned long long rec_base;
     __shared__ int anchor[3];
     for (int i = threadIdx.x; i < KCACHE; i += blockDim.x) kcache[i] = 0ULL;
     for (int i = threadIdx.x; i < SLOTSET; i += blockDim.x) sset[i] = -1;
     if (threadIdx.x == 0) {
-        nmark = 0;
         nrec = 0;
         const long long i0 = (long long)blockIdx.x * blockDim.x;
         double o0[3], e0[3];
@@ -340,6 +338,7 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     const bool ndt = mode == M_NDT_OM || mode == M_NDT_TM;
     const int lane = threadIdx.x & 31;
     unsigned long long st[3] = {0, 0, 0};  // processed, segments, range errors
+    unsigned long long nmark_local = 0;
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     Ray r;
     bool ok = false;
@@ -355,20 +354,36 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
             }
         }
     }
-    // warp-aggregated allocation of segment descriptors
-    unsigned long long dbase = 0;
+    // warp-aggregated allocation of segment descriptors in two queues: long
+    // segments (>= half the segment length) from the front of the buffer,
+    // short ones from the back, so the walk takes the long ones first and
+    // the tail of the batch is made of short segments
+    unsigned long long fbase = 0, bbase = 0;
+    bool last_long = false;
     if (emit) {
-        unsigned k = ok ? (unsigned)r.nseg : 0u, incl = k;
+        unsigned kl = 0, ks = 0;
+        if (ok) {
+            const double last_len = r.L - (double)(r.nseg - 1) * m.seg_len;
+            last_long = last_len >= 0.5 * m.seg_len;
+            kl = (unsigned)(r.nseg - 1) + (last_long ? 1u : 0u);
+            ks = last_long ? 0u : 1u;
+        }
+        unsigned il = kl, is = ks;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
+            const unsigned vl = __shfl_up_sync(0xffffffffu, il, o);
+            const unsigned vs = __shfl_up_sync(0xffffffffu, is, o);
+            if (lane >= o) {
+                il += vl;
+                is += vs;
+            }
         }
-        unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned long long base = 0;
-        if (lane == 0 && total) base = atomicAdd(m.stats + S_SEGDESC, (unsigned long long)total);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        dbase = base + (incl - k);
+        const unsigned tl = __shfl_sync(0xffffffffu, il, 31), ts = __shfl_sync(0xffffffffu, is, 31);
+        unsigned long long bl = 0, bs = 0;
+        if (lane == 0 && tl) bl = atomicAdd(m.stats + S_SEGDESC, (unsigned long long)tl);
+        if (lane == 0 && ts) bs = atomicAdd(m.stats + S_SEGDESC2, (unsigned long long)ts);
+        fbase = __shfl_sync(0xffffffffu, bl, 0) + (il - kl);
+        bbase = __shfl_sync(0xffffffffu, bs, 0) + (is - ks);
     }
     PrefetchVisitor pv{&m, &kc, sset, {INT_MAX, INT_MAX, INT_MAX}, {INT_MIN, INT_MIN, INT_MIN}};
     if (ok) {
@@ -391,31 +406,27 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                 }
             }
             walk(so, pe, m.rsize, pv);
-            if (emit && dbase + s < m.seg_cap) {
+            // queue slot of this segment (front: long, back: short)
+            const bool in_front = s < r.nseg - 1 || last_long;
+            const unsigned long long qi = in_front ? fbase + s : bbase;
+            if (emit && qi < m.seg_cap) {
                 SegDesc sd;
-                dda_init(so, se, m.vox, sd);
+                int c[3];
+                dda_init(so, se, m.vox, sd, c);
                 sd.order = (unsigned)(i * m.maxseg + s) << 1;
                 sd.flags |= sh ? 1u : 0u;
-                RegionTrack rt;
-                rt.rx = floordiv(sd.c[0], m.dim);
-                rt.ry = floordiv(sd.c[1], m.dim);
-                rt.rz = floordiv(sd.c[2], m.dim);
-                rt.lx = sd.c[0] - rt.rx * m.dim;
-                rt.ly = sd.c[1] - rt.ry * m.dim;
-                rt.lz = sd.c[2] - rt.rz * m.dim;
+                const int rx = floordiv(c[0], m.dim), ry = floordiv(c[1], m.dim),
+                          rz = floordiv(c[2], m.dim);
                 bool fresh;
-                rt.slot = cached_slot(m, kc, rt.rx, rt.ry, rt.rz, &fresh);
-                sd.slot0 = rt.slot;
-                sd.local0 = (unsigned)rt.lx | ((unsigned)rt.ly << 10) | ((unsigned)rt.lz << 20);
-                sd.r0[0] = rt.rx;
-                sd.r0[1] = rt.ry;
-                sd.r0[2] = rt.rz;
-                sd.pad = 0;
+                sd.slot0 = cached_slot(m, kc, rx, ry, rz, &fresh);
+                sd.rkey = pack_region(rx, ry, rz);
+                sd.lp0 = (unsigned)(c[0] - rx * m.dim + 1) | ((unsigned)(c[1] - ry * m.dim + 1) << 10) |
+                         ((unsigned)(c[2] - rz * m.dim + 1) << 20);
                 sd.L = norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2]);
                 const uint4 *src4 = reinterpret_cast<const uint4 *>(&sd);
-                uint4 *dst4 = reinterpret_cast<uint4 *>(m.segs + dbase + s);
+                uint4 *dst4 = reinterpret_cast<uint4 *>(m.segs + (in_front ? qi : m.seg_cap - 1 - qi));
 #pragma unroll
-                for (int q = 0; q < 7; ++q) dst4[q] = src4[q];
+                for (int q = 0; q < (int)(sizeof(SegDesc) / 16); ++q) dst4[q] = src4[q];
             }
             if (sh && (det || ndt) && !tsdf) {
                 // the sample voxel floor(end / vox) (reference.py:178-186)
@@ -440,17 +451,17 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                         // phase bit 1: after every phase-1 record of the voxel
                         srec[k] = (vid << (m.order_bits + 1)) | (1ULL << m.order_bits) | order;
                     } else {
-                        unsigned bit = 1u << (li & 31);
-                        unsigned old = atomicOr(
-                            m.marks + (size_t)rt.slot * m.mark_words + (li >> 5), bit);
-                        if (!(old & bit)) {
-                            int k = atomicAdd(&nmark, 1);
-                            smark[k] = make_int2(rt.slot, li);
+                        // stamp the sample voxel: the walk turns its visits into records
+                        unsigned *w = layer_at<unsigned>(m, L_SCRATCH, rt.slot) + li;
+                        if (!(*((volatile unsigned *)w) & MARK_FLAG) &&
+                            !(atomicOr(w, MARK_FLAG) & MARK_FLAG)) {
+                            ++nmark_local;
+                            // brick summary read by the walk (4 x 4 x 2 bricks)
                             const int bsh = m.brick_shift;
-                            const int b = bsh >= 0 ? ((rt.lx >> bsh) | ((rt.ly >> bsh) << 2) |
-                                                      ((rt.lz >> (bsh + 1)) << 4))
-                                                   : 0;
-                            atomicOr(m.bmask + rt.slot, bsh >= 0 ? (1ULL << b) : 0xFFFFFFFFULL);
+                            const unsigned bit = bsh >= 0
+                                ? 1u << ((rt.lx >> bsh) | ((rt.ly >> bsh) << 2) | ((rt.lz >> (bsh + 1)) << 4))
+                                : 0xFFFFFFFFu;
+                            atomicOr(m.bmask + rt.slot, bit);
                         }
                     }
                 }
@@ -459,20 +470,9 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (nmark) mark_base = atomicAdd(m.stats + S_MARKED, (unsigned long long)nmark);
         if (nrec) rec_base = atomicAdd(m.stats + S_RECORDS, (unsigned long long)nrec);
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < nmark; k += blockDim.x) {
-        unsigned long long mi = mark_base + k;
-        if (mi < (unsigned long long)m.marked_cap) {
-            int2 sl = smark[k];
-            m.marked[mi] = sl;
-            // the marked index lives in the (otherwise unused) scratch word
-            unsigned *scr = layer_at<unsigned>(m, L_SCRATCH, sl.x);
-            scr[sl.y] = MARK_FLAG | (unsigned)mi;
-        }
-    }
     for (int k = threadIdx.x; k < nrec; k += blockDim.x) {
         unsigned long long ri = rec_base + k;
         if (ri < m.rec_cap) {
@@ -482,6 +482,11 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     }
     const int which[3] = {S_PROCESSED, S_SEGMENTS, S_RANGE_ERR};
     if (count_stats) block_add_stats(m, st, which);
+    {
+        unsigned long long mk[1] = {nmark_local};
+        const int wm[1] = {S_MARKED};
+        block_add_stats(m, mk, wm);
+    }
     // batch bounding box of prefetched regions (+1 margin for walk-entered ones)
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -528,10 +533,9 @@ __global__ void k_rgrid(const __grid_constant__ DevMap m) {
 __global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
     int used = *((volatile int *)m.cursor);
     unsigned long long rerr = ((volatile unsigned long long *)m.stats)[S_RANGE_ERR];
-    unsigned long long marked = ((volatile unsigned long long *)m.stats)[S_MARKED];
-    unsigned long long nseg = ((volatile unsigned long long *)m.stats)[S_SEGDESC];
-    bool ok = used + margin <= m.cap && rerr == 0 && marked <= (unsigned long long)m.marked_cap &&
-              nseg <= m.seg_cap;
+    unsigned long long nseg = ((volatile unsigned long long *)m.stats)[S_SEGDESC] +
+                              ((volatile unsigned long long *)m.stats)[S_SEGDESC2];
+    bool ok = used + margin <= m.cap && rerr == 0 && nseg <= m.seg_cap;
     *m.go = ok ? 1 : 0;
 }
 
@@ -1007,34 +1011,23 @@ __device__ __forceinline__ long long lower_bound_u64(const unsigned long long *a
     return lo;
 }
 
-// Run starts of the sorted occupancy records: start[mi] = first record of
-// sample voxel mi (every sample voxel owns at least its own hit record).
-__global__ void k_heads(const __grid_constant__ DevMap m, const unsigned long long *keys,
-                        long long R, int *start) {
-    if (!read_go(m)) return;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
-         i += (long long)gridDim.x * blockDim.x) {
-        const unsigned long long mi = keys[i] >> m.order_bits;
-        if (i == 0 || (keys[i - 1] >> m.order_bits) != mi) start[mi] = (int)i;
-    }
-}
-
 // Apply one sample voxel's records [s, e) in ray order (reference.py:35-64
 // restricted to that voxel): misses between hits collapse to f_miss^k.
+// Clears the voxel's MARK'ed scratch word.
 template <class Src>
 __device__ __forceinline__ void fold_voxel_serial(const DevMap &m, const Src &src,
-                                                  const unsigned long long *keys, int s, int e,
-                                                  int2 sl) {
+                                                  const unsigned long long *keys, long long s,
+                                                  long long e, unsigned vid) {
     const unsigned long long omask = (1ULL << m.order_bits) - 1;
-    float *occ = layer_at<float>(m, L_OCC, sl.x);
-    unsigned *mean = layer_at<unsigned>(m, L_MEAN, sl.x);
-    unsigned *cnt = layer_at<unsigned>(m, L_COUNT, sl.x);
-    float l = occ[sl.y];
-    unsigned packed = mean ? mean[sl.y] : 0u, count = cnt ? cnt[sl.y] : 0u;
+    float *occ = reinterpret_cast<float *>(m.slab[L_OCC]) + vid;
+    unsigned *mean = m.slab[L_MEAN] ? reinterpret_cast<unsigned *>(m.slab[L_MEAN]) + vid : nullptr;
+    unsigned *cnt = m.slab[L_COUNT] ? reinterpret_cast<unsigned *>(m.slab[L_COUNT]) + vid : nullptr;
+    float l = *occ;
+    unsigned packed = mean ? *mean : 0u, count = cnt ? *cnt : 0u;
     int g[3];
-    slot_li_to_g(m, sl.x, sl.y, g);
+    slot_li_to_g(m, (int)(vid / (unsigned)m.vpr), (int)(vid % (unsigned)m.vpr), g);
     unsigned misses = 0;
-    for (int i = s; i < e; ++i) {
+    for (long long i = s; i < e; ++i) {
         const unsigned long long k = keys[i];
         if (!(k & 1ULL)) {
             ++misses;
@@ -1054,32 +1047,36 @@ __device__ __forceinline__ void fold_voxel_serial(const DevMap &m, const Src &sr
         }
     }
     l = miss_k(l, misses, m.miss32, m.cmin, m.cmax);
-    occ[sl.y] = l;
+    *occ = l;
     if (mean) {
-        mean[sl.y] = packed;
-        cnt[sl.y] = count;
+        *mean = packed;
+        *cnt = count;
     }
+    reinterpret_cast<unsigned *>(m.slab[L_SCRATCH])[vid] = 0u;
+    m.bmask[vid / (unsigned)m.vpr] = 0u;
 }
 
 constexpr int FOLD_SERIAL_MAX = 64;
 
-// One thread per sample voxel; voxels with long record runs are handed to
-// k_fold_occ_big (one warp each).
+// One thread per record-run head (= sample voxel); runs longer than
+// FOLD_SERIAL_MAX are handed to k_fold_occ_big (one warp each).
 template <class Src>
 __global__ void __launch_bounds__(BLOCK) k_fold_occ(const __grid_constant__ DevMap m, Src src,
                                                     const unsigned long long *keys, long long R,
-                                                    int M, const int *start, int *big,
-                                                    unsigned long long *nbig) {
+                                                    long long *big, unsigned long long *nbig) {
     if (!read_go(m)) return;
-    for (long long mi = (long long)blockIdx.x * blockDim.x + threadIdx.x; mi < M;
-         mi += (long long)gridDim.x * blockDim.x) {
-        const int s = start[mi];
-        const int e = mi + 1 < M ? start[mi + 1] : (int)R;
-        if (e - s > FOLD_SERIAL_MAX) {
-            big[atomicAdd(nbig, 1ULL)] = (int)mi;
+    const int ob = m.order_bits;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long vk = keys[i] >> ob;
+        if (i > 0 && (keys[i - 1] >> ob) == vk) continue;
+        long long e = i + 1;
+        while (e < R && e - i <= FOLD_SERIAL_MAX && (keys[e] >> ob) == vk) ++e;
+        if (e < R && (keys[e] >> ob) == vk) {
+            big[atomicAdd(nbig, 1ULL)] = i;
             continue;
         }
-        fold_voxel_serial(m, src, keys, s, e, m.marked[mi]);
+        fold_voxel_serial(m, src, keys, i, e, (unsigned)vk);
     }
 }
 
@@ -1088,34 +1085,37 @@ __global__ void __launch_bounds__(BLOCK) k_fold_occ(const __grid_constant__ DevM
 template <class Src>
 __global__ void __launch_bounds__(BLOCK) k_fold_occ_big(const __grid_constant__ DevMap m, Src src,
                                                         const unsigned long long *keys, long long R,
-                                                        int M, const int *start, const int *big,
+                                                        const long long *big,
                                                         const unsigned long long *nbig) {
     if (!read_go(m)) return;
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x / 32);
     const unsigned long long omask = (1ULL << m.order_bits) - 1;
+    const int ob = m.order_bits;
     const long long nb = (long long)*nbig;
     for (long long w = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < nb;
          w += warps) {
-        const int mi = big[w];
-        const int2 sl = m.marked[mi];
-        const int s = start[mi];
-        const int e = mi + 1 < M ? start[mi + 1] : (int)R;
-        float *occ = layer_at<float>(m, L_OCC, sl.x);
-        unsigned *mean = layer_at<unsigned>(m, L_MEAN, sl.x);
-        unsigned *cnt = layer_at<unsigned>(m, L_COUNT, sl.x);
-        float l = occ[sl.y];
-        unsigned packed = mean ? mean[sl.y] : 0u, count = cnt ? cnt[sl.y] : 0u;
+        const long long s = big[w];
+        const unsigned long long vk = keys[s] >> ob;
+        const unsigned vid = (unsigned)vk;
+        float *occ = reinterpret_cast<float *>(m.slab[L_OCC]) + vid;
+        unsigned *mean = m.slab[L_MEAN] ? reinterpret_cast<unsigned *>(m.slab[L_MEAN]) + vid : nullptr;
+        unsigned *cnt = m.slab[L_COUNT] ? reinterpret_cast<unsigned *>(m.slab[L_COUNT]) + vid : nullptr;
+        float l = *occ;
+        unsigned packed = mean ? *mean : 0u, count = cnt ? *cnt : 0u;
         int g[3];
-        slot_li_to_g(m, sl.x, sl.y, g);
-        for (int pos = s; pos < e; pos += 32) {
-            const int p = pos + lane;
-            const unsigned long long key = p < e ? keys[p] : 0ULL;
-            const unsigned hmask = __ballot_sync(0xffffffffu, p < e && (key & 1ULL));
-            const int nvalid = min(32, e - pos);
+        slot_li_to_g(m, (int)(vid / (unsigned)m.vpr), (int)(vid % (unsigned)m.vpr), g);
+        for (long long pos = s;; pos += 32) {
+            const long long p = pos + lane;
+            const unsigned long long key = p < R ? keys[p] : ~0ULL;
+            const bool mine = p < R && (key >> ob) == vk;
+            const unsigned vmask = __ballot_sync(0xffffffffu, mine);
+            const unsigned hmask = __ballot_sync(0xffffffffu, mine && (key & 1ULL));
+            const int nvalid = __popc(vmask);  // run records are a prefix of the window
             int cur = 0;
             while (cur < nvalid) {
-                const unsigned rem = hmask >> cur;
+                const unsigned rem = (hmask >> cur) & (nvalid - cur >= 32 ? 0xffffffffu
+                                                                          : ((1u << (nvalid - cur)) - 1u));
                 if (!rem) {
                     l = miss_k(l, (unsigned)(nvalid - cur), m.miss32, m.cmin, m.cmax);
                     break;
@@ -1135,13 +1135,16 @@ __global__ void __launch_bounds__(BLOCK) k_fold_occ_big(const __grid_constant__ 
                 }
                 cur = nh + 1;
             }
+            if (nvalid < 32) break;
         }
         if (lane == 0) {
-            occ[sl.y] = l;
+            *occ = l;
             if (mean) {
-                mean[sl.y] = packed;
-                cnt[sl.y] = count;
+                *mean = packed;
+                *cnt = count;
             }
+            reinterpret_cast<unsigned *>(m.slab[L_SCRATCH])[vid] = 0u;
+            m.bmask[vid / (unsigned)m.vpr] = 0u;
         }
     }
 }
@@ -1288,14 +1291,15 @@ __global__ void __launch_bounds__(BLOCK) k_fold_tsdf(const __grid_constant__ Dev
     }
 }
 
-// Clear marks and the marked-index scratch words of this batch.
-__global__ void k_cleanup(const __grid_constant__ DevMap m, int M) {
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < M;
+// Error path: a refused batch leaves its sample-voxel stamps behind; clear
+// every MARK'ed scratch word of the first nreg regions (no walk ran, so
+// MARK'ed words hold nothing else).
+__global__ void k_clear_marks(const __grid_constant__ DevMap m, long long words) {
+    unsigned *scr = reinterpret_cast<unsigned *>(m.slab[L_SCRATCH]);
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < words;
          k += (long long)gridDim.x * blockDim.x) {
-        int2 sl = m.marked[k];
-        m.marks[(size_t)sl.x * m.mark_words + (sl.y >> 5)] = 0u;
-        layer_at<unsigned>(m, L_SCRATCH, sl.x)[sl.y] = 0u;
-        m.bmask[sl.x] = 0ULL;
+        if (scr[k] & MARK_FLAG) scr[k] = 0u;
+        if (k % m.vpr == 0) m.bmask[k / m.vpr] = 0u;
     }
 }
 

@@ -67,7 +67,7 @@ struct vm_map {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    int dim = 0, vpr = 0, mark_words = 0;
+    int dim = 0, vpr = 0;
     long long max_slots = 0, cap = 0, nreg = 0, max_growth = 0;
     size_t bpr[NUM_LAYERS] = {};
     void *slab[NUM_LAYERS] = {};
@@ -78,16 +78,14 @@ struct vm_map {
     int *d_cursor = nullptr;
     long long *d_slot_keys = nullptr;
     unsigned *d_slot_touch = nullptr, *d_slot_pref = nullptr;
-    unsigned *d_marks = nullptr;
-    unsigned long long *d_bmask = nullptr;
     SegDesc *d_segs = nullptr;
     size_t seg_cap = 0;
     unsigned long long *d_work = nullptr;
     int *d_rgrid = nullptr;
-    unsigned *d_ztouch = nullptr;
+    unsigned *d_bmask = nullptr;
     int *d_rbox = nullptr;
-    int *d_start = nullptr, *d_big = nullptr;
-    size_t start_cap = 0, big_cap = 0;
+    long long *d_big = nullptr;
+    size_t big_cap = 0;
     unsigned long long *d_nbig = nullptr;
     int num_sms = 148;
     unsigned long long *d_stats = nullptr;
@@ -95,8 +93,6 @@ struct vm_map {
     unsigned long long *d_rec = nullptr, *d_rec2 = nullptr;
     unsigned *d_val = nullptr, *d_val2 = nullptr;
     size_t rec_cap = 0;
-    int2 *d_marked = nullptr;
-    size_t marked_cap = 0;
     int *d_touched = nullptr;
     void *d_sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
@@ -130,7 +126,6 @@ DevMap make_dm(const vm_map *m) {
     d.fthresh = (float)c.ndt_reset_threshold;
     d.dim = m->dim;
     d.vpr = m->vpr;
-    d.mark_words = m->mark_words;
     d.maxseg = (int)std::ceil(c.max_ray_range / c.segment_length) + 1;
     d.cell_limit = (int)std::min<long long>((1LL << 20) * (long long)m->dim - 1, (1LL << 30));
     d.tkeys = m->d_tkeys;
@@ -149,7 +144,7 @@ DevMap make_dm(const vm_map *m) {
         d.slab[l] = (char *)m->slab[l];
         d.bpr[l] = m->bpr[l];
     }
-    d.marks = m->d_marks;
+    d.rgrid = m->d_rgrid;
     d.bmask = m->d_bmask;
     {
         int bs = -1;
@@ -159,8 +154,6 @@ DevMap make_dm(const vm_map *m) {
         }
         d.brick_shift = bs;
     }
-    d.rgrid = m->d_rgrid;
-    d.ztouch = m->d_ztouch;
     d.rbox = m->d_rbox;
     d.rg_max = RG_MAX;
     d.segs = m->d_segs;
@@ -171,8 +164,6 @@ DevMap make_dm(const vm_map *m) {
     d.rec = m->d_rec;
     d.recval = m->d_val;
     d.rec_cap = m->rec_cap;
-    d.marked = m->d_marked;
-    d.marked_cap = (int)m->marked_cap;
     d.touched = m->d_touched;
     d.touched_cap = (int)m->max_slots;
     return d;
@@ -200,15 +191,6 @@ int grow_pool(vm_map *m, long long new_cap) {
         if (m->slab[l]) CK(cudaFree(m->slab[l]));
         m->slab[l] = nw;
     }
-    unsigned *nm = nullptr;
-    CK(cudaMalloc(&nm, (size_t)new_cap * m->mark_words * sizeof(unsigned)));
-    CK(cudaMemsetAsync(nm, 0, (size_t)new_cap * m->mark_words * sizeof(unsigned), m->stream));
-    if (m->d_marks)
-        CK(cudaMemcpyAsync(nm, m->d_marks, (size_t)m->cap * m->mark_words * sizeof(unsigned),
-                           cudaMemcpyDeviceToDevice, m->stream));
-    CK(cudaStreamSynchronize(m->stream));
-    if (m->d_marks) CK(cudaFree(m->d_marks));
-    m->d_marks = nm;
     m->cap = new_cap;
     return VM_OK;
 }
@@ -277,7 +259,7 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
     cudaStream_t s = m->stream;
     // persistent grid: 2 resident blocks per SM, never more than the work needs
     dim3 pgrid((unsigned)std::max<long long>(
-        1, std::min<long long>(2LL * m->num_sms, (n * 3 + BLOCK - 1) / BLOCK)));
+        1, std::min<long long>((long long)WK_BLOCKS * m->num_sms, (n * 3 + BLOCK - 1) / BLOCK)));
     if (mode == M_OCC || mode == M_DECAY) {
         cudaError_t e = cudaMemsetAsync(m->d_work, 0, sizeof(unsigned long long), s);
         if (e != cudaSuccess) return fail(VM_ERR_CUDA, cudaGetErrorString(e));
@@ -315,24 +297,18 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
 
 template <class Src>
 int launch_fold(vm_map *m, const DevMap &dm, const Src &src, const unsigned long long *keys,
-                const unsigned *vals, long long R, long long M, int mode) {
+                const unsigned *vals, long long R, int mode) {
     cudaStream_t s = m->stream;
     const unsigned grid_cap = 148 * 16;
     if (mode == M_OCC || mode == M_DECAY) {
-        if (M > 0) {
-            int rc = ensure_buf(&m->d_start, &m->start_cap, (size_t)M + 1);
-            if (rc) return rc;
-            rc = ensure_buf(&m->d_big, &m->big_cap, (size_t)M + 1);
+        if (R > 0) {
+            int rc = ensure_buf(&m->d_big, &m->big_cap, (size_t)R / FOLD_SERIAL_MAX + 2);
             if (rc) return rc;
             cudaMemsetAsync(m->d_nbig, 0, sizeof(unsigned long long), s);
-            unsigned gh = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
-            k_heads<<<gh, BLOCK, 0, s>>>(dm, keys, R, m->d_start);
-            unsigned g = (unsigned)std::min<long long>((M + BLOCK - 1) / BLOCK, grid_cap);
-            k_fold_occ<<<g, BLOCK, 0, s>>>(dm, src, keys, R, (int)M, m->d_start, m->d_big,
-                                           m->d_nbig);
-            k_fold_occ_big<<<m->num_sms * 2, BLOCK, 0, s>>>(dm, src, keys, R, (int)M, m->d_start,
-                                                            m->d_big, m->d_nbig);
-            m->launches += 3;
+            unsigned g = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
+            k_fold_occ<<<g, BLOCK, 0, s>>>(dm, src, keys, R, m->d_big, m->d_nbig);
+            k_fold_occ_big<<<m->num_sms * 2, BLOCK, 0, s>>>(dm, src, keys, R, m->d_big, m->d_nbig);
+            m->launches += 2;
         }
     } else if (mode == M_NDT_OM || mode == M_NDT_TM) {
         unsigned g = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
@@ -370,9 +346,11 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     if (order_span >= (1ULL << 32))
         return fail(VM_ERR_ARG, "batch too large for 32-bit ray order keys; split it");
     const int order_bits = std::max(1, bitlen(order_span));
+    // record keys: voxel id above the order bits, bit 63 free (walk candidates)
+    if (order_bits + 1 + bitlen((unsigned long long)m->max_slots * (unsigned long long)m->vpr) > 63)
+        return fail(VM_ERR_ARG, "batch too large for 64-bit record keys; split it");
 
     int rc;
-    if ((rc = ensure_buf(&m->d_marked, &m->marked_cap, (size_t)n + 1))) return rc;
     const bool emit = mode == M_OCC || mode == M_DECAY;
     if (emit && (rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * maxseg + 1))) return rc;
     size_t rec_need = 0;
@@ -400,7 +378,6 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             static const int box_init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
             CK(cudaMemcpyAsync(m->d_rbox, box_init, sizeof(box_init), cudaMemcpyHostToDevice,
                                m->stream));
-            CK(cudaMemsetAsync(m->d_ztouch, 0, RG_MAX * sizeof(unsigned), m->stream));
         }
         CK(cudaEventRecord(m->ev_start, m->stream));
         dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK));
@@ -442,19 +419,19 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         int go = *((const int *)(hs + NUM_STATS) + 1);
         if (hs[S_RANGE_ERR]) {
             CK(cudaStreamSynchronize(m->stream));
-            long long M = std::min<long long>((long long)hs[S_MARKED], (long long)m->marked_cap);
-            if (M) k_cleanup<<<148, BLOCK, 0, m->stream>>>(dm, (int)M);
+            if (occ_det && hs[S_MARKED]) {
+                const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
+                k_clear_marks<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
+            }
             CK(cudaStreamSynchronize(m->stream));
             m->nreg = cursor;
             return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range "
                                       "(|region| < 2**20, keys.py:76-86)");
         }
         if (!go) {
-            // pool overflow: nothing was applied; grow and replay
+            // pool overflow: nothing was applied (the sample-voxel stamps are
+            // idempotent and re-made by the replay); grow and replay
             CK(cudaStreamSynchronize(m->stream));
-            long long M = std::min<long long>((long long)hs[S_MARKED], (long long)m->marked_cap);
-            if (M) k_cleanup<<<148, BLOCK, 0, m->stream>>>(dm, (int)M);
-            if ((rc = check_launch("cleanup"))) return rc;
             m->max_growth = std::max<long long>(m->max_growth, cursor - m->nreg);
             if ((rc = grow_pool(m, std::max<long long>(2 * m->cap,
                                                        cursor + 2 * margin + headroom))))
@@ -492,11 +469,8 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 CK(cudaStreamSynchronize(m->stream));
                 R = m->h_stats[NUM_STATS + 1];
             }
-            long long M = (long long)std::min<unsigned long long>(hs[S_MARKED], m->marked_cap);
-            int end_bit;
-            if (occ_det) end_bit = order_bits + std::max(1, bitlen((unsigned long long)M));
-            else end_bit = order_bits + (ndt ? 1 : 0) +
-                           std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
+            int end_bit = order_bits + (ndt ? 1 : 0) +
+                          std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
             end_bit = std::min(end_bit, 64);
             cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
             cub::DoubleBuffer<unsigned> dv(m->d_val, m->d_val2);
@@ -510,13 +484,8 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                                                       end_bit, m->stream));
             }
             CK(cudaEventRecord(m->ev_sort, m->stream));
-            if ((rc = launch_fold(m, dm, src, db.Current(), dv.Current(), (long long)R, M, mode)))
+            if ((rc = launch_fold(m, dm, src, db.Current(), dv.Current(), (long long)R, mode)))
                 return rc;
-            if (occ_det && M) {
-                k_cleanup<<<148, BLOCK, 0, m->stream>>>(dm, (int)M);
-                m->launches += 1;
-                if ((rc = check_launch("cleanup"))) return rc;
-            }
         }
         CK(cudaEventRecord(m->ev_end, m->stream));
         CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
@@ -610,7 +579,6 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
     m->device = device;
     m->dim = cfg->region_dim;
     m->vpr = cfg->region_dim * cfg->region_dim * cfg->region_dim;
-    m->mark_words = (m->vpr + 31) / 32;
     m->max_slots = std::min<long long>(1LL << 20, (long long)(0xFFFFFFFFull / (unsigned long long)m->vpr));
     unsigned long long ts = 1;
     while (ts < 2ULL * (unsigned long long)m->max_slots) ts <<= 1;
@@ -632,9 +600,9 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         (rc = dev_alloc(&m->d_slot_touch, m->max_slots)) ||
         (rc = dev_alloc(&m->d_slot_pref, m->max_slots)) || (rc = dev_alloc(&m->d_stats, NUM_STATS)) ||
         (rc = dev_alloc(&m->d_go, 1)) || (rc = dev_alloc(&m->d_touched, m->max_slots)) ||
-        (rc = dev_alloc(&m->d_bmask, m->max_slots)) || (rc = dev_alloc(&m->d_work, 1)) ||
+        (rc = dev_alloc(&m->d_work, 1)) ||
         (rc = dev_alloc(&m->d_rgrid, RG_MAX)) || (rc = dev_alloc(&m->d_rbox, 6)) ||
-        (rc = dev_alloc(&m->d_ztouch, RG_MAX)) ||
+        (rc = dev_alloc(&m->d_bmask, m->max_slots)) ||
         (rc = dev_alloc(&m->d_nbig, 1)))
         return cleanup(rc);
     for (int l = 0; l < NUM_LAYERS; ++l)
@@ -669,13 +637,10 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_slot_keys);
     cudaFree(m->d_slot_touch);
     cudaFree(m->d_slot_pref);
-    cudaFree(m->d_marks);
-    cudaFree(m->d_bmask);
     cudaFree(m->d_segs);
     cudaFree(m->d_work);
     cudaFree(m->d_rgrid);
-    cudaFree(m->d_ztouch);
-    cudaFree(m->d_start);
+    cudaFree(m->d_bmask);
     cudaFree(m->d_big);
     cudaFree(m->d_nbig);
     cudaFree(m->d_rbox);
@@ -685,7 +650,6 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_rec2);
     cudaFree(m->d_val);
     cudaFree(m->d_val2);
-    cudaFree(m->d_marked);
     cudaFree(m->d_touched);
     cudaFree(m->d_sort_tmp);
     cudaFree(m->d_rays);
@@ -705,13 +669,10 @@ int vm_map_reset(vm_map *m) {
     for (int l = 0; l < NUM_LAYERS; ++l)
         if (m->bpr[l] && m->nreg)
             CK(cudaMemsetAsync(m->slab[l], 0, (size_t)m->nreg * m->bpr[l], m->stream));
-    if (m->nreg)
-        CK(cudaMemsetAsync(m->d_marks, 0, (size_t)m->nreg * m->mark_words * sizeof(unsigned),
-                           m->stream));
     CK(cudaMemsetAsync(m->d_tkeys, 0xFF, m->tsize * sizeof(long long), m->stream));
     CK(cudaMemsetAsync(m->d_tvals, 0xFF, m->tsize * sizeof(int), m->stream));
     CK(cudaMemsetAsync(m->d_cursor, 0, sizeof(int), m->stream));
-    CK(cudaMemsetAsync(m->d_bmask, 0, m->max_slots * sizeof(unsigned long long), m->stream));
+    CK(cudaMemsetAsync(m->d_bmask, 0, m->max_slots * sizeof(unsigned), m->stream));
     CK(cudaStreamSynchronize(m->stream));
     m->nreg = 0;
     return VM_OK;

@@ -97,7 +97,11 @@ def test_kernels_integrate_occupancy_matches_reference_kernel(decay):
     # voxels that received a hit are order-dependent under CAS; all others exact
     hitvox = host["count"] > 0
     assert np.array_equal(out["occ"][~hitvox].view(np.uint32), host["occ"][~hitvox].view(np.uint32))
-    assert np.max(np.abs(out["occ"] - host["occ"])) <= 0.5  # clamp-order envelope (finding 4)
+    # mixed voxels: clamp-order envelope (SURVEY.md finding 4) -- bounded by the
+    # clamp range, and only a small share of the hit voxels may differ at all
+    d = np.abs(out["occ"] - host["occ"])
+    assert d.max() <= cfg.clamp_max - cfg.clamp_min
+    assert np.count_nonzero(d) <= 0.05 * np.count_nonzero(hitvox)
     single = host["count"] == 1
     assert np.array_equal(out["mean"][single], host["mean"][single])
     if decay:
