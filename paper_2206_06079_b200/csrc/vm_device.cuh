@@ -27,14 +27,19 @@ enum Mode { M_OCC = 0, M_DECAY = 1, M_NDT_OM = 2, M_NDT_TM = 3, M_TSDF = 4 };
 enum Stat {
     S_RAYS_IN = 0, S_PROCESSED, S_SEGMENTS, S_VISITS, S_RETRIES, S_FAILURES,
     S_RMISS, S_PREF_TOUCHED, S_RECORDS, S_MARKED, S_WALK_TOUCHED, S_RANGE_ERR,
-    S_CUBE_FLUSH, S_SEGDESC, S_WORK, S_RGRID, S_SEGDESC2, NUM_STATS
+    S_CUBE_FLUSH, S_SEGDESC, S_WORK, S_RGRID, NUM_STATS
 };
 
 constexpr unsigned MARK_FLAG = 0x80000000u;
 constexpr int CUBE = 16;                 // smem aggregation cube edge (voxels)
 constexpr int CUBE_N = CUBE * CUBE * CUBE;
 constexpr int SLOTSET = 256;             // per-block region dedupe set
-constexpr int RG_MAX = 1 << 16;          // dense per-batch region grid cells (HBM, L1-cached)
+constexpr int RG_MAX = 1 << 16;
+constexpr int SEG_BUCKETS = 64;          // step-count buckets of the walk's longest-first order
+__host__ __device__ __forceinline__ int seg_bucket(unsigned rem) {
+    const unsigned b = rem >> 4;
+    return b < (unsigned)SEG_BUCKETS ? (int)b : SEG_BUCKETS - 1;
+}          // dense per-batch region grid cells (HBM, L1-cached)
 
 // One preprocessed segment with its DDA initial state (k_discover writes
 // it, the persistent walk consumes it): 96 bytes, 16-byte aligned.
@@ -80,13 +85,17 @@ struct DevMap {
     int *rgrid;                          // dense region-slot grid over the batch bbox
     unsigned *bmask;                     // per slot: brick summary of the batch's sample voxels
     int brick_shift;                     // log2(dim) - 2 for power-of-two dims >= 4, else -1
+    int bsh[3];                          // brick index from the local index li (see brick_of)
     int *rbox;                           // [6]: min xyz, max xyz (regions) of the batch
     int rg_max;                          // capacity of rgrid (cells)
     SegDesc *segs;                       // preprocessed segments of the batch
+    unsigned *perm;                      // walk order of the segments (longest first)
+    unsigned *seg_hist, *seg_cursor;     // [SEG_BUCKETS] counting-sort state
     unsigned long long seg_cap;
     unsigned long long *work;            // persistent-walk work counter
     unsigned long long *stats;
     int *go;                             // batch guard (0 = skip, replay later)
+    int walk_det_launched;               // k_walk_det runs before k_walk (deterministic occupancy)
     // batch outputs
     unsigned long long *rec;
     unsigned *recval;                    // per-record value (NDT deterministic phase 1)
@@ -192,6 +201,14 @@ __device__ __forceinline__ void fold_mean(unsigned &packed, unsigned &count, con
     for (int a = 0; a < 3; ++a) m[a] = m[a] + (s[a] - m[a]) / div;
     packed = pack_mean(m);
     count += 1;
+}
+
+// Brick (4 x 4 x 2 per region, i.e. 8 x 8 x 16 voxels at dim 32) of local
+// index li = lx + dim * (ly + dim * lz), for power-of-two dims: bit index of
+// the per-region sample-voxel summary.
+__device__ __forceinline__ unsigned brick_of(int li, const int bsh[3]) {
+    return (((unsigned)li >> bsh[0]) & 3u) | (((unsigned)li >> bsh[1]) & 0xCu) |
+           (((unsigned)li >> bsh[2]) & 0x10u);
 }
 
 // ---------------------------------------------------------------- rays
@@ -301,7 +318,7 @@ __device__ __forceinline__ int wait_slot(const DevMap &m, unsigned long long h) 
     return v;
 }
 
-__device__ __noinline__ int region_slot_slow(const DevMap &m, long long key) {
+__device__ __forceinline__ int region_slot_probe(const DevMap &m, long long key) {
     unsigned long long h = mix_key(key) & m.tmask;
     for (unsigned long long probe = 0; probe <= m.tmask; ++probe) {
         long long k = ((volatile long long *)m.tkeys)[h];
@@ -336,6 +353,33 @@ __device__ __noinline__ int region_find(const DevMap &m, long long key) {
         h = (h + 1) & m.tmask;
     }
     return -1;
+}
+
+__device__ __noinline__ int region_slot_slow(const DevMap &m, long long key) {
+    return region_slot_probe(m, key);
+}
+
+// Lookup only (never creates): slot or -1.
+__device__ __forceinline__ int region_find_probe(const DevMap &m, long long key) {
+    unsigned long long h = mix_key(key) & m.tmask;
+    for (unsigned long long probe = 0; probe <= m.tmask; ++probe) {
+        const long long k = ((volatile long long *)m.tkeys)[h];
+        if (k == key) return wait_slot(m, h);
+        if (k == -1) return -1;
+        h = (h + 1) & m.tmask;
+    }
+    return -1;
+}
+
+// Same as region_slot, fully inlined (no call ABI inside register-heavy loops).
+__device__ __forceinline__ int region_slot_inl(const DevMap &m, long long key) {
+    unsigned long long h = mix_key(key) & m.tmask;
+    long long k = m.tkeys[h];
+    if (k == key) {
+        int v = m.tvals[h];
+        if (v >= 0) return v;
+    }
+    return region_slot_probe(m, key);
 }
 
 __device__ __forceinline__ int region_slot(const DevMap &m, long long key) {

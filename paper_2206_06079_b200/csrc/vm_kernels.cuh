@@ -317,6 +317,8 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     __shared__ unsigned long long srec[BLOCK];
     __shared__ int nrec;
     __shared__ unsigned long long rec_base;
+    __shared__ unsigned shist[SEG_BUCKETS];
+    for (int i = threadIdx.x; i < SEG_BUCKETS; i += blockDim.x) shist[i] = 0u;
     __shared__ int anchor[3];
     for (int i = threadIdx.x; i < KCACHE; i += blockDim.x) kcache[i] = 0ULL;
     for (int i = threadIdx.x; i < SLOTSET; i += blockDim.x) sset[i] = -1;
@@ -354,36 +356,20 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
             }
         }
     }
-    // warp-aggregated allocation of segment descriptors in two queues: long
-    // segments (>= half the segment length) from the front of the buffer,
-    // short ones from the back, so the walk takes the long ones first and
-    // the tail of the batch is made of short segments
-    unsigned long long fbase = 0, bbase = 0;
-    bool last_long = false;
+    // warp-aggregated allocation of segment descriptors
+    unsigned long long dbase = 0;
     if (emit) {
-        unsigned kl = 0, ks = 0;
-        if (ok) {
-            const double last_len = r.L - (double)(r.nseg - 1) * m.seg_len;
-            last_long = last_len >= 0.5 * m.seg_len;
-            kl = (unsigned)(r.nseg - 1) + (last_long ? 1u : 0u);
-            ks = last_long ? 0u : 1u;
-        }
-        unsigned il = kl, is = ks;
+        unsigned k = ok ? (unsigned)r.nseg : 0u, incl = k;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned vl = __shfl_up_sync(0xffffffffu, il, o);
-            const unsigned vs = __shfl_up_sync(0xffffffffu, is, o);
-            if (lane >= o) {
-                il += vl;
-                is += vs;
-            }
+            unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
         }
-        const unsigned tl = __shfl_sync(0xffffffffu, il, 31), ts = __shfl_sync(0xffffffffu, is, 31);
-        unsigned long long bl = 0, bs = 0;
-        if (lane == 0 && tl) bl = atomicAdd(m.stats + S_SEGDESC, (unsigned long long)tl);
-        if (lane == 0 && ts) bs = atomicAdd(m.stats + S_SEGDESC2, (unsigned long long)ts);
-        fbase = __shfl_sync(0xffffffffu, bl, 0) + (il - kl);
-        bbase = __shfl_sync(0xffffffffu, bs, 0) + (is - ks);
+        unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (lane == 0 && total) base = atomicAdd(m.stats + S_SEGDESC, (unsigned long long)total);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        dbase = base + (incl - k);
     }
     PrefetchVisitor pv{&m, &kc, sset, {INT_MAX, INT_MAX, INT_MAX}, {INT_MIN, INT_MIN, INT_MIN}};
     if (ok) {
@@ -406,10 +392,7 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                 }
             }
             walk(so, pe, m.rsize, pv);
-            // queue slot of this segment (front: long, back: short)
-            const bool in_front = s < r.nseg - 1 || last_long;
-            const unsigned long long qi = in_front ? fbase + s : bbase;
-            if (emit && qi < m.seg_cap) {
+            if (emit && dbase + s < m.seg_cap) {
                 SegDesc sd;
                 int c[3];
                 dda_init(so, se, m.vox, sd, c);
@@ -424,7 +407,8 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                          ((unsigned)(c[2] - rz * m.dim + 1) << 20);
                 sd.L = norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2]);
                 const uint4 *src4 = reinterpret_cast<const uint4 *>(&sd);
-                uint4 *dst4 = reinterpret_cast<uint4 *>(m.segs + (in_front ? qi : m.seg_cap - 1 - qi));
+                atomicAdd(shist + seg_bucket(sd.rem), 1u);
+                uint4 *dst4 = reinterpret_cast<uint4 *>(m.segs + dbase + s);
 #pragma unroll
                 for (int q = 0; q < (int)(sizeof(SegDesc) / 16); ++q) dst4[q] = src4[q];
             }
@@ -472,6 +456,9 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     if (threadIdx.x == 0) {
         if (nrec) rec_base = atomicAdd(m.stats + S_RECORDS, (unsigned long long)nrec);
     }
+    if (emit)
+        for (int i = threadIdx.x; i < SEG_BUCKETS; i += blockDim.x)
+            if (shist[i]) atomicAdd(m.seg_hist + i, shist[i]);
     __syncthreads();
     for (int k = threadIdx.x; k < nrec; k += blockDim.x) {
         unsigned long long ri = rec_base + k;
@@ -533,10 +520,43 @@ __global__ void k_rgrid(const __grid_constant__ DevMap m) {
 __global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
     int used = *((volatile int *)m.cursor);
     unsigned long long rerr = ((volatile unsigned long long *)m.stats)[S_RANGE_ERR];
-    unsigned long long nseg = ((volatile unsigned long long *)m.stats)[S_SEGDESC] +
-                              ((volatile unsigned long long *)m.stats)[S_SEGDESC2];
+    unsigned long long nseg = ((volatile unsigned long long *)m.stats)[S_SEGDESC];
     bool ok = used + margin <= m.cap && rerr == 0 && nseg <= m.seg_cap;
     *m.go = ok ? 1 : 0;
+}
+
+// Counting sort of the batch's segments by step count, longest first: the
+// walk then hands every warp 32 segments of nearly equal length.  k_discover
+// built the histogram; one block turns it into bucket cursors.
+__global__ void k_seg_scan(const __grid_constant__ DevMap m) {
+    if (threadIdx.x != 0) return;
+    unsigned run = 0;
+    for (int b = SEG_BUCKETS - 1; b >= 0; --b) {
+        m.seg_cursor[b] = run;
+        run += m.seg_hist[b];
+        m.seg_hist[b] = 0u;  // ready for the next batch (or the replay)
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK) k_seg_scatter(const __grid_constant__ DevMap m) {
+    __shared__ unsigned cnt[SEG_BUCKETS], base[SEG_BUCKETS];
+    if (!read_go(m)) return;
+    const unsigned long long n =
+        min(*((volatile unsigned long long *)(m.stats + S_SEGDESC)), m.seg_cap);
+    for (int i = threadIdx.x; i < SEG_BUCKETS; i += blockDim.x) cnt[i] = 0u;
+    __syncthreads();
+    const unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int b = -1;
+    unsigned r = 0;
+    if (idx < n) {
+        b = seg_bucket(m.segs[idx].rem);
+        r = atomicAdd(cnt + b, 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SEG_BUCKETS; i += blockDim.x)
+        if (cnt[i]) base[i] = atomicAdd(m.seg_cursor + i, cnt[i]);
+    __syncthreads();
+    if (b >= 0) m.perm[base[b] + r] = (unsigned)idx;
 }
 
 // --------------------------------------------------------------- NDT phase 1

@@ -18,6 +18,7 @@
 #include "../../include/voxmap_b200.h"
 #include "vm_walk.cuh"
 #include "vm_compat.cuh"
+#include "vm_walk_det.cuh"
 
 using namespace vm;
 
@@ -80,6 +81,9 @@ struct vm_map {
     unsigned *d_slot_touch = nullptr, *d_slot_pref = nullptr;
     SegDesc *d_segs = nullptr;
     size_t seg_cap = 0;
+    unsigned *d_perm = nullptr;
+    size_t perm_cap = 0;
+    unsigned *d_seg_hist = nullptr, *d_seg_cursor = nullptr;
     unsigned long long *d_work = nullptr;
     int *d_rgrid = nullptr;
     unsigned *d_bmask = nullptr;
@@ -153,10 +157,19 @@ DevMap make_dm(const vm_map *m) {
             while ((1 << (bs + 2)) < m->dim) ++bs;
         }
         d.brick_shift = bs;
+        int k = 0;
+        while ((1 << k) < m->dim) ++k;
+        // lx >> bs, (ly >> bs) << 2, (lz >> (bs + 1)) << 4 taken straight from li
+        d.bsh[0] = bs < 0 ? 0 : bs;
+        d.bsh[1] = bs < 0 ? 0 : k + bs - 2;
+        d.bsh[2] = bs < 0 ? 0 : 2 * k + bs - 3;
     }
     d.rbox = m->d_rbox;
     d.rg_max = RG_MAX;
     d.segs = m->d_segs;
+    d.perm = m->d_perm;
+    d.seg_hist = m->d_seg_hist;
+    d.seg_cursor = m->d_seg_cursor;
     d.seg_cap = m->seg_cap;
     d.work = m->d_work;
     d.stats = m->d_stats;
@@ -240,6 +253,18 @@ int check_launch(const char *what) {
     return VM_OK;
 }
 
+template <bool REC_ONLY, class Src>
+void launch_wd(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
+    static bool configured = false;
+    const size_t smem = sizeof(WalkDetSmem);
+    if (!configured) {
+        cudaFuncSetAttribute(k_walk_det<REC_ONLY, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured = true;
+    }
+    k_walk_det<REC_ONLY, Src><<<grid, BLOCK, smem, s>>>(dm, src);
+}
+
 template <int MODE, bool DET, bool REC_ONLY, class Src>
 void launch_w3(dim3 grid, size_t smem, cudaStream_t s, const DevMap &dm, const Src &src) {
     static bool configured = false;
@@ -267,9 +292,19 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
     const size_t smem = sizeof(WalkSmem);
     switch (mode) {
     case M_OCC:
-        if (det && rec_only) launch_w3<M_OCC, true, true>(pgrid, smem, s, dm, src);
-        else if (det) launch_w3<M_OCC, true, false>(pgrid, smem, s, dm, src);
-        else launch_w3<M_OCC, false, false>(pgrid, smem, s, dm, src);
+        if (det) {
+            // the lean deterministic walk; the generic one below exits unless
+            // the batch's box is too large for it (walk_det_ok)
+            DevMap d2 = dm;
+            d2.walk_det_launched = 1;
+            if (rec_only) launch_wd<true>(pgrid, s, d2, src);
+            else launch_wd<false>(pgrid, s, d2, src);
+            if (rec_only) launch_w3<M_OCC, true, true>(pgrid, smem, s, d2, src);
+            else launch_w3<M_OCC, true, false>(pgrid, smem, s, d2, src);
+            m->launches += 1;
+        } else {
+            launch_w3<M_OCC, false, false>(pgrid, smem, s, dm, src);
+        }
         break;
     case M_DECAY:
         if (det && rec_only) launch_w3<M_DECAY, true, true>(pgrid, smem, s, dm, src);
@@ -353,6 +388,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     int rc;
     const bool emit = mode == M_OCC || mode == M_DECAY;
     if (emit && (rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * maxseg + 1))) return rc;
+    if (emit && (rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
     size_t rec_need = 0;
     if (ndt) rec_need = std::max<size_t>(m->rec_cap, (size_t)n * (det ? 8 : 1) + 1);
     else if (tsdf && det) {
@@ -388,7 +424,9 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
         if (emit) {
             k_rgrid<<<16, BLOCK, 0, m->stream>>>(dm);
-            m->launches += 1;
+            k_seg_scan<<<1, 32, 0, m->stream>>>(dm);
+            k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, m->stream>>>(dm);
+            m->launches += 3;
         }
         CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, m->stream));
@@ -603,6 +641,8 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         (rc = dev_alloc(&m->d_work, 1)) ||
         (rc = dev_alloc(&m->d_rgrid, RG_MAX)) || (rc = dev_alloc(&m->d_rbox, 6)) ||
         (rc = dev_alloc(&m->d_bmask, m->max_slots)) ||
+        (rc = dev_alloc(&m->d_seg_hist, SEG_BUCKETS)) ||
+        (rc = dev_alloc(&m->d_seg_cursor, SEG_BUCKETS)) ||
         (rc = dev_alloc(&m->d_nbig, 1)))
         return cleanup(rc);
     for (int l = 0; l < NUM_LAYERS; ++l)
@@ -638,6 +678,9 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_slot_touch);
     cudaFree(m->d_slot_pref);
     cudaFree(m->d_segs);
+    cudaFree(m->d_perm);
+    cudaFree(m->d_seg_hist);
+    cudaFree(m->d_seg_cursor);
     cudaFree(m->d_work);
     cudaFree(m->d_rgrid);
     cudaFree(m->d_bmask);

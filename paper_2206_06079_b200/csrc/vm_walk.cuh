@@ -29,9 +29,11 @@
 // CAS mode: the paper's clamped compare-and-swap update (_kernels.pyx:233-
 // 271); the load is issued one step ahead of the CAS.
 //
-// Lanes whose segment ends swap in the descriptor they prefetched into
-// their own smem slot (cp.async); work is pulled 32 segments at a time, long
-// segments first.
+// Work: segments are walked longest first (k_seg_scan / k_seg_scatter
+// counting-sort them by step count), 32 per warp claim, so the lanes of a
+// warp run segments of nearly equal length and the batch ends on short
+// ones.  Lanes whose segment ends swap in the descriptor they prefetched
+// into their own smem slot (cp.async).
 #pragma once
 
 #include <cuda_pipeline.h>
@@ -142,9 +144,11 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk(const __grid_constant
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WalkSmem &sm = *reinterpret_cast<WalkSmem *>(smem_raw);
     if (!read_go(m)) return;
-    const unsigned long long nfront = *((volatile unsigned long long *)(m.stats + S_SEGDESC));
+    if (DET && MODE == M_OCC && m.walk_det_launched && m.rbox[3] - m.rbox[0] < 509 &&
+        m.rbox[4] - m.rbox[1] < 509 && m.rbox[5] - m.rbox[2] < 509)
+        return;  // k_walk_det handled the batch
     const unsigned long long nseg_total =
-        min(nfront + *((volatile unsigned long long *)(m.stats + S_SEGDESC2)), m.seg_cap);
+        min(*((volatile unsigned long long *)(m.stats + S_SEGDESC)), m.seg_cap);
     const bool have_grid = *((volatile unsigned long long *)(m.stats + S_RGRID)) != 0;
     if (threadIdx.x == 0) {
         for (int a = 0; a < 3; ++a) {
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk(const __grid_constant
         }
         sm.gsmem = sm.gn[0] * sm.gn[1] * sm.gn[2] <= RG_SMEM;
         if (nseg_total) {
-            const SegDesc &d0 = m.segs[nfront ? 0 : m.seg_cap - 1];
+            const SegDesc &d0 = m.segs[0];
             int r0[3];
             unpack_region(d0.rkey, r0);
             for (int a = 0; a < 3; ++a)
@@ -450,9 +454,8 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk(const __grid_constant
             if (served) {
                 const unsigned long long w = (unsigned long long)pool_next + rank;
                 if (w < nseg_total) {
-                    // long segments from the front of the buffer, then short ones from the back
-                    const unsigned long long idx = w < nfront ? w : m.seg_cap - 1 - (w - nfront);
-                    const char *g = reinterpret_cast<const char *>(m.segs + idx);
+                    // longest segments first (k_seg_order)
+                    const char *g = reinterpret_cast<const char *>(m.segs + m.perm[w]);
 #pragma unroll
                     for (int q = 0; q < (int)(sizeof(SegDesc) / 16); ++q)
                         __pipeline_memcpy_async(reinterpret_cast<char *>(my_pf) + 16 * q,

@@ -1,0 +1,399 @@
+// vm_walk_det.cuh -- the deterministic occupancy walk (the hot kernel of the
+// default path).
+//
+// Same walk as k_walk (vm_walk.cuh): one warp = 32 lanes, each walking one
+// preprocessed segment with the exact fp64 DDA of traversal._walk_grid
+// (traversal.py:80-111), longest segments first.  What differs is the visit:
+// every visit is exactly ONE atomic add with return on the voxel's scratch
+// counter (or, around the sensor, on the block's shared-memory cube counter;
+// both through one generic-address ATOM, so there is no branch).  The counter
+// is the order-free miss count resolved as f_miss^k by k_resolve; k_discover
+// stamped MARK_FLAG into the counters of the batch's sample voxels, so the
+// returned old value says whether the visit must become an order-keyed
+// record (voxel id, ray order, hit) for the in-order fold instead.
+//
+// The step is written for the common case.  The eight steps of a window are
+// unrolled, each into its own in-flight slot (old value, voxel id), and the
+// returned values are inspected together at the end of the window: one
+// memory latency per eight visits.  Region crossings step a grid index
+// through the batch's dense region grid (shared memory); only a crossing out
+// of the grid probes the hash table.  Segment starts happen at window
+// boundaries.
+#pragma once
+
+#include "vm_walk.cuh"
+
+namespace vm {
+
+constexpr int WD_STEPS = 8;   // steps per window (in-flight visits per lane)
+constexpr int RP_BIAS = 512;  // bias of the grid-relative region coordinates
+
+struct WalkDetSmem {
+    unsigned cube[WCUBE_N];  // miss counts around the sensor (MARK_FLAG: sample voxel)
+    int grid[RG_SMEM];
+    unsigned long long wbuf[BLOCK / 32][WK_WBUF];
+    unsigned vids[WD_STEPS][BLOCK];  // voxel id of each in-flight visit
+    SegDesc pf[BLOCK];
+    int endc[BLOCK][3];
+    int gb[3], gn[3], gs[3];  // grid origin, extents, strides (1, nx, nx*ny)
+    int anchor[3];
+    int gmode;                // 1: grid in smem, 2: grid in global memory, 0: hash only
+};
+
+// region slot for grid-relative coordinates packed in rp (fields biased by
+// RP_BIAS); inserts walk-entered regions like the generic walk
+__device__ __noinline__ int wd_slow_region(const DevMap &m, const WalkDetSmem &sm, unsigned rp) {
+    const int rx = sm.gb[0] + (int)(rp & 1023u) - RP_BIAS;
+    const int ry = sm.gb[1] + (int)((rp >> 10) & 1023u) - RP_BIAS;
+    const int rz = sm.gb[2] + (int)(rp >> 20) - RP_BIAS;
+    const unsigned ux = (unsigned)(rx - sm.gb[0]), uy = (unsigned)(ry - sm.gb[1]),
+                   uz = (unsigned)(rz - sm.gb[2]);
+    if (sm.gmode && ux < (unsigned)sm.gn[0] && uy < (unsigned)sm.gn[1] && uz < (unsigned)sm.gn[2]) {
+        const int gi = ux + sm.gs[1] * uy + sm.gs[2] * uz;
+        const int s = sm.gmode == 1 ? sm.grid[gi] : __ldg(m.rgrid + gi);
+        if (s >= 0) return s;
+    }
+    const int slot = region_slot_inl(m, pack_region(rx, ry, rz));
+    if (slot >= 0 && slot < m.cap && atomicExch(m.slot_touch + slot, m.epoch) != m.epoch) {
+        const unsigned long long t = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
+        if (t < (unsigned long long)m.touched_cap) m.touched[t] = slot;
+    }
+    return slot;
+}
+
+__device__ __noinline__ unsigned wd_vid_of(const DevMap &m, const WalkDetSmem &sm, int gx, int gy,
+                                           int gz, bool insert) {
+    const int rx = floordiv(gx, m.dim), ry = floordiv(gy, m.dim), rz = floordiv(gz, m.dim);
+    int s;
+    const unsigned ux = (unsigned)(rx - sm.gb[0]), uy = (unsigned)(ry - sm.gb[1]),
+                   uz = (unsigned)(rz - sm.gb[2]);
+    if (sm.gmode && ux < (unsigned)sm.gn[0] && uy < (unsigned)sm.gn[1] && uz < (unsigned)sm.gn[2]) {
+        const int gi = ux + sm.gs[1] * uy + sm.gs[2] * uz;
+        s = sm.gmode == 1 ? sm.grid[gi] : __ldg(m.rgrid + gi);
+        if (s < 0) s = insert ? region_slot_inl(m, pack_region(rx, ry, rz)) : -1;
+    } else {
+        s = insert ? region_slot_inl(m, pack_region(rx, ry, rz))
+                   : region_find_probe(m, pack_region(rx, ry, rz));
+        if (s >= 0 && s < m.cap && atomicExch(m.slot_touch + s, m.epoch) != m.epoch) {
+            const unsigned long long t = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
+            if (t < (unsigned long long)m.touched_cap) m.touched[t] = s;
+        }
+    }
+    if (s < 0 || s >= m.cap) return 0xFFFFFFFFu;
+    return (unsigned)s * (unsigned)m.vpr +
+           (unsigned)((gx - rx * m.dim) + m.dim * ((gy - ry * m.dim) + m.dim * (gz - rz * m.dim)));
+}
+
+// The grid-relative region coordinates must stay inside their 10-bit fields:
+// batches whose prefetched box spans RP_BIAS - 2 regions or more on an axis
+// (800 m at 0.05 m voxels) take the generic walk (k_walk) instead.
+__device__ __forceinline__ bool walk_det_ok(const DevMap &m) {
+    return m.rbox[3] - m.rbox[0] < RP_BIAS - 3 && m.rbox[4] - m.rbox[1] < RP_BIAS - 3 &&
+           m.rbox[5] - m.rbox[2] < RP_BIAS - 3;
+}
+
+template <bool REC_ONLY, class Src>
+__global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_constant__ DevMap m,
+                                                               Src src) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WalkDetSmem &sm = *reinterpret_cast<WalkDetSmem *>(smem_raw);
+    if (!read_go(m) || !walk_det_ok(m)) return;
+    const unsigned long long nseg_total =
+        min(*((volatile unsigned long long *)(m.stats + S_SEGDESC)), m.seg_cap);
+    const bool have_grid = *((volatile unsigned long long *)(m.stats + S_RGRID)) != 0;
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 3; ++a) {
+            sm.gb[a] = m.rbox[a];
+            sm.gn[a] = have_grid ? m.rbox[3 + a] - m.rbox[a] + 1 : 0;
+        }
+        sm.gs[0] = 1;
+        sm.gs[1] = sm.gn[0];
+        sm.gs[2] = sm.gn[0] * sm.gn[1];
+        const int ncell = sm.gn[0] * sm.gn[1] * sm.gn[2];
+        sm.gmode = !have_grid ? 0 : (ncell <= RG_SMEM ? 1 : 2);
+        if (nseg_total) {
+            const SegDesc &d0 = m.segs[0];
+            int r0[3];
+            unpack_region(d0.rkey, r0);
+            for (int a = 0; a < 3; ++a)
+                sm.anchor[a] = r0[a] * m.dim + (int)((d0.lp0 >> (10 * a)) & 1023u) - 1 - WCUBE / 2;
+        } else {
+            sm.anchor[0] = sm.anchor[1] = sm.anchor[2] = 1 << 29;
+        }
+    }
+    __syncthreads();
+    if (sm.gmode == 1) {
+        const int ncell = sm.gn[0] * sm.gn[1] * sm.gn[2];
+        for (int k = threadIdx.x; k < ncell; k += blockDim.x) sm.grid[k] = m.rgrid[k];
+    }
+    __syncthreads();
+    unsigned *const scr = reinterpret_cast<unsigned *>(m.slab[L_SCRATCH]);
+    for (int k = threadIdx.x; k < WCUBE_N; k += blockDim.x) {
+        const unsigned vid = wd_vid_of(m, sm, sm.anchor[0] + k % WCUBE,
+                                       sm.anchor[1] + (k / WCUBE) % WCUBE,
+                                       sm.anchor[2] + k / (WCUBE * WCUBE), false);
+        sm.cube[k] = vid != 0xFFFFFFFFu ? (__ldcg(scr + vid) & MARK_FLAG) : 0u;
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+    const int dim = m.dim;
+    const unsigned vpr = (unsigned)m.vpr;
+    const int ob = m.order_bits;
+    unsigned long long *const wbuf = sm.wbuf[threadIdx.x >> 5];
+    unsigned wcnt = 0, wflushed = 0;  // warp-uniform record ring counters
+    unsigned rmiss = 0, visits = 0;
+
+    // segment state
+    double tx = 0, ty = 0, tz = 0, dx = 0, dy = 0, dz = 0;
+    unsigned lp = 0, rp = 0, vbase = 0xFFFFFFFFu, okey = 0, cp = 0;
+    int li = 0, gi = 0, rem = 0;
+    int dli0 = 0, dli1 = 0, dli2 = 0;       // local-index step per axis
+    unsigned dlp0 = 0, dlp1 = 0, dlp2 = 0;  // packed-coordinate step per axis
+    bool active = false, in_cube = false, ingrid = false;
+    // rare events park the lane until the window boundary, where they are
+    // resolved outside the unrolled steps (no call inside them)
+    int parked = 0;  // 1: region lookup after a crossing, 2: fallback jump to the end cell
+    bool jumped = false;
+    // in-flight visits of the window
+    unsigned olds[WD_STEPS];
+    unsigned live = 0, hits = 0;  // bit q: slot q holds a visit / the hit
+    // prefetch + warp work pool
+    bool pf_valid = false, exhausted = false;
+    unsigned pool_next = 0, pool_end = 0;
+    SegDesc *my_pf = &sm.pf[threadIdx.x];
+
+    auto push_records = [&](bool rec, unsigned long long key) {
+        const unsigned rb = __ballot_sync(0xffffffffu, rec);
+        if (!rb) return;
+        if (rec) wbuf[(wcnt + __popc(rb & lanemask_lt)) & (WK_WBUF - 1)] = key;
+        wcnt += __popc(rb);
+        if (wcnt - wflushed >= 32) {
+            __syncwarp();
+            unsigned long long b = 0;
+            if (lane == 0) b = atomicAdd(m.stats + S_RECORDS, 32ULL);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (b + lane < m.rec_cap) m.rec[b + lane] = wbuf[(wflushed + lane) & (WK_WBUF - 1)];
+            wflushed += 32;
+            __syncwarp();
+        }
+    };
+
+    auto set_region = [&](int s) { vbase = s >= 0 && s < m.cap ? (unsigned)s * vpr : 0xFFFFFFFFu; };
+
+    auto start = [&]() {
+        __pipeline_wait_prior(0);
+        const SegDesc &d = *my_pf;
+        tx = d.t[0]; ty = d.t[1]; tz = d.t[2];
+        dx = d.d[0]; dy = d.d[1]; dz = d.d[2];
+        const unsigned codes = d.flags;
+        okey = d.order | (codes & 1u);
+        rem = (int)d.rem;
+        visits += (unsigned)rem + 1u;
+        lp = d.lp0;
+        li = (int)(lp & 1023u) - 1 +
+             dim * ((int)((lp >> 10) & 1023u) - 1 + dim * ((int)(lp >> 20) - 1));
+        const int sx = (int)((codes >> 1) & 3u) - 1, sy = (int)((codes >> 3) & 3u) - 1,
+                  sz = (int)((codes >> 5) & 3u) - 1;
+        dli0 = sx;
+        dli1 = sy * dim;
+        dli2 = sz * dim * dim;
+        dlp0 = (unsigned)sx;
+        dlp1 = (unsigned)sy << 10;
+        dlp2 = (unsigned)sz << 20;
+        int r0[3];
+        unpack_region(d.rkey, r0);
+        const int u0 = r0[0] - sm.gb[0], u1 = r0[1] - sm.gb[1], u2 = r0[2] - sm.gb[2];
+        rp = (unsigned)(u0 + RP_BIAS) | ((unsigned)(u1 + RP_BIAS) << 10) |
+             ((unsigned)(u2 + RP_BIAS) << 20);
+        ingrid = sm.gmode && (unsigned)u0 < (unsigned)sm.gn[0] && (unsigned)u1 < (unsigned)sm.gn[1] &&
+                 (unsigned)u2 < (unsigned)sm.gn[2];
+        gi = u0 + sm.gs[1] * u1 + sm.gs[2] * u2;
+        int s = -1;
+        if (ingrid) s = sm.gmode == 1 ? sm.grid[gi] : __ldg(m.rgrid + gi);
+        if (s < 0) s = wd_slow_region(m, sm, rp);
+        set_region(s);
+        sm.endc[threadIdx.x][0] = d.e[0];
+        sm.endc[threadIdx.x][1] = d.e[1];
+        sm.endc[threadIdx.x][2] = d.e[2];
+        const unsigned ux = (unsigned)(r0[0] * dim + (int)(lp & 1023u) - 1 - sm.anchor[0]);
+        const unsigned uy = (unsigned)(r0[1] * dim + (int)((lp >> 10) & 1023u) - 1 - sm.anchor[1]);
+        const unsigned uz = (unsigned)(r0[2] * dim + (int)(lp >> 20) - 1 - sm.anchor[2]);
+        in_cube = (ux | uy | uz) < (unsigned)WCUBE;
+        cp = ux | (uy << 8) | (uz << 16);
+        pf_valid = false;
+        active = true;
+        jumped = false;
+    };
+
+    // one DDA step = one voxel visit into in-flight slot Q (common case only)
+    auto step = [&](const int Q) {
+        if (!active) return;
+        const bool last = rem == 0;
+        if (last) {
+            if (!jumped) {
+                const int gx = sm.gb[0] + (int)(rp & 1023u) - RP_BIAS;
+                const int gy = sm.gb[1] + (int)((rp >> 10) & 1023u) - RP_BIAS;
+                const int gz = sm.gb[2] + (int)(rp >> 20) - RP_BIAS;
+                const int cx = gx * dim + (int)(lp & 1023u) - 1;
+                const int cy = gy * dim + (int)((lp >> 10) & 1023u) - 1;
+                const int cz = gz * dim + (int)(lp >> 20) - 1;
+                if (cx != sm.endc[threadIdx.x][0] || cy != sm.endc[threadIdx.x][1] ||
+                    cz != sm.endc[threadIdx.x][2]) {
+                    // numerical fallback: the walk jumps to the end cell (traversal.py:88-92)
+                    parked = 2;
+                    active = false;
+                    return;
+                }
+            }
+            if (okey & 1u) hits |= 1u << Q;
+        }
+        // ---- the visit: one atomic, result checked at the end of the window ----
+        const unsigned vid = vbase + (unsigned)li;
+        if (vbase != 0xFFFFFFFFu) {
+            unsigned *p = scr + vid;
+            if (in_cube) p = sm.cube + ((cp & 7u) | ((cp >> 5) & 0x38u) | ((cp >> 10) & 0x1C0u));
+            olds[Q] = REC_ONLY ? *((volatile unsigned *)p) : atomicAdd(p, 1u);
+            sm.vids[Q][threadIdx.x] = vid;
+            live |= 1u << Q;
+        } else {
+            ++rmiss;
+        }
+        if (last) {
+            active = false;
+            return;
+        }
+        // ---- advance (t_max[axis] += t_delta[axis]) ----
+        --rem;
+        const int ax = dda_advance(tx, ty, tz, dx, dy, dz);
+        const int dl = ax == 2 ? dli2 : (ax == 1 ? dli1 : dli0);
+        const unsigned dp = ax == 2 ? dlp2 : (ax == 1 ? dlp1 : dlp0);
+        const int sh = 10 * ax;
+        lp += dp;
+        li += dl;
+        if (in_cube) {
+            cp += (unsigned)((int)dp >> sh) << (8 * ax);  // the step (+-1) into the cube field
+            in_cube = (cp & 0x00F8F8F8u) == 0;
+        }
+        if (((lp >> sh) & 1023u) - 1u >= (unsigned)dim) {
+            // region crossing: wrap the local coordinate, step the grid index
+            lp -= (unsigned)dim * dp;
+            li -= dim * dl;
+            rp += dp;
+            const unsigned f = ((rp >> sh) & 1023u) - RP_BIAS;
+            gi += ((int)dp >> sh) * sm.gs[ax];
+            ingrid = ingrid && f < (unsigned)sm.gn[ax];
+            int s = -1;
+            if (ingrid) s = sm.gmode == 1 ? sm.grid[gi] : __ldg(m.rgrid + gi);
+            if (s >= 0) {
+                set_region(s);
+            } else {
+                parked = 1;  // outside the grid or a region the prefetch did not create
+                active = false;
+            }
+        }
+    };
+
+    // window boundary: resolve parked lanes (no visit in flight)
+    auto unpark = [&]() {
+        if (parked == 1) {
+            set_region(wd_slow_region(m, sm, rp));
+        } else if (parked == 2) {
+            const unsigned vid = wd_vid_of(m, sm, sm.endc[threadIdx.x][0], sm.endc[threadIdx.x][1],
+                                           sm.endc[threadIdx.x][2], true);
+            vbase = vid == 0xFFFFFFFFu ? vid : vid - vid % vpr;
+            li = vid == 0xFFFFFFFFu ? 0 : (int)(vid % vpr);
+            in_cube = false;
+            jumped = true;
+        }
+        parked = 0;
+        active = true;
+    };
+
+    for (;;) {
+        // ---- retire the window: sample voxels become records ----
+        if (__any_sync(0xffffffffu, live != 0u)) {
+#pragma unroll
+            for (int q = 0; q < WD_STEPS; ++q) {
+                const bool rec = ((live >> q) & 1u) && (olds[q] & MARK_FLAG);
+                push_records(rec, rec ? (((unsigned long long)sm.vids[q][threadIdx.x] << ob) |
+                                         (okey & ~1u) | ((hits >> q) & 1u))
+                                      : 0ULL);
+            }
+            live = 0u;
+            hits = 0u;
+        }
+        if (parked) unpark();
+        if (!active && pf_valid) start();
+        // ---- claim work for lanes without a prefetched descriptor ----
+        unsigned need = __ballot_sync(0xffffffffu, !pf_valid && !exhausted);
+        while (need) {
+            if (pool_next >= pool_end) {
+                unsigned b = 0;
+                if (lane == 0) b = (unsigned)atomicAdd(m.work, 32ULL);
+                b = __shfl_sync(0xffffffffu, b, 0);
+                pool_next = b;
+                pool_end = b + 32;
+                if (b >= nseg_total) {
+                    if ((need >> lane) & 1u) exhausted = true;
+                    break;
+                }
+            }
+            const unsigned avail = pool_end - pool_next;
+            const unsigned rank = __popc(need & lanemask_lt);
+            const bool served = ((need >> lane) & 1u) && rank < avail;
+            if (served) {
+                const unsigned long long w = (unsigned long long)pool_next + rank;
+                if (w < nseg_total) {
+                    const char *g = reinterpret_cast<const char *>(m.segs + m.perm[w]);
+#pragma unroll
+                    for (int q = 0; q < (int)(sizeof(SegDesc) / 16); ++q)
+                        __pipeline_memcpy_async(reinterpret_cast<char *>(my_pf) + 16 * q,
+                                                g + 16 * q, 16);
+                    __pipeline_commit();
+                    pf_valid = true;
+                } else {
+                    exhausted = true;
+                }
+            }
+            const unsigned served_mask = __ballot_sync(0xffffffffu, served);
+            pool_next += __popc(served_mask);
+            need &= ~served_mask;
+        }
+        if (!__any_sync(0xffffffffu, active || pf_valid || !exhausted || parked)) break;
+        if (!__any_sync(0xffffffffu, active)) continue;
+#pragma unroll
+        for (int q = 0; q < WD_STEPS; ++q) step(q);
+    }
+    // flush the warp's remaining records
+    __syncwarp();
+    {
+        const unsigned left = wcnt - wflushed;
+        if (left) {
+            unsigned long long b = 0;
+            if (lane == 0) b = atomicAdd(m.stats + S_RECORDS, (unsigned long long)left);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if ((unsigned)lane < left && b + lane < m.rec_cap)
+                m.rec[b + lane] = wbuf[(wflushed + lane) & (WK_WBUF - 1)];
+        }
+    }
+    __syncthreads();
+    unsigned long long flushed = 0;
+    if (!REC_ONLY) {
+        for (int k = threadIdx.x; k < WCUBE_N; k += blockDim.x) {
+            const unsigned c = sm.cube[k];
+            if (!c || (c & MARK_FLAG)) continue;  // marked voxels: their visits are records
+            ++flushed;
+            const unsigned vid = wd_vid_of(m, sm, sm.anchor[0] + k % WCUBE,
+                                           sm.anchor[1] + (k / WCUBE) % WCUBE,
+                                           sm.anchor[2] + k / (WCUBE * WCUBE), true);
+            if (vid != 0xFFFFFFFFu) red_add(scr + vid, c);
+        }
+        unsigned long long st[3] = {visits, rmiss, flushed};
+        const int which[3] = {S_VISITS, S_RMISS, S_CUBE_FLUSH};
+        block_add_stats(m, st, which);
+    }
+}
+
+}  // namespace vm
