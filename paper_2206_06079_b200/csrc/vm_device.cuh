@@ -90,6 +90,7 @@ struct DevMap {
     int rg_max;                          // capacity of rgrid (cells)
     SegDesc *segs;                       // preprocessed segments of the batch
     unsigned *perm;                      // walk order of the segments (longest first)
+    unsigned char *seg_bk;               // step-count bucket of each segment
     unsigned *seg_hist, *seg_cursor;     // [SEG_BUCKETS] counting-sort state
     unsigned long long seg_cap;
     unsigned long long *work;            // persistent-walk work counter

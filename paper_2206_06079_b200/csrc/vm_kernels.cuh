@@ -356,24 +356,22 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
             }
         }
     }
+    // one thread per (ray, segment): blockIdx.y is the segment index
+    const int s = blockIdx.y;
+    const bool mine = ok && s < r.nseg;
+    if (s != 0) st[0] = st[1] = st[2] = 0;  // ray statistics are counted once
     // warp-aggregated allocation of segment descriptors
     unsigned long long dbase = 0;
     if (emit) {
-        unsigned k = ok ? (unsigned)r.nseg : 0u, incl = k;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        const unsigned bal = __ballot_sync(0xffffffffu, mine);
         unsigned long long base = 0;
-        if (lane == 0 && total) base = atomicAdd(m.stats + S_SEGDESC, (unsigned long long)total);
+        if (lane == 0 && bal) base = atomicAdd(m.stats + S_SEGDESC, (unsigned long long)__popc(bal));
         base = __shfl_sync(0xffffffffu, base, 0);
-        dbase = base + (incl - k);
+        dbase = base + __popc(bal & ((1u << lane) - 1u));
     }
     PrefetchVisitor pv{&m, &kc, sset, {INT_MAX, INT_MAX, INT_MAX}, {INT_MIN, INT_MIN, INT_MIN}};
-    if (ok) {
-        for (int s = 0; s < r.nseg; ++s) {
+    if (mine) {
+        do {
             double so[3], se[3];
             int sh;
             segment_of(m, r, s, so, se, sh);
@@ -392,7 +390,7 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                 }
             }
             walk(so, pe, m.rsize, pv);
-            if (emit && dbase + s < m.seg_cap) {
+            if (emit && dbase < m.seg_cap) {
                 SegDesc sd;
                 int c[3];
                 dda_init(so, se, m.vox, sd, c);
@@ -408,7 +406,8 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                 sd.L = norm3(se[0] - so[0], se[1] - so[1], se[2] - so[2]);
                 const uint4 *src4 = reinterpret_cast<const uint4 *>(&sd);
                 atomicAdd(shist + seg_bucket(sd.rem), 1u);
-                uint4 *dst4 = reinterpret_cast<uint4 *>(m.segs + dbase + s);
+                m.seg_bk[dbase] = (unsigned char)seg_bucket(sd.rem);
+                uint4 *dst4 = reinterpret_cast<uint4 *>(m.segs + dbase);
 #pragma unroll
                 for (int q = 0; q < (int)(sizeof(SegDesc) / 16); ++q) dst4[q] = src4[q];
             }
@@ -450,7 +449,7 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                     }
                 }
             }
-        }
+        } while (0);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -529,12 +528,17 @@ __global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
 // walk then hands every warp 32 segments of nearly equal length.  k_discover
 // built the histogram; one block turns it into bucket cursors.
 __global__ void k_seg_scan(const __grid_constant__ DevMap m) {
+    __shared__ unsigned h[SEG_BUCKETS];
+    for (int b = threadIdx.x; b < SEG_BUCKETS; b += blockDim.x) {
+        h[b] = m.seg_hist[b];
+        m.seg_hist[b] = 0u;  // ready for the next batch (or the replay)
+    }
+    __syncthreads();
     if (threadIdx.x != 0) return;
     unsigned run = 0;
     for (int b = SEG_BUCKETS - 1; b >= 0; --b) {
         m.seg_cursor[b] = run;
-        run += m.seg_hist[b];
-        m.seg_hist[b] = 0u;  // ready for the next batch (or the replay)
+        run += h[b];
     }
 }
 
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(BLOCK) k_seg_scatter(const __grid_constant__ D
     int b = -1;
     unsigned r = 0;
     if (idx < n) {
-        b = seg_bucket(m.segs[idx].rem);
+        b = m.seg_bk[idx];
         r = atomicAdd(cnt + b, 1u);
     }
     __syncthreads();

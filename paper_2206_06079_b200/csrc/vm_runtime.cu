@@ -83,6 +83,8 @@ struct vm_map {
     size_t seg_cap = 0;
     unsigned *d_perm = nullptr;
     size_t perm_cap = 0;
+    unsigned char *d_seg_bk = nullptr;
+    size_t seg_bk_cap = 0;
     unsigned *d_seg_hist = nullptr, *d_seg_cursor = nullptr;
     unsigned long long *d_work = nullptr;
     int *d_rgrid = nullptr;
@@ -168,6 +170,7 @@ DevMap make_dm(const vm_map *m) {
     d.rg_max = RG_MAX;
     d.segs = m->d_segs;
     d.perm = m->d_perm;
+    d.seg_bk = m->d_seg_bk;
     d.seg_hist = m->d_seg_hist;
     d.seg_cursor = m->d_seg_cursor;
     d.seg_cap = m->seg_cap;
@@ -389,6 +392,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     const bool emit = mode == M_OCC || mode == M_DECAY;
     if (emit && (rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * maxseg + 1))) return rc;
     if (emit && (rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
+    if (emit && (rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
     size_t rec_need = 0;
     if (ndt) rec_need = std::max<size_t>(m->rec_cap, (size_t)n * (det ? 8 : 1) + 1);
     else if (tsdf && det) {
@@ -417,14 +421,15 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         }
         CK(cudaEventRecord(m->ev_start, m->stream));
         dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK));
-        k_discover<<<grid, BLOCK, 0, m->stream>>>(dm, src, n, mode, det ? 1 : 0, emit ? 1 : 0);
+        const dim3 dgrid((unsigned)((n + BLOCK - 1) / BLOCK), tsdf ? 1 : (unsigned)maxseg);
+        k_discover<<<dgrid, BLOCK, 0, m->stream>>>(dm, src, n, mode, det ? 1 : 0, emit ? 1 : 0);
         m->launches += 2;  // discover + guard
         if ((rc = check_launch("discover"))) return rc;
         int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
         k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
         if (emit) {
             k_rgrid<<<16, BLOCK, 0, m->stream>>>(dm);
-            k_seg_scan<<<1, 32, 0, m->stream>>>(dm);
+            k_seg_scan<<<1, SEG_BUCKETS, 0, m->stream>>>(dm);
             k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, m->stream>>>(dm);
             m->launches += 3;
         }
@@ -496,7 +501,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 if (ndt) {
                     // the phase-2 hit records come from k_discover: re-emit them
                     // with a records-only discover pass (no descriptors, no marks)
-                    dim3 g2((unsigned)((n + BLOCK - 1) / BLOCK));
+                    const dim3 g2((unsigned)((n + BLOCK - 1) / BLOCK), (unsigned)maxseg);
                     k_discover<<<g2, BLOCK, 0, m->stream>>>(dm, src, n, mode, 1, 0, 0);
                     m->launches += 1;
                 }
@@ -679,6 +684,7 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_slot_pref);
     cudaFree(m->d_segs);
     cudaFree(m->d_perm);
+    cudaFree(m->d_seg_bk);
     cudaFree(m->d_seg_hist);
     cudaFree(m->d_seg_cursor);
     cudaFree(m->d_work);
