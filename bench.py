@@ -13,10 +13,13 @@ map (region creation included), batch by batch, exactly as 1000
          pinned HOST records: host->device copy of every batch and the
          device->host stats read inside the timed region
 
-N > 1 (torchrun): every rank integrates its own copy of the sequence into
-its own map (independent replicas; region sharding with record exchange is
-not in this round).  `--impl reference` times the reference's own native
-kernel on the host cores instead (oracle/ref_runner.py).
+N > 1 (torchrun): ONE region-sharded map over all ranks (sharded.py,
+SURVEY.md 8(e)), weak scaling: N copies of the scene in parallel streets,
+merged batch by batch; each rank walks 1/N of every batch, owns 1/N of the
+regions and receives its regions' miss counts / ordered records over NCCL
+all-to-all (`--replicas`: independent per-GPU maps instead).
+`--impl reference` times the reference's own native kernel on the host
+cores instead (oracle/ref_runner.py).
 """
 from __future__ import annotations
 
@@ -50,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent per-GPU maps instead of the region-sharded map")
     return ap.parse_args()
 
 
@@ -193,11 +198,17 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # VM_DIST_BACKEND=gloo lets the sharded protocol run with more ranks
+        # than GPUs (exchanges staged through host memory) -- for testing only
+        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+        dist.init_process_group(os.environ.get("VM_DIST_BACKEND", "nccl"))
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
+    if world > 1 and not args.replicas and args.workload in ("c1", "c2") and args.exec_ == "det":
+        run_sharded(args, world, rank, dev, dist)
+        dist.destroy_process_group()
+        return
 
     from paper_2206_06079_b200 import ExecutorOptions, VoxelMap, _native, submit_batch
     from paper_2206_06079_b200.layers import MODE_LAYERS
@@ -323,7 +334,7 @@ def main():
             "voxel_updates_per_s": s0["V"] * args.steps * world / (ms * 1e-3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_walk_occ", "peak_kind": peak_kind,
+                         "kernel": "k_walk_det" if det else "k_walk", "peak_kind": peak_kind,
                          "bytes_per_launch": bytes_launch, "avg_launch_ms": walk_ms},
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -337,6 +348,126 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+STREET_PITCH = 250.0  # m between the per-GPU copies of the scene (weak scaling)
+
+
+def run_sharded(args, world, rank, dev, dist):
+    """N > 1: ONE region-sharded map over all ranks.  Weak
+    scaling: the sequence is N copies of the workload's scene, each in its
+    own street STREET_PITCH m apart, merged batch by batch, so every GPU
+    walks the same number of rays as the 1-GPU run while every rank owns
+    1/N of all regions (hash of 2x2x2 region blocks) and receives the miss
+    counts / ordered records of its regions over NCCL all-to-all."""
+    import torch
+
+    from paper_2206_06079_b200.sharded import ShardedVoxelMap, submit_batch_sharded
+
+    cfg, mode, data, desc = workload(args.workload, args.batches)
+    supers = []
+    for b in data:
+        parts = []
+        for r in range(world):
+            c = b.copy()
+            c["origin"][:, 0] += np.float32(r * STREET_PITCH)
+            c["end"][:, 0] += np.float32(r * STREET_PITCH)
+            parts.append(c)
+        supers.append(np.concatenate(parts))
+    sizes = [len(x) for x in supers]
+    offsets = np.concatenate([[0], np.cumsum(sizes)])
+    total_rays = int(offsets[-1])
+    host = np.concatenate(supers)
+    d_all = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
+    d_batches = [d_all[offsets[i] * 40:offsets[i + 1] * 40] for i in range(len(supers))]
+    smap = ShardedVoxelMap(cfg, rank, world, device=dev, initial_regions=4096)
+    stream = torch.cuda.current_stream()
+
+    def step(record=False, batches=d_batches):
+        smap.vmap.clear()
+        tot = dict(S=0, V=0, walk_ms=0.0, batches=0, records=0, rmiss=0)
+        for bt in batches:
+            st = submit_batch_sharded(smap, bt)
+            if record:
+                tot["S"] += st.segments
+                tot["V"] += st.voxel_visits
+                tot["walk_ms"] += st.walk_time * 1e3
+                tot["records"] += st.records
+                tot["rmiss"] += st.region_misses
+                tot["batches"] += 1
+        return tot
+
+    for _ in range(args.warmup):
+        step()
+    clk_file = tempfile.mktemp(suffix=".csv")
+    clk = sample_clocks(clk_file) if rank == 0 else None
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    steps = [step(record=True) for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    if clk:
+        clk.terminate()
+        clk.wait()
+    t = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{dev}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = total_rays * args.steps / (ms * 1e-3)
+    # e2e: host records through the public sharded API (whole batch H2D per rank)
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(host.view(np.uint8).copy()).pin_memory()
+        hv = pinned.numpy().view(host.dtype)
+        dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        f0.record(stream)
+        smap.vmap.clear()
+        for i in range(len(supers)):
+            submit_batch_sharded(smap, hv[offsets[i]:offsets[i + 1]])
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = max(f0.elapsed_time(f1), (time.perf_counter() - t0) * 1e3)
+        t = torch.tensor([ems], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+        e2e = {"value": total_rays / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": 0, "steps": 1,
+               "api": "submit_batch_sharded(smap, pinned OHMB1 records)"}
+    if rank == 0:
+        s0 = steps[-1]
+        o = host["origin"].astype(np.float64)
+        e = host["end"].astype(np.float64)
+        L = np.sqrt(((e - o) ** 2).sum(1))
+        H = int(np.sum(((host["flags"] & 1) == 1) & (L <= cfg.max_ray_range) & (L > 0)))
+        bytes_gpu = algorithmic_bytes(s0["S"], s0["V"], H) / world / max(1, s0["batches"])
+        walk_ms = s0["walk_ms"] / max(1, s0["batches"])
+        peak, peak_kind = load_peaks()
+        achieved = bytes_gpu / (walk_ms * 1e-3) / 1e9 if walk_ms > 0 else 0.0
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (DDA) / f32 (log-odds)",
+            "data": "synthetic",
+            "config": dict(desc, exec="deterministic", rays_per_step=total_rays,
+                           copies=world, street_pitch_m=STREET_PITCH,
+                           parallelism=f"region-sharded x{world} (NCCL all-to-all of counts/records)"),
+            "voxel_updates_per_s": s0["V"] * args.steps / (ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "k_walk_det",
+                         "peak_kind": peak_kind, "bytes_per_launch": bytes_gpu,
+                         "avg_launch_ms": walk_ms},
+            "e2e": e2e, "cpu_baseline": None,
+            "gpu_launches": None,
+            "clocks": parse_clocks(clk_file, dev),
+            "stats": {"segments": s0["S"], "visits": s0["V"], "records": s0["records"],
+                      "region_misses": s0["rmiss"]},
+        }
+        print(json.dumps(line), flush=True)
 
 
 def ctypes_stats_bytes():

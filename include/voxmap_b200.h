@@ -188,6 +188,37 @@ int vm_kernels_integrate_occupancy(const double *origins, const double *ends,
                                    double clamp_min, double clamp_max, int32_t retry_limit,
                                    int32_t walk_cap, int64_t *stats_out, void *stream);
 
+/* ---- region-sharded integration over G GPUs ----
+ *
+ * Map `rank` of `world` owns the regions with vm_shard_owner(key, world) ==
+ * rank (2 x 2 x 2 region blocks hashed over the ranks) and walks the slice
+ * [rank*N/world, (rank+1)*N/world) of each batch; every rank passes the whole
+ * batch.  Deterministic occupancy only.  One batch = begin, exchange A
+ * (requests all-to-all, marks all-gather), prepare, walk, export, exchange B
+ * (items all-to-all), import, finish.  All int64_t / void buffers below are
+ * DEVICE buffers except counts_out / per_dest_out (host).  The union of the
+ * ranks' owned regions equals the single-GPU map, bit for bit. */
+int vm_shard_config(vm_map *map, int32_t rank, int32_t world);
+int vm_shard_owner(int64_t packed_key, int32_t world);
+/* Discover the slice: counts_out[2] = (#new regions, #new sample voxels). */
+int vm_shard_begin(vm_map *map, const vm_rays *rays, int32_t mode, int32_t exec, int64_t *counts_out);
+/* req_out: world segments of req_cap (>= #new regions) packed keys -- the new
+ * regions owned by rank d (creation requests) go to segment d; marks_out:
+ * (packed key, li) int64 pairs of the slice's new sample voxels;
+ * counts_out[1 + world] = (#marks, #requests for rank 0 .. world-1). */
+int vm_shard_lists(vm_map *map, int64_t *req_out, int64_t req_cap, int64_t *marks_out,
+                   int64_t marks_cap, int64_t *counts_out);
+/* req_in: requests addressed to this rank; marks_in: every rank's marks. */
+int vm_shard_prepare(vm_map *map, const int64_t *req_in, int64_t nreq, const int64_t *marks_in,
+                     int64_t nmarks);
+int vm_shard_walk(vm_map *map);
+/* out: world segments of cap_per_dest 16-byte items (region key, li | kind
+ * << 31, count or ray order | hit); per_dest_out[world] gets the sizes
+ * (VM_ERR_ARG if a segment overflowed: retry with a larger cap). */
+int vm_shard_export(vm_map *map, void *out, int64_t cap_per_dest, int64_t *per_dest_out);
+int vm_shard_import(vm_map *map, const void *in, int64_t n);
+int vm_shard_finish(vm_map *map, vm_stats *out);
+
 const char *vm_last_error(void);
 int vm_device_count(int32_t *out);
 /* Build-time identification string (arch, flags). */

@@ -24,6 +24,9 @@ EXPORTED = (
     "vm_map_region_keys", "vm_map_ensure_regions", "vm_map_find_region", "vm_map_read_layer",
     "vm_map_write_layer", "vm_map_layer_ptr", "vm_integrate", "vm_walk_voxels", "vm_hash_mix",
     "vm_kernels_integrate_occupancy", "vm_last_error", "vm_device_count", "vm_build_info",
+    "vm_shard_config", "vm_shard_owner", "vm_shard_begin", "vm_shard_lists", "vm_shard_prepare",
+    "vm_shard_walk",
+    "vm_shard_export", "vm_shard_import", "vm_shard_finish",
 )
 
 
@@ -99,6 +102,15 @@ def lib():
         "vm_kernels_integrate_occupancy": ([P, P, P, I64, P, P, I64, P, P, P, P, P, D, I64, D, D,
                                             D, D, I32, I32, P, P], ctypes.c_int),
         "vm_last_error": ([], ctypes.c_char_p),
+        "vm_shard_config": ([P, I32, I32], ctypes.c_int),
+        "vm_shard_owner": ([I64, I32], ctypes.c_int),
+        "vm_shard_begin": ([P, ctypes.POINTER(VmRays), I32, I32, P], ctypes.c_int),
+        "vm_shard_lists": ([P, P, I64, P, I64, P], ctypes.c_int),
+        "vm_shard_prepare": ([P, P, I64, P, I64], ctypes.c_int),
+        "vm_shard_walk": ([P], ctypes.c_int),
+        "vm_shard_export": ([P, P, I64, P], ctypes.c_int),
+        "vm_shard_import": ([P, P, I64], ctypes.c_int),
+        "vm_shard_finish": ([P, ctypes.POINTER(VmStats)], ctypes.c_int),
         "vm_device_count": ([ctypes.POINTER(I32)], ctypes.c_int),
         "vm_build_info": ([], ctypes.c_char_p),
     }
@@ -204,6 +216,46 @@ class NativeMap:
         check(lib().vm_map_layer_ptr(self._h, slot, layer_id, ctypes.byref(p)), "layer_ptr")
         return int(p.value or 0)
 
+    # -- region sharding (vm_shard_*; device buffers are passed as ints) --
+    def shard_config(self, rank: int, world: int):
+        check(lib().vm_shard_config(self._h, rank, world), "vm_shard_config")
+
+    def shard_begin(self, rays: VmRays) -> tuple[int, int]:
+        """Discover this rank's slice; returns (#new regions, #new sample voxels)."""
+        counts = (ctypes.c_int64 * 2)()
+        check(lib().vm_shard_begin(self._h, ctypes.byref(rays), 0, EXEC_DETERMINISTIC,
+                                   ctypes.cast(counts, ctypes.c_void_p)), "vm_shard_begin")
+        return int(counts[0]), int(counts[1])
+
+    def shard_lists(self, req_ptr: int, req_cap: int, marks_ptr: int, marks_cap: int,
+                    world: int) -> list[int]:
+        counts = (ctypes.c_int64 * (1 + world))()
+        check(lib().vm_shard_lists(self._h, ctypes.c_void_p(req_ptr), req_cap,
+                                   ctypes.c_void_p(marks_ptr), marks_cap,
+                                   ctypes.cast(counts, ctypes.c_void_p)), "vm_shard_lists")
+        return [int(x) for x in counts]
+
+    def shard_prepare(self, req_ptr: int, nreq: int, marks_ptr: int, nmarks: int):
+        check(lib().vm_shard_prepare(self._h, ctypes.c_void_p(req_ptr), nreq,
+                                     ctypes.c_void_p(marks_ptr), nmarks), "vm_shard_prepare")
+
+    def shard_walk(self):
+        check(lib().vm_shard_walk(self._h), "vm_shard_walk")
+
+    def shard_export(self, out_ptr: int, cap_per: int, world: int):
+        counts = (ctypes.c_int64 * world)()
+        rc = lib().vm_shard_export(self._h, ctypes.c_void_p(out_ptr), cap_per,
+                                   ctypes.cast(counts, ctypes.c_void_p))
+        return rc, [int(x) for x in counts]
+
+    def shard_import(self, in_ptr: int, n: int):
+        check(lib().vm_shard_import(self._h, ctypes.c_void_p(in_ptr), n), "vm_shard_import")
+
+    def shard_finish(self) -> VmStats:
+        st = VmStats()
+        check(lib().vm_shard_finish(self._h, ctypes.byref(st)), "vm_shard_finish")
+        return st
+
     def integrate(self, rays: VmRays, mode: str, deterministic: bool) -> VmStats:
         st = VmStats()
         check(lib().vm_integrate(self._h, ctypes.byref(rays), MODES.index(mode),
@@ -280,3 +332,8 @@ def kernels_integrate_occupancy(origins, ends, has_sample, n, tkeys, tvals, tsiz
         float(clamp_min), float(clamp_max), int(retry_limit), int(walk_cap),
         ctypes.cast(st, P), P(stream or 0)), "vm_kernels_integrate_occupancy")
     return tuple(int(x) for x in st)
+
+
+def shard_owner(packed_key: int, world: int) -> int:
+    """Owner rank of a region in a `world`-way sharded map (vm_shard_owner)."""
+    return int(lib().vm_shard_owner(int(packed_key), int(world)))

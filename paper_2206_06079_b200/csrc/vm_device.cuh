@@ -97,6 +97,14 @@ struct DevMap {
     unsigned long long *stats;
     int *go;                             // batch guard (0 = skip, replay later)
     int walk_det_launched;               // k_walk_det runs before k_walk (deterministic occupancy)
+    // region sharding (vm_shard_*): this map owns regions with owner(key) == shard_rank
+    int shard_rank, shard_world;
+    long long ray_lo;                    // first ray of this map's slice of the batch
+    int2 *marked;                        // new sample voxels (slot, li) of the slice
+    unsigned long long *nmarked;
+    unsigned long long marked_cap;
+    unsigned long long rec_invalid;      // voxel-id field of dropped records (skipped by the fold)
+    int walk_slot0;                      // regions with slot >= this were created by the walk
     // batch outputs
     unsigned long long *rec;
     unsigned *recval;                    // per-record value (NDT deterministic phase 1)
@@ -392,6 +400,17 @@ __device__ __forceinline__ int region_slot(const DevMap &m, long long key) {
         if (v >= 0) return v;
     }
     return region_slot_slow(m, key);
+}
+
+// Region owner for sharded maps: blocks of 2 x 2 x 2
+// regions hashed over the ranks, so the busy regions around a sensor spread
+// over all GPUs while neighbouring regions mostly stay together.
+__host__ __device__ __forceinline__ int region_owner(long long key, int world) {
+    if (world <= 1) return 0;
+    const long long B = 1LL << 20, M = (1LL << 21) - 1;
+    const long long bx = (((key >> 42) & M) - B) >> 1, by = (((key >> 21) & M) - B) >> 1,
+                    bz = ((key & M) - B) >> 1;
+    return (int)(mix_key(pack_region(bx, by, bz)) % (unsigned long long)world);
 }
 
 // ---------------------------------------------------------------- block helpers

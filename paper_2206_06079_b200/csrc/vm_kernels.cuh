@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
         double o0[3], e0[3];
         int h0;
         float it0;
-        src.load(i0 < n ? i0 : 0, o0, e0, h0, it0);
+        src.load(m.ray_lo + (i0 < n ? i0 : 0), o0, e0, h0, it0);
         for (int a = 0; a < 3; ++a) {
             const double c = floor(o0[a] / m.rsize);
             anchor[a] = (c > -1e9 && c < 1e9 ? (int)c : 0) - (1 << 12);
@@ -341,10 +341,11 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
     const int lane = threadIdx.x & 31;
     unsigned long long st[3] = {0, 0, 0};  // processed, segments, range errors
     unsigned long long nmark_local = 0;
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // ray index in the batch (sharded maps discover the slice [ray_lo, ray_lo + n))
+    long long i = m.ray_lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     Ray r;
     bool ok = false;
-    if (i < n) {
+    if (i < m.ray_lo + n) {
         src.load(i, r.o, r.e, r.has, r.inten);
         ok = prep_ray(m, r, !tsdf);
         if (ok) {
@@ -439,6 +440,11 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                         if (!(*((volatile unsigned *)w) & MARK_FLAG) &&
                             !(atomicOr(w, MARK_FLAG) & MARK_FLAG)) {
                             ++nmark_local;
+                            if (m.marked) {
+                                // sharded maps publish their new sample voxels
+                                const unsigned long long mi = atomicAdd(m.nmarked, 1ULL);
+                                if (mi < m.marked_cap) m.marked[mi] = make_int2(rt.slot, li);
+                            }
                             // brick summary read by the walk (4 x 4 x 2 bricks)
                             const int bsh = m.brick_shift;
                             const unsigned bit = bsh >= 0
@@ -1094,6 +1100,7 @@ __global__ void __launch_bounds__(BLOCK) k_fold_occ(const __grid_constant__ DevM
          i += (long long)gridDim.x * blockDim.x) {
         const unsigned long long vk = keys[i] >> ob;
         if (i > 0 && (keys[i - 1] >> ob) == vk) continue;
+        if (vk == m.rec_invalid) continue;  // records a sharded map handed to their owner
         long long e = i + 1;
         while (e < R && e - i <= FOLD_SERIAL_MAX && (keys[e] >> ob) == vk) ++e;
         if (e < R && (keys[e] >> ob) == vk) {

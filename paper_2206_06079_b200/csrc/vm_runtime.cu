@@ -19,6 +19,7 @@
 #include "vm_walk.cuh"
 #include "vm_compat.cuh"
 #include "vm_walk_det.cuh"
+#include "vm_shard.cuh"
 
 using namespace vm;
 
@@ -105,6 +106,24 @@ struct vm_map {
     unsigned char *d_rays = nullptr;
     size_t rays_bytes = 0;
     unsigned long long *h_stats = nullptr;  // pinned, NUM_STATS + 2
+    // region sharding (vm_shard_*)
+    int shard_rank = 0, shard_world = 1;
+    int2 *d_smarked = nullptr;
+    size_t smarked_cap = 0;
+    unsigned long long *d_shard_cnt = nullptr;  // [2 + world]: nmarked, nreq, per-dest counts
+    struct ShardBatch {
+        bool open = false, walked = false;
+        int format = 0;
+        const void *rays = nullptr;  // device pointer of the batch (records or f64 arrays)
+        const double *o = nullptr, *e = nullptr;
+        const unsigned char *h = nullptr;
+        const float *it = nullptr;
+        long long n_all = 0, lo = 0, n = 0;
+        int order_bits = 0, maxseg = 0, walk_slot0 = 0;
+        long long nreg0 = 0, launches0 = 0;
+        unsigned long long nmarks = 0, R = 0;
+        float ms_disc = 0.f, ms_walk = 0.f;
+    } sb;
     unsigned epoch = 0;
     long long launches = 0;
     cudaEvent_t ev_start{}, ev_end{}, ev_w0{}, ev_w1{}, ev_k1{}, ev_k2{}, ev_res{}, ev_sort{};
@@ -182,6 +201,14 @@ DevMap make_dm(const vm_map *m) {
     d.rec_cap = m->rec_cap;
     d.touched = m->d_touched;
     d.touched_cap = (int)m->max_slots;
+    d.shard_rank = m->shard_rank;
+    d.shard_world = m->shard_world;
+    d.ray_lo = 0;
+    d.marked = nullptr;
+    d.nmarked = m->d_shard_cnt;
+    d.marked_cap = 0;
+    d.rec_invalid = ~0ULL;
+    d.walk_slot0 = 1 << 30;
     return d;
 }
 
@@ -689,6 +716,8 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_seg_cursor);
     cudaFree(m->d_work);
     cudaFree(m->d_rgrid);
+    cudaFree(m->d_smarked);
+    cudaFree(m->d_shard_cnt);
     cudaFree(m->d_bmask);
     cudaFree(m->d_big);
     cudaFree(m->d_nbig);
@@ -999,6 +1028,381 @@ int vm_kernels_integrate_occupancy(const double *origins, const double *ends,
     CK(cudaFreeAsync(d_st, s));
     CK(cudaStreamSynchronize(s));
     for (int i = 0; i < 4; ++i) stats_out[i] = (int64_t)h[i];
+    return VM_OK;
+}
+
+}  // extern "C"
+
+// =================================================================== sharding
+// Region-sharded integration (vm_shard.cuh has the protocol).  Deterministic
+// occupancy only; every rank passes the whole batch and walks its slice.
+
+namespace {
+
+template <class F>
+int with_src(vm_map *m, F &&f) {
+    if (m->sb.format == VM_RAYS_OHMB1) return f(SrcOHMB1{(const unsigned char *)m->sb.rays});
+    return f(SrcF64{m->sb.o, m->sb.e, m->sb.h, m->sb.it});
+}
+
+int shard_headroom(vm_map *m, long long extra) {
+    const long long need = m->nreg + extra + std::max<long long>(512, 2 * m->max_growth);
+    if (need > m->cap) return grow_pool(m, std::max(2 * m->cap, need));
+    return VM_OK;
+}
+
+int read_cursor(vm_map *m, int *cursor) {
+    CK(cudaMemcpyAsync(m->h_stats + NUM_STATS, m->d_cursor, sizeof(int), cudaMemcpyDeviceToHost,
+                       m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    *cursor = *(const int *)(m->h_stats + NUM_STATS);
+    return VM_OK;
+}
+
+DevMap shard_dm(vm_map *m) {
+    DevMap dm = make_dm(m);
+    dm.order_bits = m->sb.order_bits;
+    dm.ray_lo = m->sb.lo;
+    dm.marked = m->d_smarked;
+    dm.nmarked = m->d_shard_cnt;
+    dm.marked_cap = m->smarked_cap;
+    dm.walk_slot0 = m->sb.walk_slot0;
+    return dm;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vm_shard_config(vm_map *m, int32_t rank, int32_t world) {
+    if (!m || world < 1 || world > 4096 || rank < 0 || rank >= world)
+        return fail(VM_ERR_ARG, "bad shard rank / world");
+    if (m->sb.open) return fail(VM_ERR_ARG, "a sharded batch is in flight");
+    CK(cudaSetDevice(m->device));
+    cudaFree(m->d_shard_cnt);
+    m->d_shard_cnt = nullptr;
+    CK(cudaMalloc((void **)&m->d_shard_cnt, (2 + (size_t)world) * sizeof(unsigned long long)));
+    m->shard_rank = rank;
+    m->shard_world = world;
+    return VM_OK;
+}
+
+int vm_shard_owner(int64_t packed_key, int32_t world) { return region_owner(packed_key, world); }
+
+int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, int64_t *counts_out) {
+    if (!m || !rays || !counts_out) return fail(VM_ERR_ARG, "null argument");
+    if (mode != VM_MODE_OCCUPANCY || exec != VM_EXEC_DETERMINISTIC)
+        return fail(VM_ERR_ARG, "sharded maps integrate deterministic occupancy");
+    if ((m->mask & MODE_MASK[0]) != MODE_MASK[0]) return fail(VM_ERR_ARG, "map lacks layers");
+    if (!m->d_shard_cnt) return fail(VM_ERR_ARG, "call vm_shard_config first");
+    CK(cudaSetDevice(m->device));
+    auto &sb = m->sb;
+    sb = vm_map::ShardBatch{};
+    const long long n_all = rays->count;
+    if (n_all <= 0) return fail(VM_ERR_ARG, "empty batch");
+    // the whole batch on the device (the fold reads any ray's end point)
+    sb.format = rays->format;
+    if (rays->format == VM_RAYS_OHMB1) {
+        const unsigned char *p = (const unsigned char *)rays->records;
+        if (!p) return fail(VM_ERR_ARG, "null records");
+        if (!rays->on_device) {
+            int rc = ensure_buf(&m->d_rays, &m->rays_bytes, (size_t)n_all * 40);
+            if (rc) return rc;
+            CK(cudaMemcpyAsync(m->d_rays, p, (size_t)n_all * 40, cudaMemcpyHostToDevice, m->stream));
+            p = m->d_rays;
+        }
+        sb.rays = p;
+    } else {
+        if (!rays->on_device) return fail(VM_ERR_ARG, "sharded f64 rays must be device arrays");
+        sb.o = rays->origins;
+        sb.e = rays->ends;
+        sb.h = rays->has_sample;
+        sb.it = rays->intensity;
+    }
+    const int W = m->shard_world, rk = m->shard_rank;
+    sb.n_all = n_all;
+    sb.lo = n_all * rk / W;
+    sb.n = n_all * (rk + 1) / W - sb.lo;
+    sb.maxseg = (int)std::ceil(m->cfg.max_ray_range / m->cfg.segment_length) + 1;
+    const unsigned long long order_span = ((unsigned long long)n_all * sb.maxseg) << 1;
+    if (order_span >= (1ULL << 32)) return fail(VM_ERR_ARG, "batch too large for 32-bit ray order keys");
+    sb.order_bits = std::max(1, bitlen(order_span));
+    const long long n = std::max<long long>(sb.n, 1);
+    int rc;
+    if ((rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * sb.maxseg + 1))) return rc;
+    if ((rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)n + 1))) return rc;
+    if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, std::max<size_t>(1 << 20, (size_t)n_all * 4)))))
+        return rc;
+    sb.launches0 = m->launches;
+    sb.nreg0 = m->nreg;
+    CK(cudaMemsetAsync(m->d_shard_cnt, 0, (2 + (size_t)W) * sizeof(unsigned long long), m->stream));
+    for (;;) {
+        const long long headroom = std::max<long long>(512, 2 * m->max_growth);
+        if ((rc = shard_headroom(m, 0))) return rc;
+        m->epoch += 1;
+        DevMap dm = shard_dm(m);
+        CK(cudaMemsetAsync(m->d_stats, 0, NUM_STATS * sizeof(unsigned long long), m->stream));
+        static const int box_init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
+        CK(cudaMemcpyAsync(m->d_rbox, box_init, sizeof(box_init), cudaMemcpyHostToDevice, m->stream));
+        CK(cudaEventRecord(m->ev_start, m->stream));
+        if (sb.n > 0) {
+            const dim3 dgrid((unsigned)((sb.n + BLOCK - 1) / BLOCK), (unsigned)sb.maxseg);
+            rc = with_src(m, [&](auto src) {
+                k_discover<<<dgrid, BLOCK, 0, m->stream>>>(dm, src, sb.n, VM_MODE_OCCUPANCY, 1, 1);
+                return check_launch("discover");
+            });
+            if (rc) return rc;
+        }
+        const int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
+        k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
+        k_seg_scan<<<1, SEG_BUCKETS, 0, m->stream>>>(dm);
+        k_seg_scatter<<<(unsigned)((n * sb.maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, m->stream>>>(dm);
+        m->launches += 4;
+        CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS, m->d_cursor, sizeof(int), cudaMemcpyDeviceToHost,
+                           m->stream));
+        CK(cudaMemcpyAsync((int *)(m->h_stats + NUM_STATS) + 1, m->d_go, sizeof(int),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        const int cursor = *(const int *)(m->h_stats + NUM_STATS);
+        const int go = *((const int *)(m->h_stats + NUM_STATS) + 1);
+        if (m->h_stats[S_RANGE_ERR]) {
+            m->nreg = cursor;
+            return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range");
+        }
+        if (!go) {
+            m->max_growth = std::max<long long>(m->max_growth, cursor - m->nreg);
+            if ((rc = grow_pool(m, std::max<long long>(2 * m->cap, cursor + 2 * margin + headroom))))
+                return rc;
+            m->nreg = cursor;
+            continue;
+        }
+        m->nreg = cursor;
+        break;
+    }
+    CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_shard_cnt, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    sb.nmarks = std::min<unsigned long long>(m->h_stats[NUM_STATS + 2], m->smarked_cap);
+    counts_out[0] = (int64_t)(m->nreg - sb.nreg0);  // new regions (bound on the requests)
+    counts_out[1] = (int64_t)sb.nmarks;
+    sb.open = true;
+    return VM_OK;
+}
+
+int vm_shard_lists(vm_map *m, int64_t *req_out, int64_t req_cap, int64_t *marks_out,
+                   int64_t marks_cap, int64_t *counts_out) {
+    if (!m || !m->sb.open || m->sb.walked || !counts_out)
+        return fail(VM_ERR_ARG, "no discovered sharded batch");
+    CK(cudaSetDevice(m->device));
+    auto &sb = m->sb;
+    const int W = m->shard_world;
+    int rc;
+    if ((long long)sb.nmarks > marks_cap || req_cap < m->nreg - sb.nreg0)
+        return fail(VM_ERR_ARG, "vm_shard_lists: buffers smaller than vm_shard_begin's counts");
+    CK(cudaMemsetAsync(m->d_shard_cnt + 2, 0, (size_t)W * sizeof(unsigned long long), m->stream));
+    DevMap dm = shard_dm(m);
+    k_shard_lists<<<m->num_sms * 2, BLOCK, 0, m->stream>>>(
+        dm, (int)sb.nreg0, (int)m->nreg, (long long *)req_out, m->d_shard_cnt + 2,
+        (unsigned long long)req_cap, (long long *)marks_out, sb.nmarks);
+    m->launches += 1;
+    if ((rc = check_launch("shard lists"))) return rc;
+    std::vector<unsigned long long> nreq((size_t)W);
+    CK(cudaMemcpyAsync(nreq.data(), m->d_shard_cnt + 2, (size_t)W * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    counts_out[0] = (int64_t)sb.nmarks;
+    for (int d = 0; d < W; ++d) counts_out[1 + d] = (int64_t)nreq[d];
+    return VM_OK;
+}
+
+int vm_shard_prepare(vm_map *m, const int64_t *req_in, int64_t nreq, const int64_t *marks_in,
+                     int64_t nmarks) {
+    if (!m || !m->sb.open || m->sb.walked) return fail(VM_ERR_ARG, "no sharded batch to prepare");
+    CK(cudaSetDevice(m->device));
+    int rc;
+    if ((rc = shard_headroom(m, nreq))) return rc;
+    DevMap dm = shard_dm(m);
+    if (nreq > 0) {
+        k_shard_prepare<<<(unsigned)std::min<long long>((nreq + BLOCK - 1) / BLOCK, 4096), BLOCK, 0,
+                          m->stream>>>(dm, (const long long *)req_in, nreq);
+        m->launches += 1;
+    }
+    // every rank's sample voxels, kept for the ghost clean-up in finish
+    // (region key, li) pairs: two int2 slots per mark
+    if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, 2 * (size_t)std::max<int64_t>(nmarks, 0) + 2)))
+        return rc;
+    if (nmarks > 0) {
+        CK(cudaMemcpyAsync(m->d_smarked, marks_in, (size_t)nmarks * 16, cudaMemcpyDeviceToDevice,
+                           m->stream));
+        k_shard_stamp<<<(unsigned)std::min<long long>((nmarks + BLOCK - 1) / BLOCK, 4096), BLOCK, 0,
+                        m->stream>>>(dm, (const long long *)m->d_smarked, nmarks);
+        m->launches += 1;
+    }
+    m->sb.nmarks = (unsigned long long)std::max<int64_t>(nmarks, 0);
+    k_rgrid<<<16, BLOCK, 0, m->stream>>>(dm);
+    m->launches += 1;
+    if ((rc = check_launch("shard prepare"))) return rc;
+    int cursor;
+    if ((rc = read_cursor(m, &cursor))) return rc;
+    m->nreg = cursor;
+    m->sb.walk_slot0 = cursor;
+    return VM_OK;
+}
+
+int vm_shard_walk(vm_map *m) {
+    if (!m || !m->sb.open || m->sb.walked) return fail(VM_ERR_ARG, "no sharded batch to walk");
+    CK(cudaSetDevice(m->device));
+    int rc;
+    if ((rc = shard_headroom(m, 0))) return rc;
+    DevMap dm = shard_dm(m);
+    CK(cudaMemsetAsync(m->d_work, 0, sizeof(unsigned long long), m->stream));
+    CK(cudaEventRecord(m->ev_w0, m->stream));
+    if (m->sb.n > 0) {
+        const dim3 pgrid((unsigned)std::max<long long>(
+            1, std::min<long long>((long long)WK_BLOCKS * m->num_sms, (m->sb.n * 3 + BLOCK - 1) / BLOCK)));
+        rc = with_src(m, [&](auto src) {
+            using S = decltype(src);
+            DevMap d2 = dm;
+            d2.walk_det_launched = 1;
+            launch_wd<false, S>(pgrid, m->stream, d2, src);
+            launch_w3<M_OCC, true, false, S>(pgrid, sizeof(WalkSmem), m->stream, d2, src);
+            return check_launch("shard walk");
+        });
+        if (rc) return rc;
+        m->launches += 2;
+    }
+    CK(cudaEventRecord(m->ev_w1, m->stream));
+    m->sb.walked = true;
+    return VM_OK;
+}
+
+int vm_shard_export(vm_map *m, void *out, int64_t cap_per_dest, int64_t *per_dest_out) {
+    if (!m || !m->sb.open || !m->sb.walked || !per_dest_out)
+        return fail(VM_ERR_ARG, "no walked sharded batch to export");
+    CK(cudaSetDevice(m->device));
+    const int W = m->shard_world;
+    CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_stats + S_RECORDS, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    const unsigned long long R = m->h_stats[NUM_STATS + 2];
+    if (R > m->rec_cap) return fail(VM_ERR_OOM, "record buffer overflow in a sharded batch");
+    m->sb.R = R;
+    DevMap dm = shard_dm(m);
+    CK(cudaMemsetAsync(m->d_shard_cnt + 2, 0, (size_t)W * sizeof(unsigned long long), m->stream));
+    const unsigned long long cap = (unsigned long long)std::max<int64_t>(cap_per_dest, 0);
+    if (R > 0)
+        k_shard_export_rec<<<(unsigned)std::min<unsigned long long>((R + BLOCK - 1) / BLOCK, 4096),
+                             BLOCK, 0, m->stream>>>(dm, m->d_rec, (long long)R, (ShardItem *)out,
+                                                    m->d_shard_cnt + 2, cap);
+    k_shard_export_cnt<<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm, (ShardItem *)out,
+                                                                m->d_shard_cnt + 2, cap);
+    m->launches += 2;
+    int rc;
+    if ((rc = check_launch("shard export"))) return rc;
+    std::vector<unsigned long long> cnt((size_t)W);
+    CK(cudaMemcpyAsync(cnt.data(), m->d_shard_cnt + 2, (size_t)W * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    bool over = false;
+    for (int d = 0; d < W; ++d) {
+        per_dest_out[d] = (int64_t)cnt[d];
+        over = over || cnt[d] > cap;
+    }
+    if (over) return fail(VM_ERR_ARG, "export buffer too small (per_dest_out holds the sizes)");
+    return VM_OK;
+}
+
+int vm_shard_import(vm_map *m, const void *in, int64_t n) {
+    if (!m || !m->sb.open || !m->sb.walked) return fail(VM_ERR_ARG, "no sharded batch to import into");
+    CK(cudaSetDevice(m->device));
+    int rc;
+    if (n > 0) {
+        const unsigned g = (unsigned)std::min<long long>((n + BLOCK - 1) / BLOCK, 8192);
+        {
+            DevMap dm = shard_dm(m);
+            k_shard_import_regions<<<g, BLOCK, 0, m->stream>>>(dm, (const ShardItem *)in, n);
+        }
+        int cursor;
+        if ((rc = read_cursor(m, &cursor))) return rc;
+        m->nreg = cursor;
+        if ((rc = shard_headroom(m, 0))) return rc;  // covers every slot pass 1 handed out
+        DevMap dm = shard_dm(m);
+        k_shard_import<<<g, BLOCK, 0, m->stream>>>(dm, (const ShardItem *)in, n);
+        m->launches += 2;
+        if ((rc = check_launch("shard import"))) return rc;
+    }
+    int cursor;
+    if ((rc = read_cursor(m, &cursor))) return rc;
+    m->nreg = cursor;
+    return VM_OK;
+}
+
+int vm_shard_finish(vm_map *m, vm_stats *out) {
+    if (!m || !m->sb.open || !m->sb.walked || !out) return fail(VM_ERR_ARG, "no sharded batch to finish");
+    CK(cudaSetDevice(m->device));
+    auto &sb = m->sb;
+    int rc;
+    int cursor;
+    if ((rc = read_cursor(m, &cursor))) return rc;
+    m->nreg = cursor;
+    CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    const unsigned long long Rtot = std::min<unsigned long long>(m->h_stats[S_RECORDS], m->rec_cap);
+    if (m->h_stats[S_RECORDS] > m->rec_cap) return fail(VM_ERR_OOM, "record buffer overflow on import");
+    const int vbits = std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
+    const int end_bit = std::min(64, sb.order_bits + vbits);
+    DevMap dm = shard_dm(m);
+    dm.rec_invalid = (1ULL << vbits) - 1;
+    const unsigned long long invalid_key = dm.rec_invalid << sb.order_bits;
+    k_shard_clear<<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm, m->d_rec, (long long)sb.R, invalid_key,
+                                                          (const long long *)m->d_smarked,
+                                                          (long long)sb.nmarks);
+    CK(cudaEventRecord(m->ev_k1, m->stream));
+    k_resolve<false, false><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
+    CK(cudaEventRecord(m->ev_res, m->stream));
+    cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
+    if (Rtot > 1) {
+        size_t bytes = m->sort_tmp_bytes;
+        CK(cub::DeviceRadixSort::SortKeys(m->d_sort_tmp, bytes, db, (int)Rtot, 0, end_bit, m->stream));
+    }
+    CK(cudaEventRecord(m->ev_sort, m->stream));
+    rc = with_src(m, [&](auto src) {
+        return launch_fold(m, dm, src, db.Current(), m->d_val, (long long)Rtot, M_OCC);
+    });
+    if (rc) return rc;
+    m->launches += 2;
+    CK(cudaEventRecord(m->ev_end, m->stream));
+    CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    if ((rc = check_launch("shard finish"))) return rc;
+    const unsigned long long *hs = m->h_stats;
+    std::memset(out, 0, sizeof(*out));
+    out->rays_in = sb.n;
+    out->rays_processed = (int64_t)hs[S_PROCESSED];
+    out->segments = (int64_t)hs[S_SEGMENTS];
+    out->voxel_visits = (int64_t)hs[S_VISITS];
+    out->region_misses = (int64_t)hs[S_RMISS];
+    out->regions_touched = (int64_t)hs[S_PREF_TOUCHED];
+    out->records = (int64_t)Rtot;
+    out->marked_voxels = (int64_t)sb.nmarks;
+    out->regions_total = cursor;
+    out->new_regions = cursor - sb.nreg0;
+    out->touched_regions_walk = (int64_t)hs[S_WALK_TOUCHED];
+    out->launches = m->launches - sb.launches0;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, m->ev_start, m->ev_end) == cudaSuccess) out->gpu_ms = ms;
+    if (cudaEventElapsedTime(&ms, m->ev_w0, m->ev_w1) == cudaSuccess) out->walk_ms = ms;
+    if (cudaEventElapsedTime(&ms, m->ev_k1, m->ev_res) == cudaSuccess) out->resolve_ms = ms;
+    if (cudaEventElapsedTime(&ms, m->ev_res, m->ev_sort) == cudaSuccess) out->sort_ms = ms;
+    if (cudaEventElapsedTime(&ms, m->ev_sort, m->ev_end) == cudaSuccess) out->fold_ms = ms;
+    m->max_growth = std::max<long long>(m->max_growth, cursor - sb.nreg0);
+    sb.open = false;
     return VM_OK;
 }
 

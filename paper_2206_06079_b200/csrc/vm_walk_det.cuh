@@ -156,6 +156,10 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
     // resolved outside the unrolled steps (no call inside them)
     int parked = 0;  // 1: region lookup after a crossing, 2: fallback jump to the end cell
     bool jumped = false;
+    // sharded maps: a region created during the walk was not stamped with the
+    // other ranks' sample voxels, so every visit in it is kept as a record
+    bool forced = false;
+    unsigned fmask = 0;
     // in-flight visits of the window
     unsigned olds[WD_STEPS];
     unsigned live = 0, hits = 0;  // bit q: slot q holds a visit / the hit
@@ -180,7 +184,10 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
         }
     };
 
-    auto set_region = [&](int s) { vbase = s >= 0 && s < m.cap ? (unsigned)s * vpr : 0xFFFFFFFFu; };
+    auto set_region = [&](int s) {
+        vbase = s >= 0 && s < m.cap ? (unsigned)s * vpr : 0xFFFFFFFFu;
+        forced = m.shard_world > 1 && s >= m.walk_slot0;
+    };
 
     auto start = [&]() {
         __pipeline_wait_prior(0);
@@ -257,6 +264,7 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
             olds[Q] = REC_ONLY ? *((volatile unsigned *)p) : atomicAdd(p, 1u);
             sm.vids[Q][threadIdx.x] = vid;
             live |= 1u << Q;
+            if (forced) fmask |= 1u << Q;
         } else {
             ++rmiss;
         }
@@ -304,6 +312,7 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
                                            sm.endc[threadIdx.x][2], true);
             vbase = vid == 0xFFFFFFFFu ? vid : vid - vid % vpr;
             li = vid == 0xFFFFFFFFu ? 0 : (int)(vid % vpr);
+            forced = m.shard_world > 1 && vid != 0xFFFFFFFFu && (int)(vid / vpr) >= m.walk_slot0;
             in_cube = false;
             jumped = true;
         }
@@ -316,13 +325,14 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
         if (__any_sync(0xffffffffu, live != 0u)) {
 #pragma unroll
             for (int q = 0; q < WD_STEPS; ++q) {
-                const bool rec = ((live >> q) & 1u) && (olds[q] & MARK_FLAG);
+                const bool rec = ((live >> q) & 1u) && ((olds[q] & MARK_FLAG) || ((fmask >> q) & 1u));
                 push_records(rec, rec ? (((unsigned long long)sm.vids[q][threadIdx.x] << ob) |
                                          (okey & ~1u) | ((hits >> q) & 1u))
                                       : 0ULL);
             }
             live = 0u;
             hits = 0u;
+            fmask = 0u;
         }
         if (parked) unpark();
         if (!active && pf_valid) start();
