@@ -437,21 +437,23 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                     } else {
                         // stamp the sample voxel: the walk turns its visits into records
                         unsigned *w = layer_at<unsigned>(m, L_SCRATCH, rt.slot) + li;
-                        if (!(*((volatile unsigned *)w) & MARK_FLAG) &&
-                            !(atomicOr(w, MARK_FLAG) & MARK_FLAG)) {
+                        const bool was = (*((volatile unsigned *)w) & MARK_FLAG) ||
+                                         (atomicOr(w, MARK_FLAG) & MARK_FLAG);
+                        if (!was) {
                             ++nmark_local;
                             if (m.marked) {
                                 // sharded maps publish their new sample voxels
                                 const unsigned long long mi = atomicAdd(m.nmarked, 1ULL);
                                 if (mi < m.marked_cap) m.marked[mi] = make_int2(rt.slot, li);
                             }
-                            // brick summary read by the walk (4 x 4 x 2 bricks)
-                            const int bsh = m.brick_shift;
-                            const unsigned bit = bsh >= 0
-                                ? 1u << ((rt.lx >> bsh) | ((rt.ly >> bsh) << 2) | ((rt.lz >> (bsh + 1)) << 4))
-                                : 0xFFFFFFFFu;
-                            atomicOr(m.bmask + rt.slot, bit);
                         }
+                        // brick summary read by the walks (4 x 4 x 2 bricks); set
+                        // for every stamp, also one left over from a dropped batch
+                        const int bsh = m.brick_shift;
+                        const unsigned bit = bsh >= 0
+                            ? 1u << ((rt.lx >> bsh) | ((rt.ly >> bsh) << 2) | ((rt.lz >> (bsh + 1)) << 4))
+                            : 0xFFFFFFFFu;
+                        if (!(__ldcg(m.bmask + rt.slot) & bit)) atomicOr(m.bmask + rt.slot, bit);
                     }
                 }
             }

@@ -71,6 +71,8 @@ __global__ void k_shard_stamp(const __grid_constant__ DevMap m, const long long 
         if (s < 0 || s >= m.cap) continue;
         const int li = (int)marks[2 * i + 1];
         atomicOr(reinterpret_cast<unsigned *>(m.slab[L_SCRATCH]) + (size_t)s * m.vpr + li, MARK_FLAG);
+        // the walk's brick summary (see k_discover)
+        atomicOr(m.bmask + s, m.brick_shift >= 0 ? 1u << brick_of(li, m.bsh) : 0xFFFFFFFFu);
     }
 }
 
@@ -173,7 +175,10 @@ __global__ void __launch_bounds__(BLOCK) k_shard_clear(const __grid_constant__ D
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nmarks;
          i += (long long)gridDim.x * blockDim.x) {
         const int s = region_find(m, marks[2 * i]);
-        if (s >= 0 && s < m.cap && is_ghost(m, s)) scr0[(size_t)s * m.vpr + marks[2 * i + 1]] = 0u;
+        if (s >= 0 && s < m.cap && is_ghost(m, s)) {
+            scr0[(size_t)s * m.vpr + marks[2 * i + 1]] = 0u;
+            m.bmask[s] = 0u;
+        }
     }
     VM_TOUCHED_REGIONS({
         unsigned *scr = scr0 + (size_t)slot * m.vpr;

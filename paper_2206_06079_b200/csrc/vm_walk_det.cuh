@@ -4,18 +4,20 @@
 // Same walk as k_walk (vm_walk.cuh): one warp = 32 lanes, each walking one
 // preprocessed segment with the exact fp64 DDA of traversal._walk_grid
 // (traversal.py:80-111), longest segments first.  What differs is the visit:
-// every visit is exactly ONE atomic add with return on the voxel's scratch
-// counter (or, around the sensor, on the block's shared-memory cube counter;
-// both through one generic-address ATOM, so there is no branch).  The counter
-// is the order-free miss count resolved as f_miss^k by k_resolve; k_discover
-// stamped MARK_FLAG into the counters of the batch's sample voxels, so the
-// returned old value says whether the visit must become an order-keyed
-// record (voxel id, ray order, hit) for the in-order fold instead.
+// a visit is a fire-and-forget RED.ADD on the voxel's scratch counter (the
+// order-free miss count, resolved as f_miss^k by k_resolve) unless the
+// voxel's brick (8 x 8 x 16 voxels at dim 32) holds one of the batch's sample
+// voxels -- a bit test against the region's brick summary, which k_discover
+// built while stamping MARK_FLAG into the sample voxels' counters.  Visits in
+// such bricks are candidates: their voxel ids wait in shared memory and are
+// resolved together at the end of the eight-step window (one batch of loads
+// of their counters: MARK_FLAG -> an order-keyed record (voxel id, ray order,
+// hit) for the in-order fold, otherwise the delayed miss count).  Around the
+// sensor, visits count into the block's shared-memory cube, which carries its
+// own sample-voxel bitmap.
 //
-// The step is written for the common case.  The eight steps of a window are
-// unrolled, each into its own in-flight slot (old value, voxel id), and the
-// returned values are inspected together at the end of the window: one
-// memory latency per eight visits.  Region crossings step a grid index
+// The step is written for the common case and the eight steps of a window
+// are unrolled.  Region crossings step a grid index
 // through the batch's dense region grid (shared memory); only a crossing out
 // of the grid probes the hash table.  Segment starts happen at window
 // boundaries.
@@ -26,11 +28,13 @@
 namespace vm {
 
 constexpr int WD_STEPS = 8;   // steps per window (in-flight visits per lane)
+constexpr int WD_BLOCKS = 3;  // resident blocks per SM
 constexpr int RP_BIAS = 512;  // bias of the grid-relative region coordinates
 
 struct WalkDetSmem {
-    unsigned cube[WCUBE_N];  // miss counts around the sensor (MARK_FLAG: sample voxel)
-    int grid[RG_SMEM];
+    unsigned cube[WCUBE_N];          // miss counts around the sensor
+    unsigned cmark[WCUBE_N / 32];    // sample-voxel bitmap of the cube
+    int2 grid[RG_SMEM];              // (slot, brick summary of sample voxels)
     unsigned long long wbuf[BLOCK / 32][WK_WBUF];
     unsigned vids[WD_STEPS][BLOCK];  // voxel id of each in-flight visit
     SegDesc pf[BLOCK];
@@ -42,7 +46,8 @@ struct WalkDetSmem {
 
 // region slot for grid-relative coordinates packed in rp (fields biased by
 // RP_BIAS); inserts walk-entered regions like the generic walk
-__device__ __noinline__ int wd_slow_region(const DevMap &m, const WalkDetSmem &sm, unsigned rp) {
+__device__ __noinline__ int wd_slow_region(const DevMap &m, const WalkDetSmem &sm, unsigned rp,
+                                           unsigned *bm) {
     const int rx = sm.gb[0] + (int)(rp & 1023u) - RP_BIAS;
     const int ry = sm.gb[1] + (int)((rp >> 10) & 1023u) - RP_BIAS;
     const int rz = sm.gb[2] + (int)(rp >> 20) - RP_BIAS;
@@ -50,10 +55,14 @@ __device__ __noinline__ int wd_slow_region(const DevMap &m, const WalkDetSmem &s
                    uz = (unsigned)(rz - sm.gb[2]);
     if (sm.gmode && ux < (unsigned)sm.gn[0] && uy < (unsigned)sm.gn[1] && uz < (unsigned)sm.gn[2]) {
         const int gi = ux + sm.gs[1] * uy + sm.gs[2] * uz;
-        const int s = sm.gmode == 1 ? sm.grid[gi] : __ldg(m.rgrid + gi);
-        if (s >= 0) return s;
+        const int s = sm.gmode == 1 ? sm.grid[gi].x : __ldg(m.rgrid + gi);
+        if (s >= 0 && s < m.cap) {
+            *bm = sm.gmode == 1 ? (unsigned)sm.grid[gi].y : __ldcg(m.bmask + s);
+            return s;
+        }
     }
     const int slot = region_slot_inl(m, pack_region(rx, ry, rz));
+    *bm = slot >= 0 && slot < m.cap ? __ldcg(m.bmask + slot) : 0xFFFFFFFFu;
     if (slot >= 0 && slot < m.cap && atomicExch(m.slot_touch + slot, m.epoch) != m.epoch) {
         const unsigned long long t = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
         if (t < (unsigned long long)m.touched_cap) m.touched[t] = slot;
@@ -69,7 +78,7 @@ __device__ __noinline__ unsigned wd_vid_of(const DevMap &m, const WalkDetSmem &s
                    uz = (unsigned)(rz - sm.gb[2]);
     if (sm.gmode && ux < (unsigned)sm.gn[0] && uy < (unsigned)sm.gn[1] && uz < (unsigned)sm.gn[2]) {
         const int gi = ux + sm.gs[1] * uy + sm.gs[2] * uz;
-        s = sm.gmode == 1 ? sm.grid[gi] : __ldg(m.rgrid + gi);
+        s = sm.gmode == 1 ? sm.grid[gi].x : __ldg(m.rgrid + gi);
         if (s < 0) s = insert ? region_slot_inl(m, pack_region(rx, ry, rz)) : -1;
     } else {
         s = insert ? region_slot_inl(m, pack_region(rx, ry, rz))
@@ -93,7 +102,7 @@ __device__ __forceinline__ bool walk_det_ok(const DevMap &m) {
 }
 
 template <bool REC_ONLY, class Src>
-__global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_constant__ DevMap m,
+__global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_constant__ DevMap m,
                                                                Src src) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WalkDetSmem &sm = *reinterpret_cast<WalkDetSmem *>(smem_raw);
@@ -124,15 +133,22 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
     __syncthreads();
     if (sm.gmode == 1) {
         const int ncell = sm.gn[0] * sm.gn[1] * sm.gn[2];
-        for (int k = threadIdx.x; k < ncell; k += blockDim.x) sm.grid[k] = m.rgrid[k];
+        for (int k = threadIdx.x; k < ncell; k += blockDim.x) {
+            const int sl = m.rgrid[k];
+            sm.grid[k] = make_int2(sl, sl >= 0 && sl < m.cap ? (int)__ldcg(m.bmask + sl) : 0);
+        }
     }
     __syncthreads();
     unsigned *const scr = reinterpret_cast<unsigned *>(m.slab[L_SCRATCH]);
+    for (int k = threadIdx.x; k < WCUBE_N / 32; k += blockDim.x) sm.cmark[k] = 0u;
+    __syncthreads();
     for (int k = threadIdx.x; k < WCUBE_N; k += blockDim.x) {
         const unsigned vid = wd_vid_of(m, sm, sm.anchor[0] + k % WCUBE,
                                        sm.anchor[1] + (k / WCUBE) % WCUBE,
                                        sm.anchor[2] + k / (WCUBE * WCUBE), false);
-        sm.cube[k] = vid != 0xFFFFFFFFu ? (__ldcg(scr + vid) & MARK_FLAG) : 0u;
+        sm.cube[k] = 0u;
+        if (vid != 0xFFFFFFFFu && (__ldcg(scr + vid) & MARK_FLAG))
+            atomicOr(sm.cmark + (k >> 5), 1u << (k & 31));
     }
     __syncthreads();
 
@@ -147,7 +163,8 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
 
     // segment state
     double tx = 0, ty = 0, tz = 0, dx = 0, dy = 0, dz = 0;
-    unsigned lp = 0, rp = 0, vbase = 0xFFFFFFFFu, okey = 0, cp = 0;
+    unsigned lp = 0, rp = 0, vbase = 0xFFFFFFFFu, okey = 0, cp = 0, bm = 0;
+    const bool bricks = m.brick_shift >= 0;
     int li = 0, gi = 0, rem = 0;
     int dli0 = 0, dli1 = 0, dli2 = 0;       // local-index step per axis
     unsigned dlp0 = 0, dlp1 = 0, dlp2 = 0;  // packed-coordinate step per axis
@@ -159,10 +176,9 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
     // sharded maps: a region created during the walk was not stamped with the
     // other ranks' sample voxels, so every visit in it is kept as a record
     bool forced = false;
-    unsigned fmask = 0;
-    // in-flight visits of the window
-    unsigned olds[WD_STEPS];
-    unsigned live = 0, hits = 0;  // bit q: slot q holds a visit / the hit
+    // candidates of the window: bit q of `live` -- slot q holds a candidate
+    // (voxel id in sm.vids); `sure` -- known record (cube sample voxel / forced)
+    unsigned live = 0, hits = 0, sure = 0;
     // prefetch + warp work pool
     bool pf_valid = false, exhausted = false;
     unsigned pool_next = 0, pool_end = 0;
@@ -184,8 +200,9 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
         }
     };
 
-    auto set_region = [&](int s) {
+    auto set_region = [&](int s, unsigned b) {
         vbase = s >= 0 && s < m.cap ? (unsigned)s * vpr : 0xFFFFFFFFu;
+        bm = bricks ? b : 0xFFFFFFFFu;
         forced = m.shard_world > 1 && s >= m.walk_slot0;
     };
 
@@ -217,10 +234,22 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
         ingrid = sm.gmode && (unsigned)u0 < (unsigned)sm.gn[0] && (unsigned)u1 < (unsigned)sm.gn[1] &&
                  (unsigned)u2 < (unsigned)sm.gn[2];
         gi = u0 + sm.gs[1] * u1 + sm.gs[2] * u2;
-        int s = -1;
-        if (ingrid) s = sm.gmode == 1 ? sm.grid[gi] : __ldg(m.rgrid + gi);
-        if (s < 0) s = wd_slow_region(m, sm, rp);
-        set_region(s);
+        {
+            int s = -1;
+            unsigned b = 0xFFFFFFFFu;
+            if (ingrid) {
+                if (sm.gmode == 1) {
+                    const int2 ge = sm.grid[gi];
+                    s = ge.x;
+                    b = (unsigned)ge.y;
+                } else {
+                    s = __ldg(m.rgrid + gi);
+                    if (s >= 0 && s < m.cap) b = __ldcg(m.bmask + s);
+                }
+            }
+            if (s < 0) s = wd_slow_region(m, sm, rp, &b);
+            set_region(s, b);
+        }
         sm.endc[threadIdx.x][0] = d.e[0];
         sm.endc[threadIdx.x][1] = d.e[1];
         sm.endc[threadIdx.x][2] = d.e[2];
@@ -235,7 +264,7 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
     };
 
     // one DDA step = one voxel visit into in-flight slot Q (common case only)
-    auto step = [&](const int Q) {
+    auto step = [&](const int Q) {  // Q: the window's step index (dynamic)
         if (!active) return;
         const bool last = rem == 0;
         if (last) {
@@ -256,15 +285,25 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
             }
             if (okey & 1u) hits |= 1u << Q;
         }
-        // ---- the visit: one atomic, result checked at the end of the window ----
+        // ---- the visit: a miss count, or a candidate checked at the window's end ----
         const unsigned vid = vbase + (unsigned)li;
         if (vbase != 0xFFFFFFFFu) {
-            unsigned *p = scr + vid;
-            if (in_cube) p = sm.cube + ((cp & 7u) | ((cp >> 5) & 0x38u) | ((cp >> 10) & 0x1C0u));
-            olds[Q] = REC_ONLY ? *((volatile unsigned *)p) : atomicAdd(p, 1u);
-            sm.vids[Q][threadIdx.x] = vid;
-            live |= 1u << Q;
-            if (forced) fmask |= 1u << Q;
+            if (in_cube) {
+                const unsigned ck = (cp & 7u) | ((cp >> 5) & 0x38u) | ((cp >> 10) & 0x1C0u);
+                if (((sm.cmark[ck >> 5] >> (ck & 31)) & 1u) || forced) {
+                    sm.vids[Q][threadIdx.x] = vid;
+                    live |= 1u << Q;
+                    sure |= 1u << Q;
+                } else if (!REC_ONLY) {
+                    atomicAdd(sm.cube + ck, 1u);
+                }
+            } else if (((bm >> brick_of(li, m.bsh)) & 1u) || forced) {
+                sm.vids[Q][threadIdx.x] = vid;
+                live |= 1u << Q;
+                if (forced) sure |= 1u << Q;
+            } else if (!REC_ONLY) {
+                red_add(scr + vid, 1u);
+            }
         } else {
             ++rmiss;
         }
@@ -293,9 +332,19 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
             gi += ((int)dp >> sh) * sm.gs[ax];
             ingrid = ingrid && f < (unsigned)sm.gn[ax];
             int s = -1;
-            if (ingrid) s = sm.gmode == 1 ? sm.grid[gi] : __ldg(m.rgrid + gi);
+            unsigned b = 0xFFFFFFFFu;
+            if (ingrid) {
+                if (sm.gmode == 1) {
+                    const int2 ge = sm.grid[gi];
+                    s = ge.x;
+                    b = (unsigned)ge.y;
+                } else {
+                    s = __ldg(m.rgrid + gi);
+                    if (s >= 0 && s < m.cap) b = __ldcg(m.bmask + s);
+                }
+            }
             if (s >= 0) {
-                set_region(s);
+                set_region(s, b);
             } else {
                 parked = 1;  // outside the grid or a region the prefetch did not create
                 active = false;
@@ -306,13 +355,16 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
     // window boundary: resolve parked lanes (no visit in flight)
     auto unpark = [&]() {
         if (parked == 1) {
-            set_region(wd_slow_region(m, sm, rp));
+            unsigned b = 0xFFFFFFFFu;
+            const int s = wd_slow_region(m, sm, rp, &b);
+            set_region(s, b);
         } else if (parked == 2) {
             const unsigned vid = wd_vid_of(m, sm, sm.endc[threadIdx.x][0], sm.endc[threadIdx.x][1],
                                            sm.endc[threadIdx.x][2], true);
             vbase = vid == 0xFFFFFFFFu ? vid : vid - vid % vpr;
             li = vid == 0xFFFFFFFFu ? 0 : (int)(vid % vpr);
             forced = m.shard_world > 1 && vid != 0xFFFFFFFFu && (int)(vid / vpr) >= m.walk_slot0;
+            bm = 0xFFFFFFFFu;  // the end voxel is a candidate
             in_cube = false;
             jumped = true;
         }
@@ -321,18 +373,26 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
     };
 
     for (;;) {
-        // ---- retire the window: sample voxels become records ----
+        // ---- retire the window: candidates become records or miss counts ----
         if (__any_sync(0xffffffffu, live != 0u)) {
+            unsigned w[WD_STEPS], v[WD_STEPS];
 #pragma unroll
             for (int q = 0; q < WD_STEPS; ++q) {
-                const bool rec = ((live >> q) & 1u) && ((olds[q] & MARK_FLAG) || ((fmask >> q) & 1u));
-                push_records(rec, rec ? (((unsigned long long)sm.vids[q][threadIdx.x] << ob) |
-                                         (okey & ~1u) | ((hits >> q) & 1u))
-                                      : 0ULL);
+                w[q] = 0u;
+                v[q] = sm.vids[q][threadIdx.x];
+                if (((live & ~sure) >> q) & 1u) w[q] = __ldcg(scr + v[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < WD_STEPS; ++q) {
+                const bool cand = (live >> q) & 1u;
+                const bool rec = cand && (((sure >> q) & 1u) || (w[q] & MARK_FLAG));
+                if (cand && !rec && !REC_ONLY) red_add(scr + v[q], 1u);
+                push_records(rec, ((unsigned long long)v[q] << ob) | (okey & ~1u) |
+                                      ((hits >> q) & 1u));
             }
             live = 0u;
             hits = 0u;
-            fmask = 0u;
+            sure = 0u;
         }
         if (parked) unpark();
         if (!active && pf_valid) start();
@@ -373,7 +433,7 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
         }
         if (!__any_sync(0xffffffffu, active || pf_valid || !exhausted || parked)) break;
         if (!__any_sync(0xffffffffu, active)) continue;
-#pragma unroll
+#pragma unroll 1
         for (int q = 0; q < WD_STEPS; ++q) step(q);
     }
     // flush the warp's remaining records
@@ -393,7 +453,7 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk_det(const __grid_cons
     if (!REC_ONLY) {
         for (int k = threadIdx.x; k < WCUBE_N; k += blockDim.x) {
             const unsigned c = sm.cube[k];
-            if (!c || (c & MARK_FLAG)) continue;  // marked voxels: their visits are records
+            if (!c) continue;
             ++flushed;
             const unsigned vid = wd_vid_of(m, sm, sm.anchor[0] + k % WCUBE,
                                            sm.anchor[1] + (k / WCUBE) % WCUBE,
