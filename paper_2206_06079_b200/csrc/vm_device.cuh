@@ -105,6 +105,8 @@ struct DevMap {
     unsigned long long marked_cap;
     unsigned long long rec_invalid;      // voxel-id field of dropped records (skipped by the fold)
     int walk_slot0;                      // regions with slot >= this were created by the walk
+    int key_mi;                          // occupancy records key on the sample-voxel index
+                                         // (marked list) instead of the voxel id
     // batch outputs
     unsigned long long *rec;
     unsigned *recval;                    // per-record value (NDT deterministic phase 1)

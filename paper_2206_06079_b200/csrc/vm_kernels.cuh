@@ -442,9 +442,13 @@ __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevM
                         if (!was) {
                             ++nmark_local;
                             if (m.marked) {
-                                // sharded maps publish their new sample voxels
+                                // the batch's sample-voxel list: published by sharded
+                                // maps; its index keys the records otherwise
                                 const unsigned long long mi = atomicAdd(m.nmarked, 1ULL);
-                                if (mi < m.marked_cap) m.marked[mi] = make_int2(rt.slot, li);
+                                if (mi < m.marked_cap) {
+                                    m.marked[mi] = make_int2(rt.slot, li);
+                                    if (m.key_mi) *w = MARK_FLAG | (unsigned)mi;
+                                }
                             }
                         }
                         // brick summary read by the walks (4 x 4 x 2 bricks); set
@@ -1043,6 +1047,13 @@ __device__ __forceinline__ long long lower_bound_u64(const unsigned long long *a
     return lo;
 }
 
+// voxel id of an occupancy record's key field (sample-voxel index or voxel id)
+__device__ __forceinline__ unsigned record_vid(const DevMap &m, unsigned long long vk) {
+    if (!m.key_mi) return (unsigned)vk;
+    const int2 sl = m.marked[vk];
+    return (unsigned)sl.x * (unsigned)m.vpr + (unsigned)sl.y;
+}
+
 // Apply one sample voxel's records [s, e) in ray order (reference.py:35-64
 // restricted to that voxel): misses between hits collapse to f_miss^k.
 // Clears the voxel's MARK'ed scratch word.
@@ -1109,7 +1120,7 @@ __global__ void __launch_bounds__(BLOCK) k_fold_occ(const __grid_constant__ DevM
             big[atomicAdd(nbig, 1ULL)] = i;
             continue;
         }
-        fold_voxel_serial(m, src, keys, i, e, (unsigned)vk);
+        fold_voxel_serial(m, src, keys, i, e, record_vid(m, vk));
     }
 }
 
@@ -1130,7 +1141,7 @@ __global__ void __launch_bounds__(BLOCK) k_fold_occ_big(const __grid_constant__ 
          w += warps) {
         const long long s = big[w];
         const unsigned long long vk = keys[s] >> ob;
-        const unsigned vid = (unsigned)vk;
+        const unsigned vid = record_vid(m, vk);
         float *occ = reinterpret_cast<float *>(m.slab[L_OCC]) + vid;
         unsigned *mean = m.slab[L_MEAN] ? reinterpret_cast<unsigned *>(m.slab[L_MEAN]) + vid : nullptr;
         unsigned *cnt = m.slab[L_COUNT] ? reinterpret_cast<unsigned *>(m.slab[L_COUNT]) + vid : nullptr;

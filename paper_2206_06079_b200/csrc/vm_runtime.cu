@@ -209,6 +209,7 @@ DevMap make_dm(const vm_map *m) {
     d.marked_cap = 0;
     d.rec_invalid = ~0ULL;
     d.walk_slot0 = 1 << 30;
+    d.key_mi = 0;
     return d;
 }
 
@@ -420,6 +421,12 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     if (emit && (rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * maxseg + 1))) return rc;
     if (emit && (rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
     if (emit && (rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
+    // occupancy / decay records key on the index in the batch's sample-voxel list
+    const bool key_mi = occ_det && m->shard_world == 1;
+    if (key_mi) {
+        if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)n + 1))) return rc;
+        CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
+    }
     size_t rec_need = 0;
     if (ndt) rec_need = std::max<size_t>(m->rec_cap, (size_t)n * (det ? 8 : 1) + 1);
     else if (tsdf && det) {
@@ -440,6 +447,12 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         m->epoch += 1;
         DevMap dm = make_dm(m);
         dm.order_bits = order_bits;
+        if (key_mi) {
+            dm.key_mi = 1;
+            dm.marked = m->d_smarked;
+            dm.nmarked = m->d_shard_cnt;
+            dm.marked_cap = m->smarked_cap;
+        }
         CK(cudaMemsetAsync(m->d_stats, 0, NUM_STATS * sizeof(unsigned long long), m->stream));
         {
             static const int box_init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
@@ -541,6 +554,11 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             }
             int end_bit = order_bits + (ndt ? 1 : 0) +
                           std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
+            if (key_mi) {
+                unsigned long long M = 0;
+                CK(cudaMemcpy(&M, m->d_shard_cnt, sizeof(M), cudaMemcpyDeviceToHost));
+                end_bit = order_bits + std::max(1, bitlen(std::min<unsigned long long>(M, m->smarked_cap)));
+            }
             end_bit = std::min(end_bit, 64);
             cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
             cub::DoubleBuffer<unsigned> dv(m->d_val, m->d_val2);
@@ -674,6 +692,7 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         (rc = dev_alloc(&m->d_rgrid, RG_MAX)) || (rc = dev_alloc(&m->d_rbox, 6)) ||
         (rc = dev_alloc(&m->d_bmask, m->max_slots)) ||
         (rc = dev_alloc(&m->d_seg_hist, SEG_BUCKETS)) ||
+        (rc = dev_alloc(&m->d_shard_cnt, 3)) ||
         (rc = dev_alloc(&m->d_seg_cursor, SEG_BUCKETS)) ||
         (rc = dev_alloc(&m->d_nbig, 1)))
         return cleanup(rc);

@@ -236,19 +236,22 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk(const __grid_constant
     };
 
     // resolve the candidates: one batch of loads of their scratch words
-    // (MARK_FLAG = sample voxel -> record; otherwise the delayed miss count)
+    // (MARK_FLAG = sample voxel -> record; otherwise the delayed miss count).
+    // key_mi: the word of a sample voxel holds MARK_FLAG | its index in the
+    // batch's sample-voxel list, which then keys the record.
     auto retire = [&]() {
         if (!DET) return;
         if (!__any_sync(0xffffffffu, ncand != 0)) return;
         unsigned long long key[WK_INNER];
         unsigned w[WK_INNER];
+        const unsigned long long omask = (1ULL << m.order_bits) - 1;
 #pragma unroll
         for (int q = 0; q < WK_INNER; ++q) {
             key[q] = q < ncand ? sm.cand[q][threadIdx.x] : ~0ULL;
             w[q] = 0u;
-            // cube candidates carry no address: they are sample voxels already
-            if (q < ncand && !(key[q] & (1ULL << 63)))
-                w[q] = __ldcg(scr + (unsigned)(key[q] >> m.order_bits));
+            // cube candidates (bit 63) are sample voxels already
+            if (q < ncand && (m.key_mi || !(key[q] & (1ULL << 63))))
+                w[q] = __ldcg(scr + (unsigned)((key[q] & ~(1ULL << 63)) >> m.order_bits));
         }
 #pragma unroll
         for (int q = 0; q < WK_INNER; ++q) {
@@ -256,7 +259,10 @@ __global__ void __launch_bounds__(BLOCK, WK_BLOCKS) k_walk(const __grid_constant
             const bool cube_rec = valid && (key[q] & (1ULL << 63));
             const bool rec = cube_rec || (valid && (w[q] & MARK_FLAG));
             if (valid && !rec && !REC_ONLY) red_add(scr + (unsigned)(key[q] >> m.order_bits), 1u);
-            push_records(rec, key[q] & ~(1ULL << 63));
+            const unsigned long long k = key[q] & ~(1ULL << 63);
+            push_records(rec, m.key_mi ? ((unsigned long long)(w[q] & ~MARK_FLAG) << m.order_bits) |
+                                             (k & omask)
+                                       : k);
         }
         ncand = 0;
     };

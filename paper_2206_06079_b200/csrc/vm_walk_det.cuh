@@ -376,19 +376,22 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         // ---- retire the window: candidates become records or miss counts ----
         if (__any_sync(0xffffffffu, live != 0u)) {
             unsigned w[WD_STEPS], v[WD_STEPS];
+            // key_mi: the counter of a sample voxel holds MARK_FLAG | its index in
+            // the batch's sample-voxel list, which then keys the record
+            const unsigned need = m.key_mi ? live : (live & ~sure);
 #pragma unroll
             for (int q = 0; q < WD_STEPS; ++q) {
                 w[q] = 0u;
                 v[q] = sm.vids[q][threadIdx.x];
-                if (((live & ~sure) >> q) & 1u) w[q] = __ldcg(scr + v[q]);
+                if ((need >> q) & 1u) w[q] = __ldcg(scr + v[q]);
             }
 #pragma unroll
             for (int q = 0; q < WD_STEPS; ++q) {
                 const bool cand = (live >> q) & 1u;
                 const bool rec = cand && (((sure >> q) & 1u) || (w[q] & MARK_FLAG));
                 if (cand && !rec && !REC_ONLY) red_add(scr + v[q], 1u);
-                push_records(rec, ((unsigned long long)v[q] << ob) | (okey & ~1u) |
-                                      ((hits >> q) & 1u));
+                const unsigned long long kf = m.key_mi ? (w[q] & ~MARK_FLAG) : v[q];
+                push_records(rec, (kf << ob) | (okey & ~1u) | ((hits >> q) & 1u));
             }
             live = 0u;
             hits = 0u;
