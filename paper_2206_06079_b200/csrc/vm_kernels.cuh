@@ -920,10 +920,14 @@ __device__ __forceinline__ void resolve_range(const DevMap &m, int slot, int v0,
     unsigned *scr = reinterpret_cast<unsigned *>(m.slab[L_SCRATCH] + (size_t)slot * m.bpr[L_SCRATCH]);
     float *occ = reinterpret_cast<float *>(m.slab[L_OCC] + (size_t)slot * m.bpr[L_OCC]);
     if (!NDT && ((v0 | v1) & 3) == 0) {
-        // 8 independent 16-byte loads in flight per thread
+        // 8 independent 16-byte scratch loads in flight per thread, then the
+        // occupancy quads of the non-zero ones, also all in flight
         const uint4 *s4 = reinterpret_cast<const uint4 *>(scr);
+        float4 *o4 = reinterpret_cast<float4 *>(occ);
         for (int q0 = (v0 >> 2) + threadIdx.x; q0 < (v1 >> 2); q0 += 8 * blockDim.x) {
             uint4 w[8];
+            float4 l[8];
+            unsigned nz = 0;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int q = q0 + u * blockDim.x;
@@ -931,18 +935,30 @@ __device__ __forceinline__ void resolve_range(const DevMap &m, int slot, int v0,
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                if (!(w[u].x | w[u].y | w[u].z | w[u].w)) continue;
+                // counted voxels (MARK'ed words -- sample voxels -- are the fold's)
+                const unsigned ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) any = any || (ws[j] != 0u && !(ws[j] & MARK_FLAG));
+                if (any) {
+                    nz |= 1u << u;
+                    l[u] = o4[q0 + u * blockDim.x];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (!((nz >> u) & 1u)) continue;
                 const int q = q0 + u * blockDim.x;
                 unsigned ks[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-                bool clear = false;
+                float ls[4] = {l[u].x, l[u].y, l[u].z, l[u].w};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     if (ks[j] == 0 || (ks[j] & MARK_FLAG)) continue;
-                    clear = true;
-                    occ[4 * q + j] = miss_k(occ[4 * q + j], ks[j], m.miss32, m.cmin, m.cmax);
+                    ls[j] = miss_k(ls[j], ks[j], m.miss32, m.cmin, m.cmax);
                     ks[j] = 0;
                 }
-                if (clear) reinterpret_cast<uint4 *>(scr)[q] = make_uint4(ks[0], ks[1], ks[2], ks[3]);
+                o4[q] = make_float4(ls[0], ls[1], ls[2], ls[3]);
+                reinterpret_cast<uint4 *>(scr)[q] = make_uint4(ks[0], ks[1], ks[2], ks[3]);
             }
         }
         return;
