@@ -105,6 +105,20 @@ struct vm_map {
     size_t sort_tmp_bytes = 0;
     unsigned char *d_rays = nullptr;
     size_t rays_bytes = 0;
+    // host rays of the batch: uploaded in chunks on copy_stream, each chunk's
+    // discover waits only for its own chunk (the copy overlaps discover)
+    cudaStream_t copy_stream = nullptr;
+    static constexpr int UP_CHUNKS = 4;
+    cudaEvent_t ev_up[UP_CHUNKS] = {};
+    struct Upload {
+        int pending = 0;            // 1: the first discover attempt uploads
+        int format = 0;
+        const unsigned char *rec = nullptr;  // OHMB1 host records
+        const double *o = nullptr, *e = nullptr;
+        const unsigned char *h = nullptr;
+        const float *it = nullptr;
+        size_t b_o = 0, b_h = 0;   // device layout of the f64 arrays
+    } up;
     unsigned long long *h_stats = nullptr;  // pinned, NUM_STATS + 2
     // region sharding (vm_shard_*)
     int shard_rank = 0, shard_world = 1;
@@ -460,10 +474,45 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                                m->stream));
         }
         CK(cudaEventRecord(m->ev_start, m->stream));
-        dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK));
-        const dim3 dgrid((unsigned)((n + BLOCK - 1) / BLOCK), tsdf ? 1 : (unsigned)maxseg);
-        k_discover<<<dgrid, BLOCK, 0, m->stream>>>(dm, src, n, mode, det ? 1 : 0, emit ? 1 : 0);
-        m->launches += 2;  // discover + guard
+        if (m->up.pending) {
+            // host rays: chunk c is copied on copy_stream while chunk c-1 is discovered
+            const int nc = n >= 65536 ? vm_map::UP_CHUNKS : 1;
+            CK(cudaEventRecord(m->ev_up[0], m->stream));  // the previous batch is done with d_rays
+            CK(cudaStreamWaitEvent(m->copy_stream, m->ev_up[0], 0));
+            for (int c = 0; c < nc; ++c) {
+                const long long lo = n * c / nc, hi = n * (c + 1) / nc;
+                if (hi <= lo) continue;
+                const auto &u = m->up;
+                if (u.format == VM_RAYS_OHMB1) {
+                    CK(cudaMemcpyAsync(m->d_rays + (size_t)lo * 40, u.rec + (size_t)lo * 40,
+                                       (size_t)(hi - lo) * 40, cudaMemcpyHostToDevice, m->copy_stream));
+                } else {
+                    unsigned char *d = m->d_rays;
+                    CK(cudaMemcpyAsync(d + lo * 24, (const unsigned char *)u.o + lo * 24, (hi - lo) * 24,
+                                       cudaMemcpyHostToDevice, m->copy_stream));
+                    CK(cudaMemcpyAsync(d + u.b_o + lo * 24, (const unsigned char *)u.e + lo * 24,
+                                       (hi - lo) * 24, cudaMemcpyHostToDevice, m->copy_stream));
+                    CK(cudaMemcpyAsync(d + 2 * u.b_o + lo, u.h + lo, hi - lo, cudaMemcpyHostToDevice,
+                                       m->copy_stream));
+                    if (u.it)
+                        CK(cudaMemcpyAsync(d + 2 * u.b_o + u.b_h + lo * 4, (const unsigned char *)u.it + lo * 4,
+                                           (hi - lo) * 4, cudaMemcpyHostToDevice, m->copy_stream));
+                }
+                CK(cudaEventRecord(m->ev_up[c], m->copy_stream));
+                CK(cudaStreamWaitEvent(m->stream, m->ev_up[c], 0));
+                DevMap dc = dm;
+                dc.ray_lo = lo;
+                const dim3 cg((unsigned)((hi - lo + BLOCK - 1) / BLOCK), tsdf ? 1 : (unsigned)maxseg);
+                k_discover<<<cg, BLOCK, 0, m->stream>>>(dc, src, hi - lo, mode, det ? 1 : 0, emit ? 1 : 0);
+                m->launches += 1;
+            }
+            m->up.pending = 0;
+            m->launches += 1;  // guard
+        } else {
+            const dim3 dgrid((unsigned)((n + BLOCK - 1) / BLOCK), tsdf ? 1 : (unsigned)maxseg);
+            k_discover<<<dgrid, BLOCK, 0, m->stream>>>(dm, src, n, mode, det ? 1 : 0, emit ? 1 : 0);
+            m->launches += 2;  // discover + guard
+        }
         if ((rc = check_launch("discover"))) return rc;
         int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
         k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
@@ -680,8 +729,12 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         vm_map_destroy(m);
         return code;
     };
-    if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup(fail(VM_ERR_CUDA, "stream create failed"));
+    for (auto &e : m->ev_up)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            return cleanup(fail(VM_ERR_CUDA, "event create"));
     m->own_stream = true;
     if ((rc = dev_alloc(&m->d_tkeys, ts, 0xFF)) || (rc = dev_alloc(&m->d_tvals, ts, 0xFF)) ||
         (rc = dev_alloc(&m->d_cursor, 1)) || (rc = dev_alloc(&m->d_slot_keys, m->max_slots)) ||
@@ -756,6 +809,9 @@ int vm_map_destroy(vm_map *m) {
     for (auto e : evs)
         if (e) cudaEventDestroy(e);
     if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
+    for (auto e : m->ev_up)
+        if (e) cudaEventDestroy(e);
+    if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
     delete m;
     return VM_OK;
 }
@@ -909,17 +965,22 @@ int vm_integrate(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, vm_
         out->regions_total = m->nreg;
         return VM_OK;
     }
+    m->up = vm_map::Upload{};
     if (rays->format == VM_RAYS_OHMB1) {
         if (!rays->records) return fail(VM_ERR_ARG, "null records");
         const unsigned char *p = (const unsigned char *)rays->records;
         if (!rays->on_device) {
             int rc = ensure_buf(&m->d_rays, &m->rays_bytes, (size_t)n * 40);
             if (rc) return rc;
-            CK(cudaMemcpyAsync(m->d_rays, p, (size_t)n * 40, cudaMemcpyHostToDevice, m->stream));
+            m->up.pending = 1;
+            m->up.format = VM_RAYS_OHMB1;
+            m->up.rec = p;
             p = m->d_rays;
         }
         SrcOHMB1 src{p};
-        return integrate_impl(m, src, n, mode, exec, out);
+        const int rc = integrate_impl(m, src, n, mode, exec, out);
+        m->up.pending = 0;
+        return rc;
     }
     if (rays->format == VM_RAYS_F64) {
         if (!rays->origins || !rays->ends || !rays->has_sample)
@@ -931,17 +992,20 @@ int vm_integrate(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, vm_
             int rc = ensure_buf(&m->d_rays, &m->rays_bytes, total);
             if (rc) return rc;
             unsigned char *d = m->d_rays;
-            CK(cudaMemcpyAsync(d, rays->origins, b_o, cudaMemcpyHostToDevice, m->stream));
-            CK(cudaMemcpyAsync(d + b_o, rays->ends, b_o, cudaMemcpyHostToDevice, m->stream));
-            CK(cudaMemcpyAsync(d + 2 * b_o, rays->has_sample, n, cudaMemcpyHostToDevice,
-                               m->stream));
-            if (rays->intensity)
-                CK(cudaMemcpyAsync(d + 2 * b_o + b_h, rays->intensity, b_i,
-                                   cudaMemcpyHostToDevice, m->stream));
+            m->up.pending = 1;
+            m->up.format = VM_RAYS_F64;
+            m->up.o = rays->origins;
+            m->up.e = rays->ends;
+            m->up.h = rays->has_sample;
+            m->up.it = rays->intensity;
+            m->up.b_o = b_o;
+            m->up.b_h = b_h;
             src = SrcF64{(const double *)d, (const double *)(d + b_o), d + 2 * b_o,
                          rays->intensity ? (const float *)(d + 2 * b_o + b_h) : nullptr};
         }
-        return integrate_impl(m, src, n, mode, exec, out);
+        const int rc = integrate_impl(m, src, n, mode, exec, out);
+        m->up.pending = 0;
+        return rc;
     }
     return fail(VM_ERR_ARG, "unknown ray format");
 }
