@@ -415,6 +415,14 @@ __host__ __device__ __forceinline__ int region_owner(long long key, int world) {
     return (int)(mix_key(pack_region(bx, by, bz)) % (unsigned long long)world);
 }
 
+// First stamp of `epoch` into a per-slot word: true for exactly one caller
+// per epoch.  A plain load first, so the common already-stamped case costs
+// no atomic on these hot words (every block touches the sensor's regions).
+__device__ __forceinline__ bool stamp_epoch(unsigned *p, unsigned epoch) {
+    if (*((volatile unsigned *)p) == epoch) return false;
+    return atomicExch(p, epoch) != epoch;
+}
+
 // ---------------------------------------------------------------- block helpers
 
 // Per-block set of region slots already recorded this kernel: turns the

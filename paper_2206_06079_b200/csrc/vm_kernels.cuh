@@ -226,7 +226,7 @@ __device__ __forceinline__ bool in_range(const DevMap &m, const double p[3]) {
 // Record the region as touched by the walk (needed by k_resolve).
 __device__ __forceinline__ void touch_region(const DevMap &m, int *sset, int slot) {
     if (!slotset_insert(sset, slot)) return;
-    if (atomicExch(m.slot_touch + slot, m.epoch) != m.epoch) {
+    if (stamp_epoch(m.slot_touch + slot, m.epoch)) {
         unsigned long long idx = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
         if (idx < (unsigned long long)m.touched_cap) m.touched[idx] = slot;
     }
@@ -299,9 +299,9 @@ struct PrefetchVisitor {
         const int slot = cached_slot(*m, *kc, x, y, z, &fresh);
         if (slot < 0 || !fresh) return;
         if (!slotset_insert(sset, slot)) return;  // first sight of the region in this block only
-        if (atomicExch(m->slot_pref + slot, m->epoch) != m->epoch)
+        if (stamp_epoch(m->slot_pref + slot, m->epoch))
             atomicAdd(m->stats + S_PREF_TOUCHED, 1ULL);
-        if (slot < m->cap && atomicExch(m->slot_touch + slot, m->epoch) != m->epoch) {
+        if (slot < m->cap && stamp_epoch(m->slot_touch + slot, m->epoch)) {
             unsigned long long t = atomicAdd(m->stats + S_WALK_TOUCHED, 1ULL);
             if (t < (unsigned long long)m->touched_cap) m->touched[t] = slot;
         }

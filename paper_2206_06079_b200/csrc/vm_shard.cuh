@@ -208,7 +208,7 @@ __global__ void k_shard_import(const __grid_constant__ DevMap m, const ShardItem
         const ShardItem it = in[i];
         const int s = region_find(m, it.rkey);
         if (s < 0 || s >= m.cap) continue;
-        if (atomicExch(m.slot_touch + s, m.epoch) != m.epoch) {
+        if (stamp_epoch(m.slot_touch + s, m.epoch)) {
             const unsigned long long t = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
             if (t < (unsigned long long)m.touched_cap) m.touched[t] = s;
         }

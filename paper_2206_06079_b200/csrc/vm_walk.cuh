@@ -90,7 +90,7 @@ __device__ __forceinline__ int walk_region(const DevMap &m, const WalkSmem &sm, 
     bm = 0xFFFFFFFFu;
     if (slot >= 0 && slot < m.cap) {
         bm = __ldcg(m.bmask + slot);
-        if (atomicExch(m.slot_touch + slot, m.epoch) != m.epoch) {
+        if (stamp_epoch(m.slot_touch + slot, m.epoch)) {
             // regions reached outside the dense grid are resolved from the touched list
             const unsigned long long t = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
             if (t < (unsigned long long)m.touched_cap) m.touched[t] = slot;

@@ -63,7 +63,7 @@ __device__ __noinline__ int wd_slow_region(const DevMap &m, const WalkDetSmem &s
     }
     const int slot = region_slot_inl(m, pack_region(rx, ry, rz));
     *bm = slot >= 0 && slot < m.cap ? __ldcg(m.bmask + slot) : 0xFFFFFFFFu;
-    if (slot >= 0 && slot < m.cap && atomicExch(m.slot_touch + slot, m.epoch) != m.epoch) {
+    if (slot >= 0 && slot < m.cap && stamp_epoch(m.slot_touch + slot, m.epoch)) {
         const unsigned long long t = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
         if (t < (unsigned long long)m.touched_cap) m.touched[t] = slot;
     }
@@ -83,7 +83,7 @@ __device__ __noinline__ unsigned wd_vid_of(const DevMap &m, const WalkDetSmem &s
     } else {
         s = insert ? region_slot_inl(m, pack_region(rx, ry, rz))
                    : region_find_probe(m, pack_region(rx, ry, rz));
-        if (s >= 0 && s < m.cap && atomicExch(m.slot_touch + s, m.epoch) != m.epoch) {
+        if (s >= 0 && s < m.cap && stamp_epoch(m.slot_touch + s, m.epoch)) {
             const unsigned long long t = atomicAdd(m.stats + S_WALK_TOUCHED, 1ULL);
             if (t < (unsigned long long)m.touched_cap) m.touched[t] = s;
         }
