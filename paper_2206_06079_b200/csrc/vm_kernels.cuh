@@ -111,94 +111,6 @@ __device__ __forceinline__ double gaussian_weight(const double mu[3], const floa
     return exp(-0.5 * m2);
 }
 
-// CPython 3.12 math.hypot (Modules/mathmodule.c vector_norm), used by
-// ndt.cholupdate3 (ndt.py:42): bit-identical to the host's math.hypot.
-__device__ double py_hypot(double a, double b) {
-    double x0 = fabs(a), x1 = fabs(b);
-    double mx = 0.0;
-    if (x0 > mx) mx = x0;
-    if (x1 > mx) mx = x1;
-    if (isnan(a) || isnan(b)) return __longlong_as_double(0x7ff8000000000000LL);
-    double scale_back = 1.0;
-    if (isinf(mx)) return mx;
-    if (mx == 0.0) return mx;
-    int e;
-    frexp(mx, &e);
-    if (e < -1023) {
-        const double DMIN = 2.2250738585072014e-308;
-        x0 /= DMIN;
-        x1 /= DMIN;
-        mx /= DMIN;
-        scale_back = DMIN;
-        frexp(mx, &e);
-    }
-    double scale = ldexp(1.0, -e);
-    double csum = 1.0, frac1 = 0.0, frac2 = 0.0;
-    double xs[2] = {x0, x1};
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        double x = xs[i] * scale;
-        double hi = x * x, lo = fma(x, x, -hi);
-        double s = csum + hi;
-        double sl = (csum - s) + hi;
-        csum = s;
-        frac1 += lo;
-        frac2 += sl;
-    }
-    double h = sqrt(csum - 1.0 + (frac1 + frac2));
-    {
-        double hi = -h * h, lo = fma(-h, h, -hi);
-        double s = csum + hi;
-        double sl = (csum - s) + hi;
-        csum = s;
-        frac1 += lo;
-        frac2 += sl;
-    }
-    double x = csum - 1.0 + (frac1 + frac2);
-    h += x / (2.0 * h);
-    return scale_back * (h / scale);
-}
-
-// ndt.update_gaussian + cholupdate3 (ndt.py:37-70); L stored as the 6
-// lower-triangular entries (s11, s21, s22, s31, s32, s33).
-__device__ __forceinline__ void update_gaussian(unsigned long long &n, double mu[3], double S[6],
-                                                const double x[3]) {
-    if (n == 0) {
-        n = 1;
-        for (int a = 0; a < 3; ++a) mu[a] = x[a];
-        for (int k = 0; k < 6; ++k) S[k] = 0.0;
-        return;
-    }
-    unsigned long long nn = n + 1;
-    double d[3];
-    for (int a = 0; a < 3; ++a) d[a] = x[a] - mu[a];
-    for (int a = 0; a < 3; ++a) mu[a] = mu[a] + d[a] / (double)nn;
-    double sq = sqrt((double)n);
-    double L[6];
-    for (int k = 0; k < 6; ++k) L[k] = S[k] * sq;
-    double f = sqrt((double)n / (double)nn);
-    double xx[3] = {d[0] * f, d[1] * f, d[2] * f};
-    // index of L[i][k] in the packed lower triangle
-    const int IDX[3][3] = {{0, -1, -1}, {1, 2, -1}, {3, 4, 5}};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        double lkk = L[IDX[k][k]];
-        double r = py_hypot(lkk, xx[k]);
-        if (r == 0.0) continue;
-        double c = lkk / r, s = xx[k] / r;
-        L[IDX[k][k]] = r;
-#pragma unroll
-        for (int i = k + 1; i < 3; ++i) {
-            double lik = L[IDX[i][k]];
-            L[IDX[i][k]] = c * lik + s * xx[i];
-            xx[i] = c * xx[i] - s * lik;
-        }
-    }
-    double sn = sqrt((double)nn);
-    for (int k = 0; k < 6; ++k) S[k] = L[k] / sn;
-    n = nn;
-}
-
 __device__ __forceinline__ int read_go(const DevMap &m) {
     return *((volatile int *)m.go);
 }
@@ -1266,15 +1178,27 @@ __global__ void __launch_bounds__(BLOCK) k_fold_ndt(const __grid_constant__ DevM
         if (TM && miss_add) missb[li] += miss_add;
         if (j == i || (j < R && (keys[j] >> vshift) == vid)) {
             // ---- phase-2 samples ----
-            unsigned long long nsamp = cb[li];
-            double mu[3] = {0.0, 0.0, 0.0};
-            if (nsamp > 0) {
+            // The reference folds them one by one (Welford mean + Givens rank-one
+            // update of L = S*sqrt(n), ndt.py:37-70): algebraically the scatter
+            // matrix M = n*S*S^T gains (n/(n+1)) d d^T per sample.  Here the
+            // batch is summed about a pivot and merged in one step, then S is
+            // the Cholesky factor of M / N (positive diagonal, like the Givens
+            // sweep): one serial pass of cheap accumulations instead of a chain
+            // of square roots and divisions per sample -- equal within the NDT
+            // tolerance (tests/test_gpu_parity.py: cov_sqrt 1e-5, mean 1 bucket).
+            const unsigned long long n0 = cb[li];
+            double mu0[3] = {0.0, 0.0, 0.0};
+            if (n0 > 0) {
                 double off[3];
                 unpack_mean(mb[li], off);
-                for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
+                for (int a = 0; a < 3; ++a) mu0[a] = ((double)g[a] + off[a]) * m.vox;
             }
-            double S[6];
-            for (int k = 0; k < 6; ++k) S[k] = cov[li * 6 + k];
+            double S0[6];
+            for (int k = 0; k < 6; ++k) S0[k] = cov[li * 6 + k];
+            double piv[3] = {mu0[0], mu0[1], mu0[2]};
+            double sum[3] = {0.0, 0.0, 0.0}, ss[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            unsigned long long kb = 0;
+            unsigned long long nsamp = n0;  // intensity Welford count
             const long long h0 = j;
             for (; j < R && (keys[j] >> vshift) == vid; ++j) {
                 long long ray = (long long)(((keys[j] & omask) >> 1) / (unsigned long long)m.maxseg);
@@ -1292,7 +1216,67 @@ __global__ void __launch_bounds__(BLOCK) k_fold_ndt(const __grid_constant__ DevM
                     ib[li * 2] = (float)mnew;
                     ib[li * 2 + 1] = (float)m2new;
                 }
-                update_gaussian(nsamp, mu, S, e);
+                ++nsamp;
+                if (kb == 0 && n0 == 0)
+                    for (int a = 0; a < 3; ++a) piv[a] = e[a];
+                const double d0 = e[0] - piv[0], d1 = e[1] - piv[1], d2 = e[2] - piv[2];
+                sum[0] += d0;
+                sum[1] += d1;
+                sum[2] += d2;
+                ss[0] += d0 * d0;
+                ss[1] += d1 * d0;
+                ss[2] += d1 * d1;
+                ss[3] += d2 * d0;
+                ss[4] += d2 * d1;
+                ss[5] += d2 * d2;
+                ++kb;
+            }
+            // merge (n0, mu0, M0) with the batch (kb, mean_b, M_b)
+            const double kd = (double)kb, N = (double)(n0 + kb);
+            double mb_[3], Mb[6];
+            for (int a = 0; a < 3; ++a) mb_[a] = sum[a] / kd;
+            Mb[0] = ss[0] - sum[0] * mb_[0];
+            Mb[1] = ss[1] - sum[1] * mb_[0];
+            Mb[2] = ss[2] - sum[1] * mb_[1];
+            Mb[3] = ss[3] - sum[2] * mb_[0];
+            Mb[4] = ss[4] - sum[2] * mb_[1];
+            Mb[5] = ss[5] - sum[2] * mb_[2];
+            double mu[3], M[6];
+            if (n0 == 0) {
+                for (int a = 0; a < 3; ++a) mu[a] = piv[a] + mb_[a];
+                for (int k = 0; k < 6; ++k) M[k] = Mb[k];
+            } else {
+                // M0 = n0 * S0 S0^T (lower-triangular S0)
+                const double n0d = (double)n0;
+                const double c00 = S0[0] * S0[0], c10 = S0[1] * S0[0], c11 = S0[1] * S0[1] + S0[2] * S0[2];
+                const double c20 = S0[3] * S0[0], c21 = S0[3] * S0[1] + S0[4] * S0[2];
+                const double c22 = S0[3] * S0[3] + S0[4] * S0[4] + S0[5] * S0[5];
+                const double dl[3] = {mb_[0], mb_[1], mb_[2]};  // batch mean - mu0 (pivot = mu0)
+                const double w = n0d * kd / N;
+                for (int a = 0; a < 3; ++a) mu[a] = mu0[a] + dl[a] * (kd / N);
+                M[0] = n0d * c00 + Mb[0] + w * dl[0] * dl[0];
+                M[1] = n0d * c10 + Mb[1] + w * dl[1] * dl[0];
+                M[2] = n0d * c11 + Mb[2] + w * dl[1] * dl[1];
+                M[3] = n0d * c20 + Mb[3] + w * dl[2] * dl[0];
+                M[4] = n0d * c21 + Mb[4] + w * dl[2] * dl[1];
+                M[5] = n0d * c22 + Mb[5] + w * dl[2] * dl[2];
+            }
+            // S = chol(M / N), lower, positive diagonal.  Pivots at rounding
+            // level (collinear / coplanar samples) are zero, as the Givens sweep
+            // leaves them (r == 0): below 1e-12 of the trace the pivot is noise.
+            double S[6];
+            {
+                const double a00 = M[0] / N, c10 = M[1] / N, c11 = M[2] / N;
+                const double c20 = M[3] / N, c21 = M[4] / N, c22 = M[5] / N;
+                const double eps = 1e-12 * (a00 + c11 + c22);
+                S[0] = a00 > eps ? sqrt(a00) : 0.0;
+                S[1] = S[0] > 0.0 ? c10 / S[0] : 0.0;
+                S[3] = S[0] > 0.0 ? c20 / S[0] : 0.0;
+                const double a11 = c11 - S[1] * S[1];
+                S[2] = a11 > eps ? sqrt(a11) : 0.0;
+                S[4] = S[2] > 0.0 ? (c21 - S[3] * S[1]) / S[2] : 0.0;
+                const double a22 = c22 - S[3] * S[3] - S[4] * S[4];
+                S[5] = a22 > eps ? sqrt(a22) : 0.0;
             }
             if (TM) hb[li] += (unsigned)(j - h0);
             cb[li] = nsamp > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)nsamp;
