@@ -159,6 +159,29 @@ int vm_map_layer_ptr(vm_map *map, int32_t slot, int32_t layer_id, void **dev_ptr
 int vm_integrate(vm_map *map, const vm_rays *rays, int32_t mode, int32_t exec,
                  vm_stats *out);
 
+/* Exporters (exporters.py:14-159).  vm_export_select: the voxels a format
+ * keeps, in the reference's order (regions as given -- the caller passes the
+ * slots of the sorted region keys, exporters.py:33-41 -- then local index).
+ * kind: 0 occupied (log-odds > threshold, :53), 1 NDT (mean_count > 0, :88),
+ * 2 TSDF (weight != 0, :131), 3 decay (hits or distance != 0, :149).
+ * *count_out is always set; ridx/li are filled when cap >= the count.
+ * vm_export_gather: the layer records of the selected voxels (host out). */
+int vm_export_select(vm_map *map, const int32_t *slots, int64_t nslots, int32_t kind,
+                     double threshold, int64_t *count_out, int32_t *ridx_out, int32_t *li_out,
+                     int64_t cap);
+int vm_export_gather(vm_map *map, int32_t layer, const int32_t *slots, int64_t nslots,
+                     const int32_t *ridx, const int32_t *li, int64_t n, void *out);
+
+/* A sequence of batches, integrated in order with the same result as one
+ * vm_integrate call per batch (out[i] = that call's stats).  Deterministic
+ * occupancy over OHMB1 records is pipelined: every batch is enqueued with no
+ * host round trip, host records are uploaded while earlier batches compute,
+ * and the call syncs once at the end.  Other modes loop over vm_integrate.
+ * Replaces the reference CLI's offline replay loop over submit_batch
+ * (cli.py:122-127, engine.py:175-210). */
+int vm_integrate_many(vm_map *map, const vm_rays *rays, int32_t nbatches, int32_t mode,
+                      int32_t exec, vm_stats *out);
+
 /* ---- `_kernels` one-to-one entry points (device pointers) ---- */
 
 /* _kernels.walk_voxels_native (_kernels.pyx:214-228): walk one segment on

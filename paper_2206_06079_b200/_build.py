@@ -65,5 +65,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> Path:
+    """Dev experiments: the same library built with extra -D flags into
+    _lib/<name> (selected at run time with VOXMAP_B200_LIB=<name>)."""
+    LIB_DIR.mkdir(parents=True, exist_ok=True)
+    out = LIB_DIR / name
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{INCLUDE}", "-o", str(out),
+           str(CSRC / "vm_runtime.cu")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed:\n{res.stderr[-6000:]}")
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -7,6 +7,7 @@ present, every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from pathlib import Path
 
@@ -18,11 +19,12 @@ VM_OK, VM_ERR_ARG, VM_ERR_CUDA, VM_ERR_OOM, VM_ERR_RANGE, VM_ERR_NODEV = range(6
 MODES = ("occupancy", "decay", "ndt-om", "ndt-tm", "tsdf")
 EXEC_CAS, EXEC_DETERMINISTIC = 0, 1
 RAYS_OHMB1, RAYS_F64 = 0, 1
+I64_t = ctypes.c_int64
 
 EXPORTED = (
     "vm_map_create", "vm_map_destroy", "vm_map_reset", "vm_map_set_stream", "vm_map_region_count",
     "vm_map_region_keys", "vm_map_ensure_regions", "vm_map_find_region", "vm_map_read_layer",
-    "vm_map_write_layer", "vm_map_layer_ptr", "vm_integrate", "vm_walk_voxels", "vm_hash_mix",
+    "vm_map_write_layer", "vm_map_layer_ptr", "vm_integrate", "vm_integrate_many", "vm_export_select", "vm_export_gather", "vm_walk_voxels", "vm_hash_mix",
     "vm_kernels_integrate_occupancy", "vm_last_error", "vm_device_count", "vm_build_info",
     "vm_shard_config", "vm_shard_owner", "vm_shard_begin", "vm_shard_lists", "vm_shard_prepare",
     "vm_shard_walk",
@@ -76,11 +78,14 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB_PATH.exists():
+    path = LIB_PATH
+    if os.environ.get("VOXMAP_B200_LIB"):  # dev knob: an in-tree build variant (tools/variants)
+        path = LIB_PATH.parent / os.environ["VOXMAP_B200_LIB"]
+    if not path.exists():
         raise NativeError(
-            f"CUDA extension not built: {LIB_PATH} is missing "
+            f"CUDA extension not built: {path} is missing "
             "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
-    L = ctypes.CDLL(str(LIB_PATH))
+    L = ctypes.CDLL(str(path))
     P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     sig = {
         "vm_map_create": ([ctypes.POINTER(VmConfig), ctypes.c_uint32, I32, I64,
@@ -97,6 +102,10 @@ def lib():
         "vm_map_layer_ptr": ([P, I32, I32, ctypes.POINTER(P)], ctypes.c_int),
         "vm_integrate": ([P, ctypes.POINTER(VmRays), I32, I32, ctypes.POINTER(VmStats)],
                          ctypes.c_int),
+        "vm_integrate_many": ([P, ctypes.POINTER(VmRays), I32, I32, I32, ctypes.POINTER(VmStats)],
+                              ctypes.c_int),
+        "vm_export_select": ([P, P, I64, I32, D, ctypes.POINTER(I64), P, P, I64], ctypes.c_int),
+        "vm_export_gather": ([P, I32, P, I64, P, P, I64, P], ctypes.c_int),
         "vm_walk_voxels": ([D] * 7 + [I64, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
         "vm_hash_mix": ([I64], ctypes.c_uint64),
         "vm_kernels_integrate_occupancy": ([P, P, P, I64, P, P, I64, P, P, P, P, P, D, I64, D, D,
@@ -202,6 +211,28 @@ class NativeMap:
               "ensure_regions")
         return slots[:len(keys)]
 
+    def export_select(self, slots, kind: int, threshold: float = 0.0):
+        """(region index into `slots`, local index) of the voxels an exporter keeps."""
+        sl = np.ascontiguousarray(slots, dtype=np.int32)
+        n = I64_t()
+        check(lib().vm_export_select(self._h, _ptr(sl), len(sl), kind, float(threshold),
+                                     ctypes.byref(n), None, None, 0), "export_select")
+        ridx = np.empty(max(n.value, 1), dtype=np.int32)
+        li = np.empty(max(n.value, 1), dtype=np.int32)
+        if n.value:
+            check(lib().vm_export_select(self._h, _ptr(sl), len(sl), kind, float(threshold),
+                                         ctypes.byref(n), _ptr(ridx), _ptr(li), len(ridx)),
+                  "export_select")
+        return ridx[:n.value], li[:n.value]
+
+    def export_gather(self, layer_id: int, slots, ridx, li, dtype, components: int):
+        sl = np.ascontiguousarray(slots, dtype=np.int32)
+        out = np.empty((max(len(li), 1), components), dtype=dtype)
+        if len(li):
+            check(lib().vm_export_gather(self._h, layer_id, _ptr(sl), len(sl), _ptr(ridx),
+                                         _ptr(li), len(li), _ptr(out)), "export_gather")
+        return out[:len(li)]
+
     def read_layer(self, slot: int, layer_id: int, out: np.ndarray):
         check(lib().vm_map_read_layer(self._h, slot, layer_id, _ptr(out), out.nbytes),
               "read_layer")
@@ -255,6 +286,16 @@ class NativeMap:
         st = VmStats()
         check(lib().vm_shard_finish(self._h, ctypes.byref(st)), "vm_shard_finish")
         return st
+
+    def integrate_many(self, rays: list, mode: str, deterministic: bool) -> list:
+        """One vm_integrate_many call over a sequence of VmRays batches."""
+        n = len(rays)
+        arr = (VmRays * max(n, 1))(*rays)
+        sts = (VmStats * max(n, 1))()
+        check(lib().vm_integrate_many(self._h, arr, n, MODES.index(mode),
+                                      EXEC_DETERMINISTIC if deterministic else EXEC_CAS, sts),
+              "vm_integrate_many")
+        return list(sts)[:n]
 
     def integrate(self, rays: VmRays, mode: str, deterministic: bool) -> VmStats:
         st = VmStats()

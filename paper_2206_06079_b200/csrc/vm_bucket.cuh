@@ -1,0 +1,288 @@
+// vm_bucket.cuh -- the in-order fold of the deterministic occupancy path
+// without a global record sort and without a host round trip.
+//
+// The walk's records are (sample-voxel index mi) << ob | (ray*maxseg + seg) << 1 | hit
+// (key_mi; k_discover numbered the batch's sample voxels).  Instead of
+// radix-sorting all of them, the records are bucketed by mi -- one counting
+// pass, a scan over the sample-voxel list, one scatter of the 32-bit
+// (order, hit) payloads -- and each bucket is put in ray order on its own:
+//
+//   <= BK_SERIAL records   one thread: insertion sort in registers/local memory
+//   <= BK_SMEM records     one block: bitonic sort in shared memory
+//   larger                 one block: presence / hit bitmaps over the batch's
+//                          order space in global scratch, scanned in order
+//
+// then folded exactly like fold_voxel_serial (reference.py:35-64 restricted
+// to the voxel: f_miss^k between hits, clamped hit, packed-mean fold).
+//
+// Every count these kernels need (records R, sample voxels M, big buckets)
+// is read on the device, so the host enqueues the whole batch and syncs once
+// at its end.  A batch whose records overflowed (R > rec_cap) or that the
+// guard refused (go == 0) is a no-op here; the host re-runs it after the sync.
+#pragma once
+
+#include "vm_kernels.cuh"
+
+namespace vm {
+
+constexpr int BK_SERIAL = 16;
+constexpr int BK_SMEM = 4096;
+
+struct BucketState {
+    unsigned *cnt;               // [M + 1] records per bucket (all zero between batches)
+    unsigned *off;               // [M + 1] exclusive scan of cnt
+    unsigned *val;               // [R] bucketed (order << 1 | hit) payloads
+    int *big;                    // buckets for the block kernels
+    unsigned long long *nbig;
+    unsigned *bits;              // huge buckets: per block 2 * bwords words
+    unsigned long long bwords;   // words of one bitmap (order space / 32)
+};
+
+__device__ __forceinline__ bool bk_live(const DevMap &m, unsigned long long &R,
+                                        unsigned long long &M) {
+    if (!read_go(m)) return false;
+    R = *((volatile unsigned long long *)(m.stats + S_RECORDS));
+    if (R > m.rec_cap) {  // overflow: the host re-emits and re-runs
+        if (m.chain) atomicCAS(m.chain, 0, m.batch_idx + 1);
+        return false;
+    }
+    M = min(*((volatile unsigned long long *)m.nmarked), m.marked_cap);
+    return true;
+}
+
+__global__ void __launch_bounds__(BLOCK) k_bk_count(const __grid_constant__ DevMap m,
+                                                    BucketState b) {
+    unsigned long long R, M;
+    if (!bk_live(m, R, M)) return;
+    const int ob = m.order_bits;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long mi = m.rec[i] >> ob;
+        if (mi < M) atomicAdd(b.cnt + mi, 1u);
+    }
+}
+
+// cnt is counted back down to zero while scattering (ready for the next batch)
+__global__ void __launch_bounds__(BLOCK) k_bk_scatter(const __grid_constant__ DevMap m,
+                                                      BucketState b) {
+    unsigned long long R, M;
+    if (!bk_live(m, R, M)) return;
+    const int ob = m.order_bits;
+    const unsigned long long omask = (1ULL << ob) - 1;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = m.rec[i];
+        const unsigned long long mi = k >> ob;
+        if (mi >= M) continue;
+        const unsigned pos = b.off[mi] + atomicSub(b.cnt + mi, 1u) - 1u;
+        b.val[pos] = (unsigned)(k & omask);
+    }
+}
+
+// Per-voxel fold state: log-odds, packed mean, count, pending misses.
+struct VoxFold {
+    float l;
+    unsigned packed, count, misses;
+    int g[3];
+    unsigned vid;
+};
+
+__device__ __forceinline__ void vf_begin(const DevMap &m, VoxFold &f, unsigned vid) {
+    f.vid = vid;
+    f.l = reinterpret_cast<const float *>(m.slab[L_OCC])[vid];
+    f.packed = m.slab[L_MEAN] ? reinterpret_cast<const unsigned *>(m.slab[L_MEAN])[vid] : 0u;
+    f.count = m.slab[L_COUNT] ? reinterpret_cast<const unsigned *>(m.slab[L_COUNT])[vid] : 0u;
+    f.misses = 0;
+    slot_li_to_g(m, (int)(vid / (unsigned)m.vpr), (int)(vid % (unsigned)m.vpr), f.g);
+}
+
+// one hit of segment order index `oi` (= ray * maxseg + seg), after the
+// misses counted so far (reference.py:43-57)
+template <class Src>
+__device__ __forceinline__ void vf_hit(const DevMap &m, const Src &src, VoxFold &f, unsigned oi) {
+    f.l = miss_k(f.l, f.misses, m.miss32, m.cmin, m.cmax);
+    f.misses = 0;
+    f.l = clamp_add(f.l, m.hit32, m.cmin, m.cmax);
+    if (m.slab[L_MEAN]) {
+        const long long ray = (long long)(oi / (unsigned)m.maxseg);
+        double ep[3];
+        float it;
+        src.load_end(ray, ep, it);
+        const double off[3] = {ep[0] / m.vox - (double)f.g[0], ep[1] / m.vox - (double)f.g[1],
+                               ep[2] / m.vox - (double)f.g[2]};
+        fold_mean(f.packed, f.count, off);
+    }
+}
+
+__device__ __forceinline__ void vf_end(const DevMap &m, VoxFold &f) {
+    f.l = miss_k(f.l, f.misses, m.miss32, m.cmin, m.cmax);
+    reinterpret_cast<float *>(m.slab[L_OCC])[f.vid] = f.l;
+    if (m.slab[L_MEAN]) {
+        reinterpret_cast<unsigned *>(m.slab[L_MEAN])[f.vid] = f.packed;
+        reinterpret_cast<unsigned *>(m.slab[L_COUNT])[f.vid] = f.count;
+    }
+    reinterpret_cast<unsigned *>(m.slab[L_SCRATCH])[f.vid] = 0u;  // the MARK stamp
+    m.bmask[f.vid / (unsigned)m.vpr] = 0u;
+}
+
+__device__ __forceinline__ unsigned marked_vid(const DevMap &m, unsigned long long mi) {
+    const int2 sl = m.marked[mi];
+    return (unsigned)sl.x * (unsigned)m.vpr + (unsigned)sl.y;
+}
+
+// One thread per sample voxel: small buckets sorted and folded in place.
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_bk_fold(const __grid_constant__ DevMap m, Src src,
+                                                   BucketState b) {
+    unsigned long long R, M;
+    if (!bk_live(m, R, M)) return;
+    for (unsigned long long mi = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; mi < M;
+         mi += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned s = b.off[mi];
+        const unsigned e = mi + 1 < M ? b.off[mi + 1] : (unsigned)R;
+        const unsigned c = e - s;
+        if (c > (unsigned)BK_SERIAL) {
+            b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
+            continue;
+        }
+        unsigned v[BK_SERIAL];
+        for (unsigned i = 0; i < c; ++i) {
+            const unsigned x = b.val[s + i];
+            int j = (int)i - 1;
+            while (j >= 0 && v[j] > x) {
+                v[j + 1] = v[j];
+                --j;
+            }
+            v[j + 1] = x;
+        }
+        VoxFold f;
+        vf_begin(m, f, marked_vid(m, mi));
+        for (unsigned i = 0; i < c; ++i) {
+            if (v[i] & 1u) vf_hit(m, src, f, v[i] >> 1);
+            else ++f.misses;
+        }
+        vf_end(m, f);
+    }
+}
+
+// Fold a sorted run held by one warp, 32 payloads at a time (lane i holds
+// element base + i; `n` valid).  Misses between hits collapse to f_miss^k.
+template <class Src>
+__device__ __forceinline__ void vf_warp_chunk(const DevMap &m, const Src &src, VoxFold &f,
+                                              unsigned x, int n) {
+    const int lane = threadIdx.x & 31;
+    const unsigned hmask = __ballot_sync(0xffffffffu, lane < n && (x & 1u));
+    int cur = 0;
+    unsigned hm = hmask;
+    while (hm) {
+        const int h = __ffs(hm) - 1;
+        hm &= hm - 1;
+        f.misses += (unsigned)(h - cur);
+        const unsigned hx = __shfl_sync(0xffffffffu, x, h);
+        vf_hit(m, src, f, hx >> 1);
+        cur = h + 1;
+    }
+    f.misses += (unsigned)(n - cur);
+}
+
+// One block per large bucket.
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_bk_fold_big(const __grid_constant__ DevMap m, Src src,
+                                                       BucketState b) {
+    __shared__ unsigned sv[BK_SMEM];
+    unsigned long long R, M;
+    if (!bk_live(m, R, M)) return;
+    const unsigned long long nb = *((volatile unsigned long long *)b.nbig);
+    const int lane = threadIdx.x & 31;
+    unsigned *pres = b.bits + (size_t)blockIdx.x * 2 * b.bwords;
+    unsigned *hitb = pres + b.bwords;
+    for (unsigned long long w = blockIdx.x; w < nb; w += gridDim.x) {
+        const unsigned long long mi = (unsigned long long)b.big[w];
+        const unsigned s = b.off[mi];
+        const unsigned e = mi + 1 < M ? b.off[mi + 1] : (unsigned)R;
+        const unsigned c = e - s;
+        VoxFold f;
+        if (c <= (unsigned)BK_SMEM) {
+            unsigned P = 32;
+            while (P < c) P <<= 1;
+            for (unsigned i = threadIdx.x; i < P; i += blockDim.x)
+                sv[i] = i < c ? b.val[s + i] : 0xFFFFFFFFu;
+            __syncthreads();
+            for (unsigned k = 2; k <= P; k <<= 1) {
+                for (unsigned j = k >> 1; j > 0; j >>= 1) {
+                    for (unsigned i = threadIdx.x; i < P; i += blockDim.x) {
+                        const unsigned p = i ^ j;
+                        if (p > i) {
+                            const unsigned a = sv[i], bb = sv[p];
+                            const bool up = (i & k) == 0;
+                            if ((a > bb) == up) {
+                                sv[i] = bb;
+                                sv[p] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            if (threadIdx.x < 32) {
+                vf_begin(m, f, marked_vid(m, mi));
+                for (unsigned base = 0; base < c; base += 32) {
+                    const int n = (int)min(32u, c - base);
+                    const unsigned x = lane < n ? sv[base + lane] : 0u;
+                    vf_warp_chunk(m, src, f, x, n);
+                }
+                if (lane == 0) vf_end(m, f);
+            }
+            __syncthreads();
+        } else {
+            // presence / hit bitmaps over the order space, scanned in order
+            for (unsigned long long i = threadIdx.x; i < 2 * b.bwords; i += blockDim.x) pres[i] = 0u;
+            __syncthreads();
+            for (unsigned i = threadIdx.x; i < c; i += blockDim.x) {
+                const unsigned x = b.val[s + i];
+                const unsigned oi = x >> 1;
+                atomicOr(pres + (oi >> 5), 1u << (oi & 31));
+                if (x & 1u) atomicOr(hitb + (oi >> 5), 1u << (oi & 31));
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                vf_begin(m, f, marked_vid(m, mi));
+                for (unsigned long long w0 = 0; w0 < b.bwords; w0 += 32) {
+                    const unsigned long long wi = w0 + lane;
+                    const unsigned p = wi < b.bwords ? __ldcg(pres + wi) : 0u;
+                    const unsigned h = wi < b.bwords ? __ldcg(hitb + wi) : 0u;
+                    const unsigned withhits = __ballot_sync(0xffffffffu, h != 0u);
+                    // lanes without hits contribute whole-word miss counts
+                    unsigned before = 0;  // misses in hit-free words of lower lanes, per segment
+                    int prev = 0;
+                    unsigned wh = withhits;
+                    while (wh) {
+                        const int L = __ffs(wh) - 1;
+                        wh &= wh - 1;
+                        // misses of the hit-free words in lanes [prev, L)
+                        const bool inr = lane >= prev && lane < L;
+                        before = __reduce_add_sync(0xffffffffu, inr ? __popc(p) : 0u);
+                        f.misses += before;
+                        const unsigned pL = __shfl_sync(0xffffffffu, p, L);
+                        const unsigned hL = __shfl_sync(0xffffffffu, h, L);
+                        unsigned bits = pL;
+                        while (bits) {
+                            const int bi = __ffs(bits) - 1;
+                            bits &= bits - 1;
+                            if ((hL >> bi) & 1u)
+                                vf_hit(m, src, f, (unsigned)((w0 + L) * 32 + bi));
+                            else
+                                ++f.misses;
+                        }
+                        prev = L + 1;
+                    }
+                    f.misses += __reduce_add_sync(0xffffffffu, lane >= prev ? __popc(p) : 0u);
+                }
+                if (lane == 0) vf_end(m, f);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace vm

@@ -107,6 +107,11 @@ struct DevMap {
     int walk_slot0;                      // regions with slot >= this were created by the walk
     int key_mi;                          // occupancy records key on the sample-voxel index
                                          // (marked list) instead of the voxel id
+    // pipelined batch sequences (vm_integrate_many): the first batch that is
+    // refused or overflows its records sets *chain (batch + 1) and every later
+    // batch of the sequence becomes a no-op; nullptr for single batches
+    int *chain;
+    int batch_idx;
     // batch outputs
     unsigned long long *rec;
     unsigned *recval;                    // per-record value (NDT deterministic phase 1)

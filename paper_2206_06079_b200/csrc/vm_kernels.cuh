@@ -224,6 +224,7 @@ template <class Src>
 __global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevMap m, Src src,
                                                     long long n, int mode, int det, int emit,
                                                     int count_stats = 1) {
+    if (m.chain && *((volatile int *)m.chain)) return;  // an earlier batch of the sequence failed
     __shared__ unsigned long long kcache[KCACHE];
     __shared__ int sset[SLOTSET];
     __shared__ unsigned long long srec[BLOCK];
@@ -441,11 +442,38 @@ __global__ void k_rgrid(const __grid_constant__ DevMap m) {
 
 // Refuse the batch if the pool could overflow or inputs were invalid.
 __global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
+    if (m.chain && *((volatile int *)m.chain)) {
+        *m.go = 0;
+        return;
+    }
     int used = *((volatile int *)m.cursor);
     unsigned long long rerr = ((volatile unsigned long long *)m.stats)[S_RANGE_ERR];
     unsigned long long nseg = ((volatile unsigned long long *)m.stats)[S_SEGDESC];
     bool ok = used + margin <= m.cap && rerr == 0 && nseg <= m.seg_cap;
     *m.go = ok ? 1 : 0;
+    if (!ok && m.chain) atomicCAS(m.chain, 0, m.batch_idx + 1);
+}
+
+// Pipelined sequences: per-batch state reset (stats slot, region box, the
+// sample-voxel list unless the batch is a replay that keeps its stamps).
+__global__ void k_batch_init(const __grid_constant__ DevMap m, int reset_marked) {
+    if (*((volatile int *)m.chain)) return;
+    const int t = threadIdx.x;
+    if (t < NUM_STATS) m.stats[t] = 0ULL;
+    if (t < 3) m.rbox[t] = INT_MAX;
+    else if (t < 6) m.rbox[t] = INT_MIN;
+    if (t == 0 && reset_marked && m.nmarked) *m.nmarked = 0ULL;
+}
+
+// ... and its outcome: regions after the batch and whether it ran.
+__global__ void k_batch_fin(const __grid_constant__ DevMap m) {
+    // sample voxels of the batch: the list length (also counts stamps a
+    // refused first attempt left for the replay)
+    if (m.key_mi && m.nmarked) m.stats[S_MARKED] = *((volatile unsigned long long *)m.nmarked);
+    m.stats[NUM_STATS] = (unsigned long long)*((volatile int *)m.cursor);
+    // bit 0: the guard let the batch run; bit 1: nothing stopped the chain
+    m.stats[NUM_STATS + 1] = (unsigned long long)(*((volatile int *)m.go) != 0) |
+                             ((unsigned long long)(*((volatile int *)m.chain) == 0) << 1);
 }
 
 // Counting sort of the batch's segments by step count, longest first: the

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -20,6 +21,8 @@
 #include "vm_compat.cuh"
 #include "vm_walk_det.cuh"
 #include "vm_shard.cuh"
+#include "vm_bucket.cuh"
+#include "vm_export.cuh"
 
 using namespace vm;
 
@@ -94,6 +97,24 @@ struct vm_map {
     long long *d_big = nullptr;
     size_t big_cap = 0;
     unsigned long long *d_nbig = nullptr;
+    // bucketed fold of the deterministic occupancy records (vm_bucket.cuh)
+    unsigned *d_bk_cnt = nullptr, *d_bk_off = nullptr;
+    size_t bk_cap = 0;
+    int *d_bk_big = nullptr;
+    unsigned *d_bk_bits = nullptr;
+    size_t bk_bits_cap = 0;
+    void *d_scan_tmp = nullptr;
+    size_t scan_tmp_bytes = 0;
+    // pipelined sequences (vm_integrate_many)
+    int *d_chain = nullptr;
+    unsigned long long *d_mstats = nullptr, *h_mstats = nullptr;
+    size_t mstats_cap = 0;  // batches
+    std::vector<cudaEvent_t> mev;  // 6 per batch
+    static constexpr int RING = 3;
+    unsigned char *d_ring[RING] = {};
+    size_t ring_bytes = 0;
+    cudaEvent_t ev_ring[RING] = {}, ev_ring_up[RING] = {};
+    long long rec_floor_override = 0;
     int num_sms = 148;
     unsigned long long *d_stats = nullptr;
     int *d_go = nullptr;
@@ -103,6 +124,7 @@ struct vm_map {
     int *d_touched = nullptr;
     void *d_sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
+    int sort_sized = 0;
     unsigned char *d_rays = nullptr;
     size_t rays_bytes = 0;
     // host rays of the batch: uploaded in chunks on copy_stream, each chunk's
@@ -278,18 +300,36 @@ int ensure_records(vm_map *m, size_t need) {
     CK(cudaMalloc((void **)&m->d_val, nc * sizeof(unsigned)));
     CK(cudaMalloc((void **)&m->d_val2, nc * sizeof(unsigned)));
     m->rec_cap = nc;
+    m->sort_sized = 0;  // CUB temp storage is sized lazily (ensure_sort_tmp)
+    return VM_OK;
+}
+
+// CUB radix-sort temp storage for rec_cap records (the sorted NDT / TSDF /
+// sharded paths; the bucketed occupancy fold never sorts).
+int ensure_sort_tmp(vm_map *m) {
+    if (m->sort_sized) return VM_OK;
     size_t bytes = 0, bytes2 = 0;
     cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
     cub::DoubleBuffer<unsigned> dv(m->d_val, m->d_val2);
-    CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, (int)std::min<size_t>(nc, INT32_MAX)));
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes2, db, dv, (int)std::min<size_t>(nc, INT32_MAX)));
+    const int nc = (int)std::min<size_t>(m->rec_cap, INT32_MAX);
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, nc));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes2, db, dv, nc));
     bytes = std::max(bytes, bytes2);
     if (bytes > m->sort_tmp_bytes) {
         if (m->d_sort_tmp) CK(cudaFree(m->d_sort_tmp));
         CK(cudaMalloc(&m->d_sort_tmp, bytes));
         m->sort_tmp_bytes = bytes;
     }
+    m->sort_sized = 1;
     return VM_OK;
+}
+
+// Initial record capacity of a deterministic occupancy batch.  The records
+// overflow path is exercised by tests through VOXMAP_B200_TEST_REC_CAP
+// (read when the map is created).
+size_t rec_floor(const vm_map *m, long long n) {
+    if (m->rec_floor_override > 0) return (size_t)m->rec_floor_override;
+    return std::max<size_t>(1 << 20, (size_t)n * 4);
 }
 
 int check_launch(const char *what) {
@@ -298,16 +338,35 @@ int check_launch(const char *what) {
     return VM_OK;
 }
 
-template <bool REC_ONLY, class Src>
-void launch_wd(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
+// One thread per (ray, segment): blockIdx.y is the segment index.  (A
+// persistent variant with warp-claimed work items measured slower on C2:
+// 28.9 vs 19.6 ms per step -- a block's region key cache then sees the whole
+// batch instead of 256 neighbouring rays.)
+template <class Src>
+int launch_discover(vm_map *m, const DevMap &dm, const Src &src, long long n, int mode, int det,
+                    int emit, int count_stats, cudaStream_t s) {
+    const dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK), mode == M_TSDF ? 1u : (unsigned)dm.maxseg);
+    k_discover<<<grid, BLOCK, 0, s>>>(dm, src, n, mode, det, emit, count_stats);
+    m->launches += 1;
+    return check_launch("discover");
+}
+
+template <bool REC_ONLY, class Src, int DIM>
+void launch_wd_dim(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
     static bool configured = false;
     const size_t smem = sizeof(WalkDetSmem);
     if (!configured) {
-        cudaFuncSetAttribute(k_walk_det<REC_ONLY, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(k_walk_det<REC_ONLY, Src, DIM>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    k_walk_det<REC_ONLY, Src><<<grid, BLOCK, smem, s>>>(dm, src);
+    k_walk_det<REC_ONLY, Src, DIM><<<grid, BLOCK, smem, s>>>(dm, src);
+}
+
+template <bool REC_ONLY, class Src>
+void launch_wd(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
+    if (dm.dim == 32 && dm.brick_shift == 3) launch_wd_dim<REC_ONLY, Src, 32>(grid, s, dm, src);
+    else launch_wd_dim<REC_ONLY, Src, 0>(grid, s, dm, src);
 }
 
 template <int MODE, bool DET, bool REC_ONLY, class Src>
@@ -405,6 +464,65 @@ int launch_fold(vm_map *m, const DevMap &dm, const Src &src, const unsigned long
     return check_launch("fold");
 }
 
+// Bucketed in-order fold (vm_bucket.cuh): no host sync, no global sort.
+int ensure_buckets(vm_map *m, size_t nmarked_cap, size_t bwords) {
+    if (nmarked_cap + 1 > m->bk_cap || !m->d_bk_cnt) {
+        size_t nc = std::max(nmarked_cap + 1, m->bk_cap * 2);
+        cudaFree(m->d_bk_cnt);
+        cudaFree(m->d_bk_off);
+        cudaFree(m->d_bk_big);
+        m->d_bk_cnt = nullptr;
+        m->d_bk_off = nullptr;
+        m->d_bk_big = nullptr;
+        CK(cudaMalloc((void **)&m->d_bk_cnt, nc * sizeof(unsigned)));
+        CK(cudaMemset(m->d_bk_cnt, 0, nc * sizeof(unsigned)));  // kept zero by k_bk_scatter
+        CK(cudaMalloc((void **)&m->d_bk_off, nc * sizeof(unsigned)));
+        CK(cudaMalloc((void **)&m->d_bk_big, nc * sizeof(int)));
+        m->bk_cap = nc;
+        size_t bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, m->d_bk_cnt, m->d_bk_off, (int)nc));
+        if (bytes > m->scan_tmp_bytes) {
+            cudaFree(m->d_scan_tmp);
+            m->d_scan_tmp = nullptr;
+            CK(cudaMalloc(&m->d_scan_tmp, bytes));
+            m->scan_tmp_bytes = bytes;
+        }
+    }
+    const size_t need = (size_t)m->num_sms * 2 * bwords;
+    if (need > m->bk_bits_cap || !m->d_bk_bits) {
+        cudaFree(m->d_bk_bits);
+        m->d_bk_bits = nullptr;
+        CK(cudaMalloc((void **)&m->d_bk_bits, need * sizeof(unsigned)));
+        m->bk_bits_cap = need;
+    }
+    return VM_OK;
+}
+
+template <class Src>
+int launch_bucket_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, int maxseg,
+                       cudaEvent_t ev_mid) {
+    cudaStream_t s = m->stream;
+    const unsigned long long bwords = ((unsigned long long)n * maxseg + 31) / 32 + 1;
+    int rc;
+    if ((rc = ensure_buckets(m, m->smarked_cap, bwords))) return rc;
+    BucketState b{m->d_bk_cnt, m->d_bk_off, reinterpret_cast<unsigned *>(m->d_rec2), m->d_bk_big,
+                  m->d_nbig, m->d_bk_bits, bwords};
+    CK(cudaMemsetAsync(m->d_nbig, 0, sizeof(unsigned long long), s));
+    const unsigned g = (unsigned)m->num_sms * 8;
+    k_bk_count<<<g, BLOCK, 0, s>>>(dm, b);
+    size_t bytes = m->scan_tmp_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(m->d_scan_tmp, bytes, m->d_bk_cnt, m->d_bk_off,
+                                     (int)m->smarked_cap, s));
+    k_bk_scatter<<<g, BLOCK, 0, s>>>(dm, b);
+    CK(cudaEventRecord(ev_mid, s));
+    const unsigned gf = (unsigned)std::max<long long>(
+        1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
+    k_bk_fold<<<gf, BLOCK, 0, s>>>(dm, src, b);
+    k_bk_fold_big<<<m->num_sms, BLOCK, 0, s>>>(dm, src, b);
+    m->launches += 6;
+    return check_launch("bucket fold");
+}
+
 const uint32_t MODE_MASK[5] = {
     (1u << 1) | (1u << 2) | (1u << 3),
     (1u << 1) | (1u << 2) | (1u << 3) | (1u << 8) | (1u << 9),
@@ -446,7 +564,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     else if (tsdf && det) {
         double band = 2.0 * m->cfg.tsdf_truncation / m->cfg.voxel_size;
         rec_need = (size_t)n * (size_t)(3.0 * (std::ceil(band) + 2.0) + 4.0);
-    } else if (occ_det) rec_need = std::max<size_t>(m->rec_cap, std::max<size_t>(1 << 20, (size_t)n * 4));
+    } else if (occ_det) rec_need = std::max<size_t>(m->rec_cap, rec_floor(m, n));
     if (sorted && (rc = ensure_records(m, rec_need))) return rc;
 
     float ms_total = 0.f, ms_walk = 0.f, ms_disc = 0.f, ms_res = 0.f, ms_sort = 0.f, ms_fold = 0.f;
@@ -502,16 +620,16 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 CK(cudaStreamWaitEvent(m->stream, m->ev_up[c], 0));
                 DevMap dc = dm;
                 dc.ray_lo = lo;
-                const dim3 cg((unsigned)((hi - lo + BLOCK - 1) / BLOCK), tsdf ? 1 : (unsigned)maxseg);
-                k_discover<<<cg, BLOCK, 0, m->stream>>>(dc, src, hi - lo, mode, det ? 1 : 0, emit ? 1 : 0);
-                m->launches += 1;
+                if ((rc = launch_discover(m, dc, src, hi - lo, mode, det ? 1 : 0, emit ? 1 : 0, 1,
+                                          m->stream)))
+                    return rc;
             }
             m->up.pending = 0;
             m->launches += 1;  // guard
         } else {
-            const dim3 dgrid((unsigned)((n + BLOCK - 1) / BLOCK), tsdf ? 1 : (unsigned)maxseg);
-            k_discover<<<dgrid, BLOCK, 0, m->stream>>>(dm, src, n, mode, det ? 1 : 0, emit ? 1 : 0);
-            m->launches += 2;  // discover + guard
+            if ((rc = launch_discover(m, dm, src, n, mode, det ? 1 : 0, emit ? 1 : 0, 1, m->stream)))
+                return rc;
+            m->launches += 1;  // guard
         }
         if ((rc = check_launch("discover"))) return rc;
         int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
@@ -545,7 +663,23 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             if ((rc = check_launch("resolve"))) return rc;
         }
         CK(cudaEventRecord(m->ev_res, m->stream));
-        CK(cudaEventSynchronize(m->ev_k1));
+        if (key_mi) {
+            // the whole batch is enqueued; one sync at its end
+            if ((rc = launch_bucket_fold(m, dm, src, n, maxseg, m->ev_sort))) return rc;
+            CK(cudaEventRecord(m->ev_end, m->stream));
+            CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, m->stream));
+            CK(cudaMemcpyAsync(m->h_stats + NUM_STATS, m->d_cursor, sizeof(int),
+                               cudaMemcpyDeviceToHost, m->stream));
+            CK(cudaMemcpyAsync((int *)(m->h_stats + NUM_STATS) + 1, m->d_go, sizeof(int),
+                               cudaMemcpyDeviceToHost, m->stream));
+            CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_shard_cnt,
+                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+            CK(cudaStreamSynchronize(m->stream));
+            if ((rc = check_launch("batch"))) return rc;
+        } else {
+            CK(cudaEventSynchronize(m->ev_k1));
+        }
         const unsigned long long *hs = m->h_stats;
         int cursor = *(const int *)(hs + NUM_STATS);
         int go = *((const int *)(hs + NUM_STATS) + 1);
@@ -574,6 +708,34 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             ++replays;
             continue;
         }
+        if (key_mi) {
+            unsigned long long R = m->h_stats[S_RECORDS];
+            if (R > m->rec_cap) {
+                // records overflowed: every fold kernel was a no-op; re-emit
+                // the records (nothing re-applied) and fold them
+                if ((rc = ensure_records(m, (size_t)R + (R >> 2)))) return rc;
+                dm.rec = m->d_rec;
+                dm.recval = m->d_val;
+                dm.rec_cap = m->rec_cap;
+                CK(cudaMemsetAsync(m->d_stats + S_RECORDS, 0, sizeof(unsigned long long),
+                                   m->stream));
+                if ((rc = launch_walk(m, dm, src, n, mode, det, true))) return rc;
+                CK(cudaEventRecord(m->ev_res, m->stream));
+                if ((rc = launch_bucket_fold(m, dm, src, n, maxseg, m->ev_sort))) return rc;
+                CK(cudaEventRecord(m->ev_end, m->stream));
+                CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, m->stream));
+                CK(cudaStreamSynchronize(m->stream));
+                if ((rc = check_launch("batch"))) return rc;
+            }
+            CK(cudaEventElapsedTime(&ms_total, m->ev_start, m->ev_end));
+            CK(cudaEventElapsedTime(&ms_walk, m->ev_w0, m->ev_w1));
+            CK(cudaEventElapsedTime(&ms_disc, m->ev_start, m->ev_w0));
+            CK(cudaEventElapsedTime(&ms_res, m->ev_w1, m->ev_res));
+            CK(cudaEventElapsedTime(&ms_sort, m->ev_res, m->ev_sort));
+            CK(cudaEventElapsedTime(&ms_fold, m->ev_sort, m->ev_end));
+            break;
+        }
         if (sorted) {
             CK(cudaEventSynchronize(m->ev_k2));
             unsigned long long R = m->h_stats[NUM_STATS + 1];
@@ -590,9 +752,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 if (ndt) {
                     // the phase-2 hit records come from k_discover: re-emit them
                     // with a records-only discover pass (no descriptors, no marks)
-                    const dim3 g2((unsigned)((n + BLOCK - 1) / BLOCK), (unsigned)maxseg);
-                    k_discover<<<g2, BLOCK, 0, m->stream>>>(dm, src, n, mode, 1, 0, 0);
-                    m->launches += 1;
+                    if ((rc = launch_discover(m, dm, src, n, mode, 1, 0, 0, m->stream))) return rc;
                 }
                 if ((rc = launch_walk(m, dm, src, n, mode, det, true))) return rc;
                 CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_stats + S_RECORDS,
@@ -612,6 +772,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
             cub::DoubleBuffer<unsigned> dv(m->d_val, m->d_val2);
             if (R > 1) {
+                if ((rc = ensure_sort_tmp(m))) return rc;
                 size_t bytes = m->sort_tmp_bytes;
                 if (ndt)
                     CK(cub::DeviceRadixSort::SortPairs(m->d_sort_tmp, bytes, db, dv, (int)R, 0,
@@ -653,7 +814,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     out->region_misses = (int64_t)hs[S_RMISS];
     out->regions_touched = (int64_t)hs[S_PREF_TOUCHED];
     out->records = (int64_t)hs[S_RECORDS];
-    out->marked_voxels = (int64_t)hs[S_MARKED];
+    out->marked_voxels = key_mi ? (int64_t)hs[NUM_STATS + 1] : (int64_t)hs[S_MARKED];
     out->regions_total = cursor;
     out->new_regions = cursor - nreg0;
     out->replays = replays;
@@ -667,6 +828,259 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     out->fold_ms = ms_fold;
     m->max_growth = std::max<long long>(m->max_growth, cursor - m->nreg);
     m->nreg = cursor;
+    return VM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined sequences of deterministic occupancy batches (vm_integrate_many).
+//
+// Every batch is enqueued behind the previous one with no host round trip
+// (the bucketed fold reads all its counts on the device); host records are
+// uploaded on copy_stream into a ring of device buffers while earlier batches
+// compute.  One sync at the end of the sequence.  The first batch the guard
+// refuses (region pool growth, invalid coordinates) or whose records
+// overflow sets the chain flag: every later batch is a no-op, the host
+// recovers that batch exactly as integrate_impl would and re-enqueues the rest.
+constexpr int MSTRIDE = NUM_STATS + 2;  // per-batch slot: stats, cursor after, fin flags
+
+void fill_stats(const unsigned long long *slot, long long n, long long regions_before,
+                vm_stats *o) {
+    std::memset(o, 0, sizeof(*o));
+    o->rays_in = n;
+    o->rays_processed = (int64_t)slot[S_PROCESSED];
+    o->segments = (int64_t)slot[S_SEGMENTS];
+    o->voxel_visits = (int64_t)slot[S_VISITS];
+    o->cas_retries = (int64_t)slot[S_RETRIES];
+    o->region_misses = (int64_t)slot[S_RMISS];
+    o->regions_touched = (int64_t)slot[S_PREF_TOUCHED];
+    o->records = (int64_t)slot[S_RECORDS];
+    o->marked_voxels = (int64_t)slot[S_MARKED];
+    o->regions_total = (int64_t)slot[NUM_STATS];
+    o->new_regions = o->regions_total - regions_before;
+    o->touched_regions_walk = (int64_t)slot[S_WALK_TOUCHED];
+}
+
+int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_stats *out) {
+    cudaStream_t s = m->stream;
+    const int maxseg = (int)std::ceil(m->cfg.max_ray_range / m->cfg.segment_length) + 1;
+    long long nmax = 0;
+    bool any_host = false;
+    for (int b = 0; b < nb; ++b) {
+        nmax = std::max<long long>(nmax, rays[b].count);
+        if (rays[b].count > 0 && !rays[b].on_device) any_host = true;
+    }
+    for (int b = 0; b < nb; ++b) std::memset(out + b, 0, sizeof(vm_stats));
+    if (nmax <= 0) {
+        for (int b = 0; b < nb; ++b) out[b].regions_total = m->nreg;
+        return VM_OK;
+    }
+    const unsigned long long span_max = ((unsigned long long)nmax * maxseg) << 1;
+    if (span_max >= (1ULL << 32))
+        return fail(VM_ERR_ARG, "batch too large for 32-bit ray order keys; split it");
+    int rc;
+    if ((rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)nmax * maxseg + 1))) return rc;
+    if ((rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)nmax + 1))) return rc;
+    if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, rec_floor(m, nmax)))))
+        return rc;
+    if ((rc = ensure_buckets(m, m->smarked_cap, ((unsigned long long)nmax * maxseg + 31) / 32 + 1)))
+        return rc;
+    if (!m->d_chain && (rc = dev_alloc(&m->d_chain, 1))) return rc;
+    if ((size_t)nb > m->mstats_cap) {
+        cudaFree(m->d_mstats);
+        if (m->h_mstats) cudaFreeHost(m->h_mstats);
+        m->d_mstats = nullptr;
+        m->h_mstats = nullptr;
+        CK(cudaMalloc((void **)&m->d_mstats, (size_t)nb * MSTRIDE * sizeof(unsigned long long)));
+        CK(cudaMallocHost((void **)&m->h_mstats, (size_t)nb * MSTRIDE * sizeof(unsigned long long)));
+        m->mstats_cap = nb;
+    }
+    while (m->mev.size() < (size_t)nb * 6) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        m->mev.push_back(e);
+    }
+    if (any_host && (size_t)nmax * 40 > m->ring_bytes) {
+        for (int r = 0; r < vm_map::RING; ++r) {
+            cudaFree(m->d_ring[r]);
+            m->d_ring[r] = nullptr;
+            CK(cudaMalloc((void **)&m->d_ring[r], (size_t)nmax * 40));
+            if (!m->ev_ring[r]) CK(cudaEventCreateWithFlags(&m->ev_ring[r], cudaEventDisableTiming));
+            if (!m->ev_ring_up[r])
+                CK(cudaEventCreateWithFlags(&m->ev_ring_up[r], cudaEventDisableTiming));
+        }
+        m->ring_bytes = (size_t)nmax * 40;
+    }
+    std::vector<DevMap> dms(nb);
+    std::vector<const unsigned char *> srcp(nb, nullptr);
+    std::vector<long long> reps(nb, 0), launches(nb, 0), before(nb, 0), first_before(nb, -1);
+    bool keep_marks = false;  // a replayed batch keeps its sample-voxel stamps
+    int b0 = 0;
+    auto upload = [&](int b, cudaStream_t st) -> int {
+        const int r = b % vm_map::RING;
+        CK(cudaStreamWaitEvent(st, m->ev_ring[r], 0));  // the slot's previous batch is done
+        CK(cudaMemcpyAsync(m->d_ring[r], rays[b].records, (size_t)rays[b].count * 40,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(m->ev_ring_up[r], st));
+        CK(cudaStreamWaitEvent(s, m->ev_ring_up[r], 0));
+        srcp[b] = m->d_ring[r];
+        return VM_OK;
+    };
+    while (b0 < nb) {
+        const long long headroom = std::max<long long>(512, 2 * m->max_growth);
+        if (m->nreg + headroom > m->cap &&
+            (rc = grow_pool(m, std::max(2 * m->cap, m->nreg + headroom))))
+            return rc;
+        const int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
+        CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
+        for (int b = b0; b < nb; ++b) {
+            const long long n = rays[b].count;
+            cudaEvent_t *ev = &m->mev[(size_t)6 * b];
+            if (n <= 0) continue;
+            m->epoch += 1;
+            DevMap dm = make_dm(m);
+            dm.order_bits = std::max(1, bitlen(((unsigned long long)n * maxseg) << 1));
+            dm.key_mi = 1;
+            dm.marked = m->d_smarked;
+            dm.nmarked = m->d_shard_cnt;
+            dm.marked_cap = m->smarked_cap;
+            dm.stats = m->d_mstats + (size_t)b * MSTRIDE;
+            dm.chain = m->d_chain;
+            dm.batch_idx = b;
+            if (rays[b].on_device) srcp[b] = (const unsigned char *)rays[b].records;
+            else if ((rc = upload(b, m->copy_stream))) return rc;
+            const SrcOHMB1 src{srcp[b]};
+            const long long l0 = m->launches;
+            k_batch_init<<<1, 32, 0, s>>>(dm, (b == b0 && keep_marks) ? 0 : 1);
+            CK(cudaEventRecord(ev[0], s));
+            if ((rc = launch_discover(m, dm, src, n, mode, 1, 1, 1, s))) return rc;
+            k_guard<<<1, 1, 0, s>>>(dm, margin);
+            k_rgrid<<<16, BLOCK, 0, s>>>(dm);
+            k_seg_scan<<<1, SEG_BUCKETS, 0, s>>>(dm);
+            k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, s>>>(dm);
+            m->launches += 5;
+            if ((rc = check_launch("discover"))) return rc;
+            CK(cudaEventRecord(ev[1], s));
+            if ((rc = launch_walk(m, dm, src, n, mode, true, false))) return rc;
+            CK(cudaEventRecord(ev[2], s));
+            k_resolve<false, false><<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
+            m->launches += 1;
+            CK(cudaEventRecord(ev[3], s));
+            if ((rc = launch_bucket_fold(m, dm, src, n, maxseg, ev[4]))) return rc;
+            k_batch_fin<<<1, 1, 0, s>>>(dm);
+            m->launches += 1;
+            CK(cudaEventRecord(ev[5], s));
+            if (!rays[b].on_device) CK(cudaEventRecord(m->ev_ring[b % vm_map::RING], s));
+            if ((rc = check_launch("batch"))) return rc;
+            dms[b] = dm;
+            launches[b] = m->launches - l0;
+        }
+        CK(cudaMemcpyAsync(m->h_mstats + (size_t)b0 * MSTRIDE, m->d_mstats + (size_t)b0 * MSTRIDE,
+                           (size_t)(nb - b0) * MSTRIDE * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if ((rc = check_launch("sequence"))) return rc;
+        keep_marks = false;
+        int f = nb;
+        long long regions = m->nreg;
+        for (int b = b0; b < nb; ++b) {
+            if (rays[b].count <= 0) {
+                out[b].regions_total = regions;
+                continue;
+            }
+            const unsigned long long *slot = m->h_mstats + (size_t)b * MSTRIDE;
+            if (slot[NUM_STATS + 1] != 3ULL) {
+                f = b;
+                break;
+            }
+            before[b] = first_before[b] >= 0 ? first_before[b] : regions;
+            regions = (long long)slot[NUM_STATS];
+        }
+        for (int b = b0; b < f; ++b) {
+            if (rays[b].count <= 0) continue;
+            const unsigned long long *slot = m->h_mstats + (size_t)b * MSTRIDE;
+            fill_stats(slot, rays[b].count, before[b], out + b);
+            m->max_growth = std::max<long long>(m->max_growth, out[b].new_regions);
+        }
+        m->nreg = regions;
+        if (f == nb) break;
+        // ---- recover batch f ----
+        const unsigned long long *slot = m->h_mstats + (size_t)f * MSTRIDE;
+        const int cursor = (int)slot[NUM_STATS];
+        DevMap dm = dms[f];
+        if (slot[S_RANGE_ERR]) {
+            if (slot[S_MARKED]) {
+                const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
+                k_clear_marks<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, words);
+            }
+            CK(cudaStreamSynchronize(s));
+            m->nreg = cursor;
+            return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range "
+                                      "(|region| < 2**20, keys.py:76-86)");
+        }
+        if (!(slot[NUM_STATS + 1] & 1ULL)) {
+            // region pool: grow and replay from f (its stamps stay valid)
+            m->max_growth = std::max<long long>(m->max_growth, cursor - m->nreg);
+            if ((rc = grow_pool(m, std::max<long long>(2 * m->cap, cursor + 2 * margin + headroom))))
+                return rc;
+            if (cursor + margin > m->cap)
+                return fail(VM_ERR_OOM, "region pool exhausted (max regions reached)");
+            if (first_before[f] < 0) first_before[f] = regions;  // new_regions spans the replays
+            m->nreg = cursor;
+            reps[f] += 1;
+            b0 = f;
+            keep_marks = true;
+            continue;
+        }
+        // records overflowed: walk + resolve were applied, the fold was not;
+        // re-emit the records (nothing re-applied) and fold them
+        const unsigned long long R = slot[S_RECORDS];
+        if ((rc = ensure_records(m, (size_t)R + (R >> 2)))) return rc;
+        dm.rec = m->d_rec;
+        dm.recval = m->d_val;
+        dm.rec_cap = m->rec_cap;
+        static const int one = 1;
+        CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
+        CK(cudaMemcpyAsync(m->d_go, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(dm.stats + S_RECORDS, 0, sizeof(unsigned long long), s));
+        if (!rays[f].on_device) {
+            CK(cudaMemcpyAsync(m->d_ring[f % vm_map::RING], rays[f].records,
+                               (size_t)rays[f].count * 40, cudaMemcpyHostToDevice, s));
+            srcp[f] = m->d_ring[f % vm_map::RING];
+        }
+        const SrcOHMB1 src{srcp[f]};
+        const long long n = rays[f].count;
+        if ((rc = launch_walk(m, dm, src, n, mode, true, true))) return rc;
+        cudaEvent_t *ev = &m->mev[(size_t)6 * f];
+        CK(cudaEventRecord(ev[3], s));
+        if ((rc = launch_bucket_fold(m, dm, src, n, maxseg, ev[4]))) return rc;
+        k_batch_fin<<<1, 1, 0, s>>>(dm);
+        CK(cudaEventRecord(ev[5], s));
+        CK(cudaMemcpyAsync(m->h_mstats + (size_t)f * MSTRIDE, dm.stats,
+                           MSTRIDE * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if ((rc = check_launch("record re-emit"))) return rc;
+        if (slot[NUM_STATS + 1] != 3ULL) return fail(VM_ERR_CUDA, "record re-emit failed");
+        fill_stats(slot, n, first_before[f] >= 0 ? first_before[f] : m->nreg, out + f);
+        m->nreg = (long long)slot[NUM_STATS];
+        b0 = f + 1;
+    }
+    for (int b = 0; b < nb; ++b) {
+        if (rays[b].count <= 0) continue;
+        cudaEvent_t *ev = &m->mev[(size_t)6 * b];
+        float t[5] = {0, 0, 0, 0, 0}, tot = 0;
+        CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
+        for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
+        out[b].gpu_ms = tot;
+        out[b].discover_ms = t[0];
+        out[b].walk_ms = t[1];
+        out[b].resolve_ms = t[2];
+        out[b].sort_ms = t[3];
+        out[b].fold_ms = t[4];
+        out[b].replays = reps[b];
+        out[b].launches = launches[b];
+    }
     return VM_OK;
 }
 
@@ -762,6 +1176,7 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         cudaDeviceProp prop;
         if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) m->num_sms = prop.multiProcessorCount;
     }
+    if (const char *rc_env = std::getenv("VOXMAP_B200_TEST_REC_CAP")) m->rec_floor_override = std::atoll(rc_env);
     if ((rc = grow_pool(m, std::max<long long>(64, initial_regions)))) return cleanup(rc);
     *out = m;
     return VM_OK;
@@ -793,6 +1208,20 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_bmask);
     cudaFree(m->d_big);
     cudaFree(m->d_nbig);
+    cudaFree(m->d_bk_cnt);
+    cudaFree(m->d_bk_off);
+    cudaFree(m->d_bk_big);
+    cudaFree(m->d_bk_bits);
+    cudaFree(m->d_chain);
+    cudaFree(m->d_mstats);
+    if (m->h_mstats) cudaFreeHost(m->h_mstats);
+    for (cudaEvent_t e : m->mev) cudaEventDestroy(e);
+    for (int r = 0; r < vm_map::RING; ++r) {
+        cudaFree(m->d_ring[r]);
+        if (m->ev_ring[r]) cudaEventDestroy(m->ev_ring[r]);
+        if (m->ev_ring_up[r]) cudaEventDestroy(m->ev_ring_up[r]);
+    }
+    cudaFree(m->d_scan_tmp);
     cudaFree(m->d_rbox);
     cudaFree(m->d_stats);
     cudaFree(m->d_go);
@@ -813,6 +1242,7 @@ int vm_map_destroy(vm_map *m) {
         if (e) cudaEventDestroy(e);
     if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
     delete m;
+    (void)cudaGetLastError();  // nothing of this map may leak into later calls
     return VM_OK;
 }
 
@@ -959,6 +1389,7 @@ int vm_integrate(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, vm_
     if ((m->mask & MODE_MASK[mode]) != MODE_MASK[mode])
         return fail(VM_ERR_ARG, "map lacks layers required by mode");
     CK(cudaSetDevice(m->device));
+    (void)cudaGetLastError();  // a stale non-sticky error of an unrelated call
     long long n = rays->count;
     std::memset(out, 0, sizeof(*out));
     if (n <= 0) {
@@ -1008,6 +1439,132 @@ int vm_integrate(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, vm_
         return rc;
     }
     return fail(VM_ERR_ARG, "unknown ray format");
+}
+
+int vm_integrate_many(vm_map *m, const vm_rays *rays, int32_t nbatches, int32_t mode, int32_t exec,
+                      vm_stats *out) {
+    if (!m || (!rays && nbatches > 0) || (!out && nbatches > 0)) return fail(VM_ERR_ARG, "null argument");
+    if (nbatches < 0) return fail(VM_ERR_ARG, "negative batch count");
+    if (mode < 0 || mode > 4) return fail(VM_ERR_ARG, "unknown mode");
+    if (exec != VM_EXEC_CAS && exec != VM_EXEC_DETERMINISTIC) return fail(VM_ERR_ARG, "bad exec");
+    if ((m->mask & MODE_MASK[mode]) != MODE_MASK[mode])
+        return fail(VM_ERR_ARG, "map lacks layers required by mode");
+    bool pipelined = mode == M_OCC && exec == VM_EXEC_DETERMINISTIC && m->shard_world == 1 &&
+                     !m->sb.open;
+    for (int b = 0; b < nbatches && pipelined; ++b) {
+        if (rays[b].count > 0 && (rays[b].format != VM_RAYS_OHMB1 || !rays[b].records))
+            pipelined = false;
+    }
+    if (!pipelined) {
+        for (int b = 0; b < nbatches; ++b) {
+            const int rc = vm_integrate(m, rays + b, mode, exec, out + b);
+            if (rc) return rc;
+        }
+        return VM_OK;
+    }
+    CK(cudaSetDevice(m->device));
+    (void)cudaGetLastError();
+    return integrate_pipelined(m, rays, nbatches, mode, out);
+}
+
+// ---------------------------------------------------------------- exporters
+
+int vm_export_select(vm_map *m, const int32_t *slots, int64_t nslots, int32_t kind,
+                     double threshold, int64_t *count_out, int32_t *ridx_out, int32_t *li_out,
+                     int64_t cap) {
+    if (!m || (!slots && nslots > 0) || !count_out) return fail(VM_ERR_ARG, "null argument");
+    if (kind < EX_OCCUPIED || kind > EX_DECAY) return fail(VM_ERR_ARG, "unknown export kind");
+    static const int need[4] = {L_OCC, L_COUNT, L_TSDF, L_DDIST};
+    if (!m->slab[need[kind]] || (kind == EX_DECAY && !m->slab[L_DHITS]))
+        return fail(VM_ERR_ARG, "map lacks the layers of this export");
+    CK(cudaSetDevice(m->device));
+    *count_out = 0;
+    if (nslots <= 0) return VM_OK;
+    for (int64_t i = 0; i < nslots; ++i)
+        if (slots[i] < 0 || slots[i] >= m->nreg) return fail(VM_ERR_ARG, "slot out of range");
+    cudaStream_t s = m->stream;
+    int *d_slots = nullptr;
+    unsigned long long *d_cnt = nullptr;
+    CK(cudaMalloc((void **)&d_slots, nslots * sizeof(int)));
+    CK(cudaMalloc((void **)&d_cnt, nslots * sizeof(unsigned long long)));
+    std::vector<unsigned long long> cnt(nslots);
+    int rc = VM_OK;
+    DevMap dm = make_dm(m);
+    do {
+        if (cudaMemcpyAsync(d_slots, slots, nslots * sizeof(int), cudaMemcpyHostToDevice, s) ||
+            cudaMemsetAsync(d_cnt, 0, nslots * sizeof(unsigned long long), s)) {
+            rc = fail(VM_ERR_CUDA, "export copy");
+            break;
+        }
+        k_export_count<<<(unsigned)nslots, EX_BLOCK, 0, s>>>(dm, d_slots, kind, threshold, d_cnt);
+        if (cudaMemcpyAsync(cnt.data(), d_cnt, nslots * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s) ||
+            cudaStreamSynchronize(s)) {
+            rc = fail(VM_ERR_CUDA, std::string("export count: ") + cudaGetErrorString(cudaGetLastError()));
+            break;
+        }
+        unsigned long long total = 0;
+        for (int64_t i = 0; i < nslots; ++i) {
+            const unsigned long long c = cnt[i];
+            cnt[i] = total;
+            total += c;
+        }
+        *count_out = (int64_t)total;
+        if (!ridx_out || !li_out || (int64_t)total > cap || total == 0) break;
+        int *d_ridx = nullptr, *d_li = nullptr;
+        if (cudaMalloc((void **)&d_ridx, total * sizeof(int)) ||
+            cudaMalloc((void **)&d_li, total * sizeof(int))) {
+            cudaFree(d_ridx);
+            rc = fail(VM_ERR_OOM, "export buffers");
+            break;
+        }
+        cudaMemcpyAsync(d_cnt, cnt.data(), nslots * sizeof(unsigned long long), cudaMemcpyHostToDevice, s);
+        k_export_write<<<(unsigned)nslots, EX_BLOCK, 0, s>>>(dm, d_slots, kind, threshold, d_cnt,
+                                                             d_ridx, d_li);
+        cudaMemcpyAsync(ridx_out, d_ridx, total * sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(li_out, d_li, total * sizeof(int), cudaMemcpyDeviceToHost, s);
+        const cudaError_t e = cudaStreamSynchronize(s);
+        cudaFree(d_ridx);
+        cudaFree(d_li);
+        if (e != cudaSuccess) rc = fail(VM_ERR_CUDA, std::string("export write: ") + cudaGetErrorString(e));
+    } while (0);
+    cudaFree(d_slots);
+    cudaFree(d_cnt);
+    return rc;
+}
+
+int vm_export_gather(vm_map *m, int32_t layer, const int32_t *slots, int64_t nslots,
+                     const int32_t *ridx, const int32_t *li, int64_t n, void *out) {
+    if (!m || !slots || (n > 0 && (!ridx || !li || !out))) return fail(VM_ERR_ARG, "null argument");
+    if (layer < 1 || layer >= NUM_LAYERS || !m->slab[layer]) return fail(VM_ERR_ARG, "layer not in map");
+    CK(cudaSetDevice(m->device));
+    if (n <= 0) return VM_OK;
+    const int bytes = (int)(m->bpr[layer] / (size_t)m->vpr);
+    cudaStream_t s = m->stream;
+    int *d_slots = nullptr, *d_ridx = nullptr, *d_li = nullptr;
+    unsigned char *d_out = nullptr;
+    int rc = VM_OK;
+    if (cudaMalloc((void **)&d_slots, nslots * sizeof(int)) ||
+        cudaMalloc((void **)&d_ridx, n * sizeof(int)) || cudaMalloc((void **)&d_li, n * sizeof(int)) ||
+        cudaMalloc((void **)&d_out, (size_t)n * bytes)) {
+        rc = fail(VM_ERR_OOM, "export gather buffers");
+    } else {
+        cudaMemcpyAsync(d_slots, slots, nslots * sizeof(int), cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(d_ridx, ridx, n * sizeof(int), cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(d_li, li, n * sizeof(int), cudaMemcpyHostToDevice, s);
+        DevMap dm = make_dm(m);
+        const long long blocks = std::min<long long>((n * bytes + 255) / 256, (long long)m->num_sms * 16);
+        k_export_gather<<<(unsigned)std::max<long long>(1, blocks), 256, 0, s>>>(
+            dm, layer, bytes, d_slots, d_ridx, d_li, n, d_out);
+        cudaMemcpyAsync(out, d_out, (size_t)n * bytes, cudaMemcpyDeviceToHost, s);
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = fail(VM_ERR_CUDA, std::string("export gather: ") + cudaGetErrorString(e));
+    }
+    cudaFree(d_slots);
+    cudaFree(d_ridx);
+    cudaFree(d_li);
+    cudaFree(d_out);
+    return rc;
 }
 
 int vm_walk_voxels(double ox, double oy, double oz, double ex, double ey, double ez, double cell,
@@ -1216,7 +1773,7 @@ int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, i
     if ((rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
     if ((rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
     if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)n + 1))) return rc;
-    if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, std::max<size_t>(1 << 20, (size_t)n_all * 4)))))
+    if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, rec_floor(m, n_all)))))
         return rc;
     sb.launches0 = m->launches;
     sb.nreg0 = m->nreg;
@@ -1231,10 +1788,8 @@ int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, i
         CK(cudaMemcpyAsync(m->d_rbox, box_init, sizeof(box_init), cudaMemcpyHostToDevice, m->stream));
         CK(cudaEventRecord(m->ev_start, m->stream));
         if (sb.n > 0) {
-            const dim3 dgrid((unsigned)((sb.n + BLOCK - 1) / BLOCK), (unsigned)sb.maxseg);
             rc = with_src(m, [&](auto src) {
-                k_discover<<<dgrid, BLOCK, 0, m->stream>>>(dm, src, sb.n, VM_MODE_OCCUPANCY, 1, 1);
-                return check_launch("discover");
+                return launch_discover(m, dm, src, sb.n, VM_MODE_OCCUPANCY, 1, 1, 1, m->stream);
             });
             if (rc) return rc;
         }
@@ -1450,6 +2005,7 @@ int vm_shard_finish(vm_map *m, vm_stats *out) {
     CK(cudaEventRecord(m->ev_res, m->stream));
     cub::DoubleBuffer<unsigned long long> db(m->d_rec, m->d_rec2);
     if (Rtot > 1) {
+        if ((rc = ensure_sort_tmp(m))) return rc;
         size_t bytes = m->sort_tmp_bytes;
         CK(cub::DeviceRadixSort::SortKeys(m->d_sort_tmp, bytes, db, (int)Rtot, 0, end_bit, m->stream));
     }

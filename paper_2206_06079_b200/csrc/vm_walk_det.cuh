@@ -101,7 +101,17 @@ __device__ __forceinline__ bool walk_det_ok(const DevMap &m) {
            m.rbox[5] - m.rbox[2] < RP_BIAS - 3;
 }
 
-template <bool REC_ONLY, class Src>
+// brick bit of local index li; DIM = 32 (the default region) folds the shifts
+template <int DIM>
+__device__ __forceinline__ unsigned wd_brick(int li, const int bsh[3]) {
+    if (DIM == 32)
+        return (((unsigned)li >> 3) & 3u) | (((unsigned)li >> 6) & 0xCu) |
+               (((unsigned)li >> 10) & 0x10u);
+    return brick_of(li, bsh);
+}
+
+// DIM: compile-time region edge (32), or 0 for any other region_dim
+template <bool REC_ONLY, class Src, int DIM = 0>
 __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_constant__ DevMap m,
                                                                Src src) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -154,8 +164,8 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
 
     const int lane = threadIdx.x & 31;
     const unsigned lanemask_lt = (1u << lane) - 1u;
-    const int dim = m.dim;
-    const unsigned vpr = (unsigned)m.vpr;
+    const int dim = DIM ? DIM : m.dim;
+    const unsigned vpr = DIM ? (unsigned)(DIM * DIM * DIM) : (unsigned)m.vpr;
     const int ob = m.order_bits;
     unsigned long long *const wbuf = sm.wbuf[threadIdx.x >> 5];
     unsigned wcnt = 0, wflushed = 0;  // warp-uniform record ring counters
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
                 } else if (!REC_ONLY) {
                     atomicAdd(sm.cube + ck, 1u);
                 }
-            } else if (((bm >> brick_of(li, m.bsh)) & 1u) || forced) {
+            } else if (((bm >> wd_brick<DIM>(li, m.bsh)) & 1u) || forced) {
                 sm.vids[Q][threadIdx.x] = vid;
                 live |= 1u << Q;
                 if (forced) sure |= 1u << Q;

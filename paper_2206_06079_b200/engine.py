@@ -138,6 +138,49 @@ def submit_batch(vmap: VoxelMap, rays, mode: str, opts: ExecutorOptions | None =
     return stats
 
 
+def _to_stats(st, wall: float) -> BatchStats:
+    stats = BatchStats(rays_in=int(st.rays_in))
+    for name in ("rays_processed", "segments", "voxel_visits", "cas_retries", "cas_failures",
+                 "region_misses", "regions_touched", "records", "marked_voxels", "new_regions",
+                 "replays"):
+        setattr(stats, name, int(getattr(st, name)))
+    stats.gpu_time = float(st.gpu_ms) * 1e-3
+    stats.walk_time = float(st.walk_ms) * 1e-3
+    stats.wall_time = wall
+    return stats
+
+
+def submit_batches(vmap: VoxelMap, batches, mode: str, opts: ExecutorOptions | None = None
+                   ) -> list[BatchStats]:
+    """Integrate a sequence of batches in order: the same map state and the
+    same per-batch stats as calling `submit_batch` once per batch (the
+    reference CLI's offline replay loop, cli.py:122-127).  Deterministic
+    occupancy over OHMB1 record arrays runs as one pipelined device sequence
+    (vm_integrate_many: host uploads overlap earlier batches' compute, one
+    sync at the end); `wall_time` of each batch is its share of the call."""
+    if opts is None:
+        opts = ExecutorOptions()
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
+    required = layers.MODE_LAYERS[mode]
+    if not vmap.has_layers(required):
+        missing = set(required) - set(vmap.layer_names)
+        raise ConfigurationError(f"map lacks layers {sorted(missing)} required by mode {mode!r}")
+    batches = list(batches)
+    if not batches:
+        return []
+    start = time.perf_counter()
+    converted = [_as_native_rays(b) for b in batches]
+    vmap.batch_counter += len(batches)
+    vmap.flush_host_writes()
+    sts = vmap._native.integrate_many([c[0] for c in converted], mode, opts.use_deterministic)
+    del converted
+    vmap._sync_regions()
+    wall = time.perf_counter() - start
+    total = sum(int(s.rays_in) for s in sts) or 1
+    return [_to_stats(s, wall * int(s.rays_in) / total) for s in sts]
+
+
 def sequential_reference(vmap: VoxelMap, rays, mode: str = "occupancy") -> BatchStats:
     """Deterministic executor: the reference's sequential results, on the GPU."""
     return submit_batch(vmap, rays, mode, ExecutorOptions(worker_count=1, kind="sequential"))
