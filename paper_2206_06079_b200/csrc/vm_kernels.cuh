@@ -153,7 +153,10 @@ __device__ __forceinline__ T *layer_at(const DevMap &m, int layer, int slot) {
 
 // Per-block direct-mapped cache region -> slot, keyed by coordinates relative
 // to a block anchor (13 bits per axis) so key + slot fit one 64-bit word.
-constexpr int KCACHE = 1024;
+#ifndef KCACHE_N
+#define KCACHE_N 1024
+#endif
+constexpr int KCACHE = KCACHE_N;
 struct KeyCache {
     unsigned long long *e;
     int ax, ay, az;
@@ -220,14 +223,19 @@ struct PrefetchVisitor {
     }
 };
 
+#ifndef DISC_BT
+#define DISC_BT 512  // k_discover block size: more rays share a block's key cache
+                     // (C2 discover: 128 -> 23.6, 256 -> 19.5, 512 -> 17.6 ms per step)
+#endif
+
 template <class Src>
-__global__ void __launch_bounds__(BLOCK) k_discover(const __grid_constant__ DevMap m, Src src,
+__global__ void __launch_bounds__(DISC_BT) k_discover(const __grid_constant__ DevMap m, Src src,
                                                     long long n, int mode, int det, int emit,
                                                     int count_stats = 1) {
     if (m.chain && *((volatile int *)m.chain)) return;  // an earlier batch of the sequence failed
     __shared__ unsigned long long kcache[KCACHE];
     __shared__ int sset[SLOTSET];
-    __shared__ unsigned long long srec[BLOCK];
+    __shared__ unsigned long long srec[DISC_BT];
     __shared__ int nrec;
     __shared__ unsigned long long rec_base;
     __shared__ unsigned shist[SEG_BUCKETS];
@@ -855,6 +863,14 @@ __global__ void __launch_bounds__(BLOCK) k_walk_tsdf(const __grid_constant__ Dev
 // NDT adds the NDT-TM miss count and the transient reset
 // (reference.py:86-93).  One block per touched region.
 // Resolve region `slot`, voxels [v0, v1): f_miss^k per counted voxel.
+#ifndef RES_U
+#define RES_U 4     // scratch quads in flight per thread
+#endif
+#ifndef RES_MINB
+#define RES_MINB 4  // k_resolve resident blocks per SM: 4 x 4 quads in flight beat
+                    // 2 x 8 (C2 resolve 11.6 -> 10.6 ms per step)
+#endif
+
 template <bool NDT, bool TM>
 __device__ __forceinline__ void resolve_range(const DevMap &m, int slot, int v0, int v1) {
     unsigned *scr = reinterpret_cast<unsigned *>(m.slab[L_SCRATCH] + (size_t)slot * m.bpr[L_SCRATCH]);
@@ -864,17 +880,17 @@ __device__ __forceinline__ void resolve_range(const DevMap &m, int slot, int v0,
         // occupancy quads of the non-zero ones, also all in flight
         const uint4 *s4 = reinterpret_cast<const uint4 *>(scr);
         float4 *o4 = reinterpret_cast<float4 *>(occ);
-        for (int q0 = (v0 >> 2) + threadIdx.x; q0 < (v1 >> 2); q0 += 8 * blockDim.x) {
-            uint4 w[8];
-            float4 l[8];
+        for (int q0 = (v0 >> 2) + threadIdx.x; q0 < (v1 >> 2); q0 += RES_U * blockDim.x) {
+            uint4 w[RES_U];
+            float4 l[RES_U];
             unsigned nz = 0;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < RES_U; ++u) {
                 const int q = q0 + u * blockDim.x;
                 w[u] = q < (v1 >> 2) ? __ldcs(s4 + q) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < RES_U; ++u) {
                 // counted voxels (MARK'ed words -- sample voxels -- are the fold's)
                 const unsigned ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
                 bool any = false;
@@ -886,7 +902,7 @@ __device__ __forceinline__ void resolve_range(const DevMap &m, int slot, int v0,
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < RES_U; ++u) {
                 if (!((nz >> u) & 1u)) continue;
                 const int q = q0 + u * blockDim.x;
                 unsigned ks[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
@@ -956,7 +972,7 @@ __device__ __forceinline__ void resolve_range(const DevMap &m, int slot, int v0,
 constexpr int RES_TILE = 8192;
 
 template <bool NDT, bool TM>
-__global__ void __launch_bounds__(BLOCK) k_resolve(const __grid_constant__ DevMap m) {
+__global__ void __launch_bounds__(BLOCK, RES_MINB) k_resolve(const __grid_constant__ DevMap m) {
     if (!read_go(m)) return;
     unsigned long long nt = *((volatile unsigned long long *)(m.stats + S_WALK_TOUCHED));
     if (nt > (unsigned long long)m.touched_cap) nt = m.touched_cap;

@@ -345,8 +345,8 @@ int check_launch(const char *what) {
 template <class Src>
 int launch_discover(vm_map *m, const DevMap &dm, const Src &src, long long n, int mode, int det,
                     int emit, int count_stats, cudaStream_t s) {
-    const dim3 grid((unsigned)((n + BLOCK - 1) / BLOCK), mode == M_TSDF ? 1u : (unsigned)dm.maxseg);
-    k_discover<<<grid, BLOCK, 0, s>>>(dm, src, n, mode, det, emit, count_stats);
+    const dim3 grid((unsigned)((n + DISC_BT - 1) / DISC_BT), mode == M_TSDF ? 1u : (unsigned)dm.maxseg);
+    k_discover<<<grid, DISC_BT, 0, s>>>(dm, src, n, mode, det, emit, count_stats);
     m->launches += 1;
     return check_launch("discover");
 }

@@ -1,3 +1,4 @@
+import gc
 import sys
 from pathlib import Path
 
@@ -19,3 +20,12 @@ def _built():
     __graft_entry__.build() (the GPU tests fail loudly without it)."""
     from oracle import oracle
     oracle.build()
+
+
+@pytest.fixture(autouse=True)
+def _release_device_maps():
+    """VoxelMap <-> Region reference cycles keep device maps (HBM pools) alive
+    until the cyclic GC runs; collect after every test so a long GPU session
+    does not accumulate them."""
+    yield
+    gc.collect()

@@ -32,6 +32,7 @@ _maps = {}
 
 def _map(case):
     if case not in _maps:
+        _maps.clear()  # one device map at a time (cases are grouped)
         p = f"c{case}_"
         mode = str(S[p + "mode"])
         vm = VoxelMap(MapConfig(**ast.literal_eval(str(S[p + "cfg"]))), MODE_LAYERS[mode])

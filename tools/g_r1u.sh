@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/u_c2.txt 2>&1
+VOXMAP_B200_LIB=libvoxmap_b200_d128.so timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/u_c2_d128.txt 2>&1
+VOXMAP_B200_LIB=libvoxmap_b200_d128.so timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider > gpurun_out/u_pytest_d128.txt 2>&1; echo "rc=$?" >> gpurun_out/u_pytest_d128.txt
