@@ -34,7 +34,7 @@ constexpr int RP_BIAS = 512;  // bias of the grid-relative region coordinates
 struct WalkDetSmem {
     unsigned cube[WCUBE_N];          // miss counts around the sensor
     unsigned cmark[WCUBE_N / 32];    // sample-voxel bitmap of the cube
-    int2 grid[RG_SMEM];              // (slot, brick summary of sample voxels)
+    int2 grid[RG_SMEM_DET];          // (slot, brick summary of sample voxels)
     unsigned long long wbuf[BLOCK / 32][WK_WBUF];
     unsigned vids[WD_STEPS][BLOCK];  // voxel id of each in-flight visit
     SegDesc pf[BLOCK];
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         sm.gs[1] = sm.gn[0];
         sm.gs[2] = sm.gn[0] * sm.gn[1];
         const int ncell = sm.gn[0] * sm.gn[1] * sm.gn[2];
-        sm.gmode = !have_grid ? 0 : (ncell <= RG_SMEM ? 1 : 2);
+        sm.gmode = !have_grid ? 0 : (ncell <= RG_SMEM_DET ? 1 : 2);
         if (nseg_total) {
             const SegDesc &d0 = m.segs[0];
             int r0[3];
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         const unsigned vid = vbase + (unsigned)li;
         if (vbase != 0xFFFFFFFFu) {
             if (in_cube) {
-                const unsigned ck = (cp & 7u) | ((cp >> 5) & 0x38u) | ((cp >> 10) & 0x1C0u);
+                const unsigned ck = cube_cell(cp);
                 if (((sm.cmark[ck >> 5] >> (ck & 31)) & 1u) || forced) {
                     sm.vids[Q][threadIdx.x] = vid;
                     live |= 1u << Q;
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         li += dl;
         if (in_cube) {
             cp += (unsigned)((int)dp >> sh) << (8 * ax);  // the step (+-1) into the cube field
-            in_cube = (cp & 0x00F8F8F8u) == 0;
+            in_cube = (cp & CUBE_OUT) == 0;
         }
         if (((lp >> sh) & 1023u) - 1u >= (unsigned)dim) {
             // region crossing: wrap the local coordinate, step the grid index
