@@ -228,8 +228,12 @@ struct PrefetchVisitor {
                      // (C2 discover: 128 -> 23.6, 256 -> 19.5, 512 -> 17.6 ms per step)
 #endif
 
+#ifndef DISC_MINB
+#define DISC_MINB 1
+#endif
+
 template <class Src>
-__global__ void __launch_bounds__(DISC_BT) k_discover(const __grid_constant__ DevMap m, Src src,
+__global__ void __launch_bounds__(DISC_BT, DISC_MINB) k_discover(const __grid_constant__ DevMap m, Src src,
                                                     long long n, int mode, int det, int emit,
                                                     int count_stats = 1) {
     if (m.chain && *((volatile int *)m.chain)) return;  // an earlier batch of the sequence failed

@@ -44,11 +44,15 @@ namespace vm {
 
 constexpr int WK_INNER = 8;     // DDA steps between warp-level bookkeeping (= max candidates)
 constexpr int WK_BLOCKS = 3;    // resident blocks per SM
-// dense region grid cells held in shared memory: sized so three blocks of
-// each walk fit an SM next to the 16^3 sensor cube (WalkSmem 73 KB,
-// WalkDetSmem 73 KB)
+// dense region grid cells held in shared memory (larger boxes read the grid
+// through L1): sized so three blocks of each walk fit an SM next to the 16^3
+// sensor cube.  k_walk_det with 2048 cells (73 KB per block) measured 4%
+// slower on C2 than with 1024 (65 KB); 64..1024 are equal.
 constexpr int RG_SMEM = 1024;      // k_walk (generic / CAS)
-constexpr int RG_SMEM_DET = 2048;  // k_walk_det
+#ifndef VM_RG_SMEM_DET
+#define VM_RG_SMEM_DET 1024
+#endif
+constexpr int RG_SMEM_DET = VM_RG_SMEM_DET;  // k_walk_det
 constexpr int WK_WBUF = 64;     // per-warp record ring (flushed 32 at a time)
 // Sensor cube: the voxels next to the sensor, which every ray of the batch
 // crosses, count in shared memory instead of as same-address L2 atomics.

@@ -27,7 +27,10 @@
 
 namespace vm {
 
-constexpr int WD_STEPS = 8;   // steps per window (in-flight visits per lane)
+#ifndef VM_WD_STEPS
+#define VM_WD_STEPS 8
+#endif
+constexpr int WD_STEPS = VM_WD_STEPS;  // steps per window (in-flight visits per lane)
 constexpr int WD_BLOCKS = 3;  // resident blocks per SM
 constexpr int RP_BIAS = 512;  // bias of the grid-relative region coordinates
 
