@@ -229,7 +229,7 @@ struct PrefetchVisitor {
 #endif
 
 #ifndef DISC_MINB
-#define DISC_MINB 1
+#define DISC_MINB 2  // 2 x 512 threads per SM: the 64-register build (96 registers / 1 block: 17.5 -> 22.7 ms)
 #endif
 
 template <class Src>
@@ -666,8 +666,12 @@ struct NdtVisitor {
     }
 };
 
+#ifndef NDT_MINB
+#define NDT_MINB 1  // k_walk_ndt resident blocks per SM (register budget)
+#endif
+
 template <bool TM, bool DET, bool REC_ONLY, class Src>
-__global__ void __launch_bounds__(BLOCK) k_walk_ndt(const __grid_constant__ DevMap m, Src src, long long n) {
+__global__ void __launch_bounds__(BLOCK, NDT_MINB) k_walk_ndt(const __grid_constant__ DevMap m, Src src, long long n) {
     __shared__ unsigned cube[CUBE_N];
     __shared__ int sset[SLOTSET];
     __shared__ int corner[3];
