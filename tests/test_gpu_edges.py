@@ -253,3 +253,34 @@ def test_tsdf_then_decay_vs_oracle():
                 assert np.max(np.abs(a - b), initial=0.0) <= 1e-9, rk
             else:  # occupancy, mean, mean_count, decay_hits, tsdf: bit-exact
                 assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (rk, name)
+
+
+@pytest.mark.slow
+def test_c2_prefix_cas_order_free_layers_exact():
+    """CAS mode (the paper's atomic update, _kernels.pyx:233-357) at C2 scale:
+    voxels that received no hit see only identical-delta misses, which
+    commute, so their occupancy is bit-exact; mean_count is exact.  Voxels
+    with hits and misses are order-dependent (SURVEY finding 4): their
+    deviation is reported and bounded by the clamp range."""
+    cfg = MapConfig(voxel_size=0.05)
+    data = scans.batch_by_period(np.concatenate(scans.os128_canyon_batches(20)))[:2]
+    names = MODE_LAYERS["occupancy"]
+    vm = VoxelMap(cfg, names)
+    om = orc.OracleMap(cfg, names)
+    for rec in data:
+        st = submit_batch(vm, rec, "occupancy", ExecutorOptions(deterministic=False))
+        ost = om.integrate_records(rec, "occupancy")
+        assert st.voxel_visits == ost["voxel_visits"] and st.region_misses == 0
+    assert set(vm.regions) == set(om.region_keys())
+    mixed, worst = 0, 0.0
+    for rk, region in vm.regions.items():
+        cnt = om.layer(rk, "mean_count")
+        assert np.array_equal(region.buffers["mean_count"], cnt), rk
+        a, b = region.buffers["occupancy"], om.layer(rk, "occupancy")
+        free = cnt == 0
+        assert np.array_equal(a[free].view(np.uint32), b[free].view(np.uint32)), rk
+        d = np.abs(a[~free].astype(np.float64) - b[~free])
+        mixed += int(np.count_nonzero(d))
+        worst = max(worst, float(d.max(initial=0.0)))
+    assert worst <= 5.5  # clamp_max - clamp_min
+    print(f"CAS vs sequential on hit voxels: {mixed} differ, max {worst:.4f} log-odds")
