@@ -120,7 +120,7 @@ def submit_batch(vmap: VoxelMap, rays, mode: str, opts: ExecutorOptions | None =
     vmap.flush_host_writes()
     st = vmap._native.integrate(native_rays, mode, opts.use_deterministic)
     del keep
-    vmap._sync_regions()
+    vmap._note_batch(int(st.regions_total))
     stats.rays_processed = int(st.rays_processed)
     stats.segments = int(st.segments)
     stats.voxel_visits = int(st.voxel_visits)
@@ -175,7 +175,11 @@ def submit_batches(vmap: VoxelMap, batches, mode: str, opts: ExecutorOptions | N
     vmap.flush_host_writes()
     sts = vmap._native.integrate_many([c[0] for c in converted], mode, opts.use_deterministic)
     del converted
-    vmap._sync_regions()
+    first = vmap.batch_counter - len(batches) + 1
+    for i, st in enumerate(sts):  # the regions each batch created were last accessed by it
+        vmap.batch_counter = first + i
+        vmap._note_batch(int(st.regions_total))
+    vmap.batch_counter = first + len(batches) - 1
     wall = time.perf_counter() - start
     total = sum(int(s.rays_in) for s in sts) or 1
     return [_to_stats(s, wall * int(s.rays_in) / total) for s in sts]

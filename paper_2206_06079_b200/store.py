@@ -77,12 +77,13 @@ class VoxelMap:
                  spill_dir=None, device: int = 0, initial_regions: int = 256):
         self.cfg = cfg
         self.layers = layermod.resolve(layer_names)
-        self.regions: dict[tuple[int, int, int], Region] = {}
+        self._regions: dict[tuple[int, int, int], Region] = {}
+        self._created: list[tuple[int, int]] = []  # (regions after batch, batch counter)
         self.batch_counter = 0
         self._spill_dir = Path(spill_dir) if spill_dir is not None else None
         self._native = _native.NativeMap(cfg, layermod.layer_mask(layer_names), device,
                                          initial_regions)
-        self._known = 0          # device slots mirrored into self.regions
+        self._known = 0          # device slots mirrored into self._regions
         self._mirrors = {}       # (slot, name) -> (array, pristine copy)
 
     # -- region access --------------------------------------------------
@@ -95,17 +96,40 @@ class VoxelMap:
         return set(names) <= set(self.layer_names)
 
     @property
+    def regions(self) -> dict:
+        """region key -> Region (store.py:45-52).  The device owns the regions;
+        this host index is built lazily, on first access after the batches
+        that created them, so integrating a batch costs no per-region Python
+        work."""
+        self._sync_regions()
+        return self._regions
+
+    @property
     def region_count(self) -> int:
-        return len(self.regions)
+        return int(self._native.region_count())
+
+    def _note_batch(self, regions_total: int):
+        """After a batch: the regions it created (slots below regions_total)
+        were last accessed by it (Region.last_access, store.py:28-39)."""
+        if regions_total > self._known and (not self._created or
+                                            regions_total > self._created[-1][0]):
+            self._created.append((int(regions_total), self.batch_counter))
 
     def _sync_regions(self):
         """Mirror device-created regions (slot order = creation order)."""
         n = self._native.region_count()
         if n > self._known:
+            created = self._created
+            j = 0
             for i, packed in enumerate(self._native.region_keys(self._known, n - self._known)):
+                slot = self._known + i
+                while j < len(created) and created[j][0] <= slot:
+                    j += 1
+                access = created[j][1] if j < len(created) else self.batch_counter
                 rk = unpack_region_coord(int(packed))
-                self.regions[rk] = Region(rk, self._known + i, self, self.batch_counter)
+                self._regions[rk] = Region(rk, slot, self, access)
             self._known = n
+            self._created = []
 
     def get_region(self, rk, create: bool = False) -> Region | None:
         rk = (int(rk[0]), int(rk[1]), int(rk[2]))
@@ -125,7 +149,8 @@ class VoxelMap:
         """Drop every region (device pool capacity is kept)."""
         self._mirrors.clear()
         self._native.reset()
-        self.regions.clear()
+        self._regions.clear()
+        self._created = []
         self._known = 0
 
     # -- host mirrors ---------------------------------------------------
