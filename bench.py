@@ -402,10 +402,11 @@ def run_sharded(args, world, rank, dev, dist):
 
     def step(record=False, batches=d_batches):
         smap.vmap.clear()
-        tot = dict(S=0, V=0, walk_ms=0.0, batches=0, records=0, rmiss=0)
+        tot = dict(S=0, V=0, walk_ms=0.0, batches=0, records=0, rmiss=0, xbytes=0)
         for bt in batches:
             st = submit_batch_sharded(smap, bt)
             if record:
+                tot["xbytes"] += st.exchange_bytes
                 tot["S"] += st.segments
                 tot["V"] += st.voxel_visits
                 tot["walk_ms"] += st.walk_time * 1e3
@@ -482,7 +483,8 @@ def run_sharded(args, world, rank, dev, dist):
             "gpu_launches": None,
             "clocks": parse_clocks(clk_file, dev),
             "stats": {"segments": s0["S"], "visits": s0["V"], "records": s0["records"],
-                      "region_misses": s0["rmiss"]},
+                      "region_misses": s0["rmiss"],
+                      "exchange_bytes_per_batch": s0["xbytes"] / max(1, s0["batches"])},
         }
         print(json.dumps(line), flush=True)
 

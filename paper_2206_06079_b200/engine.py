@@ -53,6 +53,7 @@ class BatchStats:
     marked_voxels: int = 0
     new_regions: int = 0
     replays: int = 0
+    exchange_bytes: int = 0  # region-sharded maps: bytes sent between ranks, all ranks
 
     @property
     def rays_per_second(self) -> float:

@@ -194,15 +194,23 @@ def submit_batch_sharded(smap: ShardedVoxelMap, records, group=None) -> BatchSta
     req_in = torch.cat(exchange_all_to_all([wire(t) for t in sends], group)).to(dev)
     smap.prepare(req_in, exchange_all_gather(wire(marks), group).to(dev))
     smap.walk()
-    items = torch.cat(exchange_all_to_all([wire(t) for t in smap.export()], group)).to(dev)
+    exported = smap.export()
+    items = torch.cat(exchange_all_to_all([wire(t) for t in exported], group)).to(dev)
     smap.import_(items)
     st = smap.finish()
+    # bytes this rank sent to other ranks (requests, sample-voxel marks to
+    # every peer, counts / records to their owners)
+    me = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    sent = sum(int(t.numel() * t.element_size()) for r, t in enumerate(sends) if r != me)
+    sent += int(marks.numel() * marks.element_size()) * (world - 1)
+    sent += sum(int(t.numel() * t.element_size()) for r, t in enumerate(exported) if r != me)
     v = torch.tensor([st.rays_in, st.rays_processed, st.segments, st.voxel_visits,
-                      st.region_misses, st.records], dtype=torch.int64,
+                      st.region_misses, st.records, sent], dtype=torch.int64,
                      device="cpu" if host else dev)
     dist.all_reduce(v, group=group)
     (st.rays_in, st.rays_processed, st.segments, st.voxel_visits, st.region_misses,
-     st.records) = [int(x) for x in v.cpu()]
+     st.records, st.exchange_bytes) = [int(x) for x in v.cpu()]
     return st
 
 
