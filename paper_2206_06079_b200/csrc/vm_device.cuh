@@ -97,6 +97,8 @@ struct DevMap {
     unsigned long long *stats;
     int *go;                             // batch guard (0 = skip, replay later)
     int walk_det_launched;               // k_walk_det runs before k_walk (deterministic occupancy)
+    int ray_order;                       // NDT walks: k_discover buckets rays by step count and
+                                         // the walk takes them through perm, longest first
     // region sharding (vm_shard_*): this map owns regions with owner(key) == shard_rank
     int shard_rank, shard_world;
     long long ray_lo;                    // first ray of this map's slice of the batch

@@ -281,6 +281,17 @@ __global__ void __launch_bounds__(DISC_BT, DISC_MINB) k_discover(const __grid_co
                 ok = false;
             }
         }
+        if (m.ray_order && blockIdx.y == 0) {
+            // the ray's voxel steps (Manhattan cell distance of the clipped
+            // ray): its bucket in the walk's longest-first order
+            unsigned steps = 0;
+            if (ok)
+                for (int a = 0; a < 3; ++a)
+                    steps += (unsigned)abs((int)floor(r.e[a] / m.vox) - (int)floor(r.o[a] / m.vox));
+            const int bk = seg_bucket(steps);
+            atomicAdd(shist + bk, 1u);
+            m.seg_bk[i] = (unsigned char)bk;
+        }
     }
     // one thread per (ray, segment): blockIdx.y is the segment index
     const int s = blockIdx.y;
@@ -392,7 +403,7 @@ __global__ void __launch_bounds__(DISC_BT, DISC_MINB) k_discover(const __grid_co
     if (threadIdx.x == 0) {
         if (nrec) rec_base = atomicAdd(m.stats + S_RECORDS, (unsigned long long)nrec);
     }
-    if (emit)
+    if (emit || m.ray_order)
         for (int i = threadIdx.x; i < SEG_BUCKETS; i += blockDim.x)
             if (shist[i]) atomicAdd(m.seg_hist + i, shist[i]);
     __syncthreads();
@@ -506,11 +517,14 @@ __global__ void k_seg_scan(const __grid_constant__ DevMap m) {
     }
 }
 
-__global__ void __launch_bounds__(BLOCK) k_seg_scatter(const __grid_constant__ DevMap m) {
+// count >= 0: order `count` rays (NDT walks) instead of the batch's segments
+__global__ void __launch_bounds__(BLOCK) k_seg_scatter(const __grid_constant__ DevMap m,
+                                                       long long count = -1) {
     __shared__ unsigned cnt[SEG_BUCKETS], base[SEG_BUCKETS];
     if (!read_go(m)) return;
     const unsigned long long n =
-        min(*((volatile unsigned long long *)(m.stats + S_SEGDESC)), m.seg_cap);
+        count >= 0 ? (unsigned long long)count
+                   : min(*((volatile unsigned long long *)(m.stats + S_SEGDESC)), m.seg_cap);
     for (int i = threadIdx.x; i < SEG_BUCKETS; i += blockDim.x) cnt[i] = 0u;
     __syncthreads();
     const unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -703,6 +717,7 @@ __global__ void __launch_bounds__(BLOCK, NDT_MINB) k_walk_ndt(const __grid_const
     v.visits = v.rmiss = v.retries = 0;
     long long i = first + threadIdx.x;
     if (i < n) {
+        if (m.ray_order) i = m.perm[i];  // longest rays first: a warp's lanes finish together
         Ray r;
         src.load(i, r.o, r.e, r.has, r.inten);
         if (prep_ray(m, r, true)) {

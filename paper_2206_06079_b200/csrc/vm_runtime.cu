@@ -115,6 +115,7 @@ struct vm_map {
     size_t ring_bytes = 0;
     cudaEvent_t ev_ring[RING] = {}, ev_ring_up[RING] = {};
     long long rec_floor_override = 0;
+    int no_ray_order = 0;  // VOXMAP_B200_NO_RAY_ORDER: NDT walk in input order (A/B runs)
     int num_sms = 148;
     unsigned long long *d_stats = nullptr;
     int *d_go = nullptr;
@@ -553,6 +554,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     if (emit && (rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * maxseg + 1))) return rc;
     if (emit && (rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
     if (emit && (rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
+    // NDT walks take their rays longest first (k_discover buckets, k_seg_scatter orders)
+    const bool ray_order = ndt && !m->no_ray_order;
+    if (ray_order && (rc = ensure_buf(&m->d_perm, &m->perm_cap, (size_t)n + 1))) return rc;
+    if (ray_order && (rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, (size_t)n + 1))) return rc;
     // occupancy / decay records key on the index in the batch's sample-voxel list
     const bool key_mi = occ_det && m->shard_world == 1;
     if (key_mi) {
@@ -579,6 +584,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         m->epoch += 1;
         DevMap dm = make_dm(m);
         dm.order_bits = order_bits;
+        dm.ray_order = ray_order ? 1 : 0;
         if (key_mi) {
             dm.key_mi = 1;
             dm.marked = m->d_smarked;
@@ -639,6 +645,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             k_seg_scan<<<1, SEG_BUCKETS, 0, m->stream>>>(dm);
             k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, m->stream>>>(dm);
             m->launches += 3;
+        } else if (ray_order) {
+            k_seg_scan<<<1, SEG_BUCKETS, 0, m->stream>>>(dm);
+            k_seg_scatter<<<(unsigned)((n + BLOCK - 1) / BLOCK), BLOCK, 0, m->stream>>>(dm, n);
+            m->launches += 2;
         }
         CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, m->stream));
@@ -1177,6 +1187,7 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) m->num_sms = prop.multiProcessorCount;
     }
     if (const char *rc_env = std::getenv("VOXMAP_B200_TEST_REC_CAP")) m->rec_floor_override = std::atoll(rc_env);
+    if (std::getenv("VOXMAP_B200_NO_RAY_ORDER")) m->no_ray_order = 1;
     if ((rc = grow_pool(m, std::max<long long>(64, initial_regions)))) return cleanup(rc);
     *out = m;
     return VM_OK;
