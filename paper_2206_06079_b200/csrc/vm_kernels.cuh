@@ -887,11 +887,11 @@ __global__ void __launch_bounds__(BLOCK) k_walk_tsdf(const __grid_constant__ Dev
 // (reference.py:86-93).  One block per touched region.
 // Resolve region `slot`, voxels [v0, v1): f_miss^k per counted voxel.
 #ifndef RES_U
-#define RES_U 4     // scratch quads in flight per thread
+#define RES_U 2     // scratch quads in flight per thread
 #endif
 #ifndef RES_MINB
-#define RES_MINB 4  // k_resolve resident blocks per SM: 4 x 4 quads in flight beat
-                    // 2 x 8 (C2 resolve 11.6 -> 10.6 ms per step)
+#define RES_MINB 8  // k_resolve resident blocks per SM: 8 x 2 quads in flight beat
+                    // 4 x 4 and 2 x 8 (C2 resolve 10.0 / 10.5 / 11.6 ms per step)
 #endif
 
 template <bool NDT, bool TM>
