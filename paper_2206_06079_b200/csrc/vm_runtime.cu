@@ -1467,9 +1467,53 @@ int vm_integrate_many(vm_map *m, const vm_rays *rays, int32_t nbatches, int32_t 
             pipelined = false;
     }
     if (!pipelined) {
+        // one vm_integrate per batch; host OHMB1 batches are prefetched: batch
+        // b+1 is copied on copy_stream into a ring buffer while batch b computes
+        bool prefetch = nbatches > 1;
+        long long nmax = 0;
         for (int b = 0; b < nbatches; ++b) {
-            const int rc = vm_integrate(m, rays + b, mode, exec, out + b);
-            if (rc) return rc;
+            if (rays[b].count > 0 && (rays[b].format != VM_RAYS_OHMB1 || rays[b].on_device ||
+                                      !rays[b].records))
+                prefetch = false;
+            nmax = std::max<long long>(nmax, rays[b].count);
+        }
+        if (!prefetch) {
+            for (int b = 0; b < nbatches; ++b) {
+                const int rc = vm_integrate(m, rays + b, mode, exec, out + b);
+                if (rc) return rc;
+            }
+            return VM_OK;
+        }
+        CK(cudaSetDevice(m->device));
+        if ((size_t)nmax * 40 > m->ring_bytes) {
+            for (int r = 0; r < vm_map::RING; ++r) {
+                cudaFree(m->d_ring[r]);
+                m->d_ring[r] = nullptr;
+                CK(cudaMalloc((void **)&m->d_ring[r], (size_t)nmax * 40));
+                if (!m->ev_ring[r]) CK(cudaEventCreateWithFlags(&m->ev_ring[r], cudaEventDisableTiming));
+                if (!m->ev_ring_up[r])
+                    CK(cudaEventCreateWithFlags(&m->ev_ring_up[r], cudaEventDisableTiming));
+            }
+            m->ring_bytes = (size_t)nmax * 40;
+        }
+        auto upload = [&](int b) -> int {
+            const int r = b % vm_map::RING;
+            if (rays[b].count > 0)
+                CK(cudaMemcpyAsync(m->d_ring[r], rays[b].records, (size_t)rays[b].count * 40,
+                                   cudaMemcpyHostToDevice, m->copy_stream));
+            CK(cudaEventRecord(m->ev_ring_up[r], m->copy_stream));
+            return VM_OK;
+        };
+        int rc = upload(0);
+        if (rc) return rc;
+        for (int b = 0; b < nbatches; ++b) {
+            CK(cudaStreamWaitEvent(m->stream, m->ev_ring_up[b % vm_map::RING], 0));
+            // the slot of batch b+1 was last used by batch b+1-RING, which is done
+            if (b + 1 < nbatches && (rc = upload(b + 1))) return rc;
+            vm_rays r = rays[b];
+            r.records = m->d_ring[b % vm_map::RING];
+            r.on_device = 1;
+            if ((rc = vm_integrate(m, &r, mode, exec, out + b))) return rc;
         }
         return VM_OK;
     }

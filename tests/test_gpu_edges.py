@@ -284,3 +284,26 @@ def test_c2_prefix_cas_order_free_layers_exact():
         worst = max(worst, float(d.max(initial=0.0)))
     assert worst <= 5.5  # clamp_max - clamp_min
     print(f"CAS vs sequential on hit voxels: {mixed} differ, max {worst:.4f} log-odds")
+
+
+@pytest.mark.slow
+def test_submit_batches_ndt_prefetched_matches_per_batch():
+    """Non-pipelined modes run one vm_integrate per batch inside
+    vm_integrate_many, with the next batch's host records prefetched into a
+    device ring while the current one computes: same stats, same map."""
+    from paper_2206_06079_b200 import submit_batches
+    data = scans.os64_tunnel_scans(4)
+    names = MODE_LAYERS["ndt-om"]
+    a = VoxelMap(MapConfig(), names)
+    b = VoxelMap(MapConfig(), names)
+    sa = submit_batches(a, data, "ndt-om")
+    sb = [submit_batch(b, x, "ndt-om") for x in data]
+    for x, y in zip(sa, sb):
+        assert (x.rays_processed, x.segments, x.voxel_visits, x.region_misses) == \
+            (y.rays_processed, y.segments, y.voxel_visits, y.region_misses)
+    assert set(a.regions) == set(b.regions)
+    for rk, region in a.regions.items():
+        for name in names:
+            u = region.buffers[name].astype(np.float64)
+            v = b.regions[rk].buffers[name].astype(np.float64)
+            assert np.max(np.abs(u - v), initial=0.0) <= (1e-4 if name != "mean" else 0), (rk, name)
