@@ -1196,8 +1196,12 @@ __global__ void __launch_bounds__(BLOCK) k_fold_occ_big(const __grid_constant__ 
 //    the remaining misses use g = 1);
 //  * phase 1: NDT phase 2 (reference.py:107-150): the voxel's samples in ray
 //    order, f64 Welford mean + Givens sqrt-covariance.
+#ifndef FOLD_NDT_MINB
+#define FOLD_NDT_MINB 1
+#endif
+
 template <bool TM, class Src>
-__global__ void __launch_bounds__(BLOCK) k_fold_ndt(const __grid_constant__ DevMap m, Src src,
+__global__ void __launch_bounds__(BLOCK, FOLD_NDT_MINB) k_fold_ndt(const __grid_constant__ DevMap m, Src src,
                                                     const unsigned long long *keys,
                                                     const unsigned *vals, long long R) {
     if (!read_go(m)) return;
