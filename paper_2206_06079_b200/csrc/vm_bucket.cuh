@@ -25,6 +25,10 @@
 
 namespace vm {
 
+#ifndef BK_FOLD_MINB
+#define BK_FOLD_MINB 1  // k_bk_fold resident blocks per SM (register budget)
+#endif
+
 constexpr int BK_SERIAL = 16;
 constexpr int BK_SMEM = 4096;
 
@@ -132,7 +136,7 @@ __device__ __forceinline__ unsigned marked_vid(const DevMap &m, unsigned long lo
 
 // One thread per sample voxel: small buckets sorted and folded in place.
 template <class Src>
-__global__ void __launch_bounds__(BLOCK) k_bk_fold(const __grid_constant__ DevMap m, Src src,
+__global__ void __launch_bounds__(BLOCK, BK_FOLD_MINB) k_bk_fold(const __grid_constant__ DevMap m, Src src,
                                                    BucketState b) {
     unsigned long long R, M;
     if (!bk_live(m, R, M)) return;
