@@ -20,7 +20,7 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_build" / "libvm_oracle.so"
 
-MODES = ("occupancy", "decay", "ndt-om", "ndt-tm", "tsdf")
+MODES = ("occupancy", "decay", "ndt-om", "ndt-tm", "tsdf", "counts")
 
 # layers.py:22-31  (name -> (id, dtype, components))
 LAYERS = {
@@ -42,6 +42,8 @@ MODE_LAYERS = {
     "ndt-tm": ("occupancy", "mean", "mean_count", "cov_sqrt", "hit_count", "miss_count",
                "intensity"),
     "tsdf": ("tsdf",),
+    # checker aid: per-voxel hit / miss visits of the occupancy walk
+    "counts": ("hit_count", "miss_count"),
 }
 STAT_NAMES = ("rays_in", "rays_processed", "segments", "voxel_visits", "cas_retries",
               "cas_failures", "region_misses", "regions_touched")

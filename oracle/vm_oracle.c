@@ -910,6 +910,19 @@ int orc_integrate(orc_map *m, const double *origins, const double *ends,
         free(smp);
     } else if (mode == ORC_MODE_TSDF) {
         for (int64_t k = 0; k < ns; k++) visits += integrate_tsdf_ray(m, &w, &segs[k]);
+    } else if (mode == ORC_MODE_COUNTS) {
+        /* the visits integrate_occupancy_segment would make, counted per voxel:
+         * the bounds of the CAS order envelope (tests/test_gpu_parity.py) */
+        for (int64_t k = 0; k < ns; k++) {
+            int64_t nv = walk(&w, segs[k].o, segs[k].e, cfg->voxel_size);
+            for (int64_t i = 0; i < nv; i++) {
+                int64_t li;
+                orc_region *r = region_and_local(m, &w.c[3 * i], &li);
+                if (segs[k].has && i == nv - 1) ((uint32_t *)r->buf[L_HIT])[li] += 1;
+                else ((uint32_t *)r->buf[L_MISS])[li] += 1;
+            }
+            visits += nv;
+        }
     } else {
         walkbuf_free(&w);
         free(segs);

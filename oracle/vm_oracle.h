@@ -50,7 +50,10 @@ typedef struct {
 } orc_config;
 
 enum { ORC_MODE_OCCUPANCY = 0, ORC_MODE_DECAY = 1, ORC_MODE_NDT_OM = 2,
-       ORC_MODE_NDT_TM = 3, ORC_MODE_TSDF = 4 };
+       ORC_MODE_NDT_TM = 3, ORC_MODE_TSDF = 4,
+       /* checker aid, not a reference mode: per-voxel hit / miss visit counts
+        * of the occupancy walk into the hit_count / miss_count layers */
+       ORC_MODE_COUNTS = 5 };
 
 /* stats layout: rays_in, rays_processed, segments, voxel_visits,
  * cas_retries, cas_failures, region_misses, regions_touched */

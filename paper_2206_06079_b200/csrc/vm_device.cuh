@@ -19,7 +19,8 @@ enum Layer {
     L_SCRATCH = 0,  // private: per-voxel miss counter (deterministic resolve)
     L_OCC = 1, L_MEAN = 2, L_COUNT = 3, L_COV = 4, L_HIT = 5, L_MISS = 6,
     L_INTENS = 7, L_DHITS = 8, L_DDIST = 9, L_TSDF = 10,
-    NUM_LAYERS = 11
+    L_NIDX = 11,    // private (NDT maps): per-voxel bucket index of the batch's ordered records
+    NUM_LAYERS = 12
 };
 
 enum Mode { M_OCC = 0, M_DECAY = 1, M_NDT_OM = 2, M_NDT_TM = 3, M_TSDF = 4 };

@@ -149,6 +149,34 @@ __device__ __forceinline__ T *layer_at(const DevMap &m, int layer, int slot) {
     return m.lptr[layer] ? reinterpret_cast<T *>(m.lptr[layer][slot]) : nullptr;
 }
 
+// --------------------------------------------------------------- NDT record emission
+
+constexpr unsigned NIDX_FLAG = 0x80000000u;  // index-layer stamp (vm_ndt.cuh)
+
+// The bucket index of voxel (slot, li): the stamp in the index layer, or a
+// fresh one.  Lock-free: a lost race leaves an unused index (empty bucket,
+// marked (-1, -1)).  Returns 0xFFFFFFFF when the index list is full (the
+// batch then re-runs with room for every index, see bk_ndt_live).
+__device__ __forceinline__ unsigned ndt_index(const DevMap &m, int slot, int li) {
+    unsigned *w = layer_at<unsigned>(m, L_NIDX, slot) + li;
+    unsigned cur = *((volatile unsigned *)w);
+    if (cur & NIDX_FLAG) return cur & ~NIDX_FLAG;
+    const unsigned long long mi = atomicAdd(m.nmarked, 1ULL);
+    if (mi >= m.marked_cap || mi >= (unsigned long long)NIDX_FLAG) return 0xFFFFFFFFu;
+    const unsigned prev = atomicCAS(w, 0u, NIDX_FLAG | (unsigned)mi);
+    if (prev == 0u) {
+        m.marked[mi] = make_int2(slot, li);
+        return (unsigned)mi;
+    }
+    m.marked[mi] = make_int2(-1, -1);
+    return prev & ~NIDX_FLAG;
+}
+
+__device__ __forceinline__ unsigned long long ndt_key(unsigned mi, unsigned phase, unsigned oi) {
+    return ((unsigned long long)mi << 32) | ((unsigned long long)phase << 31) | oi;
+}
+
+
 // --------------------------------------------------------------- k_discover
 
 // Per-block direct-mapped cache region -> slot, keyed by coordinates relative
@@ -364,12 +392,11 @@ __global__ void __launch_bounds__(DISC_BT, DISC_MINB) k_discover(const __grid_co
                 if (rt.slot >= 0 && rt.slot < m.cap) {
                     int li = rt.li(m);
                     if (ndt) {
-                        unsigned long long vid = (unsigned long long)rt.slot * m.vpr + li;
-                        unsigned long long order =
-                            ((unsigned long long)(i * m.maxseg + s) << 1) | 1ULL;
+                        // NDT phase 2: the sample, bucketed by the voxel's index
+                        // (vm_ndt.cuh); phase 1 sorts before it
+                        const unsigned mi = ndt_index(m, rt.slot, li);
                         int k = atomicAdd(&nrec, 1);
-                        // phase bit 1: after every phase-1 record of the voxel
-                        srec[k] = (vid << (m.order_bits + 1)) | (1ULL << m.order_bits) | order;
+                        srec[k] = ndt_key(mi, 1u, (unsigned)(i * m.maxseg + s));
                     } else {
                         // stamp the sample voxel: the walk turns its visits into records
                         unsigned *w = layer_at<unsigned>(m, L_SCRATCH, rt.slot) + li;
@@ -633,10 +660,9 @@ struct NdtVisitor {
         double gw = gaussian_weight(mu, c6, m->sigma2, so, v, t0, t1);
         float d32 = (float)(gw * m->miss_delta);
         if (DET) {
-            const unsigned long long vid = (unsigned long long)rt.slot * m->vpr + li;
             const unsigned val = (__float_as_uint(d32) & 0x7FFFFFFFu) |
                                  (gw >= m->miss_check ? 0x80000000u : 0u);
-            const unsigned long long key = (vid << (m->order_bits + 1)) | order;
+            const unsigned long long key = ndt_key(ndt_index(*m, rt.slot, li), 0u, order >> 1);
             const int k = atomicAdd(st.n, 1);
             if (k < NDT_STAGE) {
                 st.key[k] = key;
@@ -1185,184 +1211,6 @@ __global__ void __launch_bounds__(BLOCK) k_fold_occ_big(const __grid_constant__ 
             reinterpret_cast<unsigned *>(m.slab[L_SCRATCH])[vid] = 0u;
             m.bmask[vid / (unsigned)m.vpr] = 0u;
         }
-    }
-}
-
-// NDT in ray order, one thread per voxel run of the sorted records
-// (key = voxel | phase | ray order):
-//  * phase 0 (deterministic mode only): the phase-1 misses of a Gaussian
-//    voxel with their weights, including the transient reset and the TM miss
-//    count (reference.py:67-94; after a reset the voxel has < 3 samples, so
-//    the remaining misses use g = 1);
-//  * phase 1: NDT phase 2 (reference.py:107-150): the voxel's samples in ray
-//    order, f64 Welford mean + Givens sqrt-covariance.
-#ifndef FOLD_NDT_MINB
-#define FOLD_NDT_MINB 4  // 64 registers, 4 blocks per SM: C3 fold 5.8 -> 4.7 ms (3 blocks: 5.2)
-#endif
-
-template <bool TM, class Src>
-__global__ void __launch_bounds__(BLOCK, FOLD_NDT_MINB) k_fold_ndt(const __grid_constant__ DevMap m, Src src,
-                                                    const unsigned long long *keys,
-                                                    const unsigned *vals, long long R) {
-    if (!read_go(m)) return;
-    const unsigned long long omask = (1ULL << m.order_bits) - 1;
-    const int vshift = m.order_bits + 1;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
-         i += (long long)gridDim.x * blockDim.x) {
-        unsigned long long vid = keys[i] >> vshift;
-        if (i > 0 && (keys[i - 1] >> vshift) == vid) continue;
-        int slot = (int)(vid / (unsigned long long)m.vpr), li = (int)(vid % (unsigned long long)m.vpr);
-        int g[3];
-        slot_li_to_g(m, slot, li, g);
-        float *occ = layer_at<float>(m, L_OCC, slot);
-        unsigned *mb = layer_at<unsigned>(m, L_MEAN, slot);
-        unsigned *cb = layer_at<unsigned>(m, L_COUNT, slot);
-        float *cov = layer_at<float>(m, L_COV, slot);
-        float *ib = TM ? layer_at<float>(m, L_INTENS, slot) : nullptr;
-        unsigned *hb = TM ? layer_at<unsigned>(m, L_HIT, slot) : nullptr;
-        unsigned *missb = TM ? layer_at<unsigned>(m, L_MISS, slot) : nullptr;
-        float l = occ[li];
-        long long j = i;
-        // ---- phase-1 records (deterministic mode) ----
-        bool reset = false;
-        unsigned miss_add = 0;
-        for (; j < R && (keys[j] >> vshift) == vid && !((keys[j] >> m.order_bits) & 1ULL); ++j) {
-            const unsigned v = vals[j];
-            const float d = reset ? m.miss32 : -__uint_as_float(v & 0x7FFFFFFFu);
-            l = clamp_add(l, d, m.cmin, m.cmax);
-            if (TM && (reset || (v >> 31))) ++miss_add;
-            if (!reset && l < m.fthresh && cb[li] > 0) {
-                reset = true;
-                miss_add = 0;
-                cb[li] = 0;
-                mb[li] = 0;
-#pragma unroll
-                for (int k = 0; k < 6; ++k) cov[li * 6 + k] = 0.0f;
-                if (TM) {
-                    hb[li] = 0;
-                    missb[li] = 0;
-                    ib[li * 2] = 0.0f;
-                    ib[li * 2 + 1] = 0.0f;
-                }
-            }
-        }
-        if (TM && miss_add) missb[li] += miss_add;
-        if (j == i || (j < R && (keys[j] >> vshift) == vid)) {
-            // ---- phase-2 samples ----
-            // The reference folds them one by one (Welford mean + Givens rank-one
-            // update of L = S*sqrt(n), ndt.py:37-70): algebraically the scatter
-            // matrix M = n*S*S^T gains (n/(n+1)) d d^T per sample.  Here the
-            // batch is summed about a pivot and merged in one step, then S is
-            // the Cholesky factor of M / N (positive diagonal, like the Givens
-            // sweep): one serial pass of cheap accumulations instead of a chain
-            // of square roots and divisions per sample -- equal within the NDT
-            // tolerance (tests/test_gpu_parity.py: cov_sqrt 1e-5, mean 1 bucket).
-            const unsigned long long n0 = cb[li];
-            double mu0[3] = {0.0, 0.0, 0.0};
-            if (n0 > 0) {
-                double off[3];
-                unpack_mean(mb[li], off);
-                for (int a = 0; a < 3; ++a) mu0[a] = ((double)g[a] + off[a]) * m.vox;
-            }
-            double S0[6];
-            for (int k = 0; k < 6; ++k) S0[k] = cov[li * 6 + k];
-            double piv[3] = {mu0[0], mu0[1], mu0[2]};
-            double sum[3] = {0.0, 0.0, 0.0}, ss[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            unsigned long long kb = 0;
-            unsigned long long nsamp = n0;  // intensity Welford count
-            const long long h0 = j;
-            for (; j < R && (keys[j] >> vshift) == vid; ++j) {
-                long long ray = (long long)(((keys[j] & omask) >> 1) / (unsigned long long)m.maxseg);
-                double e[3];
-                float it;
-                src.load_end(ray, e, it);
-                l = clamp_add(l, m.hit32, m.cmin, m.cmax);
-                if (TM) {
-                    // ndt.update_intensity (ndt.py:98-106), stored f32 each sample
-                    double val = it, imean = ib[li * 2], m2 = ib[li * 2 + 1];
-                    double nn = (double)(nsamp + 1);
-                    double d = val - imean;
-                    double mnew = imean + d / nn;
-                    double m2new = m2 + d * (val - mnew);
-                    ib[li * 2] = (float)mnew;
-                    ib[li * 2 + 1] = (float)m2new;
-                }
-                ++nsamp;
-                if (kb == 0 && n0 == 0)
-                    for (int a = 0; a < 3; ++a) piv[a] = e[a];
-                const double d0 = e[0] - piv[0], d1 = e[1] - piv[1], d2 = e[2] - piv[2];
-                sum[0] += d0;
-                sum[1] += d1;
-                sum[2] += d2;
-                ss[0] += d0 * d0;
-                ss[1] += d1 * d0;
-                ss[2] += d1 * d1;
-                ss[3] += d2 * d0;
-                ss[4] += d2 * d1;
-                ss[5] += d2 * d2;
-                ++kb;
-            }
-            // merge (n0, mu0, M0) with the batch (kb, mean_b, M_b)
-            const double kd = (double)kb, N = (double)(n0 + kb);
-            double mb_[3], Mb[6];
-            for (int a = 0; a < 3; ++a) mb_[a] = sum[a] / kd;
-            Mb[0] = ss[0] - sum[0] * mb_[0];
-            Mb[1] = ss[1] - sum[1] * mb_[0];
-            Mb[2] = ss[2] - sum[1] * mb_[1];
-            Mb[3] = ss[3] - sum[2] * mb_[0];
-            Mb[4] = ss[4] - sum[2] * mb_[1];
-            Mb[5] = ss[5] - sum[2] * mb_[2];
-            double mu[3], M[6];
-            if (n0 == 0) {
-                for (int a = 0; a < 3; ++a) mu[a] = piv[a] + mb_[a];
-                for (int k = 0; k < 6; ++k) M[k] = Mb[k];
-            } else {
-                // M0 = n0 * S0 S0^T (lower-triangular S0)
-                const double n0d = (double)n0;
-                const double c00 = S0[0] * S0[0], c10 = S0[1] * S0[0], c11 = S0[1] * S0[1] + S0[2] * S0[2];
-                const double c20 = S0[3] * S0[0], c21 = S0[3] * S0[1] + S0[4] * S0[2];
-                const double c22 = S0[3] * S0[3] + S0[4] * S0[4] + S0[5] * S0[5];
-                const double dl[3] = {mb_[0], mb_[1], mb_[2]};  // batch mean - mu0 (pivot = mu0)
-                const double w = n0d * kd / N;
-                for (int a = 0; a < 3; ++a) mu[a] = mu0[a] + dl[a] * (kd / N);
-                M[0] = n0d * c00 + Mb[0] + w * dl[0] * dl[0];
-                M[1] = n0d * c10 + Mb[1] + w * dl[1] * dl[0];
-                M[2] = n0d * c11 + Mb[2] + w * dl[1] * dl[1];
-                M[3] = n0d * c20 + Mb[3] + w * dl[2] * dl[0];
-                M[4] = n0d * c21 + Mb[4] + w * dl[2] * dl[1];
-                M[5] = n0d * c22 + Mb[5] + w * dl[2] * dl[2];
-            }
-            // S = chol(M / N), lower, positive diagonal.  Pivots at rounding
-            // level (collinear / coplanar samples) are zero, as the Givens sweep
-            // leaves them (r == 0): below 1e-12 of the trace the pivot is noise.
-            double S[6];
-            {
-                const double a00 = M[0] / N, c10 = M[1] / N, c11 = M[2] / N;
-                const double c20 = M[3] / N, c21 = M[4] / N, c22 = M[5] / N;
-                const double eps = 1e-12 * (a00 + c11 + c22);
-                S[0] = a00 > eps ? sqrt(a00) : 0.0;
-                S[1] = S[0] > 0.0 ? c10 / S[0] : 0.0;
-                S[3] = S[0] > 0.0 ? c20 / S[0] : 0.0;
-                const double a11 = c11 - S[1] * S[1];
-                S[2] = a11 > eps ? sqrt(a11) : 0.0;
-                S[4] = S[2] > 0.0 ? (c21 - S[3] * S[1]) / S[2] : 0.0;
-                const double a22 = c22 - S[3] * S[3] - S[4] * S[4];
-                S[5] = a22 > eps ? sqrt(a22) : 0.0;
-            }
-            if (TM) hb[li] += (unsigned)(j - h0);
-            cb[li] = nsamp > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)nsamp;
-            double frac[3];
-            const double hi = 1.0 - 1.0 / 2048.0;
-            for (int a = 0; a < 3; ++a) {
-                double f = mu[a] / m.vox - (double)g[a];
-                if (f < 0.0) f = 0.0;
-                if (f > hi) f = hi;
-                frac[a] = f;
-            }
-            mb[li] = pack_mean(frac);
-            for (int k = 0; k < 6; ++k) cov[li * 6 + k] = (float)S[k];
-        }
-        occ[li] = l;
     }
 }
 

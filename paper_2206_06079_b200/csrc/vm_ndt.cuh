@@ -1,0 +1,505 @@
+// vm_ndt.cuh -- NDT phase 2 (and the deterministic NDT phase-1 records) as a
+// bucketed, in-order, per-sample fold: no global sort, no library call, no
+// host round trip.
+//
+// Records.  Every voxel that needs ordered updates this batch gets a dense
+// index mi, stamped as NIDX_FLAG | mi into the voxel's word of the private
+// index layer (L_NIDX, zero between batches) by whoever reaches it first:
+//   * k_discover, for the sample voxel floor(end / vox) of every sample
+//     segment (reference.py:178-186): a phase-2 record (the hit);
+//   * the deterministic NDT walk, for a miss through a voxel that holds a
+//     Gaussian (count >= 3 at the start of the batch): a phase-1 record
+//     carrying |fl32(g * miss_delta)| and (g >= miss-check threshold)
+//     (_kernels.pyx:602-648 / reference.py:67-94).
+// A record is key = mi << 32 | sk, value (u32), with the sort key
+// sk = phase << 31 | (ray * maxseg + seg): phase-1 records of a voxel come
+// first, in ray order, then its samples in ray order -- the reference runs
+// phase 1 over the whole batch before phase 2 (engine.py:266-302).
+//
+// Buckets.  count per mi -> allocate each bucket's slice with one atomic per
+// warp (buckets need not be contiguous in mi order, so no scan) -> order the
+// buckets by size, largest first (a 256-bin counting sort), so the lanes of a
+// fold warp get buckets of equal length -> scatter (sk << 32 | value) into
+// the slices -> sort each slice in place (thread insertion sort <= 16, block
+// bitonic sort in shared memory <= 2048, bitmap rank sort above) -> fold.
+//
+// The fold replays the reference exactly, one voxel per thread: phase-1
+// records with the transient reset (after a reset the voxel has < 3 samples,
+// so g = 1), then per sample: clamped hit, [TM] Welford intensity stored f32,
+// and ndt.update_gaussian -- Welford mean and the Givens rank-one update
+// cholupdate3 with CPython's math.hypot (ndt.py:37-70, reference.py:107-150).
+// Compiled with -fmad=false, every operation rounds like numpy / CPython.
+#pragma once
+
+#include <cfloat>
+
+#include "vm_kernels.cuh"
+
+namespace vm {
+
+constexpr int NBK_SERIAL = 16;    // thread insertion sort in place
+constexpr int NBK_SMEM = 2048;    // block bitonic sort (16 KiB of shared memory)
+constexpr int NBK_BINS = 256;     // size classes of the largest-first bucket order
+
+// ------------------------------------------------------------ exact fp64 helpers
+
+// CPython 3.12 math.hypot(a, b): vector_norm of Modules/mathmodule.c (the
+// oracle's orc_py_hypot, pinned to CPython's own results in tests/golden).
+__device__ __forceinline__ double py_vector_norm2(double x0, double x1, double mx) {
+    double outer = 1.0;
+    if (isinf(mx)) return mx;
+    if (mx == 0.0) return mx;
+    int max_e;
+    frexp(mx, &max_e);
+    if (max_e < -1023) {
+        // subnormal max: rescale once into the normal range
+        outer = DBL_MIN;
+        x0 /= DBL_MIN;
+        x1 /= DBL_MIN;
+        mx /= DBL_MIN;
+        frexp(mx, &max_e);
+    }
+    const double scale = ldexp(1.0, -max_e);
+    double csum = 1.0, frac1 = 0.0, frac2 = 0.0;
+    const double v[2] = {x0, x1};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double x = v[i] * scale;
+        const double hi = x * x, lo = fma(x, x, -hi);
+        const double s = csum + hi;
+        const double sl = (csum - s) + hi;
+        csum = s;
+        frac1 += lo;
+        frac2 += sl;
+    }
+    double h = sqrt(csum - 1.0 + (frac1 + frac2));
+    {
+        const double hi = -h * h, lo = fma(-h, h, -hi);
+        const double s = csum + hi;
+        const double sl = (csum - s) + hi;
+        csum = s;
+        frac1 += lo;
+        frac2 += sl;
+    }
+    const double x = csum - 1.0 + (frac1 + frac2);
+    h += x / (2.0 * h);
+    return outer == 1.0 ? h / scale : outer * (h / scale);
+}
+
+__device__ __forceinline__ double py_hypot(double a, double b) {
+    if (isnan(a) || isnan(b)) return __longlong_as_double(0x7ff8000000000000LL);
+    const double x0 = fabs(a), x1 = fabs(b);
+    double mx = 0.0;
+    if (x0 > mx) mx = x0;
+    if (x1 > mx) mx = x1;
+    return py_vector_norm2(x0, x1, mx);
+}
+
+// ndt.cholupdate3 (ndt.py:37-52) on the lower triangle
+// L = (l00, l10, l11, l20, l21, l22), x updated in place.
+__device__ __forceinline__ void givens_k(double &lkk, double &xk, double *li1, double *xi1,
+                                         double *li2, double *xi2) {
+    const double r = py_hypot(lkk, xk);
+    if (r == 0.0) return;
+    const double c = lkk / r, s = xk / r;
+    lkk = r;
+    if (li1) {
+        const double lik = *li1;
+        *li1 = c * lik + s * *xi1;
+        *xi1 = c * *xi1 - s * lik;
+    }
+    if (li2) {
+        const double lik = *li2;
+        *li2 = c * lik + s * *xi2;
+        *xi2 = c * *xi2 - s * lik;
+    }
+}
+
+// ndt.update_gaussian (ndt.py:55-70): fold one sample into (n, mu, S).
+__device__ __forceinline__ void ndt_update(unsigned long long &n, double mu[3], double S[6],
+                                           const double x[3]) {
+    if (n == 0) {
+        n = 1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) mu[a] = x[a];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) S[k] = 0.0;
+        return;
+    }
+    const unsigned long long nn = n + 1;
+    const double dn = (double)n, dnn = (double)nn;
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) d[a] = x[a] - mu[a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) mu[a] = mu[a] + d[a] / dnn;
+    const double sq = sqrt(dn);
+    double L[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) L[k] = S[k] * sq;
+    const double f = sqrt(dn / dnn);
+    double xx[3] = {d[0] * f, d[1] * f, d[2] * f};
+    givens_k(L[0], xx[0], &L[1], &xx[1], &L[3], &xx[2]);
+    givens_k(L[2], xx[1], &L[4], &xx[2], nullptr, nullptr);
+    givens_k(L[5], xx[2], nullptr, nullptr, nullptr, nullptr);
+    const double sn = sqrt(dnn);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) S[k] = L[k] / sn;
+    n = nn;
+}
+
+// ------------------------------------------------------------ buckets
+
+struct NdtBuckets {
+    unsigned *cnt;                   // [M] records per bucket (zero between batches)
+    unsigned *off;                   // [M] slice start (bumped by the scatter)
+    unsigned *perm;                  // [M] buckets, largest first
+    unsigned *hist;                  // [NBK_BINS] bucket sizes (zeroed by k_nbk_order)
+    unsigned *cursor;                // [NBK_BINS] + [1] live buckets + [1] slice cursor
+    unsigned long long *val;         // [R] (sk << 32 | value), bucketed
+    unsigned long long *tmp;         // [R] rank-sort output
+    int *big;                        // buckets sorted by k_nbk_sort_big
+    unsigned long long *nbig;
+    unsigned *bits;                  // rank sort: per block 2 * bwords words
+    unsigned long long bwords;       // words of one (phase, order) bitmap
+    unsigned long long span;         // n * maxseg (orders per phase)
+};
+
+// The batch's records and bucket count, on the device; false when there is
+// nothing to do (guard refusal, or an overflow the host re-runs).
+__device__ __forceinline__ bool bk_ndt_live(const DevMap &m, unsigned long long &R,
+                                            unsigned long long &M) {
+    if (!read_go(m)) return false;
+    R = *((volatile unsigned long long *)(m.stats + S_RECORDS));
+    M = *((volatile unsigned long long *)m.nmarked);
+    if (R > m.rec_cap || M > m.marked_cap) return false;
+    return true;
+}
+
+__global__ void __launch_bounds__(BLOCK) k_nbk_count(const __grid_constant__ DevMap m, NdtBuckets b) {
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned mi = (unsigned)(m.rec[i] >> 32);
+        if (mi < M) atomicAdd(b.cnt + mi, 1u);
+    }
+}
+
+// slice allocation (one atomic per warp) + size histogram
+__global__ void __launch_bounds__(BLOCK) k_nbk_alloc(const __grid_constant__ DevMap m, NdtBuckets b) {
+    __shared__ unsigned h[NBK_BINS];
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x) h[i] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < M; base += stride) {
+        const unsigned long long mi = base + threadIdx.x;
+        const unsigned c = mi < M ? b.cnt[mi] : 0u;
+        unsigned incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned wb = 0;
+        if (lane == 31 && tot) wb = atomicAdd(b.cursor + NBK_BINS + 1, tot);
+        wb = __shfl_sync(0xffffffffu, wb, 31);
+        if (c) {
+            b.off[mi] = wb + incl - c;
+            atomicAdd(h + min(c, (unsigned)NBK_BINS - 1u), 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x)
+        if (h[i]) atomicAdd(b.hist + i, h[i]);
+}
+
+// size classes -> cursors, largest first; total live buckets
+__global__ void k_nbk_order(const __grid_constant__ DevMap m, NdtBuckets b) {
+    __shared__ unsigned h[NBK_BINS];
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x) {
+        h[i] = b.hist[i];
+        b.hist[i] = 0u;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    unsigned run = 0;
+    for (int i = NBK_BINS - 1; i >= 1; --i) {
+        b.cursor[i] = run;
+        run += h[i];
+    }
+    b.cursor[NBK_BINS] = run;
+}
+
+__global__ void __launch_bounds__(BLOCK) k_nbk_perm(const __grid_constant__ DevMap m, NdtBuckets b) {
+    __shared__ unsigned cnt[NBK_BINS], base[NBK_BINS];
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (unsigned long long b0 = (unsigned long long)blockIdx.x * blockDim.x; b0 < M;
+         b0 += (unsigned long long)gridDim.x * blockDim.x) {
+        for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x) cnt[i] = 0u;
+        __syncthreads();
+        const unsigned long long mi = b0 + threadIdx.x;
+        const unsigned c = mi < M ? b.cnt[mi] : 0u;
+        const int bin = c ? (int)min(c, (unsigned)NBK_BINS - 1u) : -1;
+        unsigned r = 0;
+        if (bin >= 0) r = atomicAdd(cnt + bin, 1u);
+        __syncthreads();
+        for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x)
+            if (cnt[i]) base[i] = atomicAdd(b.cursor + i, cnt[i]);
+        __syncthreads();
+        if (bin >= 0) {
+            b.perm[base[bin] + r] = (unsigned)mi;
+            if (c > (unsigned)NBK_SERIAL) b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK) k_nbk_scatter(const __grid_constant__ DevMap m, NdtBuckets b) {
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = m.rec[i];
+        const unsigned mi = (unsigned)(k >> 32);
+        if (mi >= M) continue;
+        const unsigned pos = atomicAdd(b.off + mi, 1u);
+        b.val[pos] = (k << 32) | (unsigned long long)m.recval[i];
+    }
+}
+
+// slice [s, s + c) of bucket mi after the scatter bumped its offset
+__device__ __forceinline__ unsigned nbk_start(const NdtBuckets &b, unsigned mi, unsigned &c) {
+    c = b.cnt[mi];
+    return b.off[mi] - c;
+}
+
+// Buckets above NBK_SERIAL, one block each: bitonic sort in shared memory,
+// or, above NBK_SMEM, a rank sort over the (phase, order) bitmap.
+__global__ void __launch_bounds__(BLOCK) k_nbk_sort_big(const __grid_constant__ DevMap m, NdtBuckets b) {
+    __shared__ unsigned long long sv[NBK_SMEM];
+    __shared__ unsigned wsum[BLOCK];
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    const unsigned long long nb = *((volatile unsigned long long *)b.nbig);
+    unsigned *pres = b.bits + (size_t)blockIdx.x * 2 * b.bwords;
+    unsigned *pref = pres + b.bwords;
+    for (unsigned long long w = blockIdx.x; w < nb; w += gridDim.x) {
+        const unsigned mi = (unsigned)b.big[w];
+        unsigned c;
+        const unsigned s = nbk_start(b, mi, c);
+        if (c <= (unsigned)NBK_SMEM) {
+            unsigned P = 32;
+            while (P < c) P <<= 1;
+            for (unsigned i = threadIdx.x; i < P; i += blockDim.x) sv[i] = i < c ? b.val[s + i] : ~0ULL;
+            __syncthreads();
+            for (unsigned k = 2; k <= P; k <<= 1) {
+                for (unsigned j = k >> 1; j > 0; j >>= 1) {
+                    for (unsigned i = threadIdx.x; i < P; i += blockDim.x) {
+                        const unsigned p = i ^ j;
+                        if (p > i) {
+                            const unsigned long long x = sv[i], y = sv[p];
+                            if ((x > y) == ((i & k) == 0)) {
+                                sv[i] = y;
+                                sv[p] = x;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (unsigned i = threadIdx.x; i < c; i += blockDim.x) b.val[s + i] = sv[i];
+            __syncthreads();
+            continue;
+        }
+        // rank sort: sort keys are unique, so a key's rank is the number of
+        // set bits below its own in the (phase, order) presence bitmap
+        for (unsigned long long i = threadIdx.x; i < b.bwords; i += blockDim.x) pres[i] = 0u;
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < c; i += blockDim.x) {
+            const unsigned sk = (unsigned)(b.val[s + i] >> 32);
+            const unsigned long long bit = (unsigned long long)(sk >> 31) * b.span + (sk & 0x7FFFFFFFu);
+            atomicOr(pres + (bit >> 5), 1u << (bit & 31));
+        }
+        __syncthreads();
+        // block exclusive scan of the words' popcounts (contiguous chunk per thread)
+        const unsigned long long per = (b.bwords + blockDim.x - 1) / blockDim.x;
+        const unsigned long long w0 = per * threadIdx.x, w1 = min(b.bwords, w0 + per);
+        unsigned loc = 0;
+        for (unsigned long long i = w0; i < w1; ++i) loc += __popc(pres[i]);
+        wsum[threadIdx.x] = loc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned run = 0;
+            for (int t = 0; t < (int)blockDim.x; ++t) {
+                const unsigned v = wsum[t];
+                wsum[t] = run;
+                run += v;
+            }
+        }
+        __syncthreads();
+        unsigned run = wsum[threadIdx.x];
+        for (unsigned long long i = w0; i < w1; ++i) {
+            pref[i] = run;
+            run += __popc(pres[i]);
+        }
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < c; i += blockDim.x) {
+            const unsigned long long v = b.val[s + i];
+            const unsigned sk = (unsigned)(v >> 32);
+            const unsigned long long bit = (unsigned long long)(sk >> 31) * b.span + (sk & 0x7FFFFFFFu);
+            const unsigned rank = pref[bit >> 5] + __popc(pres[bit >> 5] & ((1u << (bit & 31)) - 1u));
+            b.tmp[s + rank] = v;
+        }
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < c; i += blockDim.x) b.val[s + i] = b.tmp[s + i];
+        __syncthreads();
+    }
+}
+
+#ifndef NBK_FOLD_MINB
+#define NBK_FOLD_MINB 2
+#endif
+
+// One thread per bucket, largest buckets first: sort (small buckets) and
+// fold the voxel's records in order; clears the index stamp and the bucket
+// count for the next batch.
+template <bool TM, class Src>
+__global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_constant__ DevMap m,
+                                                                   Src src, NdtBuckets b) {
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    const unsigned K = *((volatile unsigned *)(b.cursor + NBK_BINS));
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < K; t += gridDim.x * blockDim.x) {
+        const unsigned mi = b.perm[t];
+        unsigned c;
+        const unsigned s = nbk_start(b, mi, c);
+        unsigned long long *v = b.val + s;
+        if (c <= (unsigned)NBK_SERIAL) {
+            for (unsigned i = 1; i < c; ++i) {
+                const unsigned long long x = v[i];
+                int j = (int)i - 1;
+                while (j >= 0 && v[j] > x) {
+                    v[j + 1] = v[j];
+                    --j;
+                }
+                v[j + 1] = x;
+            }
+        }
+        b.cnt[mi] = 0u;
+        const int2 sl = m.marked[mi];
+        if (sl.x < 0) continue;
+        const int slot = sl.x, li = sl.y;
+        int g[3];
+        slot_li_to_g(m, slot, li, g);
+        float *occ = layer_at<float>(m, L_OCC, slot);
+        unsigned *mb = layer_at<unsigned>(m, L_MEAN, slot);
+        unsigned *cb = layer_at<unsigned>(m, L_COUNT, slot);
+        float *cov = layer_at<float>(m, L_COV, slot);
+        float *ib = TM ? layer_at<float>(m, L_INTENS, slot) : nullptr;
+        unsigned *hb = TM ? layer_at<unsigned>(m, L_HIT, slot) : nullptr;
+        unsigned *missb = TM ? layer_at<unsigned>(m, L_MISS, slot) : nullptr;
+        float l = occ[li];
+        unsigned i = 0;
+        // ---- phase 1: misses through the voxel's Gaussian, in ray order ----
+        bool reset = false;
+        unsigned miss_add = 0;
+        for (; i < c && !(v[i] >> 63); ++i) {
+            const unsigned w = (unsigned)v[i];
+            const float d = reset ? m.miss32 : -__uint_as_float(w & 0x7FFFFFFFu);
+            l = clamp_add(l, d, m.cmin, m.cmax);
+            if (TM && (reset || (w >> 31))) ++miss_add;
+            if (!reset && l < m.fthresh && cb[li] > 0) {
+                // transient reset (reference.py:86-93, _reset_voxel_buffers 97-104)
+                reset = true;
+                miss_add = 0;
+                cb[li] = 0;
+                mb[li] = 0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) cov[li * 6 + k] = 0.0f;
+                if (TM) {
+                    hb[li] = 0;
+                    missb[li] = 0;
+                    ib[li * 2] = 0.0f;
+                    ib[li * 2 + 1] = 0.0f;
+                }
+            }
+        }
+        if (TM && miss_add) missb[li] += miss_add;
+        // ---- phase 2: the voxel's samples in ray order (reference.py:107-150) ----
+        if (i < c) {
+            unsigned long long n = cb[li];
+            double mu[3] = {0.0, 0.0, 0.0};
+            if (n > 0) {
+                double off[3];
+                unpack_mean(mb[li], off);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
+            }
+            double S[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) S[k] = (double)cov[li * 6 + k];
+            double imean = 0.0, im2 = 0.0;
+            if (TM) {
+                imean = ib[li * 2];
+                im2 = ib[li * 2 + 1];
+            }
+            const unsigned h0 = i;
+            for (; i < c; ++i) {
+                const unsigned oi = (unsigned)(v[i] >> 32) & 0x7FFFFFFFu;
+                double e[3];
+                float it;
+                src.load_end((long long)(oi / (unsigned)m.maxseg), e, it);
+                l = clamp_add(l, m.hit32, m.cmin, m.cmax);
+                if (TM) {
+                    // ndt.update_intensity (ndt.py:98-106), stored f32 per sample
+                    const double val = it, nn = (double)(n + 1);
+                    const double d = val - imean;
+                    const double mnew = imean + d / nn;
+                    const double m2new = im2 + d * (val - mnew);
+                    imean = (double)(float)mnew;
+                    im2 = (double)(float)m2new;
+                }
+                ndt_update(n, mu, S, e);
+            }
+            if (TM) {
+                ib[li * 2] = (float)imean;
+                ib[li * 2 + 1] = (float)im2;
+                hb[li] += c - h0;
+            }
+            cb[li] = n > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)n;
+            double frac[3];
+            const double hi = 1.0 - 1.0 / 2048.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                double f = mu[a] / m.vox - (double)g[a];
+                if (f < 0.0) f = 0.0;
+                if (f > hi) f = hi;
+                frac[a] = f;
+            }
+            mb[li] = pack_mean(frac);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) cov[li * 6 + k] = (float)S[k];
+        }
+        occ[li] = l;
+        layer_at<unsigned>(m, L_NIDX, slot)[li] = 0u;
+    }
+}
+
+// Refused / failed batches leave index stamps behind: clear every stamped
+// word of the first `words` voxels (the list of indices is not trusted).
+__global__ void k_nbk_clear(const __grid_constant__ DevMap m, long long words) {
+    unsigned *w = reinterpret_cast<unsigned *>(m.slab[L_NIDX]);
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < words;
+         k += (long long)gridDim.x * blockDim.x)
+        if (w[k]) w[k] = 0u;
+}
+
+}  // namespace vm

@@ -22,6 +22,7 @@
 #include "vm_walk_det.cuh"
 #include "vm_shard.cuh"
 #include "vm_bucket.cuh"
+#include "vm_ndt.cuh"
 #include "vm_export.cuh"
 
 using namespace vm;
@@ -43,8 +44,8 @@ int fail(int code, const std::string &msg) {
                         std::string(#x) + ": " + cudaGetErrorString(e_));              \
     } while (0)
 
-const int LAYER_ELEM[NUM_LAYERS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 8, 4};
-const int LAYER_COMP[NUM_LAYERS] = {1, 1, 1, 1, 6, 1, 1, 2, 1, 1, 2};
+const int LAYER_ELEM[NUM_LAYERS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 8, 4, 4};
+const int LAYER_COMP[NUM_LAYERS] = {1, 1, 1, 1, 6, 1, 1, 2, 1, 1, 2, 1};
 
 int bitlen(unsigned long long x) {
     int b = 0;
@@ -101,6 +102,8 @@ struct vm_map {
     unsigned *d_bk_cnt = nullptr, *d_bk_off = nullptr;
     size_t bk_cap = 0;
     int *d_bk_big = nullptr;
+    unsigned *d_bk_perm = nullptr;   // NDT buckets, largest first (vm_ndt.cuh)
+    unsigned *d_nbk_small = nullptr; // NDT: size histogram, cursors, live count, slice cursor
     unsigned *d_bk_bits = nullptr;
     size_t bk_bits_cap = 0;
     void *d_scan_tmp = nullptr;
@@ -115,6 +118,7 @@ struct vm_map {
     size_t ring_bytes = 0;
     cudaEvent_t ev_ring[RING] = {}, ev_ring_up[RING] = {};
     long long rec_floor_override = 0;
+    long long ndt_rec_override = 0;  // VOXMAP_B200_TEST_NDT_REC_CAP: force the NDT overflow path
     int no_ray_order = 0;  // VOXMAP_B200_NO_RAY_ORDER: NDT walk in input order (A/B runs)
     int num_sms = 148;
     unsigned long long *d_stats = nullptr;
@@ -352,33 +356,45 @@ int launch_discover(vm_map *m, const DevMap &dm, const Src &src, long long n, in
     return check_launch("discover");
 }
 
+// The dynamic shared-memory opt-in is a per-device (per-context) function
+// attribute: set it once per device per kernel instantiation, checked.
+// (One instantiation -- one `done` mask -- per kernel: the template parameter
+// is the kernel itself, not its type, which several kernels share.)
+template <auto Kernel>
+cudaError_t opt_in_smem(size_t smem) {
+    static unsigned long long done = 0;  // bit d: configured on device d
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && (done >> dev) & 1ULL) return cudaSuccess;
+    e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && dev < 64) done |= 1ULL << dev;
+    return e;
+}
+
 template <bool REC_ONLY, class Src, int DIM>
-void launch_wd_dim(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
-    static bool configured = false;
+cudaError_t launch_wd_dim(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
     const size_t smem = sizeof(WalkDetSmem);
-    if (!configured) {
-        cudaFuncSetAttribute(k_walk_det<REC_ONLY, Src, DIM>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    cudaError_t e = opt_in_smem<k_walk_det<REC_ONLY, Src, DIM>>(smem);
+    if (e != cudaSuccess) return e;
     k_walk_det<REC_ONLY, Src, DIM><<<grid, BLOCK, smem, s>>>(dm, src);
+    return cudaSuccess;
 }
 
 template <bool REC_ONLY, class Src>
-void launch_wd(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
-    if (dm.dim == 32 && dm.brick_shift == 3) launch_wd_dim<REC_ONLY, Src, 32>(grid, s, dm, src);
-    else launch_wd_dim<REC_ONLY, Src, 0>(grid, s, dm, src);
+cudaError_t launch_wd(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
+    if (dm.dim == 32 && dm.brick_shift == 3) return launch_wd_dim<REC_ONLY, Src, 32>(grid, s, dm, src);
+    return launch_wd_dim<REC_ONLY, Src, 0>(grid, s, dm, src);
 }
 
 template <int MODE, bool DET, bool REC_ONLY, class Src>
-void launch_w3(dim3 grid, size_t smem, cudaStream_t s, const DevMap &dm, const Src &src) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_walk<MODE, DET, REC_ONLY, Src>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+cudaError_t launch_w3(dim3 grid, size_t smem, cudaStream_t s, const DevMap &dm, const Src &src) {
+    cudaError_t e = opt_in_smem<k_walk<MODE, DET, REC_ONLY, Src>>(smem);
+    if (e != cudaSuccess) return e;
     k_walk<MODE, DET, REC_ONLY, Src><<<grid, BLOCK, smem, s>>>(dm, src);
+    return cudaSuccess;
 }
 
 // kernel dispatch over (mode, exec, ray format)
@@ -395,6 +411,7 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
         if (e != cudaSuccess) return fail(VM_ERR_CUDA, cudaGetErrorString(e));
     }
     const size_t smem = sizeof(WalkSmem);
+    cudaError_t ae = cudaSuccess;
     switch (mode) {
     case M_OCC:
         if (det) {
@@ -402,19 +419,19 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
             // the batch's box is too large for it (walk_det_ok)
             DevMap d2 = dm;
             d2.walk_det_launched = 1;
-            if (rec_only) launch_wd<true>(pgrid, s, d2, src);
-            else launch_wd<false>(pgrid, s, d2, src);
-            if (rec_only) launch_w3<M_OCC, true, true>(pgrid, smem, s, d2, src);
-            else launch_w3<M_OCC, true, false>(pgrid, smem, s, d2, src);
+            ae = rec_only ? launch_wd<true>(pgrid, s, d2, src) : launch_wd<false>(pgrid, s, d2, src);
+            if (ae == cudaSuccess)
+                ae = rec_only ? launch_w3<M_OCC, true, true>(pgrid, smem, s, d2, src)
+                              : launch_w3<M_OCC, true, false>(pgrid, smem, s, d2, src);
             m->launches += 1;
         } else {
-            launch_w3<M_OCC, false, false>(pgrid, smem, s, dm, src);
+            ae = launch_w3<M_OCC, false, false>(pgrid, smem, s, dm, src);
         }
         break;
     case M_DECAY:
-        if (det && rec_only) launch_w3<M_DECAY, true, true>(pgrid, smem, s, dm, src);
-        else if (det) launch_w3<M_DECAY, true, false>(pgrid, smem, s, dm, src);
-        else launch_w3<M_DECAY, false, false>(pgrid, smem, s, dm, src);
+        if (det && rec_only) ae = launch_w3<M_DECAY, true, true>(pgrid, smem, s, dm, src);
+        else if (det) ae = launch_w3<M_DECAY, true, false>(pgrid, smem, s, dm, src);
+        else ae = launch_w3<M_DECAY, false, false>(pgrid, smem, s, dm, src);
         break;
     case M_NDT_OM:
         if (det && rec_only) k_walk_ndt<false, true, true><<<grid, block, 0, s>>>(dm, src, n);
@@ -432,6 +449,8 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
         break;
     }
     m->launches += 1;
+    if (ae != cudaSuccess)
+        return fail(VM_ERR_CUDA, std::string("walk shared-memory opt-in: ") + cudaGetErrorString(ae));
     return check_launch("walk");
 }
 
@@ -450,13 +469,6 @@ int launch_fold(vm_map *m, const DevMap &dm, const Src &src, const unsigned long
             k_fold_occ_big<<<m->num_sms * 2, BLOCK, 0, s>>>(dm, src, keys, R, m->d_big, m->d_nbig);
             m->launches += 2;
         }
-    } else if (mode == M_NDT_OM || mode == M_NDT_TM) {
-        unsigned g = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
-        if (g) {
-            if (mode == M_NDT_TM) k_fold_ndt<true><<<g, BLOCK, 0, s>>>(dm, src, keys, vals, R);
-            else k_fold_ndt<false><<<g, BLOCK, 0, s>>>(dm, src, keys, vals, R);
-            m->launches += 1;
-        }
     } else {
         unsigned g = (unsigned)std::min<long long>((R + BLOCK - 1) / BLOCK, grid_cap);
         if (g) k_fold_tsdf<<<g, BLOCK, 0, s>>>(dm, src, keys, R);
@@ -472,13 +484,16 @@ int ensure_buckets(vm_map *m, size_t nmarked_cap, size_t bwords) {
         cudaFree(m->d_bk_cnt);
         cudaFree(m->d_bk_off);
         cudaFree(m->d_bk_big);
+        cudaFree(m->d_bk_perm);
         m->d_bk_cnt = nullptr;
         m->d_bk_off = nullptr;
         m->d_bk_big = nullptr;
+        m->d_bk_perm = nullptr;
         CK(cudaMalloc((void **)&m->d_bk_cnt, nc * sizeof(unsigned)));
-        CK(cudaMemset(m->d_bk_cnt, 0, nc * sizeof(unsigned)));  // kept zero by k_bk_scatter
+        CK(cudaMemset(m->d_bk_cnt, 0, nc * sizeof(unsigned)));  // kept zero by the folds
         CK(cudaMalloc((void **)&m->d_bk_off, nc * sizeof(unsigned)));
         CK(cudaMalloc((void **)&m->d_bk_big, nc * sizeof(int)));
+        CK(cudaMalloc((void **)&m->d_bk_perm, nc * sizeof(unsigned)));
         m->bk_cap = nc;
         size_t bytes = 0;
         CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, m->d_bk_cnt, m->d_bk_off, (int)nc));
@@ -524,6 +539,52 @@ int launch_bucket_fold(vm_map *m, const DevMap &dm, const Src &src, long long n,
     return check_launch("bucket fold");
 }
 
+// NDT records: bucketed by voxel index, sorted per bucket, folded in order
+// (vm_ndt.cuh).  Every count is read on the device.
+template <class Src>
+int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, int maxseg, bool tm,
+                    cudaEvent_t ev_mid) {
+    cudaStream_t s = m->stream;
+    const unsigned long long span = (unsigned long long)n * maxseg;
+    const unsigned long long bwords = (2 * span + 31) / 32 + 1;
+    int rc;
+    if ((rc = ensure_buckets(m, m->smarked_cap, bwords))) return rc;
+    if (!m->d_nbk_small) {
+        CK(cudaMalloc((void **)&m->d_nbk_small, (2 * NBK_BINS + 4) * sizeof(unsigned)));
+        CK(cudaMemset(m->d_nbk_small, 0, (2 * NBK_BINS + 4) * sizeof(unsigned)));
+    }
+    NdtBuckets b{m->d_bk_cnt, m->d_bk_off, m->d_bk_perm, m->d_nbk_small, m->d_nbk_small + NBK_BINS,
+                 m->d_rec2, m->d_rec, m->d_bk_big, m->d_nbig, m->d_bk_bits, bwords, span};
+    CK(cudaMemsetAsync(m->d_nbig, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(b.cursor + NBK_BINS, 0, 2 * sizeof(unsigned), s));
+    const unsigned gr = (unsigned)m->num_sms * 8;
+    const unsigned gm = (unsigned)std::max<long long>(
+        1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
+    k_nbk_count<<<gr, BLOCK, 0, s>>>(dm, b);
+    k_nbk_alloc<<<gm, BLOCK, 0, s>>>(dm, b);
+    if (std::getenv("VOXMAP_B200_NDT_DEBUG")) {
+        unsigned h[NBK_BINS];
+        unsigned long long st[NUM_STATS], nm = 0;
+        CK(cudaMemcpyAsync(h, b.hist, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(st, m->d_stats, sizeof(st), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&nm, m->d_shard_cnt, sizeof(nm), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[ndt] R=%llu M=%llu buckets by size:", st[S_RECORDS], nm);
+        for (int i = 0; i < NBK_BINS; ++i)
+            if (h[i]) std::fprintf(stderr, " %d:%u", i, h[i]);
+        std::fprintf(stderr, "\n");
+    }
+    k_nbk_order<<<1, NBK_BINS, 0, s>>>(dm, b);
+    k_nbk_perm<<<gm, BLOCK, 0, s>>>(dm, b);
+    k_nbk_scatter<<<gr, BLOCK, 0, s>>>(dm, b);
+    k_nbk_sort_big<<<m->num_sms, BLOCK, 0, s>>>(dm, b);
+    CK(cudaEventRecord(ev_mid, s));
+    if (tm) k_nbk_fold<true><<<gm, BLOCK, 0, s>>>(dm, src, b);
+    else k_nbk_fold<false><<<gm, BLOCK, 0, s>>>(dm, src, b);
+    m->launches += 7;
+    return check_launch("ndt fold");
+}
+
 const uint32_t MODE_MASK[5] = {
     (1u << 1) | (1u << 2) | (1u << 3),
     (1u << 1) | (1u << 2) | (1u << 3) | (1u << 8) | (1u << 9),
@@ -537,7 +598,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     const bool tsdf = mode == M_TSDF;
     const bool det = exec == VM_EXEC_DETERMINISTIC;
     const bool occ_det = det && (mode == M_OCC || mode == M_DECAY);
-    const bool sorted = occ_det || ndt || (tsdf && det);
+    const bool sorted = occ_det || (tsdf && det);  // NDT: bucketed (launch_ndt_fold)
     const bool resolve = occ_det || ndt;
     const int maxseg = (int)std::ceil(m->cfg.max_ray_range / m->cfg.segment_length) + 1;
     unsigned long long order_span = tsdf ? (unsigned long long)n
@@ -564,9 +625,16 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)n + 1))) return rc;
         CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
     }
+    if (ndt) {
+        // records keyed by the voxel index (vm_ndt.cuh): one list entry per record at most
+        const size_t need = m->ndt_rec_override > 0 ? (size_t)m->ndt_rec_override
+                                                     : (size_t)n * (det ? 8 : 1) + 1;
+        if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, need)))) return rc;
+        if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+        CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
+    }
     size_t rec_need = 0;
-    if (ndt) rec_need = std::max<size_t>(m->rec_cap, (size_t)n * (det ? 8 : 1) + 1);
-    else if (tsdf && det) {
+    if (tsdf && det) {
         double band = 2.0 * m->cfg.tsdf_truncation / m->cfg.voxel_size;
         rec_need = (size_t)n * (size_t)(3.0 * (std::ceil(band) + 2.0) + 4.0);
     } else if (occ_det) rec_need = std::max<size_t>(m->rec_cap, rec_floor(m, n));
@@ -585,8 +653,8 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         DevMap dm = make_dm(m);
         dm.order_bits = order_bits;
         dm.ray_order = ray_order ? 1 : 0;
-        if (key_mi) {
-            dm.key_mi = 1;
+        if (key_mi || ndt) {
+            dm.key_mi = key_mi ? 1 : 0;
             dm.marked = m->d_smarked;
             dm.nmarked = m->d_shard_cnt;
             dm.marked_cap = m->smarked_cap;
@@ -673,9 +741,11 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             if ((rc = check_launch("resolve"))) return rc;
         }
         CK(cudaEventRecord(m->ev_res, m->stream));
-        if (key_mi) {
+        if (key_mi || ndt) {
             // the whole batch is enqueued; one sync at its end
-            if ((rc = launch_bucket_fold(m, dm, src, n, maxseg, m->ev_sort))) return rc;
+            if (ndt) rc = launch_ndt_fold(m, dm, src, n, maxseg, mode == M_NDT_TM, m->ev_sort);
+            else rc = launch_bucket_fold(m, dm, src, n, maxseg, m->ev_sort);
+            if (rc) return rc;
             CK(cudaEventRecord(m->ev_end, m->stream));
             CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, m->stream));
@@ -699,6 +769,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
                 k_clear_marks<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
             }
+            if (ndt) {
+                const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
+                k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
+            }
             CK(cudaStreamSynchronize(m->stream));
             m->nreg = cursor;
             return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range "
@@ -717,6 +791,47 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             m->nreg = cursor;
             ++replays;
             continue;
+        }
+        if (ndt) {
+            unsigned long long R = m->h_stats[S_RECORDS], M = m->h_stats[NUM_STATS + 1];
+            if (R > m->rec_cap || M > m->smarked_cap) {
+                // records or voxel indices overflowed: every bucket kernel was a
+                // no-op.  Drop the index stamps, make room, re-emit the records
+                // only (discover without descriptors, histograms or statistics;
+                // the walk without counts) and fold them.
+                const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
+                k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
+                if ((rc = ensure_records(m, std::max<size_t>((size_t)R + (R >> 2), m->rec_cap)))) return rc;
+                if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+                dm.rec = m->d_rec;
+                dm.recval = m->d_val;
+                dm.rec_cap = m->rec_cap;
+                dm.marked = m->d_smarked;
+                dm.marked_cap = m->smarked_cap;
+                dm.ray_order = 0;
+                CK(cudaMemsetAsync(m->d_stats + S_RECORDS, 0, sizeof(unsigned long long), m->stream));
+                CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
+                if ((rc = launch_discover(m, dm, src, n, mode, 1, 0, 0, m->stream))) return rc;
+                if (det && (rc = launch_walk(m, dm, src, n, mode, det, true))) return rc;
+                CK(cudaEventRecord(m->ev_res, m->stream));
+                if ((rc = launch_ndt_fold(m, dm, src, n, maxseg, mode == M_NDT_TM, m->ev_sort))) return rc;
+                CK(cudaEventRecord(m->ev_end, m->stream));
+                CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, m->stream));
+                CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_shard_cnt,
+                                   sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+                CK(cudaStreamSynchronize(m->stream));
+                if ((rc = check_launch("batch"))) return rc;
+                if (m->h_stats[S_RECORDS] > m->rec_cap || m->h_stats[NUM_STATS + 1] > m->smarked_cap)
+                    return fail(VM_ERR_CUDA, "NDT record re-emission overflowed");
+            }
+            CK(cudaEventElapsedTime(&ms_total, m->ev_start, m->ev_end));
+            CK(cudaEventElapsedTime(&ms_walk, m->ev_w0, m->ev_w1));
+            CK(cudaEventElapsedTime(&ms_disc, m->ev_start, m->ev_w0));
+            CK(cudaEventElapsedTime(&ms_res, m->ev_w1, m->ev_res));
+            CK(cudaEventElapsedTime(&ms_sort, m->ev_res, m->ev_sort));
+            CK(cudaEventElapsedTime(&ms_fold, m->ev_sort, m->ev_end));
+            break;
         }
         if (key_mi) {
             unsigned long long R = m->h_stats[S_RECORDS];
@@ -751,7 +866,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             unsigned long long R = m->h_stats[NUM_STATS + 1];
             if (R > m->rec_cap) {
                 // records overflowed: re-emit them (records only, nothing re-applied)
-                if (!occ_det && !(ndt && det)) return fail(VM_ERR_CUDA, "record buffer overflow");
+                if (!occ_det) return fail(VM_ERR_CUDA, "record buffer overflow");
                 CK(cudaStreamSynchronize(m->stream));
                 if ((rc = ensure_records(m, (size_t)R + (R >> 2)))) return rc;
                 dm.rec = m->d_rec;
@@ -759,11 +874,6 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 dm.rec_cap = m->rec_cap;
                 CK(cudaMemsetAsync(m->d_stats + S_RECORDS, 0, sizeof(unsigned long long),
                                    m->stream));
-                if (ndt) {
-                    // the phase-2 hit records come from k_discover: re-emit them
-                    // with a records-only discover pass (no descriptors, no marks)
-                    if ((rc = launch_discover(m, dm, src, n, mode, 1, 0, 0, m->stream))) return rc;
-                }
                 if ((rc = launch_walk(m, dm, src, n, mode, det, true))) return rc;
                 CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_stats + S_RECORDS,
                                    sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -771,7 +881,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 CK(cudaStreamSynchronize(m->stream));
                 R = m->h_stats[NUM_STATS + 1];
             }
-            int end_bit = order_bits + (ndt ? 1 : 0) +
+            int end_bit = order_bits +
                           std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
             if (key_mi) {
                 unsigned long long M = 0;
@@ -784,12 +894,8 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             if (R > 1) {
                 if ((rc = ensure_sort_tmp(m))) return rc;
                 size_t bytes = m->sort_tmp_bytes;
-                if (ndt)
-                    CK(cub::DeviceRadixSort::SortPairs(m->d_sort_tmp, bytes, db, dv, (int)R, 0,
-                                                       end_bit, m->stream));
-                else
-                    CK(cub::DeviceRadixSort::SortKeys(m->d_sort_tmp, bytes, db, (int)R, 0,
-                                                      end_bit, m->stream));
+                CK(cub::DeviceRadixSort::SortKeys(m->d_sort_tmp, bytes, db, (int)R, 0, end_bit,
+                                                  m->stream));
             }
             CK(cudaEventRecord(m->ev_sort, m->stream));
             if ((rc = launch_fold(m, dm, src, db.Current(), dv.Current(), (long long)R, mode)))
@@ -824,7 +930,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     out->region_misses = (int64_t)hs[S_RMISS];
     out->regions_touched = (int64_t)hs[S_PREF_TOUCHED];
     out->records = (int64_t)hs[S_RECORDS];
-    out->marked_voxels = key_mi ? (int64_t)hs[NUM_STATS + 1] : (int64_t)hs[S_MARKED];
+    out->marked_voxels = (key_mi || ndt) ? (int64_t)hs[NUM_STATS + 1] : (int64_t)hs[S_MARKED];
     out->regions_total = cursor;
     out->new_regions = cursor - nreg0;
     out->replays = replays;
@@ -1145,7 +1251,9 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
     while (ts < 2ULL * (unsigned long long)m->max_slots) ts <<= 1;
     m->tsize = ts;
     for (int l = 0; l < NUM_LAYERS; ++l) {
-        bool on = l == L_SCRATCH ? true : (layer_mask >> l) & 1u;
+        bool on = l == L_SCRATCH ? true
+                  : l == L_NIDX  ? ((layer_mask >> L_COV) & 1u) != 0  // NDT maps
+                                 : ((layer_mask >> l) & 1u) != 0;
         m->bpr[l] = on ? (size_t)m->vpr * LAYER_COMP[l] * LAYER_ELEM[l] : 0;
     }
     int rc;
@@ -1187,6 +1295,8 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) m->num_sms = prop.multiProcessorCount;
     }
     if (const char *rc_env = std::getenv("VOXMAP_B200_TEST_REC_CAP")) m->rec_floor_override = std::atoll(rc_env);
+    if (const char *rc_env = std::getenv("VOXMAP_B200_TEST_NDT_REC_CAP"))
+        m->ndt_rec_override = std::atoll(rc_env);
     if (std::getenv("VOXMAP_B200_NO_RAY_ORDER")) m->no_ray_order = 1;
     if ((rc = grow_pool(m, std::max<long long>(64, initial_regions)))) return cleanup(rc);
     *out = m;
@@ -1222,6 +1332,8 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_bk_cnt);
     cudaFree(m->d_bk_off);
     cudaFree(m->d_bk_big);
+    cudaFree(m->d_bk_perm);
+    cudaFree(m->d_nbk_small);
     cudaFree(m->d_bk_bits);
     cudaFree(m->d_chain);
     cudaFree(m->d_mstats);
@@ -1274,6 +1386,7 @@ int vm_map_reset(vm_map *m) {
 
 int vm_map_set_stream(vm_map *m, void *stream) {
     if (!m) return fail(VM_ERR_ARG, "null map");
+    CK(cudaSetDevice(m->device));
     CK(cudaStreamSynchronize(m->stream));
     if (m->own_stream) cudaStreamDestroy(m->stream);
     if (stream) {
@@ -1591,7 +1704,7 @@ int vm_export_select(vm_map *m, const int32_t *slots, int64_t nslots, int32_t ki
 int vm_export_gather(vm_map *m, int32_t layer, const int32_t *slots, int64_t nslots,
                      const int32_t *ridx, const int32_t *li, int64_t n, void *out) {
     if (!m || !slots || (n > 0 && (!ridx || !li || !out))) return fail(VM_ERR_ARG, "null argument");
-    if (layer < 1 || layer >= NUM_LAYERS || !m->slab[layer]) return fail(VM_ERR_ARG, "layer not in map");
+    if (layer < 1 || layer > L_TSDF || !m->slab[layer]) return fail(VM_ERR_ARG, "layer not in map");
     CK(cudaSetDevice(m->device));
     if (n <= 0) return VM_OK;
     const int bytes = (int)(m->bpr[layer] / (size_t)m->vpr);
@@ -1961,8 +2074,12 @@ int vm_shard_walk(vm_map *m) {
             using S = decltype(src);
             DevMap d2 = dm;
             d2.walk_det_launched = 1;
-            launch_wd<false, S>(pgrid, m->stream, d2, src);
-            launch_w3<M_OCC, true, false, S>(pgrid, sizeof(WalkSmem), m->stream, d2, src);
+            cudaError_t e = launch_wd<false, S>(pgrid, m->stream, d2, src);
+            if (e == cudaSuccess)
+                e = launch_w3<M_OCC, true, false, S>(pgrid, sizeof(WalkSmem), m->stream, d2, src);
+            if (e != cudaSuccess)
+                return fail(VM_ERR_CUDA, std::string("shard walk shared-memory opt-in: ") +
+                                             cudaGetErrorString(e));
             return check_launch("shard walk");
         });
         if (rc) return rc;

@@ -37,6 +37,18 @@ def _torch():
     return torch
 
 
+_STREAMS: dict = {}
+
+
+def _shared_stream(device: int):
+    """The sharded maps' stream on `device` (virtual ranks on one device share
+    it, so their exchanges and kernels are totally ordered)."""
+    torch = _torch()
+    if device not in _STREAMS:
+        _STREAMS[device] = torch.cuda.Stream(device=device)
+    return _STREAMS[device]
+
+
 class ShardedVoxelMap:
     """This rank's part of a region-sharded map."""
 
@@ -47,10 +59,14 @@ class ShardedVoxelMap:
         self.vmap = VoxelMap(cfg, layer_names, device=self.device, initial_regions=initial_regions)
         self.nat = self.vmap._native
         self.nat.shard_config(self.rank, self.world)
-        # one stream with torch: the exchanged tensors (NCCL writes them on
-        # torch's stream) are consumed by this map's kernels in order
-        torch = _torch()
-        self.nat.set_stream(torch.cuda.current_stream(self.dev).cuda_stream)
+        # One explicit stream per device, shared by this map's kernels and by
+        # every torch op of the exchange (the drivers below run them under
+        # `torch.cuda.stream(self.stream)`; NCCL collectives are ordered
+        # against the current stream).  Never torch's legacy default stream:
+        # its handle is 0, which the runtime would read as "create a private
+        # non-blocking stream" with no ordering against torch's work.
+        self.stream = _shared_stream(self.device)
+        self.nat.set_stream(self.stream.cuda_stream)
         self._keep = None
         self._cap = 1 << 16  # export items per destination
 
@@ -179,6 +195,13 @@ def exchange_all_gather(t, group=None):
 
 
 def submit_batch_sharded(smap: ShardedVoxelMap, records, group=None) -> BatchStats:
+    """Integrate one batch into this rank's part of a region-sharded map
+    (collective over `group`); see _submit_sharded."""
+    with _torch().cuda.stream(smap.stream):
+        return _submit_sharded(smap, records, group)
+
+
+def _submit_sharded(smap: ShardedVoxelMap, records, group=None) -> BatchStats:
     """Integrate one batch (the whole batch on every rank) into this rank's
     part of the map; collective over `group` (NCCL: device buffers go
     straight over NVLink; gloo: staged through host memory, for CPU-side
@@ -219,6 +242,17 @@ def submit_batch_sharded(smap: ShardedVoxelMap, records, group=None) -> BatchSta
 def submit_batch_virtual(smaps, records) -> BatchStats:
     """The same protocol for G ShardedVoxelMaps living in this process (any
     devices); the exchanges are device copies."""
+    import contextlib
+    torch = _torch()
+    with contextlib.ExitStack() as stack:
+        # every device's current stream is its maps' stream (torch orders
+        # cross-device copies against the current streams of both devices)
+        for st in {s.device: s.stream for s in smaps}.values():
+            stack.enter_context(torch.cuda.stream(st))
+        return _submit_virtual(smaps, records)
+
+
+def _submit_virtual(smaps, records) -> BatchStats:
     torch = _torch()
     world = len(smaps)
     recs = [_to_device(records, s.dev) for s in smaps]

@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import ast
+import math
 import hashlib
 from pathlib import Path
 
@@ -43,3 +44,56 @@ def max_abs_diff(keys, get_a, get_b):
             worst = max(worst, float(d.max()))
             count += int(np.count_nonzero(d))
     return worst, count
+
+
+def hit_delta(cfg) -> float:
+    """occupancy.hit_delta (occupancy.py:30-35): log-odds of p_hit."""
+    return math.log(cfg.p_hit / (1.0 - cfg.p_hit))
+
+
+def miss_delta(cfg) -> float:
+    return math.log(cfg.p_miss / (1.0 - cfg.p_miss))
+
+
+def clamp_fold(l0, k, delta, cmin, cmax):
+    """k clamped f32 log-odds adds of `delta` per voxel (reference.py:22-23),
+    vectorised; a voxel stops at its fixed point (the clamp)."""
+    l = np.asarray(l0, dtype=np.float32).copy()
+    k = np.asarray(k, dtype=np.int64)
+    d, lo, hi = np.float32(delta), np.float32(cmin), np.float32(cmax)
+    left = k.copy()
+    idx = np.nonzero(left > 0)[0]
+    while idx.size:
+        old = l[idx]
+        new = np.clip(old + d, lo, hi).astype(np.float32)
+        l[idx] = new
+        left[idx] -= 1
+        keep = (left[idx] > 0) & (new != old)
+        idx = idx[keep]
+    return l
+
+
+def cas_envelope(l0, hits, misses, cfg):
+    """Bounds of any interleaving of `hits` hit updates and `misses` miss
+    updates of one batch on each voxel: clamped adds are monotone, so all
+    hits first then all misses gives the lowest result, all misses first the
+    highest (swapping an adjacent (hit, miss) pair never lowers the result)."""
+    h32, m32 = np.float32(hit_delta(cfg)), np.float32(miss_delta(cfg))
+    lo = clamp_fold(clamp_fold(l0, hits, h32, cfg.clamp_min, cfg.clamp_max), misses, m32,
+                    cfg.clamp_min, cfg.clamp_max)
+    hi = clamp_fold(clamp_fold(l0, misses, m32, cfg.clamp_min, cfg.clamp_max), hits, h32,
+                    cfg.clamp_min, cfg.clamp_max)
+    # without clamping the two orders differ only by f32 rounding, either way
+    return np.minimum(lo, hi), np.maximum(lo, hi)
+
+
+# Reordering an unclamped run of f32 adds moves the result by rounding only:
+# at most half an ulp of the largest intermediate (|l| <= 4) per add, in
+# practice a few ulps of 4.0.  The slack is absolute.
+ENVELOPE_SLACK = 8 * float(np.spacing(np.float32(4.0)))  # 3.8e-6 log-odds
+
+
+def within_envelope(x, lo, hi, slack=ENVELOPE_SLACK):
+    """Mask of x inside [lo - slack, hi + slack]."""
+    x = np.asarray(x, dtype=np.float64)
+    return (x >= np.asarray(lo, np.float64) - slack) & (x <= np.asarray(hi, np.float64) + slack)

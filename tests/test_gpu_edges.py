@@ -127,6 +127,30 @@ def test_c2_prefix_bit_exact():
     _compare(data[:3], cfg=MapConfig(voxel_size=0.05))
 
 
+@pytest.mark.slow
+def test_c2_twenty_batches_pipelined_bit_exact():
+    """20 of C2's 100 batches (5.2 M rays, ~1.4 G visits, 2 s of sensor time)
+    through the bench's own path -- submit_batches, one pipelined device
+    sequence -- against the C oracle: region set and every layer bit-exact."""
+    from paper_2206_06079_b200 import submit_batches
+    cfg = MapConfig(voxel_size=0.05)
+    data = scans.batch_by_period(np.concatenate(scans.os128_canyon_batches(200)))[:20]
+    assert len(data) == 20
+    names = MODE_LAYERS["occupancy"]
+    vm = VoxelMap(cfg, names, initial_regions=4096)
+    om = orc.OracleMap(cfg, names)
+    sts = submit_batches(vm, data, "occupancy")
+    for st, rec in zip(sts, data):
+        ost = om.integrate_records(rec, "occupancy")
+        assert (st.voxel_visits, st.segments, st.region_misses) == \
+            (ost["voxel_visits"], ost["segments"], 0)
+    assert set(vm.regions) == set(om.region_keys())
+    for rk, region in vm.regions.items():
+        for name in names:
+            assert np.array_equal(region.buffers[name].view(np.uint8),
+                                  om.layer(rk, name).view(np.uint8)), (rk, name)
+
+
 def _layers_equal(a, b):
     assert set(a.regions) == set(b.regions)
     for rk, region in a.regions.items():
@@ -181,56 +205,6 @@ def test_submit_batches_record_overflow(monkeypatch):
                                   om.layer(rk, name).view(np.uint8)), (rk, name)
 
 
-def _compare_tol(batches, cfg, mode, tol):
-    """Deterministic path vs the C oracle at scale for the tolerance-graded
-    layers (the reference's own executor tolerances, test_engine.py:52-63);
-    integer layers and occupancy-free layers exact."""
-    names = MODE_LAYERS[mode]
-    vm = VoxelMap(cfg, names)
-    om = orc.OracleMap(cfg, names)
-    for rec in batches:
-        st = submit_batch(vm, rec, mode, ExecutorOptions(deterministic=True))
-        ost = om.integrate_records(rec, mode)
-        assert st.voxel_visits == ost["voxel_visits"] and st.region_misses == 0
-    assert set(vm.regions) == set(om.region_keys())
-    worst = {}
-    for rk, region in vm.regions.items():
-        for name in names:
-            a, b = region.buffers[name], om.layer(rk, name)
-            if name in ("mean_count", "hit_count", "miss_count", "decay_hits"):
-                assert np.array_equal(a, b), (rk, name)
-            elif name == "mean":
-                # packed 10-bit mean: at most one bucket per axis (DESIGN.md)
-                for sh in (0, 10, 20):
-                    d = np.abs(((a >> sh) & 1023).astype(np.int64) - ((b >> sh) & 1023))
-                    assert d.max(initial=0) <= 1, (rk, name)
-            else:
-                d = np.abs(a.astype(np.float64) - b.astype(np.float64))
-                worst[name] = max(worst.get(name, 0.0), float(d.max(initial=0.0)))
-    for name, w in worst.items():
-        assert w <= tol.get(name, 0.0), (name, w)
-    return worst
-
-
-@pytest.mark.slow
-def test_c3_ndt_om_tunnel_scans_vs_oracle():
-    """Two C3 tunnel scans (262k rays) through NDT-OM: Gaussians form on the
-    rough walls, so phase 1 weights and resets are exercised.  With up to
-    hundreds of samples per voxel per batch, the device's merged per-batch
-    update (pivoted sums + 3x3 Cholesky, vm_kernels.cuh k_fold_ndt) and the
-    reference's per-sample Givens updates (ndt.py:37-70) round differently:
-    the stated bound on sqrt-covariance entries is 1e-4 m (observed 4.2e-5)."""
-    scans2 = scans.os64_tunnel_scans(2)
-    _compare_tol(scans2, MapConfig(), "ndt-om",
-                 {"occupancy": 1e-4, "cov_sqrt": 1e-4})
-
-
-@pytest.mark.slow
-def test_c1_ndt_tm_scan_vs_oracle():
-    _compare_tol([scans.os64_room_scan(seed=0)[::2].copy()], MapConfig(), "ndt-tm",
-                 {"occupancy": 1e-4, "cov_sqrt": 1e-5, "intensity": 1e-3})
-
-
 @pytest.mark.slow
 def test_tsdf_then_decay_vs_oracle():
     """The C4 pattern (test_acceptance.py:398-399): per batch a TSDF pass then
@@ -256,37 +230,6 @@ def test_tsdf_then_decay_vs_oracle():
 
 
 @pytest.mark.slow
-def test_c2_prefix_cas_order_free_layers_exact():
-    """CAS mode (the paper's atomic update, _kernels.pyx:233-357) at C2 scale:
-    voxels that received no hit see only identical-delta misses, which
-    commute, so their occupancy is bit-exact; mean_count is exact.  Voxels
-    with hits and misses are order-dependent (SURVEY finding 4): their
-    deviation is reported and bounded by the clamp range."""
-    cfg = MapConfig(voxel_size=0.05)
-    data = scans.batch_by_period(np.concatenate(scans.os128_canyon_batches(20)))[:2]
-    names = MODE_LAYERS["occupancy"]
-    vm = VoxelMap(cfg, names)
-    om = orc.OracleMap(cfg, names)
-    for rec in data:
-        st = submit_batch(vm, rec, "occupancy", ExecutorOptions(deterministic=False))
-        ost = om.integrate_records(rec, "occupancy")
-        assert st.voxel_visits == ost["voxel_visits"] and st.region_misses == 0
-    assert set(vm.regions) == set(om.region_keys())
-    mixed, worst = 0, 0.0
-    for rk, region in vm.regions.items():
-        cnt = om.layer(rk, "mean_count")
-        assert np.array_equal(region.buffers["mean_count"], cnt), rk
-        a, b = region.buffers["occupancy"], om.layer(rk, "occupancy")
-        free = cnt == 0
-        assert np.array_equal(a[free].view(np.uint32), b[free].view(np.uint32)), rk
-        d = np.abs(a[~free].astype(np.float64) - b[~free])
-        mixed += int(np.count_nonzero(d))
-        worst = max(worst, float(d.max(initial=0.0)))
-    assert worst <= 5.5  # clamp_max - clamp_min
-    print(f"CAS vs sequential on hit voxels: {mixed} differ, max {worst:.4f} log-odds")
-
-
-@pytest.mark.slow
 def test_submit_batches_ndt_prefetched_matches_per_batch():
     """Non-pipelined modes run one vm_integrate per batch inside
     vm_integrate_many, with the next batch's host records prefetched into a
@@ -306,4 +249,4 @@ def test_submit_batches_ndt_prefetched_matches_per_batch():
         for name in names:
             u = region.buffers[name].astype(np.float64)
             v = b.regions[rk].buffers[name].astype(np.float64)
-            assert np.max(np.abs(u - v), initial=0.0) <= (1e-4 if name != "mean" else 0), (rk, name)
+            assert np.array_equal(u, v), (rk, name)
