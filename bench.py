@@ -56,6 +56,8 @@ def parse():
                     help="one vm_integrate / submit_batch call per batch instead of one "
                          "pipelined vm_integrate_many / submit_batches call per step")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="default run: skip the NDT-OM (C3) and C1 blocks and the CPU sweep")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent per-GPU maps instead of the region-sharded map")
     return ap.parse_args()
@@ -189,6 +191,147 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _h_and_u(host, cfg, sizes):
+    """H (sample segments: has_sample rays within max range) and U (distinct
+    sample voxels, summed over batches) of a record sequence -- the SURVEY
+    8(d) byte-model terms the device does not count."""
+    o = host["origin"].astype(np.float64)
+    e = host["end"].astype(np.float64)
+    L = np.sqrt(((e - o) ** 2).sum(1))
+    smp = ((host["flags"] & 1) == 1) & (L <= cfg.max_ray_range) & (L > 0)
+    H = int(np.sum(smp))
+    U = 0
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    for b in range(len(sizes)):
+        sl = slice(offs[b], offs[b + 1])
+        g = np.floor(e[sl][smp[sl]] / cfg.voxel_size).astype(np.int64)
+        if len(g):
+            U += len(np.unique(g, axis=0))
+    return H, U
+
+
+def ndt_bytes(S, V, H, V3, U):
+    """SURVEY.md 8(d) NDT-OM: phase 1 reads count + RMW log-odds per visit
+    (12 B), + mean and cov when the voxel holds a Gaussian (40 B); phase 2
+    reads each sample (24 B) and RMWs log-odds, mean, count, cov per
+    distinct sample voxel (72 B).  Returns (walk bytes, fold bytes)."""
+    return 49 * S + 12 * (V - H - V3) + 40 * V3, 24 * H + 72 * U
+
+
+def run_gpu_workload(name, args, dev, torch, world=1, dist=None, steps=None, e2e_steps=3,
+                     det=True):
+    """One workload on this GPU: device-resident `value`, host-record `e2e`,
+    stage times and the byte model.  A step integrates the workload's whole
+    batch sequence into a freshly cleared map."""
+    from paper_2206_06079_b200 import (ExecutorOptions, VoxelMap, _native, submit_batch,
+                                       submit_batches)
+    from paper_2206_06079_b200.layers import MODE_LAYERS
+
+    steps = steps or args.steps
+    cfg, mode, data, desc = workload(name, args.batches)
+    sizes = [len(b) for b in data]
+    offsets = np.concatenate([[0], np.cumsum(sizes)])
+    total_rays = int(offsets[-1])
+    host = np.concatenate(data)
+    d_rec = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
+    base = d_rec.data_ptr()
+    stream = torch.cuda.current_stream()
+    vmap = VoxelMap(cfg, MODE_LAYERS[mode], device=dev, initial_regions=4096)
+    vmap._native.set_stream(stream.cuda_stream)
+    keys = ("discover_ms", "walk_ms", "resolve_ms", "sort_ms", "fold_ms", "gpu_ms")
+
+    def step(record=False):
+        vmap.clear()
+        tot = dict(S=0, V=0, launches=0, batches=0, records=0, rmiss=0, **{k: 0.0 for k in keys})
+        rays = [_native.rays_from_records(sizes[b], base + int(offsets[b]) * 40)
+                for b in range(len(data))]
+        if args.per_batch:
+            sts = [vmap._native.integrate(r, mode, det) for r in rays]
+        else:
+            sts = vmap._native.integrate_many(rays, mode, det)
+        if record:
+            for st in sts:
+                tot["S"] += st.segments
+                tot["V"] += st.voxel_visits
+                tot["launches"] += st.launches
+                tot["records"] += st.records
+                tot["rmiss"] += st.region_misses
+                tot["batches"] += 1
+                for k in keys:
+                    tot[k] += getattr(st, k)
+        return tot
+
+    for _ in range(args.warmup):
+        step()
+    clk_file = tempfile.mktemp(suffix=".csv")
+    clk = sample_clocks(clk_file)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    recs = [step(record=True) for _ in range(steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    if clk:
+        clk.terminate()
+        clk.wait()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    e2e = None
+    if e2e_steps:
+        pinned = torch.from_numpy(host.view(np.uint8).copy()).pin_memory()
+        hv = pinned.numpy().view(host.dtype)
+        opts = ExecutorOptions(deterministic=det)
+        slices = [hv[offsets[b]:offsets[b + 1]] for b in range(len(data))]
+
+        def run_e2e(batches):
+            if args.per_batch or len(batches) == 1:
+                for x in batches:
+                    submit_batch(vmap, x, mode, opts)
+            else:
+                submit_batches(vmap, batches, mode, opts)
+
+        vmap.clear()
+        run_e2e(slices[:50])
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(e2e_steps):
+            vmap.clear()
+            run_e2e(slices)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = max(f0.elapsed_time(f1), (time.perf_counter() - t0) * 1e3)
+        if dist:
+            t = torch.tensor([ems], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": total_rays * e2e_steps * world / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(host.nbytes),
+               "d2h_bytes_per_step": int(len(data) * ctypes_stats_bytes()),
+               "steps": e2e_steps,
+               "api": ("submit_batch(vmap, pinned OHMB1 records) per batch"
+                       if args.per_batch or len(data) == 1 else
+                       f"submit_batches(vmap, [pinned OHMB1 records per batch]) ({mode})")}
+    H, U = _h_and_u(host, cfg, sizes)
+    s0 = recs[-1]
+    del d_rec
+    return dict(cfg=cfg, mode=mode, desc=desc, total_rays=total_rays, ms=ms, steps=steps,
+                value=total_rays * steps * world / (ms * 1e-3), e2e=e2e, s0=s0, H=H, U=U,
+                launches=int(sum(r["launches"] for r in recs)), clocks=parse_clocks(clk_file, dev),
+                data=data)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -208,163 +351,159 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    if world > 1 and not args.replicas and args.workload in ("c1", "c2") and args.exec_ == "det":
+    if world > 1 and not args.replicas and args.workload in ("c1", "c2") and \
+            args.exec_ == "det":
         run_sharded(args, world, rank, dev, dist)
         dist.destroy_process_group()
         return
 
-    from paper_2206_06079_b200 import (ExecutorOptions, VoxelMap, _native, submit_batch,
-                                       submit_batches)
-    from paper_2206_06079_b200.layers import MODE_LAYERS
+    from paper_2206_06079_b200 import _native
 
-    cfg, mode, data, desc = workload(args.workload, args.batches)
     det = args.exec_ == "det"
-    sizes = [len(b) for b in data]
-    offsets = np.concatenate([[0], np.cumsum(sizes)])
-    total_rays = int(offsets[-1])
-    host = np.concatenate(data)
-    # device-resident copy of all records (inputs already in HBM for `value`)
-    d_rec = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
-    base = d_rec.data_ptr()
-    stream = torch.cuda.current_stream()
-
-    vmap = VoxelMap(cfg, MODE_LAYERS[mode], device=dev, initial_regions=4096)
-    vmap._native.set_stream(stream.cuda_stream)
-
-    agg = {}
-
-    def step(record=False):
-        vmap.clear()
-        tot = dict(S=0, V=0, walk_ms=0.0, launches=0, batches=0, records=0, rmiss=0,
-                   discover_ms=0.0, resolve_ms=0.0, sort_ms=0.0, fold_ms=0.0, gpu_ms=0.0)
-        rays = [_native.rays_from_records(sizes[b], base + int(offsets[b]) * 40)
-                for b in range(len(data))]
-        if args.per_batch:
-            sts = [vmap._native.integrate(r, mode, det) for r in rays]
-        else:
-            sts = vmap._native.integrate_many(rays, mode, det)
-        for st in sts:
-            if record:
-                tot["S"] += st.segments
-                tot["V"] += st.voxel_visits
-                tot["walk_ms"] += st.walk_ms
-                tot["launches"] += st.launches
-                tot["records"] += st.records
-                tot["rmiss"] += st.region_misses
-                tot["batches"] += 1
-                for k in ("discover_ms", "resolve_ms", "sort_ms", "fold_ms", "gpu_ms"):
-                    tot[k] += getattr(st, k)
-        return tot
-
-    for _ in range(args.warmup):
-        step()
-    clk_file = tempfile.mktemp(suffix=".csv")
-    clk = sample_clocks(clk_file)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    steps = [step(record=True) for _ in range(args.steps)]
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    if clk:
-        clk.terminate()
-        clk.wait()
-    ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = total_rays * args.steps * world / (ms * 1e-3)
-
-    # H (hit visits): sample segments = has_sample rays not clipped (<= max range)
-    o = host["origin"].astype(np.float64)
-    e = host["end"].astype(np.float64)
-    L = np.sqrt(((e - o) ** 2).sum(1))
-    H = int(np.sum(((host["flags"] & 1) == 1) & (L <= cfg.max_ray_range) & (L > 0)))
-    s0 = steps[-1]
-    bytes_step = algorithmic_bytes(s0["S"], s0["V"], H)
-    walk_ms = s0["walk_ms"] / max(1, s0["batches"])
-    bytes_launch = bytes_step / max(1, s0["batches"])
+    r = run_gpu_workload(args.workload, args, dev, torch, world, dist,
+                         e2e_steps=0 if args.no_e2e else max(1, min(args.steps, 3)), det=det)
+    cfg, mode, s0 = r["cfg"], r["mode"], r["s0"]
     peak, peak_kind = load_peaks()
+    red_peak = _native.probe_red_rate(dev, 64 << 20, 5)
+    walk_ms = s0["walk_ms"] / max(1, s0["batches"])
+    if mode == "occupancy":
+        bytes_launch = algorithmic_bytes(s0["S"], s0["V"], r["H"]) / max(1, s0["batches"])
+        kernel = "k_walk_det" if det else "k_walk"
+    else:
+        wb, _ = ndt_bytes(s0["S"], s0["V"], r["H"], s0["records"] - r["H"], r["U"])
+        bytes_launch = wb / max(1, s0["batches"])
+        kernel = "k_walk_ndt"
     achieved = bytes_launch / (walk_ms * 1e-3) / 1e9 if walk_ms > 0 else 0.0
-    traffic = load_traffic(args.workload, args.exec_)
-
-    e2e = None
-    if not args.no_e2e:
-        pinned = torch.from_numpy(host.view(np.uint8).copy()).pin_memory()
-        hv = pinned.numpy().view(host.dtype)
-        opts = ExecutorOptions(deterministic=det)
-        n_e2e = max(1, min(args.steps, 3))
-        slices = [hv[offsets[b]:offsets[b + 1]] for b in range(len(data))]
-
-        def run_e2e(batches):
-            if args.per_batch:
-                for x in batches:
-                    submit_batch(vmap, x, mode, opts)
-            else:
-                submit_batches(vmap, batches, mode, opts)
-
-        vmap.clear()
-        run_e2e(slices[:50])
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(n_e2e):
-            vmap.clear()
-            run_e2e(slices)
-        f1.record(stream)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        ems = max(f0.elapsed_time(f1), wall * 1e3)
-        if dist:
-            t = torch.tensor([ems], device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": total_rays * n_e2e * world / (ems * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(host.nbytes),
-               "d2h_bytes_per_step": int(len(data) * ctypes_stats_bytes()),
-               "steps": n_e2e,
-               "api": ("submit_batch(vmap, pinned OHMB1 records) per batch" if args.per_batch else
-                       "submit_batches(vmap, [pinned OHMB1 records per 0.1 s batch])")}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, data, args.cpu_budget, mode)
-
+    visits_launch = s0["V"] / max(1, s0["batches"])
+    line = None
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
+            "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["ms"] / r["steps"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64 (DDA) / f32 (log-odds)", "data": "synthetic",
-            "config": dict(desc, exec="deterministic" if det else "cas",
-                           rays_per_step=total_rays, parallelism=f"replicas{world}",
-                           l2="inputs (1.05 GB/step) and map exceed L2; map cleared each step"),
-            "voxel_updates_per_s": s0["V"] * args.steps * world / (ms * 1e-3),
+            "config": dict(r["desc"], exec="deterministic" if det else "cas",
+                           rays_per_step=r["total_rays"], parallelism=f"replicas{world}",
+                           l2="inputs and map exceed L2; map cleared each step"),
+            "voxel_updates_per_s": s0["V"] * r["steps"] * world / (r["ms"] * 1e-3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_walk_det" if det else "k_walk", "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": load_traffic(args.workload, args.exec_),
+                         "kernel": kernel, "peak_kind": peak_kind,
                          "bytes_per_launch": bytes_launch, "avg_launch_ms": walk_ms},
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "gpu_launches": int(sum(s["launches"] for s in steps)),
-            "clocks": parse_clocks(clk_file, dev),
-            "stats": {"segments": s0["S"], "visits": s0["V"], "hits": H,
+            # the walk's real ceiling: one atomic update per visit; peak = this
+            # GPU's measured RED.ADD rate at L2-resident random addresses
+            "roofline_l2_atomic": {"bound": "l2-atomic", "kernel": kernel,
+                                   "achieved": visits_launch / (walk_ms * 1e-3) if walk_ms else 0.0,
+                                   "peak": red_peak, "unit": "updates/s",
+                                   "frac": (visits_launch / (walk_ms * 1e-3) / red_peak)
+                                   if walk_ms and red_peak else None,
+                                   "peak_kind": "measured (vm_probe_red_rate, 64 MiB footprint)"},
+            "e2e": r["e2e"],
+            "cpu_baseline": None,
+            "gpu_launches": r["launches"],
+            "clocks": r["clocks"],
+            "stats": {"segments": s0["S"], "visits": s0["V"], "hits": r["H"],
                       "records": s0["records"], "region_misses": s0["rmiss"]},
             "stages_ms_per_step": {k: round(s0[k], 4) for k in (
                 "discover_ms", "walk_ms", "resolve_ms", "sort_ms", "fold_ms", "gpu_ms")},
         }
+    default_run = args.workload == "c2" and det and world == 1 and not args.per_batch
+    if default_run and not args.no_extra:
+        # the NDT-OM half of the metric (configs[2], C3) and the 0.1 m
+        # occupancy scan (configs[0], C1), measured in the same run
+        n = run_gpu_workload("c3", args, dev, torch, steps=min(args.steps, 3), e2e_steps=1)
+        ns = n["s0"]
+        V3 = ns["records"] - n["H"]
+        wb, fb = ndt_bytes(ns["S"], ns["V"], n["H"], V3, n["U"])
+        nb = max(1, ns["batches"])
+        nwalk = ns["walk_ms"] / nb
+        c1 = run_gpu_workload("c1", args, dev, torch, steps=50, e2e_steps=20)
+        if rank == 0:
+            line["ndt_om"] = {
+                "workload": n["desc"]["workload"], "config": n["desc"], "value": n["value"],
+                "unit": UNIT, "ms_per_step": n["ms"] / n["steps"], "steps": n["steps"],
+                "e2e": n["e2e"], "clocks": n["clocks"], "gpu_launches": n["launches"],
+                "roofline": {"bound": "hbm", "kernel": "k_walk_ndt", "unit": "GB/s",
+                             "achieved": wb / nb / (nwalk * 1e-3) / 1e9 if nwalk else 0.0,
+                             "peak": peak, "peak_kind": peak_kind,
+                             "frac": (wb / nb / (nwalk * 1e-3) / 1e9) / peak if nwalk else None,
+                             "bytes_per_launch": wb / nb, "avg_launch_ms": nwalk,
+                             "step_bytes": wb + fb,
+                             "step_frac": (wb + fb) / (ns["gpu_ms"] * 1e-3) / 1e9 / peak},
+                "stats": {"segments": ns["S"], "visits": ns["V"], "hits": n["H"],
+                          "gaussian_visits_V3": V3, "sample_voxels_U": n["U"],
+                          "records": ns["records"], "region_misses": ns["rmiss"]},
+                "stages_ms_per_step": {k: round(ns[k], 4) for k in (
+                    "discover_ms", "walk_ms", "resolve_ms", "sort_ms", "fold_ms", "gpu_ms")},
+                "cpu_baseline": None,
+            }
+            line["c1"] = {"workload": c1["desc"]["workload"], "value": c1["value"], "unit": UNIT,
+                          "ms_per_step": c1["ms"] / c1["steps"], "steps": c1["steps"],
+                          "e2e": c1["e2e"], "clocks": c1["clocks"],
+                          "gpu_ms_per_scan": c1["s0"]["gpu_ms"]}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, r["data"], args.cpu_budget, mode)
+        if default_run and not args.no_extra:
+            sweep = cpu_sweep(r["data"], line.get("ndt_om"))
+            line["cpu_sweep"] = sweep
+            if "ndt_om" in line and sweep.get("ndt_om_e2e"):
+                best_w, best = max(sweep["ndt_om_e2e"].items(), key=lambda kv: kv[1])
+                line["ndt_om"]["cpu_baseline"] = {
+                    "value": best, "unit": UNIT, "cores": int(best_w), "kind": "reference",
+                    "sample": sweep["ndt_om_sample"]}
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def cpu_sweep(c2_batches, ndt_block):
+    """The reference on the host cores, W in {1, 2, 4, ..., cores}:
+    kernel-only occupancy (the reference's compiled _kernels.integrate_occupancy,
+    best of 3 on one C2 batch) and end-to-end submit_batch (the reference
+    package's own engine, Python preprocessing and -- for NDT-OM -- Python
+    phase 2 included) for occupancy and NDT-OM."""
+    from oracle import oracle as orc
+    from oracle import ref_engine, ref_runner
+    from paper_2206_06079_b200 import MapConfig, scans
+    cores = orc.host_cores()
+    ws = sorted({w for w in (1, 2, 4, 8, 16, 32, 64) if w <= cores} | {cores})
+    out = {"cores": cores, "workers": ws}
+    cfg2 = MapConfig(voxel_size=0.05)
+    kern = {}
+    for w in ws:
+        best = 0.0
+        for _ in range(3):
+            t = ref_runner.time_reference(cfg2, c2_batches[:1], w, budget_s=0.0)
+            best = max(best, t["rays"] / t["seconds"] if t["seconds"] else 0.0)
+        kern[str(w)] = best
+    out["occupancy_kernel"] = kern
+    out["occupancy_kernel_sample"] = ("one C2 batch (262,400 rays, 0.05 m), reference "
+                                      "_kernels.integrate_occupancy, best of 3")
+    if ref_engine.load_voxmap() is None:
+        out["e2e_unavailable"] = "reference package not installed in baseline/_ref"
+        return out
+    occ = {}
+    sub = c2_batches[0][::8].copy()
+    for w in sorted({1, min(4, cores), cores}):
+        occ[str(w)] = ref_engine.time_submit_batch({"voxel_size": 0.05}, "occupancy", [],
+                                                   sub, w)
+    out["occupancy_e2e"] = occ
+    out["occupancy_e2e_sample"] = ("every 8th ray of the first C2 batch (32,800 rays), "
+                                   "reference voxmap.submit_batch, BatchStats.rays_per_second")
+    if ndt_block is not None:
+        tun = scans.os64_tunnel_scans(3)
+        warm = [t[::4].copy() for t in tun[:2]]
+        timed = tun[2][::4].copy()
+        nd = {}
+        for w in sorted({1, min(4, cores), cores}):
+            nd[str(w)] = ref_engine.time_submit_batch({"voxel_size": 0.1}, "ndt-om", warm,
+                                                      timed, w)
+        out["ndt_om_e2e"] = nd
+        out["ndt_om_sample"] = ("every 4th ray of C3 tunnel scan 3 (32,768 rays) after scans "
+                                "1-2 built the Gaussians; reference voxmap.submit_batch "
+                                "(native phase 1 on W threads + Python phase 2)")
+    return out
 
 
 STREET_PITCH = 250.0  # m between the per-GPU copies of the scene (weak scaling)

@@ -234,13 +234,29 @@ int vm_shard_lists(vm_map *map, int64_t *req_out, int64_t req_cap, int64_t *mark
 /* req_in: requests addressed to this rank; marks_in: every rank's marks. */
 int vm_shard_prepare(vm_map *map, const int64_t *req_in, int64_t nreq, const int64_t *marks_in,
                      int64_t nmarks);
+/* NDT-OM batches (vm_shard_ndt.cuh): vm_shard_lists' req_out holds every
+ * ghost region of the slice's prefetch set, per owner.  The owner answers a
+ * request list with the regions' Gaussian bitmaps -- ceil(vpr / 32) u32 words
+ * per region, bit li set when voxel li holds >= 3 samples -- creating the
+ * regions it lacks; the requester marks its ghost voxels from them. */
+int vm_shard_ndt_bits(vm_map *map, const int64_t *req_in, int64_t nreq, uint32_t *bits_out);
+int vm_shard_ndt_mark(vm_map *map, const int64_t *keys, const uint32_t *bits, int64_t n);
 int vm_shard_walk(vm_map *map);
 /* out: world segments of cap_per_dest 16-byte items (region key, li | kind
- * << 31, count or ray order | hit); per_dest_out[world] gets the sizes
+ * << 31, count or ray order | hit) -- 32-byte items for NDT-OM batches
+ * (region key, li | kind << 30, count or segment order, chord t0, t1);
+ * per_dest_out[world] gets the sizes
  * (VM_ERR_ARG if a segment overflowed: retry with a larger cap). */
 int vm_shard_export(vm_map *map, void *out, int64_t cap_per_dest, int64_t *per_dest_out);
 int vm_shard_import(vm_map *map, const void *in, int64_t n);
 int vm_shard_finish(vm_map *map, vm_stats *out);
+
+/* Ceiling probe for the contended walk path (not a reference interface):
+ * fire-and-forget u32 reductions (RED.ADD, the walk's per-visit update) at
+ * pseudo-random word addresses inside a `footprint_bytes` buffer on `device`
+ * -- small enough to stay in L2, as the walk's touched scratch words do.
+ * reds_per_s_out: the measured L2 atomic throughput (best of `reps` launches). */
+int vm_probe_red_rate(int32_t device, int64_t footprint_bytes, int32_t reps, double *reds_per_s_out);
 
 const char *vm_last_error(void);
 int vm_device_count(int32_t *out);

@@ -27,8 +27,8 @@ EXPORTED = (
     "vm_map_write_layer", "vm_map_layer_ptr", "vm_integrate", "vm_integrate_many", "vm_export_select", "vm_export_gather", "vm_walk_voxels", "vm_hash_mix",
     "vm_kernels_integrate_occupancy", "vm_last_error", "vm_device_count", "vm_build_info",
     "vm_shard_config", "vm_shard_owner", "vm_shard_begin", "vm_shard_lists", "vm_shard_prepare",
-    "vm_shard_walk",
-    "vm_shard_export", "vm_shard_import", "vm_shard_finish",
+    "vm_shard_walk", "vm_shard_ndt_bits", "vm_shard_ndt_mark",
+    "vm_shard_export", "vm_shard_import", "vm_shard_finish", "vm_probe_red_rate",
 )
 
 
@@ -117,11 +117,14 @@ def lib():
         "vm_shard_lists": ([P, P, I64, P, I64, P], ctypes.c_int),
         "vm_shard_prepare": ([P, P, I64, P, I64], ctypes.c_int),
         "vm_shard_walk": ([P], ctypes.c_int),
+        "vm_shard_ndt_bits": ([P, P, I64, P], ctypes.c_int),
+        "vm_shard_ndt_mark": ([P, P, P, I64], ctypes.c_int),
         "vm_shard_export": ([P, P, I64, P], ctypes.c_int),
         "vm_shard_import": ([P, P, I64], ctypes.c_int),
         "vm_shard_finish": ([P, ctypes.POINTER(VmStats)], ctypes.c_int),
         "vm_device_count": ([ctypes.POINTER(I32)], ctypes.c_int),
         "vm_build_info": ([], ctypes.c_char_p),
+        "vm_probe_red_rate": ([I32, I64, I32, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     }
     for name, (argt, rest) in sig.items():
         fn = getattr(L, name)
@@ -251,12 +254,22 @@ class NativeMap:
     def shard_config(self, rank: int, world: int):
         check(lib().vm_shard_config(self._h, rank, world), "vm_shard_config")
 
-    def shard_begin(self, rays: VmRays) -> tuple[int, int]:
-        """Discover this rank's slice; returns (#new regions, #new sample voxels)."""
+    def shard_begin(self, rays: VmRays, mode: str = "occupancy") -> tuple[int, int]:
+        """Discover this rank's slice; returns (bound on the requests, #new
+        sample voxels): occupancy -- new regions; NDT-OM -- prefetched
+        regions (every ghost among them is requested)."""
         counts = (ctypes.c_int64 * 2)()
-        check(lib().vm_shard_begin(self._h, ctypes.byref(rays), 0, EXEC_DETERMINISTIC,
+        check(lib().vm_shard_begin(self._h, ctypes.byref(rays), MODES.index(mode), EXEC_DETERMINISTIC,
                                    ctypes.cast(counts, ctypes.c_void_p)), "vm_shard_begin")
         return int(counts[0]), int(counts[1])
+
+    def shard_ndt_bits(self, req_ptr: int, nreq: int, bits_ptr: int):
+        check(lib().vm_shard_ndt_bits(self._h, ctypes.c_void_p(req_ptr), nreq,
+                                      ctypes.c_void_p(bits_ptr)), "vm_shard_ndt_bits")
+
+    def shard_ndt_mark(self, keys_ptr: int, bits_ptr: int, n: int):
+        check(lib().vm_shard_ndt_mark(self._h, ctypes.c_void_p(keys_ptr), ctypes.c_void_p(bits_ptr),
+                                      n), "vm_shard_ndt_mark")
 
     def shard_lists(self, req_ptr: int, req_cap: int, marks_ptr: int, marks_cap: int,
                     world: int) -> list[int]:
@@ -378,3 +391,12 @@ def kernels_integrate_occupancy(origins, ends, has_sample, n, tkeys, tvals, tsiz
 def shard_owner(packed_key: int, world: int) -> int:
     """Owner rank of a region in a `world`-way sharded map (vm_shard_owner)."""
     return int(lib().vm_shard_owner(int(packed_key), int(world)))
+
+
+def probe_red_rate(device: int = 0, footprint_bytes: int = 64 << 20, reps: int = 5) -> float:
+    """Measured L2 atomic (RED.ADD u32, random addresses) throughput, /s: the
+    ceiling of the walk's per-visit update (vm_probe_red_rate)."""
+    out = ctypes.c_double()
+    check(lib().vm_probe_red_rate(device, footprint_bytes, reps, ctypes.byref(out)),
+          "vm_probe_red_rate")
+    return out.value

@@ -121,6 +121,11 @@ struct DevMap {
     unsigned long long rec_cap;
     int *touched;                        // regions touched by the walk
     int touched_cap;
+    // region-sharded NDT (vm_shard_ndt.cuh): the walk's visits through
+    // Gaussian voxels of regions other ranks own, for their owners
+    void *gx;
+    unsigned long long *ngx;
+    unsigned long long gx_cap;
 };
 
 // ---------------------------------------------------------------- arithmetic

@@ -575,6 +575,28 @@ __global__ void __launch_bounds__(BLOCK) k_seg_scatter(const __grid_constant__ D
 // (voxel | phase 0 | ray order) -> value = |fl32(g * miss_delta)| bits with
 // bit 31 = (g >= miss-likelihood threshold), folded in ray order by
 // k_fold_ndt together with the reset (reference.py:67-94).
+// Region-sharded NDT: a ghost voxel's scratch word carries GAUSS_FLAG when
+// its owner holds a Gaussian there (count >= 3 at the start of the batch);
+// the low bits count the order-free misses.
+constexpr unsigned GAUSS_FLAG = 0x40000000u;
+
+// 32-byte exchange item of the sharded NDT protocol
+struct ShardItemN {
+    long long rkey;
+    unsigned li_kind;  // li | kind << 30: 0 miss count, 1 sample (phase 2), 2 visit (phase 1)
+    unsigned val;      // count, or segment order ray * maxseg + seg
+    double t0, t1;     // kind 2: the visit's chord on the segment
+};
+static_assert(sizeof(ShardItemN) == 32, "ShardItemN layout");
+
+__device__ __forceinline__ void shard_ghost_visit(const DevMap &m, long long key, int li,
+                                                  unsigned oi, double t0, double t1) {
+    const unsigned long long k = atomicAdd(m.ngx, 1ULL);
+    if (k < m.gx_cap)
+        reinterpret_cast<ShardItemN *>(m.gx)[k] =
+            ShardItemN{key, (unsigned)li | (2u << 30), oi, t0, t1};
+}
+
 struct NdtRecStage {
     unsigned long long *key;
     unsigned *val;
@@ -598,9 +620,18 @@ struct NdtVisitor {
     unsigned order;
     NdtRecStage st;
     unsigned long long visits, rmiss, retries;
+    // region-sharded maps: the current region is another rank's (ghost);
+    // `unknown`: no Gaussian bitmap of it arrived this batch
+    bool ghost, unknown;
 
     __device__ __forceinline__ void bind() {
         int s = rt.slot;
+        ghost = false;
+        if (DET && m->shard_world > 1 && s >= 0 && s < m->cap) {
+            const long long key = m->slot_keys[s];
+            ghost = region_owner(key, m->shard_world) != m->shard_rank;
+            unknown = ghost && __ldcg(m->slot_pref + s) != m->epoch;
+        }
         if (s >= 0 && s < m->cap) {
             occ = layer_at<float>(*m, L_OCC, s);
             cov = layer_at<float>(*m, L_COV, s);
@@ -637,6 +668,17 @@ struct NdtVisitor {
             return;
         }
         const int li = rt.li(*m);
+        if (DET && ghost) {
+            // another rank's voxel: a Gaussian there (its bitmap bit, or no
+            // bitmap) -> the visit goes to the owner, who weighs it; else a
+            // miss count (vm_shard_ndt.cuh)
+            if (REC_ONLY) return;
+            if (unknown || (__ldcg(scr + li) & GAUSS_FLAG))
+                shard_ghost_visit(*m, m->slot_keys[rt.slot], li, order >> 1, t0, t1);
+            else
+                atomicAdd(scr + li, 1u);
+            return;
+        }
         unsigned ns = __ldcg(cnt + li);
         if (ns < 3) {
             if (REC_ONLY) return;
@@ -727,7 +769,7 @@ __global__ void __launch_bounds__(BLOCK, NDT_MINB) k_walk_ndt(const __grid_const
         double o[3], e[3];
         int h;
         float it;
-        src.load(first, o, e, h, it);
+        src.load(m.ray_lo + (first < n ? first : 0), o, e, h, it);
         for (int a = 0; a < 3; ++a) corner[a] = (int)floor(o[a] / m.vox) - CUBE / 2;
         nrec = 0;
     }
@@ -744,6 +786,7 @@ __global__ void __launch_bounds__(BLOCK, NDT_MINB) k_walk_ndt(const __grid_const
     long long i = first + threadIdx.x;
     if (i < n) {
         if (m.ray_order) i = m.perm[i];  // longest rays first: a warp's lanes finish together
+        i += m.ray_lo;                   // sharded maps walk the slice [ray_lo, ray_lo + n)
         Ray r;
         src.load(i, r.o, r.e, r.has, r.inten);
         if (prep_ray(m, r, true)) {

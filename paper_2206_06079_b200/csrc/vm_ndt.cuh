@@ -152,18 +152,22 @@ __device__ __forceinline__ void ndt_update(unsigned long long &n, double mu[3], 
 
 struct NdtBuckets {
     unsigned *cnt;                   // [M] records per bucket (zero between batches)
+    unsigned *cnt2;                  // [M] samples (phase-2 records) per bucket (zero between batches)
     unsigned *off;                   // [M] slice start (bumped by the scatter)
-    unsigned *perm;                  // [M] buckets, largest first
-    unsigned *hist;                  // [NBK_BINS] bucket sizes (zeroed by k_nbk_order)
+    unsigned *perm;                  // [M] buckets, most samples first
+    unsigned *hist;                  // [NBK_BINS] size classes (zeroed by k_nbk_order)
     unsigned *cursor;                // [NBK_BINS] + [1] live buckets + [1] slice cursor
     unsigned long long *val;         // [R] (sk << 32 | value), bucketed
     unsigned long long *tmp;         // [R] rank-sort output
-    int *big;                        // buckets sorted by k_nbk_sort_big
-    unsigned long long *nbig;
-    unsigned *bits;                  // rank sort: per block 2 * bwords words
+    double4 *pos;                    // [R] sample end point (x, y, z, intensity) of phase-2 slots
+    int *mid, *big;                  // buckets for the warp / block sorts
+    unsigned long long *nmid, *nbig;
+    unsigned *bits;                  // huge buckets: per block 2 * bwords words
     unsigned long long bwords;       // words of one (phase, order) bitmap
     unsigned long long span;         // n * maxseg (orders per phase)
 };
+
+constexpr int NBK_WARP_MAX = 512;  // warp rank sort (shared-memory staging: 4 KiB per warp)
 
 // The batch's records and bucket count, on the device; false when there is
 // nothing to do (guard refusal, or an overflow the host re-runs).
@@ -181,12 +185,22 @@ __global__ void __launch_bounds__(BLOCK) k_nbk_count(const __grid_constant__ Dev
     if (!bk_ndt_live(m, R, M)) return;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned mi = (unsigned)(m.rec[i] >> 32);
-        if (mi < M) atomicAdd(b.cnt + mi, 1u);
+        const unsigned long long k = m.rec[i];
+        const unsigned mi = (unsigned)(k >> 32);
+        if (mi >= M) continue;
+        atomicAdd(b.cnt + mi, 1u);
+        if ((k >> 31) & 1ULL) atomicAdd(b.cnt2 + mi, 1u);
     }
 }
 
-// slice allocation (one atomic per warp) + size histogram
+// The fold's cost is its samples (a Givens update each; a phase-1 record is
+// one clamped add), so the buckets are ordered by sample count: class
+// 1 + min(samples, 254), class 0 for phase-1-only buckets.
+__device__ __forceinline__ int nbk_class(unsigned samples) {
+    return samples ? 1 + (int)min(samples, (unsigned)NBK_BINS - 2u) : 0;
+}
+
+// slice allocation (one atomic per warp), class histogram, sort lists
 __global__ void __launch_bounds__(BLOCK) k_nbk_alloc(const __grid_constant__ DevMap m, NdtBuckets b) {
     __shared__ unsigned h[NBK_BINS];
     unsigned long long R, M;
@@ -210,7 +224,9 @@ __global__ void __launch_bounds__(BLOCK) k_nbk_alloc(const __grid_constant__ Dev
         wb = __shfl_sync(0xffffffffu, wb, 31);
         if (c) {
             b.off[mi] = wb + incl - c;
-            atomicAdd(h + min(c, (unsigned)NBK_BINS - 1u), 1u);
+            atomicAdd(h + nbk_class(b.cnt2[mi]), 1u);
+            if (c > (unsigned)NBK_WARP_MAX) b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
+            else if (c > (unsigned)NBK_SERIAL) b.mid[atomicAdd(b.nmid, 1ULL)] = (int)mi;
         }
     }
     __syncthreads();
@@ -218,7 +234,7 @@ __global__ void __launch_bounds__(BLOCK) k_nbk_alloc(const __grid_constant__ Dev
         if (h[i]) atomicAdd(b.hist + i, h[i]);
 }
 
-// size classes -> cursors, largest first; total live buckets
+// classes -> cursors, most samples first; total live buckets
 __global__ void k_nbk_order(const __grid_constant__ DevMap m, NdtBuckets b) {
     __shared__ unsigned h[NBK_BINS];
     unsigned long long R, M;
@@ -230,7 +246,7 @@ __global__ void k_nbk_order(const __grid_constant__ DevMap m, NdtBuckets b) {
     __syncthreads();
     if (threadIdx.x != 0) return;
     unsigned run = 0;
-    for (int i = NBK_BINS - 1; i >= 1; --i) {
+    for (int i = NBK_BINS - 1; i >= 0; --i) {
         b.cursor[i] = run;
         run += h[i];
     }
@@ -247,17 +263,14 @@ __global__ void __launch_bounds__(BLOCK) k_nbk_perm(const __grid_constant__ DevM
         __syncthreads();
         const unsigned long long mi = b0 + threadIdx.x;
         const unsigned c = mi < M ? b.cnt[mi] : 0u;
-        const int bin = c ? (int)min(c, (unsigned)NBK_BINS - 1u) : -1;
+        const int bin = c ? nbk_class(b.cnt2[mi]) : -1;
         unsigned r = 0;
         if (bin >= 0) r = atomicAdd(cnt + bin, 1u);
         __syncthreads();
         for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x)
             if (cnt[i]) base[i] = atomicAdd(b.cursor + i, cnt[i]);
         __syncthreads();
-        if (bin >= 0) {
-            b.perm[base[bin] + r] = (unsigned)mi;
-            if (c > (unsigned)NBK_SERIAL) b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
-        }
+        if (bin >= 0) b.perm[base[bin] + r] = (unsigned)mi;
         __syncthreads();
     }
 }
@@ -281,7 +294,35 @@ __device__ __forceinline__ unsigned nbk_start(const NdtBuckets &b, unsigned mi, 
     return b.off[mi] - c;
 }
 
-// Buckets above NBK_SERIAL, one block each: bitonic sort in shared memory,
+// Buckets of NBK_SERIAL < c <= NBK_WARP_MAX records, one warp each: staged
+// in shared memory, every lane ranks its records against the whole bucket
+// (sort keys are unique) and writes them back at their ranks.
+constexpr int NBK_MID_WARPS = BLOCK / 32;
+__global__ void __launch_bounds__(BLOCK) k_nbk_sort_mid(const __grid_constant__ DevMap m, NdtBuckets b) {
+    __shared__ unsigned long long sv[NBK_MID_WARPS][NBK_WARP_MAX];
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    unsigned long long *my = sv[wi];
+    const unsigned long long nm = *((volatile unsigned long long *)b.nmid);
+    for (unsigned long long w = (unsigned long long)blockIdx.x * NBK_MID_WARPS + wi; w < nm;
+         w += (unsigned long long)gridDim.x * NBK_MID_WARPS) {
+        const unsigned mi = (unsigned)b.mid[w];
+        unsigned c;
+        const unsigned s = nbk_start(b, mi, c);
+        for (unsigned i = lane; i < c; i += 32) my[i] = b.val[s + i];
+        __syncwarp();
+        for (unsigned i = lane; i < c; i += 32) {
+            const unsigned long long x = my[i];
+            unsigned rank = 0;
+            for (unsigned j = 0; j < c; ++j) rank += my[j] < x ? 1u : 0u;
+            b.val[s + rank] = x;
+        }
+        __syncwarp();
+    }
+}
+
+// Buckets above NBK_WARP_MAX, one block each: bitonic sort in shared memory,
 // or, above NBK_SMEM, a rank sort over the (phase, order) bitmap.
 __global__ void __launch_bounds__(BLOCK) k_nbk_sort_big(const __grid_constant__ DevMap m, NdtBuckets b) {
     __shared__ unsigned long long sv[NBK_SMEM];
@@ -364,115 +405,199 @@ __global__ void __launch_bounds__(BLOCK) k_nbk_sort_big(const __grid_constant__ 
     }
 }
 
-#ifndef NBK_FOLD_MINB
-#define NBK_FOLD_MINB 2
-#endif
+// Buckets of <= NBK_SERIAL (16) records: one thread each, a bitonic sorting
+// network on registers (static indices: no local memory), written back.
+__device__ __forceinline__ void cswap(unsigned long long &a, unsigned long long &b, bool up) {
+    const unsigned long long x = a, y = b;
+    const bool sw = (x > y) == up;
+    a = sw ? y : x;
+    b = sw ? x : y;
+}
 
-// One thread per bucket, largest buckets first: sort (small buckets) and
-// fold the voxel's records in order; clears the index stamp and the bucket
-// count for the next batch.
-template <bool TM, class Src>
-__global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_constant__ DevMap m,
-                                                                   Src src, NdtBuckets b) {
+__global__ void __launch_bounds__(BLOCK) k_nbk_sort_small(const __grid_constant__ DevMap m, NdtBuckets b) {
     unsigned long long R, M;
     if (!bk_ndt_live(m, R, M)) return;
     const unsigned K = *((volatile unsigned *)(b.cursor + NBK_BINS));
     for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < K; t += gridDim.x * blockDim.x) {
-        const unsigned mi = b.perm[t];
         unsigned c;
-        const unsigned s = nbk_start(b, mi, c);
-        unsigned long long *v = b.val + s;
-        if (c <= (unsigned)NBK_SERIAL) {
-            for (unsigned i = 1; i < c; ++i) {
-                const unsigned long long x = v[i];
-                int j = (int)i - 1;
-                while (j >= 0 && v[j] > x) {
-                    v[j + 1] = v[j];
-                    --j;
-                }
-                v[j + 1] = x;
-            }
+        const unsigned s = nbk_start(b, b.perm[t], c);
+        if (c < 2 || c > (unsigned)NBK_SERIAL) continue;
+        unsigned long long r[NBK_SERIAL];
+#pragma unroll
+        for (int i = 0; i < NBK_SERIAL; ++i) r[i] = (unsigned)i < c ? b.val[s + i] : ~0ULL;
+#pragma unroll
+        for (int k = 2; k <= NBK_SERIAL; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+                for (int i = 0; i < NBK_SERIAL; ++i)
+                    if ((i ^ j) > i) cswap(r[i], r[i ^ j], (i & k) == 0);
+#pragma unroll
+        for (int i = 0; i < NBK_SERIAL; ++i)
+            if ((unsigned)i < c) b.val[s + i] = r[i];
+    }
+}
+
+// Every sample slot gets its end point and intensity next to it, so the
+// serial fold streams them instead of chasing record -> ray -> end point.
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_nbk_gather(const __grid_constant__ DevMap m, Src src, NdtBuckets b) {
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; p < R;
+         p += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long v = b.val[p];
+        if (!(v >> 63)) continue;
+        const unsigned oi = (unsigned)(v >> 32) & 0x7FFFFFFFu;
+        double e[3];
+        float it;
+        src.load_end((long long)(oi / (unsigned)m.maxseg), e, it);
+        b.pos[p] = make_double4(e[0], e[1], e[2], (double)it);
+    }
+}
+
+#ifndef NBK_FOLD_MINB
+#define NBK_FOLD_MINB 2
+#endif
+__device__ __forceinline__ double4 ld_d4(const double4 *p) {  // read-only path, 2 x 16 B
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    const double2 a = __ldg(q), c = __ldg(q + 1);
+    return make_double4(a.x, a.y, c.x, c.y);
+}
+constexpr int NBK_PF = 4;  // phase-1 records loaded ahead
+
+// One lane per bucket, buckets with the most samples first, so the 32 lanes
+// of a warp hold buckets with (nearly) the same number of samples; the
+// record loops are warp-uniform (bounded by the warp's maximum, inactive
+// lanes masked), so the lanes step through their samples together, and the
+// (sorted, read-only) records and sample end points are loaded ahead of the
+// serial chain.  Clears the index stamp and the bucket counts.
+template <bool TM>
+__global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_constant__ DevMap m,
+                                                                   NdtBuckets b) {
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    const unsigned K = *((volatile unsigned *)(b.cursor + NBK_BINS));
+    const int lane = threadIdx.x & 31;
+    const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+    for (unsigned w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 32 < K; w += nwarps) {
+        const unsigned t = w * 32 + lane;
+        bool act = t < K;
+        unsigned c = 0, ns = 0, s = 0, mi = 0;
+        int slot = 0, li = 0;
+        if (act) {
+            mi = b.perm[t];
+            s = nbk_start(b, mi, c);
+            ns = b.cnt2[mi];
+            b.cnt[mi] = 0u;
+            b.cnt2[mi] = 0u;
+            const int2 sl = m.marked[mi];
+            slot = sl.x;
+            li = sl.y;
+            act = slot >= 0;
         }
-        b.cnt[mi] = 0u;
-        const int2 sl = m.marked[mi];
-        if (sl.x < 0) continue;
-        const int slot = sl.x, li = sl.y;
-        int g[3];
-        slot_li_to_g(m, slot, li, g);
-        float *occ = layer_at<float>(m, L_OCC, slot);
-        unsigned *mb = layer_at<unsigned>(m, L_MEAN, slot);
-        unsigned *cb = layer_at<unsigned>(m, L_COUNT, slot);
-        float *cov = layer_at<float>(m, L_COV, slot);
-        float *ib = TM ? layer_at<float>(m, L_INTENS, slot) : nullptr;
-        unsigned *hb = TM ? layer_at<unsigned>(m, L_HIT, slot) : nullptr;
-        unsigned *missb = TM ? layer_at<unsigned>(m, L_MISS, slot) : nullptr;
-        float l = occ[li];
-        unsigned i = 0;
+        if (!act) c = ns = 0;
+        const unsigned long long *__restrict__ v = b.val + s;
+        const unsigned np1 = c - ns;  // phase-1 records sort first
+        float *occ = nullptr, *cov = nullptr, *ib = nullptr;
+        unsigned *mb = nullptr, *cb = nullptr, *hb = nullptr, *missb = nullptr;
+        int g[3] = {0, 0, 0};
+        float l = 0.0f;
+        unsigned n0 = 0;
+        if (act) {
+            slot_li_to_g(m, slot, li, g);
+            occ = layer_at<float>(m, L_OCC, slot);
+            mb = layer_at<unsigned>(m, L_MEAN, slot);
+            cb = layer_at<unsigned>(m, L_COUNT, slot);
+            cov = layer_at<float>(m, L_COV, slot);
+            if (TM) {
+                ib = layer_at<float>(m, L_INTENS, slot);
+                hb = layer_at<unsigned>(m, L_HIT, slot);
+                missb = layer_at<unsigned>(m, L_MISS, slot);
+            }
+            l = occ[li];
+            n0 = cb[li];
+        }
         // ---- phase 1: misses through the voxel's Gaussian, in ray order ----
         bool reset = false;
         unsigned miss_add = 0;
-        for (; i < c && !(v[i] >> 63); ++i) {
-            const unsigned w = (unsigned)v[i];
-            const float d = reset ? m.miss32 : -__uint_as_float(w & 0x7FFFFFFFu);
-            l = clamp_add(l, d, m.cmin, m.cmax);
-            if (TM && (reset || (w >> 31))) ++miss_add;
-            if (!reset && l < m.fthresh && cb[li] > 0) {
-                // transient reset (reference.py:86-93, _reset_voxel_buffers 97-104)
-                reset = true;
-                miss_add = 0;
-                cb[li] = 0;
-                mb[li] = 0;
+        const unsigned mp1 = __reduce_max_sync(0xffffffffu, np1);
+        for (unsigned i0 = 0; i0 < mp1; i0 += NBK_PF) {
+            unsigned wv[NBK_PF];
 #pragma unroll
-                for (int k = 0; k < 6; ++k) cov[li * 6 + k] = 0.0f;
-                if (TM) {
-                    hb[li] = 0;
-                    missb[li] = 0;
-                    ib[li * 2] = 0.0f;
-                    ib[li * 2 + 1] = 0.0f;
+            for (int q = 0; q < NBK_PF; ++q) wv[q] = i0 + q < np1 ? (unsigned)__ldg(v + i0 + q) : 0u;
+#pragma unroll
+            for (int q = 0; q < NBK_PF; ++q) {
+                if (i0 + q < np1) {
+                    const float d = reset ? m.miss32 : -__uint_as_float(wv[q] & 0x7FFFFFFFu);
+                    l = clamp_add(l, d, m.cmin, m.cmax);
+                    if (TM && (reset || (wv[q] >> 31))) ++miss_add;
+                    // transient reset (reference.py:86-93, _reset_voxel_buffers 97-104)
+                    if (!reset && l < m.fthresh && n0 > 0) {
+                        reset = true;
+                        miss_add = 0;
+                    }
                 }
+            }
+        }
+        if (reset) {
+            n0 = 0;
+            cb[li] = 0;
+            mb[li] = 0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) cov[li * 6 + k] = 0.0f;
+            if (TM) {
+                hb[li] = 0;
+                missb[li] = 0;
+                ib[li * 2] = 0.0f;
+                ib[li * 2 + 1] = 0.0f;
             }
         }
         if (TM && miss_add) missb[li] += miss_add;
         // ---- phase 2: the voxel's samples in ray order (reference.py:107-150) ----
-        if (i < c) {
-            unsigned long long n = cb[li];
-            double mu[3] = {0.0, 0.0, 0.0};
+        unsigned long long n = n0;
+        double mu[3] = {0.0, 0.0, 0.0}, S[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        double imean = 0.0, im2 = 0.0;
+        if (ns) {
             if (n > 0) {
                 double off[3];
                 unpack_mean(mb[li], off);
 #pragma unroll
                 for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
             }
-            double S[6];
 #pragma unroll
             for (int k = 0; k < 6; ++k) S[k] = (double)cov[li * 6 + k];
-            double imean = 0.0, im2 = 0.0;
             if (TM) {
                 imean = ib[li * 2];
                 im2 = ib[li * 2 + 1];
             }
-            const unsigned h0 = i;
-            for (; i < c; ++i) {
-                const unsigned oi = (unsigned)(v[i] >> 32) & 0x7FFFFFFFu;
-                double e[3];
-                float it;
-                src.load_end((long long)(oi / (unsigned)m.maxseg), e, it);
+        }
+        const double4 *__restrict__ ps = b.pos + s + np1;
+        const unsigned ms = __reduce_max_sync(0xffffffffu, ns);
+        double4 cur = ns ? ld_d4(ps) : make_double4(0.0, 0.0, 0.0, 0.0);
+        for (unsigned i = 0; i < ms; ++i) {
+            if (i < ns) {
+                const double4 nxt = i + 1 < ns ? ld_d4(ps + i + 1) : cur;
                 l = clamp_add(l, m.hit32, m.cmin, m.cmax);
                 if (TM) {
                     // ndt.update_intensity (ndt.py:98-106), stored f32 per sample
-                    const double val = it, nn = (double)(n + 1);
+                    const double val = cur.w, nn = (double)(n + 1);
                     const double d = val - imean;
                     const double mnew = imean + d / nn;
                     const double m2new = im2 + d * (val - mnew);
                     imean = (double)(float)mnew;
                     im2 = (double)(float)m2new;
                 }
+                const double e[3] = {cur.x, cur.y, cur.z};
                 ndt_update(n, mu, S, e);
+                cur = nxt;
             }
+        }
+        if (ns) {
             if (TM) {
                 ib[li * 2] = (float)imean;
                 ib[li * 2 + 1] = (float)im2;
-                hb[li] += c - h0;
+                hb[li] += ns;
             }
             cb[li] = n > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)n;
             double frac[3];
@@ -488,8 +613,10 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
 #pragma unroll
             for (int k = 0; k < 6; ++k) cov[li * 6 + k] = (float)S[k];
         }
-        occ[li] = l;
-        layer_at<unsigned>(m, L_NIDX, slot)[li] = 0u;
+        if (act) {
+            occ[li] = l;
+            layer_at<unsigned>(m, L_NIDX, slot)[li] = 0u;
+        }
     }
 }
 

@@ -23,6 +23,7 @@
 #include "vm_shard.cuh"
 #include "vm_bucket.cuh"
 #include "vm_ndt.cuh"
+#include "vm_shard_ndt.cuh"
 #include "vm_export.cuh"
 
 using namespace vm;
@@ -102,7 +103,12 @@ struct vm_map {
     unsigned *d_bk_cnt = nullptr, *d_bk_off = nullptr;
     size_t bk_cap = 0;
     int *d_bk_big = nullptr;
-    unsigned *d_bk_perm = nullptr;   // NDT buckets, largest first (vm_ndt.cuh)
+    unsigned *d_bk_perm = nullptr;   // NDT buckets, most samples first (vm_ndt.cuh)
+    unsigned *d_bk_cnt2 = nullptr;   // NDT: samples per bucket
+    int *d_bk_big2 = nullptr;        // NDT: buckets for the block sort
+    unsigned long long *d_nbk_ctr = nullptr;  // NDT: [mid, big] sort-list lengths
+    double4 *d_nbk_pos = nullptr;    // NDT: sample end points beside their bucket slots
+    size_t nbk_pos_cap = 0;
     unsigned *d_nbk_small = nullptr; // NDT: size histogram, cursors, live count, slice cursor
     unsigned *d_bk_bits = nullptr;
     size_t bk_bits_cap = 0;
@@ -152,6 +158,9 @@ struct vm_map {
     int2 *d_smarked = nullptr;
     size_t smarked_cap = 0;
     unsigned long long *d_shard_cnt = nullptr;  // [2 + world]: nmarked, nreq, per-dest counts
+    ShardItemN *d_gx = nullptr;      // sharded NDT: the walk's ghost visit items
+    size_t gx_cap = 0;
+    unsigned long long *d_ngx = nullptr;
     struct ShardBatch {
         bool open = false, walked = false;
         int format = 0;
@@ -163,6 +172,7 @@ struct vm_map {
         int order_bits = 0, maxseg = 0, walk_slot0 = 0;
         long long nreg0 = 0, launches0 = 0;
         unsigned long long nmarks = 0, R = 0;
+        int ndt = 0;                 // NDT-OM batch (vm_shard_ndt.cuh)
         float ms_disc = 0.f, ms_walk = 0.f;
     } sb;
     unsigned epoch = 0;
@@ -485,10 +495,17 @@ int ensure_buckets(vm_map *m, size_t nmarked_cap, size_t bwords) {
         cudaFree(m->d_bk_off);
         cudaFree(m->d_bk_big);
         cudaFree(m->d_bk_perm);
+        cudaFree(m->d_bk_cnt2);
+        cudaFree(m->d_bk_big2);
         m->d_bk_cnt = nullptr;
         m->d_bk_off = nullptr;
         m->d_bk_big = nullptr;
         m->d_bk_perm = nullptr;
+        m->d_bk_cnt2 = nullptr;
+        m->d_bk_big2 = nullptr;
+        CK(cudaMalloc((void **)&m->d_bk_cnt2, nc * sizeof(unsigned)));
+        CK(cudaMemset(m->d_bk_cnt2, 0, nc * sizeof(unsigned)));
+        CK(cudaMalloc((void **)&m->d_bk_big2, nc * sizeof(int)));
         CK(cudaMalloc((void **)&m->d_bk_cnt, nc * sizeof(unsigned)));
         CK(cudaMemset(m->d_bk_cnt, 0, nc * sizeof(unsigned)));  // kept zero by the folds
         CK(cudaMalloc((void **)&m->d_bk_off, nc * sizeof(unsigned)));
@@ -553,9 +570,12 @@ int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, in
         CK(cudaMalloc((void **)&m->d_nbk_small, (2 * NBK_BINS + 4) * sizeof(unsigned)));
         CK(cudaMemset(m->d_nbk_small, 0, (2 * NBK_BINS + 4) * sizeof(unsigned)));
     }
-    NdtBuckets b{m->d_bk_cnt, m->d_bk_off, m->d_bk_perm, m->d_nbk_small, m->d_nbk_small + NBK_BINS,
-                 m->d_rec2, m->d_rec, m->d_bk_big, m->d_nbig, m->d_bk_bits, bwords, span};
-    CK(cudaMemsetAsync(m->d_nbig, 0, sizeof(unsigned long long), s));
+    if (!m->d_nbk_ctr) CK(cudaMalloc((void **)&m->d_nbk_ctr, 2 * sizeof(unsigned long long)));
+    if ((rc = ensure_buf(&m->d_nbk_pos, &m->nbk_pos_cap, m->rec_cap))) return rc;
+    NdtBuckets b{m->d_bk_cnt, m->d_bk_cnt2, m->d_bk_off, m->d_bk_perm, m->d_nbk_small,
+                 m->d_nbk_small + NBK_BINS, m->d_rec2, m->d_rec, m->d_nbk_pos, m->d_bk_big,
+                 m->d_bk_big2, m->d_nbk_ctr, m->d_nbk_ctr + 1, m->d_bk_bits, bwords, span};
+    CK(cudaMemsetAsync(m->d_nbk_ctr, 0, 2 * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(b.cursor + NBK_BINS, 0, 2 * sizeof(unsigned), s));
     const unsigned gr = (unsigned)m->num_sms * 8;
     const unsigned gm = (unsigned)std::max<long long>(
@@ -577,11 +597,14 @@ int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, in
     k_nbk_order<<<1, NBK_BINS, 0, s>>>(dm, b);
     k_nbk_perm<<<gm, BLOCK, 0, s>>>(dm, b);
     k_nbk_scatter<<<gr, BLOCK, 0, s>>>(dm, b);
+    k_nbk_sort_small<<<gm, BLOCK, 0, s>>>(dm, b);
+    k_nbk_sort_mid<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, b);
     k_nbk_sort_big<<<m->num_sms, BLOCK, 0, s>>>(dm, b);
+    k_nbk_gather<<<gr, BLOCK, 0, s>>>(dm, src, b);
     CK(cudaEventRecord(ev_mid, s));
-    if (tm) k_nbk_fold<true><<<gm, BLOCK, 0, s>>>(dm, src, b);
-    else k_nbk_fold<false><<<gm, BLOCK, 0, s>>>(dm, src, b);
-    m->launches += 7;
+    if (tm) k_nbk_fold<true><<<gm, BLOCK, 0, s>>>(dm, b);
+    else k_nbk_fold<false><<<gm, BLOCK, 0, s>>>(dm, b);
+    m->launches += 10;
     return check_launch("ndt fold");
 }
 
@@ -1326,6 +1349,8 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_rgrid);
     cudaFree(m->d_smarked);
     cudaFree(m->d_shard_cnt);
+    cudaFree(m->d_gx);
+    cudaFree(m->d_ngx);
     cudaFree(m->d_bmask);
     cudaFree(m->d_big);
     cudaFree(m->d_nbig);
@@ -1333,6 +1358,10 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_bk_off);
     cudaFree(m->d_bk_big);
     cudaFree(m->d_bk_perm);
+    cudaFree(m->d_bk_cnt2);
+    cudaFree(m->d_bk_big2);
+    cudaFree(m->d_nbk_ctr);
+    cudaFree(m->d_nbk_pos);
     cudaFree(m->d_nbk_small);
     cudaFree(m->d_bk_bits);
     cudaFree(m->d_chain);
@@ -1875,6 +1904,9 @@ DevMap shard_dm(vm_map *m) {
     dm.nmarked = m->d_shard_cnt;
     dm.marked_cap = m->smarked_cap;
     dm.walk_slot0 = m->sb.walk_slot0;
+    dm.gx = m->d_gx;
+    dm.ngx = m->d_ngx;
+    dm.gx_cap = m->gx_cap;
     return dm;
 }
 
@@ -1899,9 +1931,9 @@ int vm_shard_owner(int64_t packed_key, int32_t world) { return region_owner(pack
 
 int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, int64_t *counts_out) {
     if (!m || !rays || !counts_out) return fail(VM_ERR_ARG, "null argument");
-    if (mode != VM_MODE_OCCUPANCY || exec != VM_EXEC_DETERMINISTIC)
-        return fail(VM_ERR_ARG, "sharded maps integrate deterministic occupancy");
-    if ((m->mask & MODE_MASK[0]) != MODE_MASK[0]) return fail(VM_ERR_ARG, "map lacks layers");
+    if ((mode != VM_MODE_OCCUPANCY && mode != VM_MODE_NDT_OM) || exec != VM_EXEC_DETERMINISTIC)
+        return fail(VM_ERR_ARG, "sharded maps integrate deterministic occupancy or NDT-OM");
+    if ((m->mask & MODE_MASK[mode]) != MODE_MASK[mode]) return fail(VM_ERR_ARG, "map lacks layers");
     if (!m->d_shard_cnt) return fail(VM_ERR_ARG, "call vm_shard_config first");
     CK(cudaSetDevice(m->device));
     auto &sb = m->sb;
@@ -1936,13 +1968,23 @@ int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, i
     if (order_span >= (1ULL << 32)) return fail(VM_ERR_ARG, "batch too large for 32-bit ray order keys");
     sb.order_bits = std::max(1, bitlen(order_span));
     const long long n = std::max<long long>(sb.n, 1);
+    sb.ndt = mode == VM_MODE_NDT_OM;
     int rc;
-    if ((rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * sb.maxseg + 1))) return rc;
-    if ((rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
-    if ((rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
-    if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)n + 1))) return rc;
-    if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, rec_floor(m, n_all)))))
-        return rc;
+    if (sb.ndt) {
+        // records: the slice's samples and walk records plus imported ones
+        if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, (size_t)n_all * 8 + 1)))) return rc;
+        if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_gx, &m->gx_cap, (size_t)n * 16 + 1))) return rc;
+        if (!m->d_ngx) CK(cudaMalloc((void **)&m->d_ngx, sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(m->d_ngx, 0, sizeof(unsigned long long), m->stream));
+    } else {
+        if ((rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * sb.maxseg + 1))) return rc;
+        if ((rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)n + 1))) return rc;
+        if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, rec_floor(m, n_all)))))
+            return rc;
+    }
     sb.launches0 = m->launches;
     sb.nreg0 = m->nreg;
     CK(cudaMemsetAsync(m->d_shard_cnt, 0, (2 + (size_t)W) * sizeof(unsigned long long), m->stream));
@@ -1957,15 +1999,18 @@ int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, i
         CK(cudaEventRecord(m->ev_start, m->stream));
         if (sb.n > 0) {
             rc = with_src(m, [&](auto src) {
-                return launch_discover(m, dm, src, sb.n, VM_MODE_OCCUPANCY, 1, 1, 1, m->stream);
+                return launch_discover(m, dm, src, sb.n, mode, 1, sb.ndt ? 0 : 1, 1, m->stream);
             });
             if (rc) return rc;
         }
         const int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
         k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
-        k_seg_scan<<<1, SEG_BUCKETS, 0, m->stream>>>(dm);
-        k_seg_scatter<<<(unsigned)((n * sb.maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, m->stream>>>(dm);
-        m->launches += 4;
+        m->launches += 2;
+        if (!sb.ndt) {
+            k_seg_scan<<<1, SEG_BUCKETS, 0, m->stream>>>(dm);
+            k_seg_scatter<<<(unsigned)((n * sb.maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, m->stream>>>(dm);
+            m->launches += 2;
+        }
         CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, m->stream));
         CK(cudaMemcpyAsync(m->h_stats + NUM_STATS, m->d_cursor, sizeof(int), cudaMemcpyDeviceToHost,
@@ -1992,6 +2037,17 @@ int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, i
     CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_shard_cnt, sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
+    if (sb.ndt) {
+        // requests: every ghost region of the slice's prefetch set (touched list)
+        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_stats + S_WALK_TOUCHED,
+                           sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        counts_out[0] = (int64_t)m->h_stats[NUM_STATS + 2];
+        counts_out[1] = 0;
+        sb.nmarks = 0;
+        sb.open = true;
+        return VM_OK;
+    }
     sb.nmarks = std::min<unsigned long long>(m->h_stats[NUM_STATS + 2], m->smarked_cap);
     counts_out[0] = (int64_t)(m->nreg - sb.nreg0);  // new regions (bound on the requests)
     counts_out[1] = (int64_t)sb.nmarks;
@@ -2007,13 +2063,18 @@ int vm_shard_lists(vm_map *m, int64_t *req_out, int64_t req_cap, int64_t *marks_
     auto &sb = m->sb;
     const int W = m->shard_world;
     int rc;
-    if ((long long)sb.nmarks > marks_cap || req_cap < m->nreg - sb.nreg0)
+    if ((long long)sb.nmarks > marks_cap || (!sb.ndt && req_cap < m->nreg - sb.nreg0))
         return fail(VM_ERR_ARG, "vm_shard_lists: buffers smaller than vm_shard_begin's counts");
     CK(cudaMemsetAsync(m->d_shard_cnt + 2, 0, (size_t)W * sizeof(unsigned long long), m->stream));
     DevMap dm = shard_dm(m);
-    k_shard_lists<<<m->num_sms * 2, BLOCK, 0, m->stream>>>(
-        dm, (int)sb.nreg0, (int)m->nreg, (long long *)req_out, m->d_shard_cnt + 2,
-        (unsigned long long)req_cap, (long long *)marks_out, sb.nmarks);
+    if (sb.ndt)
+        k_shard_ndt_req<<<m->num_sms * 2, BLOCK, 0, m->stream>>>(dm, (long long *)req_out,
+                                                                 m->d_shard_cnt + 2,
+                                                                 (unsigned long long)req_cap);
+    else
+        k_shard_lists<<<m->num_sms * 2, BLOCK, 0, m->stream>>>(
+            dm, (int)sb.nreg0, (int)m->nreg, (long long *)req_out, m->d_shard_cnt + 2,
+            (unsigned long long)req_cap, (long long *)marks_out, sb.nmarks);
     m->launches += 1;
     if ((rc = check_launch("shard lists"))) return rc;
     std::vector<unsigned long long> nreq((size_t)W);
@@ -2059,6 +2120,43 @@ int vm_shard_prepare(vm_map *m, const int64_t *req_in, int64_t nreq, const int64
     return VM_OK;
 }
 
+int vm_shard_ndt_bits(vm_map *m, const int64_t *req_in, int64_t nreq, uint32_t *bits_out) {
+    if (!m || !m->sb.open || m->sb.walked || !m->sb.ndt)
+        return fail(VM_ERR_ARG, "no discovered sharded NDT batch");
+    if (nreq > 0 && (!req_in || !bits_out)) return fail(VM_ERR_ARG, "null argument");
+    CK(cudaSetDevice(m->device));
+    int rc;
+    if ((rc = shard_headroom(m, nreq))) return rc;
+    DevMap dm = shard_dm(m);
+    if (nreq > 0) {
+        const int words = (m->vpr + 31) / 32;
+        k_shard_ndt_bits<<<(unsigned)std::min<long long>(nreq, 4096), BLOCK, 0, m->stream>>>(
+            dm, (const long long *)req_in, nreq, bits_out, words);
+        m->launches += 1;
+        if ((rc = check_launch("shard ndt bits"))) return rc;
+    }
+    int cursor;
+    if ((rc = read_cursor(m, &cursor))) return rc;
+    m->nreg = cursor;
+    return VM_OK;
+}
+
+int vm_shard_ndt_mark(vm_map *m, const int64_t *keys, const uint32_t *bits, int64_t n) {
+    if (!m || !m->sb.open || m->sb.walked || !m->sb.ndt)
+        return fail(VM_ERR_ARG, "no discovered sharded NDT batch");
+    if (n > 0 && (!keys || !bits)) return fail(VM_ERR_ARG, "null argument");
+    CK(cudaSetDevice(m->device));
+    DevMap dm = shard_dm(m);
+    if (n > 0) {
+        const int words = (m->vpr + 31) / 32;
+        k_shard_ndt_mark<<<(unsigned)std::min<long long>(n, 4096), BLOCK, 0, m->stream>>>(
+            dm, (const long long *)keys, bits, n, words);
+        m->launches += 1;
+    }
+    m->sb.walk_slot0 = (int)m->nreg;
+    return check_launch("shard ndt mark");
+}
+
 int vm_shard_walk(vm_map *m) {
     if (!m || !m->sb.open || m->sb.walked) return fail(VM_ERR_ARG, "no sharded batch to walk");
     CK(cudaSetDevice(m->device));
@@ -2067,7 +2165,17 @@ int vm_shard_walk(vm_map *m) {
     DevMap dm = shard_dm(m);
     CK(cudaMemsetAsync(m->d_work, 0, sizeof(unsigned long long), m->stream));
     CK(cudaEventRecord(m->ev_w0, m->stream));
-    if (m->sb.n > 0) {
+    if (m->sb.n > 0 && m->sb.ndt) {
+        dm.ray_order = 0;
+        const long long n = m->sb.n;
+        rc = with_src(m, [&](auto src) {
+            k_walk_ndt<false, true, false><<<(unsigned)((n + BLOCK - 1) / BLOCK), BLOCK, 0,
+                                             m->stream>>>(dm, src, n);
+            return check_launch("shard ndt walk");
+        });
+        if (rc) return rc;
+        m->launches += 1;
+    } else if (m->sb.n > 0) {
         const dim3 pgrid((unsigned)std::max<long long>(
             1, std::min<long long>((long long)WK_BLOCKS * m->num_sms, (m->sb.n * 3 + BLOCK - 1) / BLOCK)));
         rc = with_src(m, [&](auto src) {
@@ -2104,13 +2212,22 @@ int vm_shard_export(vm_map *m, void *out, int64_t cap_per_dest, int64_t *per_des
     DevMap dm = shard_dm(m);
     CK(cudaMemsetAsync(m->d_shard_cnt + 2, 0, (size_t)W * sizeof(unsigned long long), m->stream));
     const unsigned long long cap = (unsigned long long)std::max<int64_t>(cap_per_dest, 0);
-    if (R > 0)
+    if (m->sb.ndt) {
+        unsigned long long ng = 0;
+        CK(cudaMemcpy(&ng, m->d_ngx, sizeof(ng), cudaMemcpyDeviceToHost));
+        if (ng > m->gx_cap) return fail(VM_ERR_OOM, "ghost visit buffer overflow in a sharded batch");
+        k_shard_ndt_export<<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm, R, (ShardItemN *)out,
+                                                                    m->d_shard_cnt + 2, cap);
+        m->launches += 1;
+    } else if (R > 0)
         k_shard_export_rec<<<(unsigned)std::min<unsigned long long>((R + BLOCK - 1) / BLOCK, 4096),
                              BLOCK, 0, m->stream>>>(dm, m->d_rec, (long long)R, (ShardItem *)out,
                                                     m->d_shard_cnt + 2, cap);
-    k_shard_export_cnt<<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm, (ShardItem *)out,
-                                                                m->d_shard_cnt + 2, cap);
-    m->launches += 2;
+    if (!m->sb.ndt) {
+        k_shard_export_cnt<<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm, (ShardItem *)out,
+                                                                    m->d_shard_cnt + 2, cap);
+        m->launches += 2;
+    }
     int rc;
     if ((rc = check_launch("shard export"))) return rc;
     std::vector<unsigned long long> cnt((size_t)W);
@@ -2134,14 +2251,25 @@ int vm_shard_import(vm_map *m, const void *in, int64_t n) {
         const unsigned g = (unsigned)std::min<long long>((n + BLOCK - 1) / BLOCK, 8192);
         {
             DevMap dm = shard_dm(m);
-            k_shard_import_regions<<<g, BLOCK, 0, m->stream>>>(dm, (const ShardItem *)in, n);
+            if (m->sb.ndt)
+                k_shard_ndt_import_regions<<<g, BLOCK, 0, m->stream>>>(dm, (const ShardItemN *)in, n);
+            else
+                k_shard_import_regions<<<g, BLOCK, 0, m->stream>>>(dm, (const ShardItem *)in, n);
         }
         int cursor;
         if ((rc = read_cursor(m, &cursor))) return rc;
         m->nreg = cursor;
         if ((rc = shard_headroom(m, 0))) return rc;  // covers every slot pass 1 handed out
         DevMap dm = shard_dm(m);
-        k_shard_import<<<g, BLOCK, 0, m->stream>>>(dm, (const ShardItem *)in, n);
+        if (m->sb.ndt) {
+            rc = with_src(m, [&](auto src) {
+                k_shard_ndt_import<<<g, BLOCK, 0, m->stream>>>(dm, src, (const ShardItemN *)in, n);
+                return VM_OK;
+            });
+            if (rc) return rc;
+        } else {
+            k_shard_import<<<g, BLOCK, 0, m->stream>>>(dm, (const ShardItem *)in, n);
+        }
         m->launches += 2;
         if ((rc = check_launch("shard import"))) return rc;
     }
@@ -2164,6 +2292,51 @@ int vm_shard_finish(vm_map *m, vm_stats *out) {
     CK(cudaStreamSynchronize(m->stream));
     const unsigned long long Rtot = std::min<unsigned long long>(m->h_stats[S_RECORDS], m->rec_cap);
     if (m->h_stats[S_RECORDS] > m->rec_cap) return fail(VM_ERR_OOM, "record buffer overflow on import");
+    if (sb.ndt) {
+        // ghost state out, then the single-GPU tail: resolve, buckets, fold
+        DevMap dm = shard_dm(m);
+        k_shard_ndt_clear<<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
+        CK(cudaEventRecord(m->ev_k1, m->stream));
+        k_resolve<true, false><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
+        CK(cudaEventRecord(m->ev_res, m->stream));
+        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_shard_cnt, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        if (m->h_stats[NUM_STATS + 2] > m->smarked_cap)
+            return fail(VM_ERR_OOM, "voxel index overflow in a sharded NDT batch");
+        rc = with_src(m, [&](auto src) {
+            return launch_ndt_fold(m, dm, src, sb.n_all, sb.maxseg, false, m->ev_sort);
+        });
+        if (rc) return rc;
+        m->launches += 2;
+        CK(cudaEventRecord(m->ev_end, m->stream));
+        CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, m->stream));
+        CK(cudaStreamSynchronize(m->stream));
+        if ((rc = check_launch("shard finish"))) return rc;
+        const unsigned long long *hs = m->h_stats;
+        std::memset(out, 0, sizeof(*out));
+        out->rays_in = sb.n;
+        out->rays_processed = (int64_t)hs[S_PROCESSED];
+        out->segments = (int64_t)hs[S_SEGMENTS];
+        out->voxel_visits = (int64_t)hs[S_VISITS];
+        out->region_misses = (int64_t)hs[S_RMISS];
+        out->regions_touched = (int64_t)hs[S_PREF_TOUCHED];
+        out->records = (int64_t)Rtot;
+        out->regions_total = cursor;
+        out->new_regions = cursor - sb.nreg0;
+        out->touched_regions_walk = (int64_t)hs[S_WALK_TOUCHED];
+        out->launches = m->launches - sb.launches0;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, m->ev_start, m->ev_end) == cudaSuccess) out->gpu_ms = ms;
+        if (cudaEventElapsedTime(&ms, m->ev_w0, m->ev_w1) == cudaSuccess) out->walk_ms = ms;
+        if (cudaEventElapsedTime(&ms, m->ev_k1, m->ev_res) == cudaSuccess) out->resolve_ms = ms;
+        if (cudaEventElapsedTime(&ms, m->ev_res, m->ev_sort) == cudaSuccess) out->sort_ms = ms;
+        if (cudaEventElapsedTime(&ms, m->ev_sort, m->ev_end) == cudaSuccess) out->fold_ms = ms;
+        m->max_growth = std::max<long long>(m->max_growth, cursor - sb.nreg0);
+        sb.open = false;
+        return VM_OK;
+    }
     const int vbits = std::max(1, bitlen((unsigned long long)(cursor + 1) * m->vpr));
     const int end_bit = std::min(64, sb.order_bits + vbits);
     DevMap dm = shard_dm(m);
@@ -2218,3 +2391,51 @@ int vm_shard_finish(vm_map *m, vm_stats *out) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// L2-atomic ceiling probe (vm_probe_red_rate): the roofline of the walk's
+// per-visit RED.ADD, measured on the device at hand.
+namespace {
+__global__ void __launch_bounds__(256) k_red_probe(unsigned *buf, unsigned mask, int per_thread) {
+    unsigned x = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u + 12345u;
+#pragma unroll 8
+    for (int i = 0; i < per_thread; ++i) {
+        x = x * 1664525u + 1013904223u;  // LCG: one IMAD per RED
+        red_add(buf + ((x >> 7) & mask), 1u);
+    }
+}
+}  // namespace
+
+int vm_probe_red_rate(int32_t device, int64_t footprint_bytes, int32_t reps, double *out) {
+    if (!out || footprint_bytes < 4096 || reps < 1) return fail(VM_ERR_ARG, "bad probe arguments");
+    CK(cudaSetDevice(device));
+    unsigned long long words = 1;
+    while (words * 2 * 4 <= (unsigned long long)footprint_bytes) words <<= 1;
+    unsigned *buf = nullptr;
+    CK(cudaMalloc(&buf, words * 4));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int blocks = sms * 8, per = 1024;
+    double best = 0.0;
+    cudaMemset(buf, 0, words * 4);
+    k_red_probe<<<blocks, 256>>>(buf, (unsigned)(words - 1), per);  // warm-up
+    for (int r = 0; r < reps; ++r) {
+        cudaEventRecord(e0);
+        k_red_probe<<<blocks, 256>>>(buf, (unsigned)(words - 1), per);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms > 0.f) best = std::max(best, (double)blocks * 256.0 * per / (ms * 1e-3));
+    }
+    cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    if (err != cudaSuccess) return fail(VM_ERR_CUDA, std::string("red probe: ") + cudaGetErrorString(err));
+    *out = best;
+    return VM_OK;
+}

@@ -16,8 +16,16 @@ handed the whole batch.  Per batch (protocol in csrc/vm_shard.cuh):
   exchange B      payload all-to-all
   import, finish  owners apply the payload, then resolve / sort / fold
 
+NDT-OM (mode="ndt-om", csrc/vm_shard_ndt.cuh) replaces the sample-voxel
+marks with Gaussian bitmaps: every rank requests the bitmaps (count >= 3 at
+the start of the batch) of the ghost regions its slice prefetched, its walk
+sends each visit through a ghost Gaussian voxel to the owner with the
+segment order and chord (t0, t1), and the owner weighs it with its own
+Gaussian -- so phase 1 is complete before any phase-2 update, as in the
+reference (engine.py:285).
+
 The union of the ranks' owned regions is the single-GPU map, bit for bit
-(tests/test_gpu_sharded.py).  Deterministic occupancy only.
+(tests/test_gpu_sharded.py), for deterministic occupancy and NDT-OM.
 """
 from __future__ import annotations
 
@@ -29,7 +37,8 @@ from .keys import unpack_region_coord
 from .layers import MODE_LAYERS
 from .store import VoxelMap
 
-ITEM_WORDS = 2  # a 16-byte ShardItem as two int64
+ITEM_WORDS = 2      # a 16-byte ShardItem as two int64
+ITEM_WORDS_NDT = 4  # a 32-byte ShardItemN (NDT-OM) as four int64
 
 
 def _torch():
@@ -53,7 +62,11 @@ class ShardedVoxelMap:
     """This rank's part of a region-sharded map."""
 
     def __init__(self, cfg, rank: int, world: int, device: int = 0,
-                 layer_names=MODE_LAYERS["occupancy"], initial_regions: int = 1024):
+                 layer_names=None, initial_regions: int = 1024, mode: str = "occupancy"):
+        if mode not in ("occupancy", "ndt-om"):
+            raise ValueError("sharded maps integrate deterministic occupancy or NDT-OM")
+        self.mode = mode
+        layer_names = MODE_LAYERS[mode] if layer_names is None else layer_names
         self.cfg = cfg
         self.rank, self.world, self.device = int(rank), int(world), int(device)
         self.vmap = VoxelMap(cfg, layer_names, device=self.device, initial_regions=initial_regions)
@@ -94,13 +107,33 @@ class ShardedVoxelMap:
         self._keep = records_dev
         self.vmap.flush_host_writes()
         self.vmap.batch_counter += 1
-        nnew, nmarks = self.nat.shard_begin(rays)
+        nnew, nmarks = self.nat.shard_begin(rays, self.mode)
         req = torch.empty((self.world, max(nnew, 1)), dtype=torch.int64, device=self.dev)
         marks = torch.empty((max(nmarks, 1), 2), dtype=torch.int64, device=self.dev)
         counts = self.nat.shard_lists(req.data_ptr(), req.shape[1], marks.data_ptr(), marks.shape[0],
                                       self.world)
         sends = [req[d, :counts[1 + d]] for d in range(self.world)]
         return sends, marks[:counts[0]]
+
+    # ---- NDT-OM: Gaussian bitmaps of the ghost regions ------------------
+
+    @property
+    def bit_words(self) -> int:
+        return (self.cfg.region_dim ** 3 + 31) // 32
+
+    def ndt_bits(self, req_in):
+        """Owner side: the bitmaps of the regions other ranks requested
+        (int32 [n, words] device tensor, in request order)."""
+        torch = _torch()
+        req_in = req_in.contiguous()
+        out = torch.empty((max(req_in.numel(), 1), self.bit_words), dtype=torch.int32, device=self.dev)
+        self.nat.shard_ndt_bits(req_in.data_ptr(), req_in.numel(), out.data_ptr())
+        return out[:req_in.numel()]
+
+    def ndt_mark(self, keys, bits):
+        keys = keys.contiguous()
+        bits = bits.contiguous()
+        self.nat.shard_ndt_mark(keys.data_ptr(), bits.data_ptr(), keys.numel())
 
     def prepare(self, req_in, marks_all):
         req_in = req_in.contiguous()
@@ -113,8 +146,9 @@ class ShardedVoxelMap:
 
     def export(self):
         torch = _torch()
+        words = ITEM_WORDS if self.mode == "occupancy" else ITEM_WORDS_NDT
         while True:
-            out = torch.empty((self.world, self._cap, ITEM_WORDS), dtype=torch.int64, device=self.dev)
+            out = torch.empty((self.world, self._cap, words), dtype=torch.int64, device=self.dev)
             rc, counts = self.nat.shard_export(out.data_ptr(), self._cap, self.world)
             if rc == _native.VM_OK:
                 return [out[d, :counts[d]] for d in range(self.world)]
@@ -214,8 +248,18 @@ def _submit_sharded(smap: ShardedVoxelMap, records, group=None) -> BatchStats:
     wire = (lambda t: t.cpu()) if host else (lambda t: t)
     rec = _to_device(records, dev)
     sends, marks = smap.begin(rec)
-    req_in = torch.cat(exchange_all_to_all([wire(t) for t in sends], group)).to(dev)
-    smap.prepare(req_in, exchange_all_gather(wire(marks), group).to(dev))
+    if smap.mode == "ndt-om":
+        # requests out, Gaussian bitmaps back (in request order), then mark
+        got = exchange_all_to_all([wire(t) for t in sends], group)
+        answers = [smap.ndt_bits(t.to(dev)) for t in got]
+        back = exchange_all_to_all([wire(a) for a in answers], group)
+        smap.ndt_mark(torch.cat(sends), torch.cat([b.to(dev) for b in back]))
+        answered = sum(int(a.numel() * a.element_size()) for r, a in enumerate(answers)
+                       if r != dist.get_rank(group))
+    else:
+        req_in = torch.cat(exchange_all_to_all([wire(t) for t in sends], group)).to(dev)
+        smap.prepare(req_in, exchange_all_gather(wire(marks), group).to(dev))
+        answered = 0
     smap.walk()
     exported = smap.export()
     items = torch.cat(exchange_all_to_all([wire(t) for t in exported], group)).to(dev)
@@ -228,6 +272,7 @@ def _submit_sharded(smap: ShardedVoxelMap, records, group=None) -> BatchStats:
     sent = sum(int(t.numel() * t.element_size()) for r, t in enumerate(sends) if r != me)
     sent += int(marks.numel() * marks.element_size()) * (world - 1)
     sent += sum(int(t.numel() * t.element_size()) for r, t in enumerate(exported) if r != me)
+    sent += answered
     v = torch.tensor([st.rays_in, st.rays_processed, st.segments, st.voxel_visits,
                       st.region_misses, st.records, sent], dtype=torch.int64,
                      device="cpu" if host else dev)
@@ -257,10 +302,19 @@ def _submit_virtual(smaps, records) -> BatchStats:
     world = len(smaps)
     recs = [_to_device(records, s.dev) for s in smaps]
     begun = [s.begin(r) for s, r in zip(smaps, recs)]
-    marks_all = [torch.cat([m.to(s.dev) for _, m in begun]) for s in smaps]
-    for r, s in enumerate(smaps):
-        req_in = torch.cat([begun[q][0][r].to(s.dev) for q in range(world)])
-        s.prepare(req_in, marks_all[r])
+    if smaps[0].mode == "ndt-om":
+        # answers[r][q]: rank r's bitmaps for rank q's requests
+        answers = [[s.ndt_bits(begun[q][0][r].to(s.dev)) for q in range(world)]
+                   for r, s in enumerate(smaps)]
+        for q, s in enumerate(smaps):
+            keys = torch.cat([begun[q][0][r] for r in range(world)])
+            bits = torch.cat([answers[r][q].to(s.dev) for r in range(world)])
+            s.ndt_mark(keys, bits)
+    else:
+        marks_all = [torch.cat([m.to(s.dev) for _, m in begun]) for s in smaps]
+        for r, s in enumerate(smaps):
+            req_in = torch.cat([begun[q][0][r].to(s.dev) for q in range(world)])
+            s.prepare(req_in, marks_all[r])
     for s in smaps:
         s.walk()
     exports = [s.export() for s in smaps]

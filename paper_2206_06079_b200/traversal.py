@@ -92,27 +92,26 @@ def walk_regions(ray: RaySample, cfg) -> list[tuple[int, int, int]]:
 
 
 def clip_ray(ray: RaySample, cfg) -> RaySample:
-    """traversal.py:140-150: rays beyond max range become miss-only."""
+    """traversal.py:140-150: a ray longer than max_ray_range is cut to it and
+    keeps no sample (miss evidence only)."""
     length = ray.length
-    if length <= cfg.max_ray_range:
-        return ray
-    direction = (ray.end - ray.origin) / length
-    return replace(ray, end=ray.origin + direction * cfg.max_ray_range, has_sample=False)
+    if length > cfg.max_ray_range:
+        unit = (ray.end - ray.origin) / length
+        ray = replace(ray, end=ray.origin + unit * cfg.max_ray_range, has_sample=False)
+    return ray
 
 
 def segment_ray(ray: RaySample, cfg) -> list[RaySample]:
-    """traversal.py:153-178: split into <= segment_length pieces."""
-    length = ray.length
-    seg = cfg.segment_length
-    if length <= seg:
+    """traversal.py:153-178: pieces of at most segment_length along the ray;
+    the last piece ends exactly at ray.end and alone keeps has_sample.  (The
+    device does the same arithmetic: csrc/vm_device.cuh segment_of.)"""
+    length, step = ray.length, cfg.segment_length
+    if length <= step:
         return [ray]
-    count = math.ceil(length / seg)
-    direction = (ray.end - ray.origin) / length
-    out = []
-    for i in range(count):
-        t1 = min((i + 1) * seg, length)
-        last = i == count - 1
-        out.append(replace(ray, origin=ray.origin + direction * (i * seg),
-                           end=ray.end if last else ray.origin + direction * t1,
-                           has_sample=ray.has_sample if last else False))
-    return out
+    pieces = math.ceil(length / step)
+    unit = (ray.end - ray.origin) / length
+    starts = [ray.origin + unit * (i * step) for i in range(pieces)]
+    ends = [ray.origin + unit * min((i + 1) * step, length) for i in range(pieces - 1)]
+    ends.append(ray.end)
+    flags = [False] * (pieces - 1) + [ray.has_sample]
+    return [replace(ray, origin=o, end=e, has_sample=h) for o, e, h in zip(starts, ends, flags)]

@@ -250,3 +250,51 @@ def test_submit_batches_ndt_prefetched_matches_per_batch():
             u = region.buffers[name].astype(np.float64)
             v = b.regions[rk].buffers[name].astype(np.float64)
             assert np.array_equal(u, v), (rk, name)
+
+
+@pytest.mark.slow
+def test_c4_uav_tsdf_then_decay_prefix_vs_oracle():
+    """configs[3] (C4): the UAV lawnmower scans at 0.05 m, per batch a TSDF
+    pass then a decay pass over one map holding both layer sets
+    (test_acceptance.py:398-399); two scans (262k rays).  tsdf, occupancy,
+    mean, mean_count and decay_hits bit-exact, decay_distance within 1e-9
+    (f64 REDs, test_engine.py:56-58)."""
+    cfg = MapConfig(voxel_size=0.05)
+    names = tuple(dict.fromkeys(MODE_LAYERS["tsdf"] + MODE_LAYERS["decay"]))
+    vm = VoxelMap(cfg, names)
+    om = orc.OracleMap(cfg, names)
+    for rec in scans.uav_lawnmower_scans(2):
+        for mode in ("tsdf", "decay"):
+            st = submit_batch(vm, rec, mode, ExecutorOptions(deterministic=True))
+            ost = om.integrate_records(rec, mode)
+            assert (st.voxel_visits, st.segments) == (ost["voxel_visits"], ost["segments"])
+            assert st.region_misses == 0
+    assert set(vm.regions) == set(om.region_keys())
+    for rk, region in vm.regions.items():
+        for name in names:
+            a, b = region.buffers[name], om.layer(rk, name)
+            if name == "decay_distance":
+                assert np.max(np.abs(a - b), initial=0.0) <= 1e-9, rk
+            else:
+                assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (rk, name)
+
+
+@pytest.mark.slow
+def test_c5_town_ndt_om_prefix_bit_exact():
+    """configs[4] (C5) on one GPU: town scans from the start of the drive and
+    from a corner 1.5 km in (the sequence regenerates from any scan), NDT-OM
+    at 0.1 m, bit-exact to the C oracle on every layer."""
+    data = scans.town_scans(0, 3) + scans.town_scans(2400, 2)
+    names = MODE_LAYERS["ndt-om"]
+    vm = VoxelMap(MapConfig(), names)
+    om = orc.OracleMap(MapConfig(), names)
+    for rec in data:
+        st = submit_batch(vm, rec, "ndt-om", ExecutorOptions(deterministic=True))
+        ost = om.integrate_records(rec, "ndt-om")
+        assert (st.voxel_visits, st.segments) == (ost["voxel_visits"], ost["segments"])
+        assert st.region_misses == 0
+    assert set(vm.regions) == set(om.region_keys())
+    for rk, region in vm.regions.items():
+        for name in names:
+            assert np.array_equal(region.buffers[name].view(np.uint8),
+                                  om.layer(rk, name).view(np.uint8)), (rk, name)

@@ -18,8 +18,8 @@ LAYERS = MODE_LAYERS["occupancy"]
 CASES = [c for c in load_cases() if c["mode"] == "occupancy"]
 
 
-def _sharded(cfg, batches, world):
-    smaps = [ShardedVoxelMap(cfg, r, world, device=0) for r in range(world)]
+def _sharded(cfg, batches, world, mode="occupancy"):
+    smaps = [ShardedVoxelMap(cfg, r, world, device=0, mode=mode) for r in range(world)]
     stats = [submit_batch_virtual(smaps, b) for b in batches]
     return smaps, stats
 
@@ -54,7 +54,7 @@ def test_sharded_scan_sequence_matches_single_gpu():
             assert np.array_equal(buf.view(np.uint8), single.regions[rk].buffers[name].view(np.uint8)), (rk, name)
 
 
-def _dist_worker(rank, world, port, batches, q):
+def _dist_worker(rank, world, port, batches, q, mode="occupancy", vox=0.05):
     import os
 
     import torch
@@ -65,11 +65,11 @@ def _dist_worker(rank, world, port, batches, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
-        smap = ShardedVoxelMap(MapConfig(voxel_size=0.05), rank, world, device=0)
+        smap = ShardedVoxelMap(MapConfig(voxel_size=vox), rank, world, device=0, mode=mode)
         tot = 0
         for b in batches:
             tot += submit_batch_sharded(smap, b).voxel_visits
-        owned = {rk: {n: r.buffers[n].copy() for n in LAYERS}
+        owned = {rk: {n: r.buffers[n].copy() for n in MODE_LAYERS[mode]}
                  for rk, r in smap.owned_regions().items()}
         q.put((rank, tot, owned))
     finally:
@@ -109,3 +109,97 @@ def test_sharded_distributed_driver_two_processes():
     for rk, layers in merged.items():
         for n in LAYERS:
             assert np.array_equal(layers[n].view(np.uint8), single.regions[rk].buffers[n].view(np.uint8))
+
+
+# ---- NDT-OM: Gaussian bitmaps out, weighed ghost visits in (vm_shard_ndt.cuh)
+
+NDT_CASES = [c for c in load_cases() if c["mode"] == "ndt-om"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", NDT_CASES, ids=[c["name"] for c in NDT_CASES])
+def test_sharded_ndt_matches_reference_golden(case, world):
+    """Every NDT-OM layer of the union of owned regions has the reference's
+    own digest (the single-GPU NDT path is bit-exact to it)."""
+    cfg = MapConfig(**case["cfg"])
+    smaps, stats = _sharded(cfg, case["batches"], world, "ndt-om")
+    for j, st in enumerate(stats):
+        want = case["stats"][j].tolist()
+        assert [st.rays_in, st.rays_processed, st.segments, st.voxel_visits] == want[:4]
+        assert st.region_misses == 0
+    for name in MODE_LAYERS["ndt-om"]:
+        bufs = gather_owned(smaps, name)
+        assert sorted(bufs) == [tuple(r) for r in case["regions"].tolist()]
+        assert digest(list(bufs), lambda rk: bufs[rk]) == case["digests"][name], name
+
+
+def _single(cfg, batches, mode):
+    single = VoxelMap(cfg, MODE_LAYERS[mode])
+    visits = 0
+    for b in batches:
+        visits += submit_batch(single, b, mode, ExecutorOptions(deterministic=True)).voxel_visits
+    return single, visits
+
+
+def _assert_union_equals(bufs_by_name, single, names):
+    for name in names:
+        bufs = bufs_by_name(name)
+        assert set(bufs) == set(single.regions)
+        for rk, buf in bufs.items():
+            assert np.array_equal(buf.view(np.uint8),
+                                  single.regions[rk].buffers[name].view(np.uint8)), (rk, name)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_ndt_tunnel_scans_match_single_gpu(world):
+    """Four C3 tunnel scans: from the second scan on, most misses cross
+    Gaussian voxels, many of them other ranks' -- weighed by their owners."""
+    cfg = MapConfig()
+    batches = scans.os64_tunnel_scans(4)
+    single, visits = _single(cfg, batches, "ndt-om")
+    smaps, stats = _sharded(cfg, batches, world, "ndt-om")
+    assert sum(s.voxel_visits for s in stats) == visits
+    _assert_union_equals(lambda n: gather_owned(smaps, n), single, MODE_LAYERS["ndt-om"])
+
+
+@pytest.mark.slow
+def test_sharded_ndt_town_scans_match_single_gpu():
+    """configs[4] (C5) -- NDT-OM over region-sharded ranks -- on a prefix:
+    three town scans, 8 virtual ranks."""
+    cfg = MapConfig()
+    batches = scans.town_scans(0, 3)
+    single, visits = _single(cfg, batches, "ndt-om")
+    smaps, stats = _sharded(cfg, batches, 8, "ndt-om")
+    assert sum(s.voxel_visits for s in stats) == visits
+    _assert_union_equals(lambda n: gather_owned(smaps, n), single, MODE_LAYERS["ndt-om"])
+
+
+def test_sharded_ndt_distributed_driver_two_processes():
+    """submit_batch_sharded for NDT-OM in two processes over gloo."""
+    import socket
+
+    import torch.multiprocessing as mp
+    cfg = MapConfig()
+    batches = [t[::4].copy() for t in scans.os64_tunnel_scans(3)]
+    single, visits = _single(cfg, batches, "ndt-om")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, batches, q, "ndt-om", 0.1))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    merged = {}
+    for rank, tot, owned in res:
+        assert tot == visits
+        assert not set(merged) & set(owned)
+        merged.update(owned)
+    _assert_union_equals(lambda n: {rk: v[n] for rk, v in merged.items()}, single,
+                         MODE_LAYERS["ndt-om"])
