@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=("c2", "c1", "c3"), default="c2")
+    ap.add_argument("--workload", choices=("c2", "c1", "c3", "c4", "c5"), default="c2")
     ap.add_argument("--exec", dest="exec_", choices=("det", "cas"), default="det")
     ap.add_argument("--batches", type=int, default=1000, help="C2 batches per step")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -81,11 +81,29 @@ def workload(name: str, batches: int):
         desc = dict(workload="C1: one synthetic OS1-64 scan", scans=1, rays_per_batch=131072,
                     voxel_size=0.1, region_dim=32, mode="occupancy")
         mode = "occupancy"
-    else:
+    elif name == "c3":
         cfg = MapConfig(voxel_size=0.1)
         data = scans.os64_tunnel_scans(77)
         desc = dict(workload="C3: synthetic OS1-64 tunnel, NDT-OM", scans=77,
                     rays_per_batch=131072, voxel_size=0.1, region_dim=32, mode="ndt-om")
+        mode = "ndt-om"
+    elif name == "c4":
+        # configs[3]: TSDF + decay at 0.05 m from the UAV; a bounded prefix of
+        # the 382-scan flight (the modes alternate per batch on one map)
+        cfg = MapConfig(voxel_size=0.05)
+        data = scans.uav_lawnmower_scans(min(batches, 40))
+        desc = dict(workload="C4: synthetic UAV lawnmower, TSDF then decay per scan",
+                    scans=len(data), of_scans=scans.UAV_SCANS, rays_per_batch=131072,
+                    voxel_size=0.05, region_dim=32, mode="tsdf+decay")
+        mode = "tsdf+decay"
+    else:
+        # configs[4]: NDT-OM at 0.1 m through the procedural town; a bounded
+        # window of the 7,630-scan loop (any window regenerates on its own)
+        cfg = MapConfig(voxel_size=0.1)
+        data = scans.town_scans(0, min(batches, 77))
+        desc = dict(workload="C5: synthetic town loop, NDT-OM", scans=len(data),
+                    of_scans=scans.TOWN_SCANS, rays_per_batch=131072, voxel_size=0.1,
+                    region_dim=32, mode="ndt-om")
         mode = "ndt-om"
     return cfg, mode, data, desc
 
@@ -252,7 +270,10 @@ def run_gpu_workload(name, args, dev, torch, world=1, dist=None, steps=None, e2e
     d_rec = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
     base = d_rec.data_ptr()
     stream = torch.cuda.current_stream()
-    vmap = VoxelMap(cfg, MODE_LAYERS[mode], device=dev, initial_regions=4096)
+    # C4 alternates two modes per batch on one map (test_acceptance.py:398-399)
+    modes = mode.split("+")
+    names = tuple(dict.fromkeys(sum((MODE_LAYERS[x] for x in modes), ())))
+    vmap = VoxelMap(cfg, names, device=dev, initial_regions=4096)
     vmap._native.set_stream(stream.cuda_stream)
     keys = ("discover_ms", "walk_ms", "resolve_ms", "sort_ms", "fold_ms", "gpu_ms")
 
@@ -261,7 +282,9 @@ def run_gpu_workload(name, args, dev, torch, world=1, dist=None, steps=None, e2e
         tot = dict(S=0, V=0, launches=0, batches=0, records=0, rmiss=0, **{k: 0.0 for k in keys})
         rays = [_native.rays_from_records(sizes[b], base + int(offsets[b]) * 40)
                 for b in range(len(data))]
-        if args.per_batch:
+        if len(modes) > 1:
+            sts = [vmap._native.integrate(r, x, det) for r in rays for x in modes]
+        elif args.per_batch:
             sts = [vmap._native.integrate(r, mode, det) for r in rays]
         else:
             sts = vmap._native.integrate_many(rays, mode, det)
@@ -308,7 +331,11 @@ def run_gpu_workload(name, args, dev, torch, world=1, dist=None, steps=None, e2e
         slices = [hv[offsets[b]:offsets[b + 1]] for b in range(len(data))]
 
         def run_e2e(batches):
-            if args.per_batch or len(batches) == 1:
+            if len(modes) > 1:
+                for x in batches:
+                    for md in modes:
+                        submit_batch(vmap, x, md, opts)
+            elif args.per_batch or len(batches) == 1:
                 for x in batches:
                     submit_batch(vmap, x, mode, opts)
             else:
@@ -367,7 +394,7 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    if world > 1 and not args.replicas and args.workload in ("c1", "c2") and \
+    if world > 1 and not args.replicas and args.workload in ("c1", "c2", "c3", "c5") and \
             args.exec_ == "det":
         run_sharded(args, world, rank, dev, dist)
         dist.destroy_process_group()
@@ -385,6 +412,11 @@ def main():
     if mode == "occupancy":
         bytes_launch = algorithmic_bytes(s0["S"], s0["V"], r["H"]) / max(1, s0["batches"])
         kernel = "k_walk_det" if det else "k_walk"
+    elif mode == "tsdf+decay":
+        # TSDF 49 S_sample + 16 V_band, decay B_occ + 16 V + 8 H (both
+        # passes' visits are summed in V; the byte figure is a lower bound)
+        bytes_launch = (algorithmic_bytes(s0["S"], s0["V"], r["H"]) + 16 * s0["V"]) / max(1, s0["batches"])
+        kernel = "k_walk (tsdf, decay)"
     else:
         wb, _ = ndt_bytes(s0["S"], s0["V"], r["H"], s0["records"] - r["H"], r["U"])
         bytes_launch = wb / max(1, s0["batches"])
@@ -552,7 +584,7 @@ def run_sharded(args, world, rank, dev, dist):
     host = np.concatenate(supers)
     d_all = torch.from_numpy(host.view(np.uint8).copy()).to(f"cuda:{dev}")
     d_batches = [d_all[offsets[i] * 40:offsets[i + 1] * 40] for i in range(len(supers))]
-    smap = ShardedVoxelMap(cfg, rank, world, device=dev, initial_regions=4096)
+    smap = ShardedVoxelMap(cfg, rank, world, device=dev, initial_regions=4096, mode=mode)
     stream = torch.cuda.current_stream()
 
     def step(record=False, batches=d_batches):
@@ -617,7 +649,11 @@ def run_sharded(args, world, rank, dev, dist):
         e = host["end"].astype(np.float64)
         L = np.sqrt(((e - o) ** 2).sum(1))
         H = int(np.sum(((host["flags"] & 1) == 1) & (L <= cfg.max_ray_range) & (L > 0)))
-        bytes_gpu = algorithmic_bytes(s0["S"], s0["V"], H) / world / max(1, s0["batches"])
+        if mode == "occupancy":
+            bytes_gpu = algorithmic_bytes(s0["S"], s0["V"], H) / world / max(1, s0["batches"])
+        else:
+            bytes_gpu = ndt_bytes(s0["S"], s0["V"], H, max(0, s0["records"] - H), 0)[0] / world / \
+                max(1, s0["batches"])
         walk_ms = s0["walk_ms"] / max(1, s0["batches"])
         peak, peak_kind = load_peaks()
         achieved = bytes_gpu / (walk_ms * 1e-3) / 1e9 if walk_ms > 0 else 0.0
@@ -628,10 +664,12 @@ def run_sharded(args, world, rank, dev, dist):
             "data": "synthetic",
             "config": dict(desc, exec="deterministic", rays_per_step=total_rays,
                            copies=world, street_pitch_m=STREET_PITCH,
-                           parallelism=f"region-sharded x{world} (NCCL all-to-all of counts/records)"),
+                           parallelism=f"region-sharded x{world} (NCCL all-to-all of counts/records)",
+                           mode=mode),
             "voxel_updates_per_s": s0["V"] * args.steps / (ms * 1e-3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "k_walk_det",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_walk_det" if mode == "occupancy" else "k_walk_ndt",
                          "peak_kind": peak_kind, "bytes_per_launch": bytes_gpu,
                          "avg_launch_ms": walk_ms},
             "e2e": e2e, "cpu_baseline": None,

@@ -128,6 +128,30 @@ int vm_map_destroy(vm_map *map);
 int vm_map_reset(vm_map *map);
 /* Use an external CUDA stream (cudaStream_t) for all map work; NULL = own stream. */
 int vm_map_set_stream(vm_map *map, void *cuda_stream);
+
+/* Region recency and eviction (store.py:28-39, 112-174).
+ * vm_map_set_batch_counter: the VoxelMap.batch_counter value the next batch
+ *   stamps on every region its prefetch touches (engine.py:99-118 refreshes
+ *   Region.last_access the same way); a pipelined sequence counts on from it.
+ * vm_map_region_last_access: those stamps for slots [first, first + count).
+ * vm_map_set_spill: the spill directory and the host map's layer order (the
+ *   OHMS1 payload order).
+ * vm_map_evict_regions: write each region in keys[] to
+ *   <dir>/region_<x>_<y>_<z>.bin -- b"OHMS1", <3q I> key and layer count, u32
+ *   layer ids, zlib level 6 of the layer bytes, byte-compatible with the
+ *   reference's _write_spill -- drop it from HBM and compact the pool (slots
+ *   stay dense and creation-ordered; host mirrors must be re-read).  A failed
+ *   write keeps the region.  *evicted_out counts the regions spilled.
+ * A batch whose prefetch reaches a spilled region reloads it first (the
+ *   guard refuses the attempt, the runtime reloads, the batch replays);
+ *   vm_map_reload_region / vm_map_ensure_regions reload on demand.  Reloading
+ *   consumes the file. */
+int vm_map_set_batch_counter(vm_map *map, uint32_t counter);
+int vm_map_region_last_access(vm_map *map, int64_t first, int64_t count, uint32_t *out);
+int vm_map_set_spill(vm_map *map, const char *dir, const int32_t *layer_ids, int32_t n);
+int vm_map_evict_regions(vm_map *map, const int64_t *keys, int64_t n, int64_t *evicted_out);
+int vm_map_reload_region(vm_map *map, int64_t key, int32_t *slot_out);
+int vm_map_spilled_keys(vm_map *map, int64_t *out, int64_t cap, int64_t *n_out);
 int vm_map_region_count(const vm_map *map, int64_t *out);
 /* Packed region keys (keys.py:76-86) of slots [first, first+count), in slot
  * (creation) order. */

@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     LIB_DIR.mkdir(parents=True, exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, f"-I{INCLUDE}", "-o", str(tmp), str(CSRC / "vm_runtime.cu")]
+    cmd = [nvcc(), *NVCC_FLAGS, f"-I{INCLUDE}", "-o", str(tmp), str(CSRC / "vm_runtime.cu"), "-lz"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
@@ -71,7 +71,7 @@ def build_variant(name: str, defines: list[str]) -> Path:
     LIB_DIR.mkdir(parents=True, exist_ok=True)
     out = LIB_DIR / name
     cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{INCLUDE}", "-o", str(out),
-           str(CSRC / "vm_runtime.cu")]
+           str(CSRC / "vm_runtime.cu"), "-lz"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stderr[-6000:]}")

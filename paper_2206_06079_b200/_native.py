@@ -23,6 +23,8 @@ I64_t = ctypes.c_int64
 
 EXPORTED = (
     "vm_map_create", "vm_map_destroy", "vm_map_reset", "vm_map_set_stream", "vm_map_region_count",
+    "vm_map_set_batch_counter", "vm_map_region_last_access", "vm_map_set_spill",
+    "vm_map_evict_regions", "vm_map_reload_region", "vm_map_spilled_keys",
     "vm_map_region_keys", "vm_map_ensure_regions", "vm_map_find_region", "vm_map_read_layer",
     "vm_map_write_layer", "vm_map_layer_ptr", "vm_integrate", "vm_integrate_many", "vm_export_select", "vm_export_gather", "vm_walk_voxels", "vm_hash_mix",
     "vm_kernels_integrate_occupancy", "vm_last_error", "vm_device_count", "vm_build_info",
@@ -125,6 +127,12 @@ def lib():
         "vm_device_count": ([ctypes.POINTER(I32)], ctypes.c_int),
         "vm_build_info": ([], ctypes.c_char_p),
         "vm_probe_red_rate": ([I32, I64, I32, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        "vm_map_set_batch_counter": ([P, ctypes.c_uint32], ctypes.c_int),
+        "vm_map_region_last_access": ([P, I64, I64, P], ctypes.c_int),
+        "vm_map_set_spill": ([P, ctypes.c_char_p, P, I32], ctypes.c_int),
+        "vm_map_evict_regions": ([P, P, I64, P], ctypes.c_int),
+        "vm_map_reload_region": ([P, I64, ctypes.POINTER(I32)], ctypes.c_int),
+        "vm_map_spilled_keys": ([P, P, I64, P], ctypes.c_int),
     }
     for name, (argt, rest) in sig.items():
         fn = getattr(L, name)
@@ -249,6 +257,44 @@ class NativeMap:
         p = ctypes.c_void_p()
         check(lib().vm_map_layer_ptr(self._h, slot, layer_id, ctypes.byref(p)), "layer_ptr")
         return int(p.value or 0)
+
+    # -- recency and eviction (vm_map_evict_regions) ----------------------
+    def set_batch_counter(self, counter: int):
+        check(lib().vm_map_set_batch_counter(self._h, int(counter) & 0xFFFFFFFF),
+              "vm_map_set_batch_counter")
+
+    def region_last_access(self, first: int, count: int) -> np.ndarray:
+        out = np.zeros(max(count, 0), dtype=np.uint32)
+        if count > 0:
+            check(lib().vm_map_region_last_access(self._h, first, count, _ptr(out)),
+                  "vm_map_region_last_access")
+        return out
+
+    def set_spill(self, directory: str, layer_ids):
+        ids = np.asarray(list(layer_ids), dtype=np.int32)
+        check(lib().vm_map_set_spill(self._h, str(directory).encode(), _ptr(ids), len(ids)),
+              "vm_map_set_spill")
+
+    def evict_regions(self, packed_keys) -> int:
+        keys = np.asarray(list(packed_keys), dtype=np.int64)
+        n = ctypes.c_int64()
+        check(lib().vm_map_evict_regions(self._h, _ptr(keys), len(keys), ctypes.byref(n)),
+              "vm_map_evict_regions")
+        return int(n.value)
+
+    def reload_region(self, packed_key: int) -> int:
+        slot = ctypes.c_int32()
+        check(lib().vm_map_reload_region(self._h, int(packed_key), ctypes.byref(slot)),
+              "vm_map_reload_region")
+        return int(slot.value)
+
+    def spilled_keys(self) -> list[int]:
+        n = ctypes.c_int64()
+        check(lib().vm_map_spilled_keys(self._h, None, 0, ctypes.byref(n)), "vm_map_spilled_keys")
+        out = np.zeros(max(n.value, 1), dtype=np.int64)
+        check(lib().vm_map_spilled_keys(self._h, _ptr(out), n.value, ctypes.byref(n)),
+              "vm_map_spilled_keys")
+        return [int(x) for x in out[:n.value]]
 
     # -- region sharding (vm_shard_*; device buffers are passed as ints) --
     def shard_config(self, rank: int, world: int):

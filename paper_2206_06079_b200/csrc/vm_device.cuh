@@ -28,10 +28,11 @@ enum Mode { M_OCC = 0, M_DECAY = 1, M_NDT_OM = 2, M_NDT_TM = 3, M_TSDF = 4 };
 enum Stat {
     S_RAYS_IN = 0, S_PROCESSED, S_SEGMENTS, S_VISITS, S_RETRIES, S_FAILURES,
     S_RMISS, S_PREF_TOUCHED, S_RECORDS, S_MARKED, S_WALK_TOUCHED, S_RANGE_ERR,
-    S_CUBE_FLUSH, S_SEGDESC, S_WORK, S_RGRID, NUM_STATS
+    S_CUBE_FLUSH, S_SEGDESC, S_WORK, S_RGRID, S_SPILLED, NUM_STATS
 };
 
 constexpr unsigned MARK_FLAG = 0x80000000u;
+constexpr int SLOT_SPILLED = -3;         // region-table value of a region spilled to disk
 constexpr int CUBE = 16;                 // smem aggregation cube edge (voxels)
 constexpr int CUBE_N = CUBE * CUBE * CUBE;
 constexpr int SLOTSET = 256;             // per-block region dedupe set
@@ -126,6 +127,13 @@ struct DevMap {
     void *gx;
     unsigned long long *ngx;
     unsigned long long gx_cap;
+    // eviction (vm_map_evict_regions): region key table values of spilled
+    // regions are SLOT_SPILLED; the prefetch lists the ones a batch reaches
+    // (the guard refuses it, the host reloads them and replays)
+    long long *reload;
+    int reload_cap;
+    unsigned batch_no;                   // the batch counter (Region.last_access)
+    unsigned *slot_last;                 // per slot: last batch whose prefetch touched it
 };
 
 // ---------------------------------------------------------------- arithmetic

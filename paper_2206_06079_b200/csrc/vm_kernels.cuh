@@ -240,7 +240,14 @@ struct PrefetchVisitor {
         hi[0] = max(hi[0], x); hi[1] = max(hi[1], y); hi[2] = max(hi[2], z);
         bool fresh;
         const int slot = cached_slot(*m, *kc, x, y, z, &fresh);
+        if (slot == SLOT_SPILLED) {
+            // a region evicted to disk: the batch must wait for its reload
+            const unsigned long long k = atomicAdd(m->stats + S_SPILLED, 1ULL);
+            if (m->reload && k < (unsigned long long)m->reload_cap) m->reload[k] = pack_region(x, y, z);
+            return;
+        }
         if (slot < 0 || !fresh) return;
+        if (m->slot_last) m->slot_last[slot] = m->batch_no;
         if (!slotset_insert(sset, slot)) return;  // first sight of the region in this block only
         if (stamp_epoch(m->slot_pref + slot, m->epoch))
             atomicAdd(m->stats + S_PREF_TOUCHED, 1ULL);
@@ -499,7 +506,8 @@ __global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
     int used = *((volatile int *)m.cursor);
     unsigned long long rerr = ((volatile unsigned long long *)m.stats)[S_RANGE_ERR];
     unsigned long long nseg = ((volatile unsigned long long *)m.stats)[S_SEGDESC];
-    bool ok = used + margin <= m.cap && rerr == 0 && nseg <= m.seg_cap;
+    unsigned long long spilled = ((volatile unsigned long long *)m.stats)[S_SPILLED];
+    bool ok = used + margin <= m.cap && rerr == 0 && nseg <= m.seg_cap && spilled == 0;
     *m.go = ok ? 1 : 0;
     if (!ok && m.chain) atomicCAS(m.chain, 0, m.batch_idx + 1);
 }

@@ -13,8 +13,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
+
+#include <zlib.h>
 
 #include "../../include/voxmap_b200.h"
 #include "vm_walk.cuh"
@@ -44,6 +47,8 @@ int fail(int code, const std::string &msg) {
             return fail(e_ == cudaErrorMemoryAllocation ? VM_ERR_OOM : VM_ERR_CUDA,     \
                         std::string(#x) + ": " + cudaGetErrorString(e_));              \
     } while (0)
+
+constexpr int RELOAD_CAP = 4096;  // spilled regions one refused attempt can list
 
 const int LAYER_ELEM[NUM_LAYERS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 8, 4, 4};
 const int LAYER_COMP[NUM_LAYERS] = {1, 1, 1, 1, 6, 1, 1, 2, 1, 1, 2, 1};
@@ -123,6 +128,13 @@ struct vm_map {
     unsigned char *d_ring[RING] = {};
     size_t ring_bytes = 0;
     cudaEvent_t ev_ring[RING] = {}, ev_ring_up[RING] = {};
+    // eviction / spill (vm_map_evict_regions): OHMS1 files in spill_dir
+    std::string spill_dir;
+    std::vector<int> spill_ids;      // user layers in the host map's order (payload order)
+    std::set<long long> spilled;     // packed keys of the regions on disk
+    long long *d_reload = nullptr;   // keys of spilled regions a refused batch reached
+    unsigned *d_slot_last = nullptr; // per slot: last batch whose prefetch touched it
+    unsigned batch_no = 0;           // Region.last_access value of the next batch
     long long rec_floor_override = 0;
     long long ndt_rec_override = 0;  // VOXMAP_B200_TEST_NDT_REC_CAP: force the NDT overflow path
     int no_ray_order = 0;  // VOXMAP_B200_NO_RAY_ORDER: NDT walk in input order (A/B runs)
@@ -261,6 +273,10 @@ DevMap make_dm(const vm_map *m) {
     d.rec_invalid = ~0ULL;
     d.walk_slot0 = 1 << 30;
     d.key_mi = 0;
+    d.reload = m->d_reload;
+    d.reload_cap = RELOAD_CAP;
+    d.batch_no = m->batch_no;
+    d.slot_last = m->d_slot_last;
     return d;
 }
 
@@ -615,6 +631,126 @@ const uint32_t MODE_MASK[5] = {
     (1u << 1) | (1u << 2) | (1u << 3) | (1u << 4) | (1u << 5) | (1u << 6) | (1u << 7),
     (1u << 10)};
 
+// ---------------------------------------------------------------------------
+// Eviction and spill (store.py:120-174): OHMS1 files, byte-compatible with
+// the reference's _write_spill / _reload_region: b"OHMS1", <3q I> region key
+// and layer count, u32 layer ids, zlib(level 6) of the layers' bytes in the
+// host map's layer order.  A spilled region keeps its key in the device
+// table with SLOT_SPILLED, so a batch that reaches it is refused by the guard
+// and replayed after the reload (integrate_impl, integrate_pipelined).
+
+std::string spill_path(const vm_map *m, long long key) {
+    int r[3];
+    unpack_region(key, r);
+    return m->spill_dir + "/region_" + std::to_string(r[0]) + "_" + std::to_string(r[1]) + "_" +
+           std::to_string(r[2]) + ".bin";
+}
+
+__global__ void k_revive(const __grid_constant__ DevMap m, long long key, int *slot_out) {
+    // the table entry of a spilled key takes a fresh slot
+    unsigned long long h = mix_key(key) & m.tmask;
+    for (unsigned long long p = 0; p <= m.tmask; ++p) {
+        const long long k = m.tkeys[h];
+        if (k == key) {
+            const int v = m.tvals[h];
+            if (v == SLOT_SPILLED) {
+                const int s = atomicAdd(m.cursor, 1);
+                m.slot_keys[s] = key;
+                m.tvals[h] = s;
+                *slot_out = s;
+            } else {
+                *slot_out = v;
+            }
+            return;
+        }
+        if (k == -1) break;
+        h = (h + 1) & m.tmask;
+    }
+    *slot_out = -1;
+}
+
+// Reload one spilled region from its file into a fresh slot (the file is
+// consumed, store.py:145-170).  *slot_out = -1 if the key is not spilled.
+int reload_region(vm_map *m, long long key, int *slot_out) {
+    *slot_out = -1;
+    if (!m->spilled.count(key)) return VM_OK;
+    const std::string path = spill_path(m, key);
+    FILE *f = std::fopen(path.c_str(), "rb");
+    if (!f) return fail(VM_ERR_ARG, "spill file missing: " + path);
+    std::vector<unsigned char> raw;
+    {
+        unsigned char buf[1 << 16];
+        size_t k;
+        while ((k = std::fread(buf, 1, sizeof(buf), f)) > 0) raw.insert(raw.end(), buf, buf + k);
+        std::fclose(f);
+    }
+    const size_t nl = m->spill_ids.size();
+    const size_t hdr = 5 + 28 + 4 * nl;
+    if (raw.size() < hdr || std::memcmp(raw.data(), "OHMS1", 5) != 0)
+        return fail(VM_ERR_ARG, "bad spill file " + path);
+    long long k3[3];
+    uint32_t nlayers;
+    std::memcpy(k3, raw.data() + 5, 24);
+    std::memcpy(&nlayers, raw.data() + 29, 4);
+    int r[3];
+    unpack_region(key, r);
+    bool ok = k3[0] == r[0] && k3[1] == r[1] && k3[2] == r[2] && nlayers == nl;
+    for (size_t i = 0; ok && i < nl; ++i) {
+        uint32_t id;
+        std::memcpy(&id, raw.data() + 33 + 4 * i, 4);
+        ok = (int)id == m->spill_ids[i];
+    }
+    if (!ok) return fail(VM_ERR_ARG, "spill file " + path + " does not match map layout");
+    size_t total = 0;
+    for (int id : m->spill_ids) total += m->bpr[id];
+    std::vector<unsigned char> payload(total);
+    uLongf got = (uLongf)total;
+    if (uncompress(payload.data(), &got, raw.data() + hdr, (uLong)(raw.size() - hdr)) != Z_OK ||
+        got != total)
+        return fail(VM_ERR_ARG, "corrupt spill file " + path);
+    CK(cudaSetDevice(m->device));
+    if (m->nreg + 1 > m->cap) {
+        int rc = grow_pool(m, std::max<long long>(2 * m->cap, m->nreg + 64));
+        if (rc) return rc;
+    }
+    int *d_slot = nullptr;
+    CK(cudaMalloc(&d_slot, sizeof(int)));
+    k_revive<<<1, 1, 0, m->stream>>>(make_dm(m), key, d_slot);
+    int slot = -1;
+    CK(cudaMemcpyAsync(&slot, d_slot, sizeof(int), cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    cudaFree(d_slot);
+    if (slot < 0 || slot >= m->cap) return fail(VM_ERR_CUDA, "spilled region lost its table entry");
+    size_t pos = 0;
+    for (int id : m->spill_ids) {
+        CK(cudaMemcpyAsync((char *)m->slab[id] + (size_t)slot * m->bpr[id], payload.data() + pos,
+                           m->bpr[id], cudaMemcpyHostToDevice, m->stream));
+        pos += m->bpr[id];
+    }
+    const unsigned last = m->batch_no;
+    CK(cudaMemcpyAsync(m->d_slot_last + slot, &last, sizeof(unsigned), cudaMemcpyHostToDevice,
+                       m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    m->spilled.erase(key);
+    std::remove(path.c_str());
+    m->nreg = std::max<long long>(m->nreg, slot + 1);
+    *slot_out = slot;
+    return VM_OK;
+}
+
+// the spilled regions a refused attempt listed (stats already on the host)
+int reload_listed(vm_map *m, unsigned long long listed) {
+    const unsigned long long n = std::min<unsigned long long>(listed, RELOAD_CAP);
+    std::vector<long long> keys(n);
+    if (n) CK(cudaMemcpy(keys.data(), m->d_reload, n * sizeof(long long), cudaMemcpyDeviceToHost));
+    std::set<long long> uniq(keys.begin(), keys.end());
+    for (long long k : uniq) {
+        int slot, rc = reload_region(m, k, &slot);
+        if (rc) return rc;
+    }
+    return VM_OK;
+}
+
 template <class Src>
 int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, vm_stats *out) {
     const bool ndt = mode == M_NDT_OM || mode == M_NDT_TM;
@@ -800,6 +936,14 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             m->nreg = cursor;
             return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range "
                                       "(|region| < 2**20, keys.py:76-86)");
+        }
+        if (!go && hs[S_SPILLED]) {
+            // the batch reaches regions spilled to disk: reload them, replay
+            CK(cudaStreamSynchronize(m->stream));
+            m->nreg = cursor;
+            if ((rc = reload_listed(m, hs[S_SPILLED]))) return rc;
+            ++replays;
+            continue;
         }
         if (!go) {
             // pool overflow: nothing was applied (the sample-voxel stamps are
@@ -1079,6 +1223,7 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
             if (n <= 0) continue;
             m->epoch += 1;
             DevMap dm = make_dm(m);
+            dm.batch_no = m->batch_no + (unsigned)b;  // the sequence's batches count on
             dm.order_bits = std::max(1, bitlen(((unsigned long long)n * maxseg) << 1));
             dm.key_mi = 1;
             dm.marked = m->d_smarked;
@@ -1157,6 +1302,16 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
             m->nreg = cursor;
             return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range "
                                       "(|region| < 2**20, keys.py:76-86)");
+        }
+        if (!(slot[NUM_STATS + 1] & 1ULL) && slot[S_SPILLED]) {
+            // spilled regions reached: reload them and replay from f
+            m->nreg = cursor;
+            if ((rc = reload_listed(m, slot[S_SPILLED]))) return rc;
+            if (first_before[f] < 0) first_before[f] = regions;
+            reps[f] += 1;
+            b0 = f;
+            keep_marks = true;
+            continue;
         }
         if (!(slot[NUM_STATS + 1] & 1ULL)) {
             // region pool: grow and replay from f (its stamps stay valid)
@@ -1302,7 +1457,8 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         (rc = dev_alloc(&m->d_seg_hist, SEG_BUCKETS)) ||
         (rc = dev_alloc(&m->d_shard_cnt, 3)) ||
         (rc = dev_alloc(&m->d_seg_cursor, SEG_BUCKETS)) ||
-        (rc = dev_alloc(&m->d_nbig, 1)))
+        (rc = dev_alloc(&m->d_nbig, 1)) || (rc = dev_alloc(&m->d_reload, RELOAD_CAP)) ||
+        (rc = dev_alloc(&m->d_slot_last, m->max_slots)))
         return cleanup(rc);
     for (int l = 0; l < NUM_LAYERS; ++l)
         if (m->bpr[l] && (rc = dev_alloc(&m->d_lptr[l], m->max_slots))) return cleanup(rc);
@@ -1351,6 +1507,8 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_shard_cnt);
     cudaFree(m->d_gx);
     cudaFree(m->d_ngx);
+    cudaFree(m->d_reload);
+    cudaFree(m->d_slot_last);
     cudaFree(m->d_bmask);
     cudaFree(m->d_big);
     cudaFree(m->d_nbig);
@@ -1408,8 +1566,167 @@ int vm_map_reset(vm_map *m) {
     CK(cudaMemsetAsync(m->d_tvals, 0xFF, m->tsize * sizeof(int), m->stream));
     CK(cudaMemsetAsync(m->d_cursor, 0, sizeof(int), m->stream));
     CK(cudaMemsetAsync(m->d_bmask, 0, m->max_slots * sizeof(unsigned), m->stream));
+    CK(cudaMemsetAsync(m->d_slot_last, 0, m->max_slots * sizeof(unsigned), m->stream));
     CK(cudaStreamSynchronize(m->stream));
     m->nreg = 0;
+    m->spilled.clear();  // the files stay on disk
+    return VM_OK;
+}
+
+int vm_map_set_batch_counter(vm_map *m, uint32_t counter) {
+    if (!m) return fail(VM_ERR_ARG, "null map");
+    m->batch_no = counter;
+    return VM_OK;
+}
+
+int vm_map_region_last_access(vm_map *m, int64_t first, int64_t count, uint32_t *out) {
+    if (!m || !out || first < 0 || count < 0 || first + count > m->nreg)
+        return fail(VM_ERR_ARG, "bad region range");
+    if (!count) return VM_OK;
+    CK(cudaSetDevice(m->device));
+    CK(cudaMemcpyAsync(out, m->d_slot_last + first, count * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                       m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    return VM_OK;
+}
+
+int vm_map_set_spill(vm_map *m, const char *dir, const int32_t *layer_ids, int32_t n) {
+    if (!m || !dir || (n && !layer_ids)) return fail(VM_ERR_ARG, "null argument");
+    std::vector<int> ids(layer_ids, layer_ids + n);
+    for (int id : ids)
+        if (id < 1 || id > L_TSDF || !m->bpr[id]) return fail(VM_ERR_ARG, "spill layer not in map");
+    m->spill_dir = dir;
+    m->spill_ids = ids;
+    return VM_OK;
+}
+
+int vm_map_evict_regions(vm_map *m, const int64_t *keys, int64_t n, int64_t *evicted_out) {
+    if (!m || !evicted_out || (n && !keys)) return fail(VM_ERR_ARG, "null argument");
+    *evicted_out = 0;
+    if (m->spill_dir.empty()) return fail(VM_ERR_ARG, "map was created without a spill directory");
+    if (!n) return VM_OK;
+    CK(cudaSetDevice(m->device));
+    CK(cudaStreamSynchronize(m->stream));
+    const long long nreg = m->nreg;
+    std::vector<long long> skeys((size_t)nreg);
+    std::vector<unsigned> last((size_t)nreg);
+    if (nreg) {
+        CK(cudaMemcpy(skeys.data(), m->d_slot_keys, nreg * sizeof(long long), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(last.data(), m->d_slot_last, nreg * sizeof(unsigned), cudaMemcpyDeviceToHost));
+    }
+    std::set<long long> want(keys, keys + n);
+    std::vector<char> gone((size_t)nreg, 0);
+    size_t total = 0;
+    for (int id : m->spill_ids) total += m->bpr[id];
+    std::vector<unsigned char> payload(total);
+    std::vector<unsigned char> blob(compressBound((uLong)total));
+    long long evicted = 0;
+    for (long long s = 0; s < nreg; ++s) {
+        if (!want.count(skeys[s])) continue;
+        size_t pos = 0;
+        for (int id : m->spill_ids) {
+            CK(cudaMemcpy(payload.data() + pos, (char *)m->slab[id] + (size_t)s * m->bpr[id], m->bpr[id],
+                          cudaMemcpyDeviceToHost));
+            pos += m->bpr[id];
+        }
+        uLongf bl = (uLongf)blob.size();
+        if (compress2(blob.data(), &bl, payload.data(), (uLong)total, 6) != Z_OK)
+            return fail(VM_ERR_OOM, "zlib compression failed");
+        int r[3];
+        unpack_region(skeys[s], r);
+        const long long k3[3] = {r[0], r[1], r[2]};
+        const uint32_t nl = (uint32_t)m->spill_ids.size();
+        const std::string path = spill_path(m, skeys[s]);
+        FILE *f = std::fopen(path.c_str(), "wb");
+        bool ok = f != nullptr;
+        if (ok) {
+            ok = std::fwrite("OHMS1", 1, 5, f) == 5 && std::fwrite(k3, 8, 3, f) == 3 &&
+                 std::fwrite(&nl, 4, 1, f) == 1;
+            for (int id : m->spill_ids) {
+                const uint32_t u = (uint32_t)id;
+                ok = ok && std::fwrite(&u, 4, 1, f) == 1;
+            }
+            ok = ok && std::fwrite(blob.data(), 1, bl, f) == bl;
+            ok = (std::fclose(f) == 0) && ok;
+        }
+        if (!ok) {
+            // store.py:127-131: a failed spill keeps the region in memory
+            std::fprintf(stderr, "voxmap_b200: spill of region (%d, %d, %d) failed, keeping it\n",
+                         r[0], r[1], r[2]);
+            std::remove(path.c_str());
+            continue;
+        }
+        gone[(size_t)s] = 1;
+        m->spilled.insert(skeys[s]);
+        ++evicted;
+    }
+    if (!evicted) return VM_OK;
+    // compact the pool: survivors move down in slot (= creation) order
+    std::vector<long long> keep;
+    std::vector<unsigned> keep_last;
+    for (long long s = 0; s < nreg; ++s) {
+        if (gone[(size_t)s]) continue;
+        const long long t = (long long)keep.size();
+        if (t != s)
+            for (int l = 0; l < NUM_LAYERS; ++l)
+                if (m->bpr[l])
+                    CK(cudaMemcpyAsync((char *)m->slab[l] + (size_t)t * m->bpr[l],
+                                       (char *)m->slab[l] + (size_t)s * m->bpr[l], m->bpr[l],
+                                       cudaMemcpyDeviceToDevice, m->stream));
+        keep.push_back(skeys[(size_t)s]);
+        keep_last.push_back(last[(size_t)s]);
+    }
+    const long long nk = (long long)keep.size();
+    for (int l = 0; l < NUM_LAYERS; ++l)
+        if (m->bpr[l] && nreg > nk)
+            CK(cudaMemsetAsync((char *)m->slab[l] + (size_t)nk * m->bpr[l], 0,
+                               (size_t)(nreg - nk) * m->bpr[l], m->stream));
+    // the region table: survivors at their new slots, spilled keys marked
+    std::vector<long long> tk(m->tsize, -1);
+    std::vector<int> tv(m->tsize, -1);
+    auto put = [&](long long key, int v) {
+        unsigned long long h = mix_key(key) & (m->tsize - 1);
+        while (tk[h] != -1) h = (h + 1) & (m->tsize - 1);
+        tk[h] = key;
+        tv[h] = v;
+    };
+    for (long long t = 0; t < nk; ++t) put(keep[(size_t)t], (int)t);
+    for (long long k : m->spilled) put(k, SLOT_SPILLED);
+    CK(cudaMemcpyAsync(m->d_tkeys, tk.data(), m->tsize * sizeof(long long), cudaMemcpyHostToDevice, m->stream));
+    CK(cudaMemcpyAsync(m->d_tvals, tv.data(), m->tsize * sizeof(int), cudaMemcpyHostToDevice, m->stream));
+    if (nk) {
+        CK(cudaMemcpyAsync(m->d_slot_keys, keep.data(), nk * sizeof(long long), cudaMemcpyHostToDevice, m->stream));
+        CK(cudaMemcpyAsync(m->d_slot_last, keep_last.data(), nk * sizeof(unsigned), cudaMemcpyHostToDevice,
+                           m->stream));
+    }
+    const int cur = (int)nk;
+    CK(cudaMemcpyAsync(m->d_cursor, &cur, sizeof(int), cudaMemcpyHostToDevice, m->stream));
+    CK(cudaMemsetAsync(m->d_bmask, 0, (size_t)nreg * sizeof(unsigned), m->stream));
+    CK(cudaMemsetAsync(m->d_slot_touch, 0, (size_t)nreg * sizeof(unsigned), m->stream));
+    CK(cudaMemsetAsync(m->d_slot_pref, 0, (size_t)nreg * sizeof(unsigned), m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+    m->nreg = nk;
+    *evicted_out = evicted;
+    return VM_OK;
+}
+
+int vm_map_reload_region(vm_map *m, int64_t key, int32_t *slot_out) {
+    if (!m || !slot_out) return fail(VM_ERR_ARG, "null argument");
+    CK(cudaSetDevice(m->device));
+    int slot = -1;
+    const int rc = reload_region(m, key, &slot);
+    *slot_out = slot;
+    return rc;
+}
+
+int vm_map_spilled_keys(vm_map *m, int64_t *out, int64_t cap, int64_t *n_out) {
+    if (!m || !n_out || (cap && !out)) return fail(VM_ERR_ARG, "null argument");
+    int64_t i = 0;
+    for (long long k : m->spilled) {
+        if (i < cap) out[i] = k;
+        ++i;
+    }
+    *n_out = i;
     return VM_OK;
 }
 
@@ -1459,6 +1776,10 @@ int ensure_or_find(vm_map *m, const int64_t *keys, int64_t n, int32_t *slots_out
     if (!n) return VM_OK;
     CK(cudaSetDevice(m->device));
     int rc;
+    for (int64_t i = 0; i < n && !m->spilled.empty(); ++i) {  // spilled: reload transparently
+        int slot;
+        if ((rc = reload_region(m, keys[i], &slot))) return rc;
+    }
     if (insert && m->nreg + n > m->cap) {
         if ((rc = grow_pool(m, std::max<long long>(2 * m->cap, m->nreg + n + 64)))) return rc;
     }
@@ -1619,8 +1940,10 @@ int vm_integrate_many(vm_map *m, const vm_rays *rays, int32_t nbatches, int32_t 
                 prefetch = false;
             nmax = std::max<long long>(nmax, rays[b].count);
         }
+        const unsigned base = m->batch_no;  // each batch stamps its own counter
         if (!prefetch) {
             for (int b = 0; b < nbatches; ++b) {
+                m->batch_no = base + (unsigned)b;
                 const int rc = vm_integrate(m, rays + b, mode, exec, out + b);
                 if (rc) return rc;
             }
@@ -1655,6 +1978,7 @@ int vm_integrate_many(vm_map *m, const vm_rays *rays, int32_t nbatches, int32_t 
             vm_rays r = rays[b];
             r.records = m->d_ring[b % vm_map::RING];
             r.on_device = 1;
+            m->batch_no = base + (unsigned)b;
             if ((rc = vm_integrate(m, &r, mode, exec, out + b))) return rc;
         }
         return VM_OK;

@@ -119,6 +119,7 @@ def submit_batch(vmap: VoxelMap, rays, mode: str, opts: ExecutorOptions | None =
     stats = BatchStats(rays_in=int(native_rays.count))
     vmap.batch_counter += 1
     vmap.flush_host_writes()
+    vmap._begin_batch()
     st = vmap._native.integrate(native_rays, mode, opts.use_deterministic)
     del keep
     vmap._note_batch(int(st.regions_total))
@@ -172,15 +173,13 @@ def submit_batches(vmap: VoxelMap, batches, mode: str, opts: ExecutorOptions | N
         return []
     start = time.perf_counter()
     converted = [_as_native_rays(b) for b in batches]
-    vmap.batch_counter += len(batches)
+    vmap.batch_counter += 1  # the sequence's first batch; the device counts on
     vmap.flush_host_writes()
+    vmap._begin_batch()
     sts = vmap._native.integrate_many([c[0] for c in converted], mode, opts.use_deterministic)
     del converted
-    first = vmap.batch_counter - len(batches) + 1
-    for i, st in enumerate(sts):  # the regions each batch created were last accessed by it
-        vmap.batch_counter = first + i
-        vmap._note_batch(int(st.regions_total))
-    vmap.batch_counter = first + len(batches) - 1
+    vmap.batch_counter += len(batches) - 1
+    vmap._note_batch(int(sts[-1].regions_total))
     wall = time.perf_counter() - start
     total = sum(int(s.rays_in) for s in sts) or 1
     return [_to_stats(s, wall * int(s.rays_in) / total) for s in sts]

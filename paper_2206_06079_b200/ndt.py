@@ -1,10 +1,15 @@
-"""NDT voxel Gaussian queries (mirror of voxmap.ndt queries, ndt.py:108-165).
+"""NDT voxel Gaussians: queries (voxmap.ndt, ndt.py:108-165) and the host
+mirror of the per-sample update.
 
-The per-sample updates (Welford mean + Givens sqrt-covariance, miss
-likelihood) run on the device: csrc/vm_kernels.cuh update_gaussian /
-gaussian_weight.
+The batch path updates Gaussians on the device (csrc/vm_ndt.cuh ndt_update:
+Welford mean + Givens sqrt-covariance with CPython's hypot, per sample in ray
+order; csrc/vm_kernels.cuh gaussian_weight for the miss likelihood).
+`update_gaussian` is the same arithmetic on the host, for callers that fold
+samples themselves.
 """
 from __future__ import annotations
+
+import math
 
 import numpy as np
 
@@ -21,6 +26,31 @@ def sqrt_to_matrix(flat6) -> np.ndarray:
     L[1, 0], L[1, 1] = s[1], s[2]
     L[2, 0], L[2, 1], L[2, 2] = s[3], s[4], s[5]
     return L
+
+
+def update_gaussian(n: int, mu, S, sample):
+    """Fold one sample into (count, mean, sqrt-covariance) -- ndt.py:55-70.
+    The deviation factor L = S * sqrt(n) takes the rank-one Welford term
+    sqrt(n / (n + 1)) * (x - mu) by Givens rotations (cholupdate3,
+    ndt.py:37-52), column by column; the population factor is L / sqrt(n + 1).
+    With fewer than two samples the factor is zero."""
+    x = np.asarray(sample, dtype=np.float64)
+    if n == 0:
+        return 1, x.copy(), np.zeros((3, 3))
+    m = n + 1
+    d = x - mu
+    L = np.array(S, dtype=np.float64) * math.sqrt(n)
+    v = d * math.sqrt(n / m)
+    for k in range(3):
+        r = math.hypot(L[k, k], v[k])
+        if r == 0.0:
+            continue
+        c, s = L[k, k] / r, v[k] / r
+        L[k, k] = r
+        col, tail = L[k + 1:, k].copy(), v[k + 1:].copy()
+        L[k + 1:, k] = c * col + s * tail
+        v[k + 1:] = c * tail - s * col
+    return m, mu + d / m, L / math.sqrt(m)
 
 
 def intensity_stats(n: int, mean: float, m2: float):

@@ -107,6 +107,7 @@ class ShardedVoxelMap:
         self._keep = records_dev
         self.vmap.flush_host_writes()
         self.vmap.batch_counter += 1
+        self.vmap._begin_batch()
         nnew, nmarks = self.nat.shard_begin(rays, self.mode)
         req = torch.empty((self.world, max(nnew, 1)), dtype=torch.int64, device=self.dev)
         marks = torch.empty((max(nmarks, 1), 2), dtype=torch.int64, device=self.dev)

@@ -57,13 +57,22 @@ class _Buffers:
 class Region:
     """One dense block of voxels (store.py:28-39), backed by a device slot."""
 
-    __slots__ = ("key", "slot", "last_access", "_vmap")
+    __slots__ = ("key", "slot", "_vmap")
 
-    def __init__(self, key, slot: int, vmap, last_access: int = 0):
+    def __init__(self, key, slot: int, vmap):
         self.key = key
         self.slot = slot
-        self.last_access = last_access
         self._vmap = vmap
+
+    @property
+    def last_access(self) -> int:
+        """The last batch whose prefetch reached the region (the device
+        stamps it, engine.py:99-118) or host access (get_region)."""
+        return self._vmap._last_access(self)
+
+    @last_access.setter
+    def last_access(self, value: int):
+        self._vmap._host_touch[self.key] = int(value)
 
     @property
     def buffers(self) -> _Buffers:
@@ -78,13 +87,16 @@ class VoxelMap:
         self.cfg = cfg
         self.layers = layermod.resolve(layer_names)
         self._regions: dict[tuple[int, int, int], Region] = {}
-        self._created: list[tuple[int, int]] = []  # (regions after batch, batch counter)
         self.batch_counter = 0
         self._spill_dir = Path(spill_dir) if spill_dir is not None else None
         self._native = _native.NativeMap(cfg, layermod.layer_mask(layer_names), device,
                                          initial_regions)
+        if self._spill_dir is not None:
+            self._native.set_spill(str(self._spill_dir), [s.layer_id for s in self.layers])
         self._known = 0          # device slots mirrored into self._regions
         self._mirrors = {}       # (slot, name) -> (array, pristine copy)
+        self._host_touch = {}    # region key -> batch counter of the last host access
+        self._last = None        # device last-access stamps per slot (cached per batch)
 
     # -- region access --------------------------------------------------
 
@@ -109,38 +121,54 @@ class VoxelMap:
         return int(self._native.region_count())
 
     def _note_batch(self, regions_total: int):
-        """After a batch: the regions it created (slots below regions_total)
-        were last accessed by it (Region.last_access, store.py:28-39)."""
-        if regions_total > self._known and (not self._created or
-                                            regions_total > self._created[-1][0]):
-            self._created.append((int(regions_total), self.batch_counter))
+        """After a batch: the device's last-access stamps changed."""
+        self._last = None
+
+    def _begin_batch(self):
+        """Before a batch: its Region.last_access stamp (the counter the
+        caller just advanced, engine.py:190)."""
+        self._native.set_batch_counter(self.batch_counter)
+        self._last = None
+
+    def _last_access(self, region: Region) -> int:
+        if self._last is None or len(self._last) < self._known:
+            self._last = self._native.region_last_access(0, self._known)
+        dev = int(self._last[region.slot]) if region.slot < len(self._last) else 0
+        return max(dev, self._host_touch.get(region.key, 0))
 
     def _sync_regions(self):
         """Mirror device-created regions (slot order = creation order)."""
         n = self._native.region_count()
         if n > self._known:
-            created = self._created
-            j = 0
             for i, packed in enumerate(self._native.region_keys(self._known, n - self._known)):
-                slot = self._known + i
-                while j < len(created) and created[j][0] <= slot:
-                    j += 1
-                access = created[j][1] if j < len(created) else self.batch_counter
                 rk = unpack_region_coord(int(packed))
-                self._regions[rk] = Region(rk, slot, self, access)
+                self._regions[rk] = Region(rk, self._known + i, self)
             self._known = n
-            self._created = []
+            self._last = None
+
+    def _reindex(self):
+        """The device compacted its pool (eviction): rebuild the host index."""
+        self._mirrors.clear()
+        self._regions = {}
+        self._known = 0
+        self._last = None
+        self._sync_regions()
 
     def get_region(self, rk, create: bool = False) -> Region | None:
         rk = (int(rk[0]), int(rk[1]), int(rk[2]))
         region = self.regions.get(rk)
-        if region is None and create:
+        if region is None and (create or rk in self._spilled_set()):
+            # ensure_regions reloads a spilled region transparently
+            # (store.py:67-77: get_region reloads from the spill file)
             self._native.ensure_regions([pack_region_coord(rk)])
             self._sync_regions()
-            region = self.regions[rk]
+            region = self.regions.get(rk)
         if region is not None:
             region.last_access = self.batch_counter
         return region
+
+    def _spilled_set(self) -> set:
+        return {unpack_region_coord(k) for k in self._native.spilled_keys()}
 
     def get_or_create_region(self, rk) -> Region:
         return self.get_region(rk, create=True)
@@ -150,8 +178,38 @@ class VoxelMap:
         self._mirrors.clear()
         self._native.reset()
         self._regions.clear()
-        self._created = []
+        self._host_touch.clear()
         self._known = 0
+        self._last = None
+
+    # -- eviction (store.py:112-174; OHMS1 written by the runtime) ----------
+
+    def spill_dir(self) -> Path:
+        if self._spill_dir is None:
+            raise RuntimeError("map was created without a spill directory")
+        self._spill_dir.mkdir(parents=True, exist_ok=True)
+        return self._spill_dir
+
+    def evict_stale_regions(self, age: int) -> int:
+        """Spill regions not touched within the last `age` batches to disk
+        (zlib, lossless; the same OHMS1 files as the reference) and release
+        their HBM.  A later batch -- or get_region -- that reaches a spilled
+        region reloads it transparently."""
+        self.spill_dir()
+        self.flush_host_writes()
+        cutoff = self.batch_counter - age
+        stale = [pack_region_coord(rk) for rk, r in self.regions.items() if r.last_access < cutoff]
+        if not stale:
+            return 0
+        evicted = self._native.evict_regions(stale)
+        if evicted:
+            self._reindex()
+        return evicted
+
+    def _reload_all_spilled(self) -> None:
+        for packed in sorted(self._native.spilled_keys()):
+            self._native.reload_region(packed)
+        self._sync_regions()
 
     # -- host mirrors ---------------------------------------------------
 
@@ -204,6 +262,7 @@ class VoxelMap:
     # -- persistence (store.py:178-225, OHMR1; device -> host sync) -------
 
     def save(self, path) -> None:
+        self._reload_all_spilled()
         with open(path, "wb") as fh:
             fh.write(MAP_MAGIC)
             fh.write(struct.pack("<d I I", self.cfg.voxel_size, self.cfg.region_dim,

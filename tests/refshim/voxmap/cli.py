@@ -1,0 +1,6 @@
+"""Alias of paper_2206_06079_b200.cli (test infrastructure, see __init__)."""
+import sys
+
+from paper_2206_06079_b200 import cli as _m
+
+sys.modules[__name__] = _m

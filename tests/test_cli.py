@@ -1,0 +1,77 @@
+"""`voxmap bench` / `voxmap export` on the GPU path (paper_2206_06079_b200.cli),
+after the reference's own CLI tests (test_exporters.py:85-144, subprocess
+with exit codes) and the online criterion (test_acceptance.py:421-456)."""
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+
+def run_cli(*args):
+    return subprocess.run([sys.executable, "-m", "paper_2206_06079_b200.cli", *args],
+                          capture_output=True, text=True, timeout=600)
+
+
+def test_cli_bad_arguments_exit_2():
+    res = run_cli("bench", "--scene", "os64-room", "--voxel-size", "-1")
+    assert res.returncode == 2
+
+
+def test_cli_missing_file_exit_1(tmp_path):
+    res = run_cli("export", str(tmp_path / "nope.bin"), "occupied-ply", str(tmp_path / "x.ply"))
+    assert res.returncode == 1
+
+
+@pytest.mark.gpu
+def test_cli_bench_offline(tmp_path):
+    out, mp = tmp_path / "bench.csv", tmp_path / "map.bin"
+    res = run_cli("bench", "--scene", "os128-canyon", "--duration", "0.3", "--voxel-size", "0.05",
+                  "--out", str(out), "--save-map", str(mp))
+    assert res.returncode == 0, res.stderr
+    lines = out.read_text().splitlines()
+    assert lines[0].startswith("second,")
+    assert len(lines) == 3 + 3  # three 0.1 s batches, total, dropped
+    assert lines[-2].startswith("total,") and lines[-1].startswith("# dropped_rays=0 ")
+    total = lines[-2].split(",")
+    assert int(total[1]) == int(total[2]) == 30 * 128 * 205  # 30 OS1-128 slices of 10 ms
+    assert mp.exists()
+
+
+@pytest.mark.gpu
+def test_cli_bench_rayset_replay_ndt_pinned(tmp_path):
+    rays = tmp_path / "rays.bin"
+    res = run_cli("bench", "--scene", "os64-tunnel", "--duration", "0.2", "--save-rays", str(rays))
+    assert res.returncode == 0, res.stderr
+    res = run_cli("bench", "--rays", str(rays), "--mode", "ndt-om", "--pin")
+    assert res.returncode == 0, res.stderr
+    assert "total,262144,262144," in res.stdout
+
+
+@pytest.mark.gpu
+def test_cli_export_subcommand_and_layer_mismatch(tmp_path):
+    mp = tmp_path / "map.bin"
+    assert run_cli("bench", "--scene", "os64-room", "--save-map", str(mp)).returncode == 0
+    res = run_cli("export", str(mp), "occupied-ply", str(tmp_path / "map.ply"))
+    assert res.returncode == 0, res.stderr
+    assert (tmp_path / "map.ply").read_bytes().startswith(b"ply")
+    res = run_cli("export", str(mp), "tsdf-csv", str(tmp_path / "x.csv"))
+    assert res.returncode == 2
+
+
+@pytest.mark.gpu
+def test_online_replay_keeps_up_at_sensor_rate():
+    """Criterion 11's online loop (cli.py:130-162): batches released on the
+    sensor clock into a 2-slot queue.  An OS1-128 at 2.6 M rays/s is two
+    orders of magnitude below the GPU path's rate, so nothing is dropped --
+    and each batch's integration takes a small part of its 0.1 s period."""
+    from paper_2206_06079_b200 import ExecutorOptions, MapConfig, VoxelMap, cli, scans
+    from paper_2206_06079_b200.layers import MODE_LAYERS
+    rec = np.concatenate(scans.os128_canyon_batches(100))  # 1 s of sensor time
+    batches = cli._batches(rec)
+    vm = VoxelMap(MapConfig(voxel_size=0.05), MODE_LAYERS["occupancy"])
+    cli._run_offline(vm, batches[:1], "occupancy", ExecutorOptions())  # device warm-up
+    vm.clear()
+    rows, dropped = cli._run_online(vm, batches, "occupancy", ExecutorOptions())
+    assert dropped == 0 and len(rows) == len(batches) == 10
+    assert max(st.wall_time for _, st in rows) < 0.05
