@@ -31,6 +31,13 @@ namespace vm {
 #define VM_WD_STEPS 8
 #endif
 constexpr int WD_STEPS = VM_WD_STEPS;  // steps per window (in-flight visits per lane)
+#ifndef VM_WD_AGG
+#define VM_WD_AGG 0  // measured: 31% fewer REDs but +16% instructions and MATCH latency
+                     // (short-scoreboard stalls): C2 walk 60.9 -> 94.2 ms per step
+#endif
+constexpr bool WD_AGG = VM_WD_AGG;       // warp-merged miss counts (match_any per step)
+constexpr unsigned long long WD_NONE = ~0ULL;
+constexpr unsigned long long WD_CUBE_TAG = 1ULL << 40;  // key = cube cell, not a voxel id
 constexpr int WD_BLOCKS = 3;  // resident blocks per SM
 constexpr int RP_BIAS = 512;  // bias of the grid-relative region coordinates
 
@@ -192,6 +199,11 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
     // candidates of the window: bit q of `live` -- slot q holds a candidate
     // (voxel id in sm.vids); `sure` -- known record (cube sample voxel / forced)
     unsigned live = 0, hits = 0, sure = 0;
+    // WD_AGG (off): the step's miss count applied after the step by the warp
+    // as a whole -- lanes counting the same voxel at the same step merge into
+    // one atomic (~46% of C2's per-step counts outside the sensor cube share
+    // a voxel with another lane); the MATCH per step costs more than it saves
+    unsigned long long pend = WD_NONE;
     // prefetch + warp work pool
     bool pf_valid = false, exhausted = false;
     unsigned pool_next = 0, pool_end = 0;
@@ -308,14 +320,16 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
                     live |= 1u << Q;
                     sure |= 1u << Q;
                 } else if (!REC_ONLY) {
-                    atomicAdd(sm.cube + ck, 1u);
+                    if (WD_AGG) pend = WD_CUBE_TAG | ck;
+                    else atomicAdd(sm.cube + ck, 1u);
                 }
             } else if (((bm >> wd_brick<DIM>(li, m.bsh)) & 1u) || forced) {
                 sm.vids[Q][threadIdx.x] = vid;
                 live |= 1u << Q;
                 if (forced) sure |= 1u << Q;
             } else if (!REC_ONLY) {
-                red_add(scr + vid, 1u);
+                if (WD_AGG) pend = vid;
+                else red_add(scr + vid, 1u);
             }
         } else {
             ++rmiss;
@@ -450,7 +464,19 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         if (!__any_sync(0xffffffffu, active || pf_valid || !exhausted || parked)) break;
         if (!__any_sync(0xffffffffu, active)) continue;
 #pragma unroll 1
-        for (int q = 0; q < WD_STEPS; ++q) step(q);
+        for (int q = 0; q < WD_STEPS; ++q) {
+            step(q);
+            if (WD_AGG && !REC_ONLY) {
+                const unsigned long long key = pend;
+                pend = WD_NONE;
+                const unsigned grp = __match_any_sync(0xffffffffu, key);
+                if (key != WD_NONE && (grp & lanemask_lt) == 0u) {  // the group's lowest lane
+                    const unsigned c = __popc(grp);
+                    if (key & WD_CUBE_TAG) atomicAdd(sm.cube + (unsigned)key, c);
+                    else red_add(scr + (unsigned)key, c);
+                }
+            }
+        }
     }
     // flush the warp's remaining records
     __syncwarp();
