@@ -359,7 +359,19 @@ def run_gpu_workload(name, args, dev, torch, world=1, dist=None, steps=None, e2e
             t = torch.tensor([ems], device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
+        pageable = None
+        if name == "c2" and not args.per_batch:
+            # the same through ordinary (pageable) numpy records: the driver
+            # stages each copy through its own pinned buffer
+            pslices = [host[offsets[b]:offsets[b + 1]] for b in range(len(data))]
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            vmap.clear()
+            run_e2e(pslices)
+            torch.cuda.synchronize()
+            pageable = total_rays / (time.perf_counter() - t1)
         e2e = {"value": total_rays * e2e_steps * world / (ems * 1e-3), "unit": UNIT,
+               "pageable_value": pageable,
                "h2d_bytes_per_step": int(host.nbytes),
                "d2h_bytes_per_step": int(len(data) * ctypes_stats_bytes()),
                "steps": e2e_steps,

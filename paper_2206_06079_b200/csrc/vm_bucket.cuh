@@ -4,8 +4,8 @@
 // The walk's records are (sample-voxel index mi) << ob | (ray*maxseg + seg) << 1 | hit
 // (key_mi; k_discover numbered the batch's sample voxels).  Instead of
 // radix-sorting all of them, the records are bucketed by mi -- one counting
-// pass, a scan over the sample-voxel list, one scatter of the 32-bit
-// (order, hit) payloads -- and each bucket is put in ray order on its own:
+// pass, a slice allocation (one atomic per warp, no scan), one scatter of the
+// 32-bit (order, hit) payloads -- and each bucket is put in ray order on its own:
 //
 //   <= BK_SERIAL records   one thread: insertion sort in registers/local memory
 //   <= BK_SMEM records     one block: bitonic sort in shared memory
@@ -34,7 +34,8 @@ constexpr int BK_SMEM = 4096;
 
 struct BucketState {
     unsigned *cnt;               // [M + 1] records per bucket (all zero between batches)
-    unsigned *off;               // [M + 1] exclusive scan of cnt
+    unsigned *off;               // [M + 1] slice offset (k_bk_alloc), bumped by the scatter
+    unsigned *cursor;            // slice allocation cursor (zeroed per batch)
     unsigned *val;               // [R] bucketed (order << 1 | hit) payloads
     int *big;                    // buckets for the block kernels
     unsigned long long *nbig;
@@ -66,7 +67,32 @@ __global__ void __launch_bounds__(BLOCK) k_bk_count(const __grid_constant__ DevM
     }
 }
 
-// cnt is counted back down to zero while scattering (ready for the next batch)
+// Each bucket's slice: one atomic per warp on a slice cursor (the slices need
+// not follow the sample-voxel order, so no scan)
+__global__ void __launch_bounds__(BLOCK) k_bk_alloc(const __grid_constant__ DevMap m, BucketState b) {
+    unsigned long long R, M;
+    if (!bk_live(m, R, M)) return;
+    const int lane = threadIdx.x & 31;
+    for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < M;
+         base += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long mi = base + threadIdx.x;
+        const unsigned c = mi < M ? b.cnt[mi] : 0u;
+        unsigned incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned wb = 0;
+        if (lane == 31 && tot) wb = atomicAdd(b.cursor, tot);
+        wb = __shfl_sync(0xffffffffu, wb, 31);
+        if (mi < M) b.off[mi] = wb + incl - c;
+    }
+}
+
+// the scatter bumps each bucket's offset past its records; the slice is then
+// [off - cnt, off) (bk_slice), and the folds zero cnt for the next batch
 __global__ void __launch_bounds__(BLOCK) k_bk_scatter(const __grid_constant__ DevMap m,
                                                       BucketState b) {
     unsigned long long R, M;
@@ -78,9 +104,14 @@ __global__ void __launch_bounds__(BLOCK) k_bk_scatter(const __grid_constant__ De
         const unsigned long long k = m.rec[i];
         const unsigned long long mi = k >> ob;
         if (mi >= M) continue;
-        const unsigned pos = b.off[mi] + atomicSub(b.cnt + mi, 1u) - 1u;
+        const unsigned pos = atomicAdd(b.off + mi, 1u);
         b.val[pos] = (unsigned)(k & omask);
     }
+}
+
+__device__ __forceinline__ unsigned bk_slice(const BucketState &b, unsigned long long mi, unsigned &c) {
+    c = b.cnt[mi];
+    return b.off[mi] - c;
 }
 
 // Per-voxel fold state: log-odds, packed mean, count, pending misses.
@@ -142,13 +173,13 @@ __global__ void __launch_bounds__(BLOCK, BK_FOLD_MINB) k_bk_fold(const __grid_co
     if (!bk_live(m, R, M)) return;
     for (unsigned long long mi = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; mi < M;
          mi += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned s = b.off[mi];
-        const unsigned e = mi + 1 < M ? b.off[mi + 1] : (unsigned)R;
-        const unsigned c = e - s;
+        unsigned c;
+        const unsigned s = bk_slice(b, mi, c);
         if (c > (unsigned)BK_SERIAL) {
             b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
             continue;
         }
+        b.cnt[mi] = 0u;
         unsigned v[BK_SERIAL];
         for (unsigned i = 0; i < c; ++i) {
             const unsigned x = b.val[s + i];
@@ -202,9 +233,10 @@ __global__ void __launch_bounds__(BLOCK) k_bk_fold_big(const __grid_constant__ D
     unsigned *hitb = pres + b.bwords;
     for (unsigned long long w = blockIdx.x; w < nb; w += gridDim.x) {
         const unsigned long long mi = (unsigned long long)b.big[w];
-        const unsigned s = b.off[mi];
-        const unsigned e = mi + 1 < M ? b.off[mi + 1] : (unsigned)R;
-        const unsigned c = e - s;
+        unsigned c;
+        const unsigned s = bk_slice(b, mi, c);
+        __syncthreads();  // every thread has read cnt before it is zeroed
+        if (threadIdx.x == 0) b.cnt[mi] = 0u;
         VoxFold f;
         if (c <= (unsigned)BK_SMEM) {
             unsigned P = 32;

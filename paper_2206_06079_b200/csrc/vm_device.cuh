@@ -86,6 +86,8 @@ struct DevMap {
     unsigned long long bpr[NUM_LAYERS];  // bytes per region per layer
     int *rgrid;                          // dense region-slot grid over the batch bbox
     unsigned *bmask;                     // per slot: brick summary of the batch's sample voxels
+    unsigned *gmask;                     // per slot (NDT maps): bricks that may hold a Gaussian
+                                         // (count >= 3); set by the fold, conservative
     int brick_shift;                     // log2(dim) - 2 for power-of-two dims >= 4, else -1
     int bsh[3];                          // brick index from the local index li (see brick_of)
     int *rbox;                           // [6]: min xyz, max xyz (regions) of the batch
@@ -119,6 +121,8 @@ struct DevMap {
     // batch outputs
     unsigned long long *rec;
     unsigned *recval;                    // per-record value (NDT deterministic phase 1)
+    double2 *rec_t;                      // NDT phase-1 records: the visit's chord (t0, t1),
+                                         // weighed after the walk (k_ndt_weigh)
     unsigned long long rec_cap;
     int *touched;                        // regions touched by the walk
     int touched_cap;

@@ -607,10 +607,10 @@ __device__ __forceinline__ void shard_ghost_visit(const DevMap &m, long long key
 
 struct NdtRecStage {
     unsigned long long *key;
-    unsigned *val;
+    double2 *t;
     int *n;
 };
-constexpr int NDT_STAGE = 1536;
+constexpr int NDT_STAGE = 1024;
 
 template <bool TM, bool DET = false, bool REC_ONLY = false>
 struct NdtVisitor {
@@ -631,10 +631,13 @@ struct NdtVisitor {
     // region-sharded maps: the current region is another rank's (ghost);
     // `unknown`: no Gaussian bitmap of it arrived this batch
     bool ghost, unknown;
+    unsigned gm;  // the region's Gaussian brick summary (all ones: unknown)
 
     __device__ __forceinline__ void bind() {
         int s = rt.slot;
         ghost = false;
+        gm = (m->gmask && m->brick_shift >= 0 && s >= 0 && s < m->cap) ? __ldcg(m->gmask + s)
+                                                                        : 0xFFFFFFFFu;
         if (DET && m->shard_world > 1 && s >= 0 && s < m->cap) {
             const long long key = m->slot_keys[s];
             ghost = region_owner(key, m->shard_world) != m->shard_rank;
@@ -687,7 +690,26 @@ struct NdtVisitor {
                 atomicAdd(scr + li, 1u);
             return;
         }
-        unsigned ns = __ldcg(cnt + li);
+        // a brick without a Gaussian: no count to load, g == 1
+        const unsigned ns = ((gm >> brick_of(li, m->bsh)) & 1u) ? __ldcg(cnt + li) : 0u;
+        if (DET && ns >= 3) {
+            // a miss through a Gaussian: a phase-1 record with its chord; the
+            // weight is computed after the walk, for all records at once
+            // (k_ndt_weigh), so no lane of the walk stalls the others on it
+            const unsigned long long key = ndt_key(ndt_index(*m, rt.slot, li), 0u, order >> 1);
+            const int k = atomicAdd(st.n, 1);
+            if (k < NDT_STAGE) {
+                st.key[k] = key;
+                st.t[k] = make_double2(t0, t1);
+            } else {
+                const unsigned long long g = atomicAdd(m->stats + S_RECORDS, 1ULL);
+                if (g < m->rec_cap) {
+                    m->rec[g] = key;
+                    m->rec_t[g] = make_double2(t0, t1);
+                }
+            }
+            return;
+        }
         if (ns < 3) {
             if (REC_ONLY) return;
             // g == 1: identical deltas, order-free -> counted, resolved exactly
@@ -709,23 +731,6 @@ struct NdtVisitor {
         mu[2] = ((double)z + off[2]) * m->vox;
         double gw = gaussian_weight(mu, c6, m->sigma2, so, v, t0, t1);
         float d32 = (float)(gw * m->miss_delta);
-        if (DET) {
-            const unsigned val = (__float_as_uint(d32) & 0x7FFFFFFFu) |
-                                 (gw >= m->miss_check ? 0x80000000u : 0u);
-            const unsigned long long key = ndt_key(ndt_index(*m, rt.slot, li), 0u, order >> 1);
-            const int k = atomicAdd(st.n, 1);
-            if (k < NDT_STAGE) {
-                st.key[k] = key;
-                st.val[k] = val;
-            } else {
-                const unsigned long long g = atomicAdd(m->stats + S_RECORDS, 1ULL);
-                if (g < m->rec_cap) {
-                    m->rec[g] = key;
-                    m->recval[g] = val;
-                }
-            }
-            return;
-        }
         {
             float *p = occ + li;
             unsigned old = __float_as_uint(__ldcg(p));
@@ -766,7 +771,7 @@ __global__ void __launch_bounds__(BLOCK, NDT_MINB) k_walk_ndt(const __grid_const
     __shared__ int sset[SLOTSET];
     __shared__ int corner[3];
     __shared__ unsigned long long skey[DET ? NDT_STAGE : 1];
-    __shared__ unsigned sval[DET ? NDT_STAGE : 1];
+    __shared__ double2 st_t[DET ? NDT_STAGE : 1];
     __shared__ int nrec;
     __shared__ unsigned long long rec_base;
     if (!read_go(m)) return;
@@ -789,7 +794,7 @@ __global__ void __launch_bounds__(BLOCK, NDT_MINB) k_walk_ndt(const __grid_const
     v.c0 = corner[0];
     v.c1 = corner[1];
     v.c2 = corner[2];
-    v.st = NdtRecStage{skey, sval, &nrec};
+    v.st = NdtRecStage{skey, st_t, &nrec};
     v.visits = v.rmiss = v.retries = 0;
     long long i = first + threadIdx.x;
     if (i < n) {
@@ -817,7 +822,7 @@ __global__ void __launch_bounds__(BLOCK, NDT_MINB) k_walk_ndt(const __grid_const
             const unsigned long long ri = rec_base + k;
             if (ri < m.rec_cap) {
                 m.rec[ri] = skey[k];
-                m.recval[ri] = sval[k];
+                m.rec_t[ri] = st_t[k];
             }
         }
     }
@@ -872,8 +877,9 @@ struct TsdfVisitor {
         }
         const int li = rt.li(*m);
         if (DET) {
-            unsigned long long vid = (unsigned long long)rt.slot * m->vpr + li;
-            stage->push((vid << m->order_bits) | ray, m->rec, m->stats + S_RECORDS, m->rec_cap);
+            // bucketed by the voxel's claimed index (vm_ndt.cuh), ray order
+            stage->push(ndt_key(ndt_index(*m, rt.slot, li), 0u, ray), m->rec, m->stats + S_RECORDS,
+                        m->rec_cap);
             return;
         }
         // reference.py:167-174

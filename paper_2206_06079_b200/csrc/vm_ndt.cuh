@@ -180,6 +180,50 @@ __device__ __forceinline__ bool bk_ndt_live(const DevMap &m, unsigned long long 
     return true;
 }
 
+// The deterministic walk files each miss through a Gaussian as a record with
+// its chord (rec_t); the weight is computed here, one thread per record,
+// exactly as _kernels.pyx:612-626 does it inline: the voxel's Gaussian at
+// the start of the batch (resets are applied later, in the fold), the
+// segment's origin and direction (engine.py:82-96), the chord (t0, t1).
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_ndt_weigh(const __grid_constant__ DevMap m, Src src) {
+    unsigned long long R, M;
+    if (!read_go(m)) return;
+    R = *((volatile unsigned long long *)(m.stats + S_RECORDS));
+    M = *((volatile unsigned long long *)m.nmarked);
+    if (R > m.rec_cap || M > m.marked_cap) return;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = m.rec[i];
+        if ((k >> 31) & 1ULL) continue;  // a sample (phase 2): no weight
+        const unsigned mi = (unsigned)(k >> 32);
+        if (mi >= M) continue;
+        const int2 sl = m.marked[mi];
+        if (sl.x < 0) continue;
+        const int s = sl.x, li = sl.y;
+        const unsigned oi = (unsigned)k & 0x7FFFFFFFu;
+        Ray r;
+        src.load((long long)(oi / (unsigned)m.maxseg), r.o, r.e, r.has, r.inten);
+        prep_ray(m, r, true);
+        double so[3], se[3];
+        int sh;
+        segment_of(m, r, (int)(oi % (unsigned)m.maxseg), so, se, sh);
+        const double v[3] = {se[0] - so[0], se[1] - so[1], se[2] - so[2]};
+        int g[3];
+        slot_li_to_g(m, s, li, g);
+        double off[3], mu[3];
+        unpack_mean(layer_at<unsigned>(m, L_MEAN, s)[li], off);
+        for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
+        float c6[6];
+        const float *cov = layer_at<float>(m, L_COV, s) + li * 6;
+        for (int j = 0; j < 6; ++j) c6[j] = cov[j];
+        const double2 t = m.rec_t[i];
+        const double gw = gaussian_weight(mu, c6, m.sigma2, so, v, t.x, t.y);
+        const float d32 = (float)(gw * m.miss_delta);
+        m.recval[i] = (__float_as_uint(d32) & 0x7FFFFFFFu) | (gw >= m.miss_check ? 0x80000000u : 0u);
+    }
+}
+
 __global__ void __launch_bounds__(BLOCK) k_nbk_count(const __grid_constant__ DevMap m, NdtBuckets b) {
     unsigned long long R, M;
     if (!bk_ndt_live(m, R, M)) return;
@@ -284,7 +328,7 @@ __global__ void __launch_bounds__(BLOCK) k_nbk_scatter(const __grid_constant__ D
         const unsigned mi = (unsigned)(k >> 32);
         if (mi >= M) continue;
         const unsigned pos = atomicAdd(b.off + mi, 1u);
-        b.val[pos] = (k << 32) | (unsigned long long)m.recval[i];
+        b.val[pos] = (k << 32) | (m.recval ? (unsigned long long)m.recval[i] : 0ULL);
     }
 }
 
@@ -600,6 +644,8 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
                 hb[li] += ns;
             }
             cb[li] = n > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)n;
+            if (n >= 3 && m.gmask)  // the walk loads this brick's counts from now on
+                atomicOr(m.gmask + slot, m.brick_shift >= 0 ? 1u << brick_of(li, m.bsh) : 0xFFFFFFFFu);
             double frac[3];
             const double hi = 1.0 - 1.0 / 2048.0;
 #pragma unroll
@@ -617,6 +663,53 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
             occ[li] = l;
             layer_at<unsigned>(m, L_NIDX, slot)[li] = 0u;
         }
+    }
+}
+
+// Deterministic TSDF (reference.py:153-175): one thread per voxel bucket
+// merges the voxel's band visits in ray order; clears the index stamp and
+// the bucket count.
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_tsdf_fold(const __grid_constant__ DevMap m, Src src,
+                                                     NdtBuckets b) {
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    const unsigned K = *((volatile unsigned *)(b.cursor + NBK_BINS));
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < K; t += gridDim.x * blockDim.x) {
+        const unsigned mi = b.perm[t];
+        unsigned c;
+        const unsigned s = nbk_start(b, mi, c);
+        b.cnt[mi] = 0u;
+        b.cnt2[mi] = 0u;
+        const int2 sl = m.marked[mi];
+        if (sl.x < 0) continue;
+        const int slot = sl.x, li = sl.y;
+        int g[3];
+        slot_li_to_g(m, slot, li, g);
+        float *buf = layer_at<float>(m, L_TSDF, slot);
+        float fd = buf[2 * li], fw = buf[2 * li + 1];
+        for (unsigned i = 0; i < c; ++i) {
+            const long long ray = (long long)((b.val[s + i] >> 32) & 0x7FFFFFFFULL);
+            Ray r;
+            src.load(ray, r.o, r.e, r.has, r.inten);
+            prep_ray(m, r, false);
+            double d[3];
+            for (int a = 0; a < 3; ++a) d[a] = (r.e[a] - r.o[a]) / r.L;
+            const double cc[3] = {((double)g[0] + 0.5) * m.vox - r.o[0],
+                                  ((double)g[1] + 0.5) * m.vox - r.o[1],
+                                  ((double)g[2] + 0.5) * m.vox - r.o[2]};
+            double dv = r.L - dot3(cc, d);
+            if (dv < -m.tsdf_trunc) dv = -m.tsdf_trunc;
+            if (dv > m.tsdf_trunc) dv = m.tsdf_trunc;
+            const double w = fw;
+            fd = (float)((w * (double)fd + dv) / (w + 1.0));
+            double nw = w + 1.0;
+            if (nw > m.tsdf_maxw) nw = m.tsdf_maxw;
+            fw = (float)nw;
+        }
+        buf[2 * li] = fd;
+        buf[2 * li + 1] = fw;
+        layer_at<unsigned>(m, L_NIDX, slot)[li] = 0u;
     }
 }
 

@@ -100,6 +100,7 @@ struct vm_map {
     unsigned long long *d_work = nullptr;
     int *d_rgrid = nullptr;
     unsigned *d_bmask = nullptr;
+    unsigned *d_gmask = nullptr;     // NDT: bricks that may hold a Gaussian (walk skips the count load)
     int *d_rbox = nullptr;
     long long *d_big = nullptr;
     size_t big_cap = 0;
@@ -114,11 +115,11 @@ struct vm_map {
     unsigned long long *d_nbk_ctr = nullptr;  // NDT: [mid, big] sort-list lengths
     double4 *d_nbk_pos = nullptr;    // NDT: sample end points beside their bucket slots
     size_t nbk_pos_cap = 0;
+    double2 *d_rec_t = nullptr;      // NDT: chords of the phase-1 records (k_ndt_weigh)
+    size_t rec_t_cap = 0;
     unsigned *d_nbk_small = nullptr; // NDT: size histogram, cursors, live count, slice cursor
     unsigned *d_bk_bits = nullptr;
     size_t bk_bits_cap = 0;
-    void *d_scan_tmp = nullptr;
-    size_t scan_tmp_bytes = 0;
     // pipelined sequences (vm_integrate_many)
     int *d_chain = nullptr;
     unsigned long long *d_mstats = nullptr, *h_mstats = nullptr;
@@ -234,6 +235,7 @@ DevMap make_dm(const vm_map *m) {
     }
     d.rgrid = m->d_rgrid;
     d.bmask = m->d_bmask;
+    d.gmask = m->d_gmask;
     {
         int bs = -1;
         if (m->dim >= 4 && (m->dim & (m->dim - 1)) == 0) {
@@ -261,6 +263,7 @@ DevMap make_dm(const vm_map *m) {
     d.go = m->d_go;
     d.rec = m->d_rec;
     d.recval = m->d_val;
+    d.rec_t = m->d_rec_t;
     d.rec_cap = m->rec_cap;
     d.touched = m->d_touched;
     d.touched_cap = (int)m->max_slots;
@@ -528,14 +531,6 @@ int ensure_buckets(vm_map *m, size_t nmarked_cap, size_t bwords) {
         CK(cudaMalloc((void **)&m->d_bk_big, nc * sizeof(int)));
         CK(cudaMalloc((void **)&m->d_bk_perm, nc * sizeof(unsigned)));
         m->bk_cap = nc;
-        size_t bytes = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, m->d_bk_cnt, m->d_bk_off, (int)nc));
-        if (bytes > m->scan_tmp_bytes) {
-            cudaFree(m->d_scan_tmp);
-            m->d_scan_tmp = nullptr;
-            CK(cudaMalloc(&m->d_scan_tmp, bytes));
-            m->scan_tmp_bytes = bytes;
-        }
     }
     const size_t need = (size_t)m->num_sms * 2 * bwords;
     if (need > m->bk_bits_cap || !m->d_bk_bits) {
@@ -554,14 +549,20 @@ int launch_bucket_fold(vm_map *m, const DevMap &dm, const Src &src, long long n,
     const unsigned long long bwords = ((unsigned long long)n * maxseg + 31) / 32 + 1;
     int rc;
     if ((rc = ensure_buckets(m, m->smarked_cap, bwords))) return rc;
-    BucketState b{m->d_bk_cnt, m->d_bk_off, reinterpret_cast<unsigned *>(m->d_rec2), m->d_bk_big,
-                  m->d_nbig, m->d_bk_bits, bwords};
+    if (!m->d_nbk_small) {
+        CK(cudaMalloc((void **)&m->d_nbk_small, (2 * NBK_BINS + 4) * sizeof(unsigned)));
+        CK(cudaMemset(m->d_nbk_small, 0, (2 * NBK_BINS + 4) * sizeof(unsigned)));
+    }
+    unsigned *cursor = m->d_nbk_small + 2 * NBK_BINS + 2;
+    BucketState b{m->d_bk_cnt, m->d_bk_off, cursor, reinterpret_cast<unsigned *>(m->d_rec2),
+                  m->d_bk_big, m->d_nbig, m->d_bk_bits, bwords};
     CK(cudaMemsetAsync(m->d_nbig, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(cursor, 0, sizeof(unsigned), s));
     const unsigned g = (unsigned)m->num_sms * 8;
+    const unsigned ga = (unsigned)std::max<long long>(
+        1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
     k_bk_count<<<g, BLOCK, 0, s>>>(dm, b);
-    size_t bytes = m->scan_tmp_bytes;
-    CK(cub::DeviceScan::ExclusiveSum(m->d_scan_tmp, bytes, m->d_bk_cnt, m->d_bk_off,
-                                     (int)m->smarked_cap, s));
+    k_bk_alloc<<<ga, BLOCK, 0, s>>>(dm, b);
     k_bk_scatter<<<g, BLOCK, 0, s>>>(dm, b);
     CK(cudaEventRecord(ev_mid, s));
     const unsigned gf = (unsigned)std::max<long long>(
@@ -596,6 +597,7 @@ int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, in
     const unsigned gr = (unsigned)m->num_sms * 8;
     const unsigned gm = (unsigned)std::max<long long>(
         1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
+    k_ndt_weigh<<<gr, BLOCK, 0, s>>>(dm, src);
     k_nbk_count<<<gr, BLOCK, 0, s>>>(dm, b);
     k_nbk_alloc<<<gm, BLOCK, 0, s>>>(dm, b);
     if (std::getenv("VOXMAP_B200_NDT_DEBUG")) {
@@ -620,8 +622,47 @@ int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, in
     CK(cudaEventRecord(ev_mid, s));
     if (tm) k_nbk_fold<true><<<gm, BLOCK, 0, s>>>(dm, b);
     else k_nbk_fold<false><<<gm, BLOCK, 0, s>>>(dm, b);
-    m->launches += 10;
+    m->launches += 11;
     return check_launch("ndt fold");
+}
+
+// Deterministic TSDF: the band visits bucketed by voxel (the NDT bucket
+// kernels, every record a plain ray-order key) and merged per voxel in ray
+// order (k_tsdf_fold).
+template <class Src>
+int launch_tsdf_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, cudaEvent_t ev_mid) {
+    cudaStream_t s = m->stream;
+    const unsigned long long span = (unsigned long long)n;
+    const unsigned long long bwords = (2 * span + 31) / 32 + 1;
+    int rc;
+    if ((rc = ensure_buckets(m, m->smarked_cap, bwords))) return rc;
+    if (!m->d_nbk_small) {
+        CK(cudaMalloc((void **)&m->d_nbk_small, (2 * NBK_BINS + 4) * sizeof(unsigned)));
+        CK(cudaMemset(m->d_nbk_small, 0, (2 * NBK_BINS + 4) * sizeof(unsigned)));
+    }
+    if (!m->d_nbk_ctr) CK(cudaMalloc((void **)&m->d_nbk_ctr, 2 * sizeof(unsigned long long)));
+    NdtBuckets b{m->d_bk_cnt, m->d_bk_cnt2, m->d_bk_off, m->d_bk_perm, m->d_nbk_small,
+                 m->d_nbk_small + NBK_BINS, m->d_rec2, m->d_rec, nullptr, m->d_bk_big,
+                 m->d_bk_big2, m->d_nbk_ctr, m->d_nbk_ctr + 1, m->d_bk_bits, bwords, span};
+    CK(cudaMemsetAsync(m->d_nbk_ctr, 0, 2 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(b.cursor + NBK_BINS, 0, 2 * sizeof(unsigned), s));
+    DevMap d2 = dm;
+    d2.recval = nullptr;  // plain keys
+    const unsigned gr = (unsigned)m->num_sms * 8;
+    const unsigned gm = (unsigned)std::max<long long>(
+        1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
+    k_nbk_count<<<gr, BLOCK, 0, s>>>(d2, b);
+    k_nbk_alloc<<<gm, BLOCK, 0, s>>>(d2, b);
+    k_nbk_order<<<1, NBK_BINS, 0, s>>>(d2, b);
+    k_nbk_perm<<<gm, BLOCK, 0, s>>>(d2, b);
+    k_nbk_scatter<<<gr, BLOCK, 0, s>>>(d2, b);
+    k_nbk_sort_small<<<gm, BLOCK, 0, s>>>(d2, b);
+    k_nbk_sort_mid<<<m->num_sms * 4, BLOCK, 0, s>>>(d2, b);
+    k_nbk_sort_big<<<m->num_sms, BLOCK, 0, s>>>(d2, b);
+    CK(cudaEventRecord(ev_mid, s));
+    k_tsdf_fold<<<gm, BLOCK, 0, s>>>(d2, src, b);
+    m->launches += 9;
+    return check_launch("tsdf fold");
 }
 
 const uint32_t MODE_MASK[5] = {
@@ -730,6 +771,7 @@ int reload_region(vm_map *m, long long key, int *slot_out) {
     const unsigned last = m->batch_no;
     CK(cudaMemcpyAsync(m->d_slot_last + slot, &last, sizeof(unsigned), cudaMemcpyHostToDevice,
                        m->stream));
+    CK(cudaMemsetAsync(m->d_gmask + slot, 0xFF, sizeof(unsigned), m->stream));  // conservative
     CK(cudaStreamSynchronize(m->stream));
     m->spilled.erase(key);
     std::remove(path.c_str());
@@ -757,7 +799,12 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     const bool tsdf = mode == M_TSDF;
     const bool det = exec == VM_EXEC_DETERMINISTIC;
     const bool occ_det = det && (mode == M_OCC || mode == M_DECAY);
-    const bool sorted = occ_det || (tsdf && det);  // NDT: bucketed (launch_ndt_fold)
+    const bool tsdf_det = tsdf && det;
+    // occupancy on a sharded map: a sorted fold; NDT and TSDF: voxel buckets
+    // (launch_ndt_fold / launch_tsdf_fold); occupancy on one GPU: sample-voxel
+    // buckets (launch_bucket_fold)
+    const bool sorted = occ_det;
+    const bool vbuck = ndt || tsdf_det;  // records keyed by a claimed voxel index (L_NIDX)
     const bool resolve = occ_det || ndt;
     const int maxseg = (int)std::ceil(m->cfg.max_ray_range / m->cfg.segment_length) + 1;
     unsigned long long order_span = tsdf ? (unsigned long long)n
@@ -790,13 +837,19 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                                                      : (size_t)n * (det ? 8 : 1) + 1;
         if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, need)))) return rc;
         if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_rec_t, &m->rec_t_cap, m->rec_cap))) return rc;
+        CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
+    }
+    if (tsdf_det) {
+        // at most one record per band visit: an upper bound, no overflow path
+        const double band = 2.0 * m->cfg.tsdf_truncation / m->cfg.voxel_size;
+        const size_t need = (size_t)n * (size_t)(3.0 * (std::ceil(band) + 2.0) + 4.0) + 1;
+        if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, need)))) return rc;
+        if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
         CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
     }
     size_t rec_need = 0;
-    if (tsdf && det) {
-        double band = 2.0 * m->cfg.tsdf_truncation / m->cfg.voxel_size;
-        rec_need = (size_t)n * (size_t)(3.0 * (std::ceil(band) + 2.0) + 4.0);
-    } else if (occ_det) rec_need = std::max<size_t>(m->rec_cap, rec_floor(m, n));
+    if (occ_det) rec_need = std::max<size_t>(m->rec_cap, rec_floor(m, n));
     if (sorted && (rc = ensure_records(m, rec_need))) return rc;
 
     float ms_total = 0.f, ms_walk = 0.f, ms_disc = 0.f, ms_res = 0.f, ms_sort = 0.f, ms_fold = 0.f;
@@ -812,7 +865,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         DevMap dm = make_dm(m);
         dm.order_bits = order_bits;
         dm.ray_order = ray_order ? 1 : 0;
-        if (key_mi || ndt) {
+        if (key_mi || vbuck) {
             dm.key_mi = key_mi ? 1 : 0;
             dm.marked = m->d_smarked;
             dm.nmarked = m->d_shard_cnt;
@@ -900,9 +953,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             if ((rc = check_launch("resolve"))) return rc;
         }
         CK(cudaEventRecord(m->ev_res, m->stream));
-        if (key_mi || ndt) {
+        if (key_mi || vbuck) {
             // the whole batch is enqueued; one sync at its end
             if (ndt) rc = launch_ndt_fold(m, dm, src, n, maxseg, mode == M_NDT_TM, m->ev_sort);
+            else if (tsdf_det) rc = launch_tsdf_fold(m, dm, src, n, m->ev_sort);
             else rc = launch_bucket_fold(m, dm, src, n, maxseg, m->ev_sort);
             if (rc) return rc;
             CK(cudaEventRecord(m->ev_end, m->stream));
@@ -928,7 +982,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
                 k_clear_marks<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
             }
-            if (ndt) {
+            if (vbuck) {
                 const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
                 k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
             }
@@ -959,6 +1013,17 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             ++replays;
             continue;
         }
+        if (tsdf_det) {
+            if (m->h_stats[S_RECORDS] > m->rec_cap || m->h_stats[NUM_STATS + 1] > m->smarked_cap)
+                return fail(VM_ERR_CUDA, "TSDF record bound exceeded");
+            CK(cudaEventElapsedTime(&ms_total, m->ev_start, m->ev_end));
+            CK(cudaEventElapsedTime(&ms_walk, m->ev_w0, m->ev_w1));
+            CK(cudaEventElapsedTime(&ms_disc, m->ev_start, m->ev_w0));
+            CK(cudaEventElapsedTime(&ms_res, m->ev_w1, m->ev_res));
+            CK(cudaEventElapsedTime(&ms_sort, m->ev_res, m->ev_sort));
+            CK(cudaEventElapsedTime(&ms_fold, m->ev_sort, m->ev_end));
+            break;
+        }
         if (ndt) {
             unsigned long long R = m->h_stats[S_RECORDS], M = m->h_stats[NUM_STATS + 1];
             if (R > m->rec_cap || M > m->smarked_cap) {
@@ -970,8 +1035,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
                 if ((rc = ensure_records(m, std::max<size_t>((size_t)R + (R >> 2), m->rec_cap)))) return rc;
                 if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+                if ((rc = ensure_buf(&m->d_rec_t, &m->rec_t_cap, m->rec_cap))) return rc;
                 dm.rec = m->d_rec;
                 dm.recval = m->d_val;
+                dm.rec_t = m->d_rec_t;
                 dm.rec_cap = m->rec_cap;
                 dm.marked = m->d_smarked;
                 dm.marked_cap = m->smarked_cap;
@@ -1097,7 +1164,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     out->region_misses = (int64_t)hs[S_RMISS];
     out->regions_touched = (int64_t)hs[S_PREF_TOUCHED];
     out->records = (int64_t)hs[S_RECORDS];
-    out->marked_voxels = (key_mi || ndt) ? (int64_t)hs[NUM_STATS + 1] : (int64_t)hs[S_MARKED];
+    out->marked_voxels = (key_mi || vbuck) ? (int64_t)hs[NUM_STATS + 1] : (int64_t)hs[S_MARKED];
     out->regions_total = cursor;
     out->new_regions = cursor - nreg0;
     out->replays = replays;
@@ -1430,7 +1497,8 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
     m->tsize = ts;
     for (int l = 0; l < NUM_LAYERS; ++l) {
         bool on = l == L_SCRATCH ? true
-                  : l == L_NIDX  ? ((layer_mask >> L_COV) & 1u) != 0  // NDT maps
+                  : l == L_NIDX  ? ((layer_mask >> L_COV) & 1u) != 0 ||   // NDT and TSDF maps
+                                       ((layer_mask >> L_TSDF) & 1u) != 0
                                  : ((layer_mask >> l) & 1u) != 0;
         m->bpr[l] = on ? (size_t)m->vpr * LAYER_COMP[l] * LAYER_ELEM[l] : 0;
     }
@@ -1453,7 +1521,7 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         (rc = dev_alloc(&m->d_go, 1)) || (rc = dev_alloc(&m->d_touched, m->max_slots)) ||
         (rc = dev_alloc(&m->d_work, 1)) ||
         (rc = dev_alloc(&m->d_rgrid, RG_MAX)) || (rc = dev_alloc(&m->d_rbox, 6)) ||
-        (rc = dev_alloc(&m->d_bmask, m->max_slots)) ||
+        (rc = dev_alloc(&m->d_bmask, m->max_slots)) || (rc = dev_alloc(&m->d_gmask, m->max_slots)) ||
         (rc = dev_alloc(&m->d_seg_hist, SEG_BUCKETS)) ||
         (rc = dev_alloc(&m->d_shard_cnt, 3)) ||
         (rc = dev_alloc(&m->d_seg_cursor, SEG_BUCKETS)) ||
@@ -1510,6 +1578,7 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_reload);
     cudaFree(m->d_slot_last);
     cudaFree(m->d_bmask);
+    cudaFree(m->d_gmask);
     cudaFree(m->d_big);
     cudaFree(m->d_nbig);
     cudaFree(m->d_bk_cnt);
@@ -1520,6 +1589,7 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_bk_big2);
     cudaFree(m->d_nbk_ctr);
     cudaFree(m->d_nbk_pos);
+    cudaFree(m->d_rec_t);
     cudaFree(m->d_nbk_small);
     cudaFree(m->d_bk_bits);
     cudaFree(m->d_chain);
@@ -1531,7 +1601,6 @@ int vm_map_destroy(vm_map *m) {
         if (m->ev_ring[r]) cudaEventDestroy(m->ev_ring[r]);
         if (m->ev_ring_up[r]) cudaEventDestroy(m->ev_ring_up[r]);
     }
-    cudaFree(m->d_scan_tmp);
     cudaFree(m->d_rbox);
     cudaFree(m->d_stats);
     cudaFree(m->d_go);
@@ -1566,6 +1635,7 @@ int vm_map_reset(vm_map *m) {
     CK(cudaMemsetAsync(m->d_tvals, 0xFF, m->tsize * sizeof(int), m->stream));
     CK(cudaMemsetAsync(m->d_cursor, 0, sizeof(int), m->stream));
     CK(cudaMemsetAsync(m->d_bmask, 0, m->max_slots * sizeof(unsigned), m->stream));
+    CK(cudaMemsetAsync(m->d_gmask, 0, m->max_slots * sizeof(unsigned), m->stream));
     CK(cudaMemsetAsync(m->d_slot_last, 0, m->max_slots * sizeof(unsigned), m->stream));
     CK(cudaStreamSynchronize(m->stream));
     m->nreg = 0;
@@ -1702,6 +1772,7 @@ int vm_map_evict_regions(vm_map *m, const int64_t *keys, int64_t n, int64_t *evi
     const int cur = (int)nk;
     CK(cudaMemcpyAsync(m->d_cursor, &cur, sizeof(int), cudaMemcpyHostToDevice, m->stream));
     CK(cudaMemsetAsync(m->d_bmask, 0, (size_t)nreg * sizeof(unsigned), m->stream));
+    CK(cudaMemsetAsync(m->d_gmask, 0xFF, (size_t)nreg * sizeof(unsigned), m->stream));  // conservative
     CK(cudaMemsetAsync(m->d_slot_touch, 0, (size_t)nreg * sizeof(unsigned), m->stream));
     CK(cudaMemsetAsync(m->d_slot_pref, 0, (size_t)nreg * sizeof(unsigned), m->stream));
     CK(cudaStreamSynchronize(m->stream));
@@ -1841,6 +1912,8 @@ int vm_map_write_layer(vm_map *m, int32_t slot, int32_t layer, const void *src, 
     int rc = layer_io(m, slot, layer, bytes, &off);
     if (rc) return rc;
     CK(cudaSetDevice(m->device));
+    if (layer == L_COUNT)  // the host may have made Gaussians anywhere in the region
+        CK(cudaMemsetAsync(m->d_gmask + slot, 0xFF, sizeof(unsigned), m->stream));
     CK(cudaMemcpyAsync((char *)m->slab[layer] + off, src, bytes, cudaMemcpyHostToDevice,
                        m->stream));
     CK(cudaStreamSynchronize(m->stream));
@@ -2298,6 +2371,7 @@ int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, i
         // records: the slice's samples and walk records plus imported ones
         if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, (size_t)n_all * 8 + 1)))) return rc;
         if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_rec_t, &m->rec_t_cap, m->rec_cap))) return rc;
         if ((rc = ensure_buf(&m->d_gx, &m->gx_cap, (size_t)n * 16 + 1))) return rc;
         if (!m->d_ngx) CK(cudaMalloc((void **)&m->d_ngx, sizeof(unsigned long long)));
         CK(cudaMemsetAsync(m->d_ngx, 0, sizeof(unsigned long long), m->stream));

@@ -20,9 +20,9 @@
 //   export   visit items, ghost miss counts, the phase-2 records of ghost
 //            sample voxels -- all per owner
 //   -- exchange B: items all-to-all --
-//   import   the owner computes each visit's Gaussian weight from the
-//            segment (every rank holds the whole batch) and its own
-//            Gaussian, exactly as its own walk does, and files the records
+//   import   the owner files each visit as a phase-1 record of its own
+//            Gaussian voxel; k_ndt_weigh weighs it from the segment (every
+//            rank holds the whole batch) exactly like its own walk's records
 //   finish   drop the ghost state; resolve, bucket, fold as on one GPU
 //
 // Every record carries its global segment order, so each owner folds the
@@ -192,36 +192,17 @@ __global__ void __launch_bounds__(BLOCK) k_shard_ndt_import(const __grid_constan
             }
             continue;
         }
-        // a phase-1 visit: weighed here, with this rank's Gaussian, exactly as
-        // the NDT walk weighs its own (NdtVisitor::visit)
+        // a phase-1 visit: a record of this rank's Gaussian voxel
         const unsigned ns = layer_at<unsigned>(m, L_COUNT, s)[li];
         if (ns < 3u) {
             red_add(scr, 1u);
             continue;
         }
-        const long long ray = (long long)(it.val / (unsigned)m.maxseg);
-        const int seg = (int)(it.val % (unsigned)m.maxseg);
-        Ray r;
-        src.load(ray, r.o, r.e, r.has, r.inten);
-        prep_ray(m, r, true);
-        double so[3], se[3];
-        int sh;
-        segment_of(m, r, seg, so, se, sh);
-        const double v[3] = {se[0] - so[0], se[1] - so[1], se[2] - so[2]};
-        int g[3];
-        slot_li_to_g(m, s, li, g);
-        double off[3], mu[3];
-        unpack_mean(layer_at<unsigned>(m, L_MEAN, s)[li], off);
-        for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
-        float c6[6];
-        const float *cov = layer_at<float>(m, L_COV, s) + li * 6;
-        for (int j = 0; j < 6; ++j) c6[j] = cov[j];
-        const double gw = gaussian_weight(mu, c6, m.sigma2, so, v, it.t0, it.t1);
-        const float d32 = (float)(gw * m.miss_delta);
+        // (k_ndt_weigh weighs it with this rank's Gaussian, like its own records)
         const unsigned long long k = atomicAdd(m.stats + S_RECORDS, 1ULL);
         if (k < m.rec_cap) {
             m.rec[k] = ndt_key(ndt_index(m, s, li), 0u, it.val);
-            m.recval[k] = (__float_as_uint(d32) & 0x7FFFFFFFu) | (gw >= m.miss_check ? 0x80000000u : 0u);
+            m.rec_t[k] = make_double2(it.t0, it.t1);
         }
     }
 }

@@ -57,7 +57,10 @@ constexpr int WK_WBUF = 64;     // per-warp record ring (flushed 32 at a time)
 // Sensor cube: the voxels next to the sensor, which every ray of the batch
 // crosses, count in shared memory instead of as same-address L2 atomics.
 // 16^3 instead of 8^3: C2 walk 63.7 -> 61.0 ms per step.
-constexpr int WCB = 4;                // log2 of the sensor cube edge
+#ifndef VM_WCB
+#define VM_WCB 4
+#endif
+constexpr int WCB = VM_WCB;           // log2 of the sensor cube edge
 constexpr int WCUBE = 1 << WCB;       // sensor cube edge (voxels)
 constexpr int WCUBE_N = WCUBE * WCUBE * WCUBE;
 // cube coordinates packed one per byte in cp: cube cell index, and the

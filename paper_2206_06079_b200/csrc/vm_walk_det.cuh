@@ -38,7 +38,10 @@ constexpr int WD_STEPS = VM_WD_STEPS;  // steps per window (in-flight visits per
 constexpr bool WD_AGG = VM_WD_AGG;       // warp-merged miss counts (match_any per step)
 constexpr unsigned long long WD_NONE = ~0ULL;
 constexpr unsigned long long WD_CUBE_TAG = 1ULL << 40;  // key = cube cell, not a voxel id
-constexpr int WD_BLOCKS = 3;  // resident blocks per SM
+#ifndef VM_WD_BLOCKS
+#define VM_WD_BLOCKS 3
+#endif
+constexpr int WD_BLOCKS = VM_WD_BLOCKS;  // resident blocks per SM
 constexpr int RP_BIAS = 512;  // bias of the grid-relative region coordinates
 
 struct WalkDetSmem {
