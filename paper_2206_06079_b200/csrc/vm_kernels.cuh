@@ -111,7 +111,13 @@ __device__ __forceinline__ double gaussian_weight(const double mu[3], const floa
     return exp(-0.5 * m2);
 }
 
+// the batch may run: its guard let it, and no earlier batch of a pipelined
+// sequence stopped the chain (chain = failing batch + 1)
 __device__ __forceinline__ int read_go(const DevMap &m) {
+    if (m.chain) {
+        const int c = *((volatile int *)m.chain);
+        if (c && c <= m.batch_idx) return 0;
+    }
     return *((volatile int *)m.go);
 }
 
@@ -169,6 +175,24 @@ __device__ __forceinline__ unsigned ndt_index(const DevMap &m, int slot, int li)
         return (unsigned)mi;
     }
     m.marked[mi] = make_int2(-1, -1);
+    return prev & ~NIDX_FLAG;
+}
+
+// ndt_index for the occupancy sample-voxel list: counts the lost races in
+// nmarked[1], so the list's live length is nmarked[0] - nmarked[1]
+__device__ __forceinline__ unsigned claim_sample_voxel(const DevMap &m, int slot, int li) {
+    unsigned *w = layer_at<unsigned>(m, L_NIDX, slot) + li;
+    const unsigned cur = *((volatile unsigned *)w);
+    if (cur & NIDX_FLAG) return cur & ~NIDX_FLAG;
+    const unsigned long long mi = atomicAdd(m.nmarked, 1ULL);
+    if (mi >= m.marked_cap || mi >= (unsigned long long)NIDX_FLAG) return 0xFFFFFFFFu;
+    const unsigned prev = atomicCAS(w, 0u, NIDX_FLAG | (unsigned)mi);
+    if (prev == 0u) {
+        m.marked[mi] = make_int2(slot, li);
+        return (unsigned)mi;
+    }
+    m.marked[mi] = make_int2(-1, -1);
+    atomicAdd(m.nmarked + 1, 1ULL);
     return prev & ~NIDX_FLAG;
 }
 
@@ -404,6 +428,12 @@ __global__ void __launch_bounds__(DISC_BT, DISC_MINB) k_discover(const __grid_co
                         const unsigned mi = ndt_index(m, rt.slot, li);
                         int k = atomicAdd(&nrec, 1);
                         srec[k] = ndt_key(mi, 1u, (unsigned)(i * m.maxseg + s));
+                    } else if (m.key_mi) {
+                        // claim the sample voxel's index; k_stamp writes MARK_FLAG | mi
+                        // into its scratch word and the brick summary once the
+                        // previous batch has folded (pipelined sequences run this
+                        // discover concurrently with that fold)
+                        claim_sample_voxel(m, rt.slot, li);
                     } else {
                         // stamp the sample voxel: the walk turns its visits into records
                         unsigned *w = layer_at<unsigned>(m, L_SCRATCH, rt.slot) + li;
@@ -513,25 +543,54 @@ __global__ void k_guard(const __grid_constant__ DevMap m, int margin) {
 }
 
 // Pipelined sequences: per-batch state reset (stats slot, region box, the
-// sample-voxel list unless the batch is a replay that keeps its stamps).
+// sample-voxel list unless the batch is a replay that keeps its claims).
 __global__ void k_batch_init(const __grid_constant__ DevMap m, int reset_marked) {
     if (*((volatile int *)m.chain)) return;
     const int t = threadIdx.x;
     if (t < NUM_STATS) m.stats[t] = 0ULL;
     if (t < 3) m.rbox[t] = INT_MAX;
     else if (t < 6) m.rbox[t] = INT_MIN;
-    if (t == 0 && reset_marked && m.nmarked) *m.nmarked = 0ULL;
+    if (t < 2 && reset_marked && m.nmarked) m.nmarked[t] = 0ULL;
+}
+
+// Occupancy sample voxels: MARK_FLAG | mi into the scratch word, the brick
+// bit into the region's summary, the claim released.  Runs after the previous
+// batch's fold (which clears its own stamps) and before this batch's walk.
+__global__ void __launch_bounds__(BLOCK) k_stamp(const __grid_constant__ DevMap m) {
+    if (!read_go(m)) return;
+    const unsigned long long M = min(*((volatile unsigned long long *)m.nmarked), m.marked_cap);
+    const int bsh = m.brick_shift;
+    for (unsigned long long mi = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; mi < M;
+         mi += (unsigned long long)gridDim.x * blockDim.x) {
+        const int2 sl = m.marked[mi];
+        if (sl.x < 0 || sl.x >= m.cap) continue;
+        const unsigned long long vid = (unsigned long long)sl.x * m.vpr + sl.y;
+        reinterpret_cast<unsigned *>(m.slab[L_SCRATCH])[vid] = MARK_FLAG | (unsigned)mi;
+        reinterpret_cast<unsigned *>(m.slab[L_NIDX])[vid] = 0u;
+        const unsigned bit = bsh >= 0 ? 1u << brick_of(sl.y, m.bsh) : 0xFFFFFFFFu;
+        if (!(__ldcg(m.bmask + sl.x) & bit)) atomicOr(m.bmask + sl.x, bit);
+    }
 }
 
 // ... and its outcome: regions after the batch and whether it ran.
-__global__ void k_batch_fin(const __grid_constant__ DevMap m) {
-    // sample voxels of the batch: the list length (also counts stamps a
-    // refused first attempt left for the replay)
-    if (m.key_mi && m.nmarked) m.stats[S_MARKED] = *((volatile unsigned long long *)m.nmarked);
+// The regions after the batch, snapshot right after its walk (the next
+// batch's discover may already be creating regions while this one folds).
+__global__ void k_batch_regions(const __grid_constant__ DevMap m) {
     m.stats[NUM_STATS] = (unsigned long long)*((volatile int *)m.cursor);
-    // bit 0: the guard let the batch run; bit 1: nothing stopped the chain
+}
+
+__global__ void k_batch_fin(const __grid_constant__ DevMap m) {
+    // sample voxels of the batch: the list's live length (also counts claims a
+    // refused first attempt left for the replay)
+    if (m.key_mi && m.nmarked)
+        m.stats[S_MARKED] = *((volatile unsigned long long *)m.nmarked) -
+                            *((volatile unsigned long long *)(m.nmarked + 1));
+    // bit 0: the guard let the batch run; bit 1: neither this batch nor an
+    // earlier one stopped the chain (a later batch's guard, running
+    // concurrently with this fold, may already have set it)
+    const int c = *((volatile int *)m.chain);
     m.stats[NUM_STATS + 1] = (unsigned long long)(*((volatile int *)m.go) != 0) |
-                             ((unsigned long long)(*((volatile int *)m.chain) == 0) << 1);
+                             ((unsigned long long)(c == 0 || c > m.batch_idx + 1) << 1);
 }
 
 // Counting sort of the batch's segments by step count, longest first: the

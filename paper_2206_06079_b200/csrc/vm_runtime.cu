@@ -154,6 +154,14 @@ struct vm_map {
     // host rays of the batch: uploaded in chunks on copy_stream, each chunk's
     // discover waits only for its own chunk (the copy overlaps discover)
     cudaStream_t copy_stream = nullptr;
+    // pipelined sequences: batch b+1's discover runs on disc_stream while batch
+    // b resolves and folds; batch-scoped buffers alternate by batch parity
+    cudaStream_t disc_stream = nullptr;
+    cudaEvent_t ev_seq0 = nullptr;
+    int *d_touched2 = nullptr, *d_rgrid2 = nullptr, *d_rbox2 = nullptr, *d_go2 = nullptr;
+    int2 *d_smarked2 = nullptr;
+    size_t smarked2_cap = 0;
+    unsigned long long *d_mk2 = nullptr;  // parity-1 [nmarked, lost claims]
     static constexpr int UP_CHUNKS = 4;
     cudaEvent_t ev_up[UP_CHUNKS] = {};
     struct Upload {
@@ -829,7 +837,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     const bool key_mi = occ_det && m->shard_world == 1;
     if (key_mi) {
         if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)n + 1))) return rc;
-        CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
+        CK(cudaMemsetAsync(m->d_shard_cnt, 0, 2 * sizeof(unsigned long long), m->stream));
     }
     if (ndt) {
         // records keyed by the voxel index (vm_ndt.cuh): one list entry per record at most
@@ -921,6 +929,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
         k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
         if (emit) {
+            if (key_mi) {
+                k_stamp<<<m->num_sms * 2, BLOCK, 0, m->stream>>>(dm);
+                m->launches += 1;
+            }
             k_rgrid<<<16, BLOCK, 0, m->stream>>>(dm);
             k_seg_scan<<<1, SEG_BUCKETS, 0, m->stream>>>(dm);
             k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, m->stream>>>(dm);
@@ -967,9 +979,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             CK(cudaMemcpyAsync((int *)(m->h_stats + NUM_STATS) + 1, m->d_go, sizeof(int),
                                cudaMemcpyDeviceToHost, m->stream));
             CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_shard_cnt,
-                               sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+                               2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
             CK(cudaStreamSynchronize(m->stream));
             if ((rc = check_launch("batch"))) return rc;
+            if (!key_mi) m->h_stats[NUM_STATS + 2] = 0;
         } else {
             CK(cudaEventSynchronize(m->ev_k1));
         }
@@ -982,7 +995,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
                 k_clear_marks<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
             }
-            if (vbuck) {
+            if (vbuck || key_mi) {
                 const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
                 k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, m->stream>>>(dm, words);
             }
@@ -1014,8 +1027,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             continue;
         }
         if (tsdf_det) {
-            if (m->h_stats[S_RECORDS] > m->rec_cap || m->h_stats[NUM_STATS + 1] > m->smarked_cap)
+            if (m->h_stats[S_RECORDS] > m->rec_cap || m->h_stats[NUM_STATS + 1] > m->smarked_cap) {
+                m->nreg = cursor;  // the regions the discover created stay (like the reference's prefetch)
                 return fail(VM_ERR_CUDA, "TSDF record bound exceeded");
+            }
             CK(cudaEventElapsedTime(&ms_total, m->ev_start, m->ev_end));
             CK(cudaEventElapsedTime(&ms_walk, m->ev_w0, m->ev_w1));
             CK(cudaEventElapsedTime(&ms_disc, m->ev_start, m->ev_w0));
@@ -1056,8 +1071,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                                    sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
                 CK(cudaStreamSynchronize(m->stream));
                 if ((rc = check_launch("batch"))) return rc;
-                if (m->h_stats[S_RECORDS] > m->rec_cap || m->h_stats[NUM_STATS + 1] > m->smarked_cap)
+                if (m->h_stats[S_RECORDS] > m->rec_cap || m->h_stats[NUM_STATS + 1] > m->smarked_cap) {
+                    m->nreg = cursor;
                     return fail(VM_ERR_CUDA, "NDT record re-emission overflowed");
+                }
             }
             CK(cudaEventElapsedTime(&ms_total, m->ev_start, m->ev_end));
             CK(cudaEventElapsedTime(&ms_walk, m->ev_w0, m->ev_w1));
@@ -1164,7 +1181,9 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     out->region_misses = (int64_t)hs[S_RMISS];
     out->regions_touched = (int64_t)hs[S_PREF_TOUCHED];
     out->records = (int64_t)hs[S_RECORDS];
-    out->marked_voxels = (key_mi || vbuck) ? (int64_t)hs[NUM_STATS + 1] : (int64_t)hs[S_MARKED];
+    out->marked_voxels = key_mi   ? (int64_t)(hs[NUM_STATS + 1] - hs[NUM_STATS + 2])
+                         : vbuck ? (int64_t)hs[NUM_STATS + 1]
+                                 : (int64_t)hs[S_MARKED];
     out->regions_total = cursor;
     out->new_regions = cursor - nreg0;
     out->replays = replays;
@@ -1237,6 +1256,16 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
     if ((rc = ensure_buckets(m, m->smarked_cap, ((unsigned long long)nmax * maxseg + 31) / 32 + 1)))
         return rc;
     if (!m->d_chain && (rc = dev_alloc(&m->d_chain, 1))) return rc;
+    if (!m->disc_stream) {
+        CK(cudaStreamCreateWithFlags(&m->disc_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&m->ev_seq0, cudaEventDisableTiming));
+        if ((rc = dev_alloc(&m->d_touched2, m->max_slots)) || (rc = dev_alloc(&m->d_rgrid2, RG_MAX)) ||
+            (rc = dev_alloc(&m->d_rbox2, 6)) || (rc = dev_alloc(&m->d_go2, 1)) ||
+            (rc = dev_alloc(&m->d_mk2, 2)))
+            return rc;
+    }
+    if ((rc = ensure_buf(&m->d_smarked2, &m->smarked2_cap, m->smarked_cap))) return rc;
+    cudaStream_t ds = m->disc_stream;
     if ((size_t)nb > m->mstats_cap) {
         cudaFree(m->d_mstats);
         if (m->h_mstats) cudaFreeHost(m->h_mstats);
@@ -1246,7 +1275,7 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         CK(cudaMallocHost((void **)&m->h_mstats, (size_t)nb * MSTRIDE * sizeof(unsigned long long)));
         m->mstats_cap = nb;
     }
-    while (m->mev.size() < (size_t)nb * 6) {
+    while (m->mev.size() < (size_t)nb * 8) {
         cudaEvent_t e;
         CK(cudaEventCreate(&e));
         m->mev.push_back(e);
@@ -1273,9 +1302,19 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         CK(cudaMemcpyAsync(m->d_ring[r], rays[b].records, (size_t)rays[b].count * 40,
                            cudaMemcpyHostToDevice, st));
         CK(cudaEventRecord(m->ev_ring_up[r], st));
-        CK(cudaStreamWaitEvent(s, m->ev_ring_up[r], 0));
+        CK(cudaStreamWaitEvent(ds, m->ev_ring_up[r], 0));  // the batch's discover reads it
         srcp[b] = m->d_ring[r];
         return VM_OK;
+    };
+    // batch-scoped buffers of parity 1 (parity 0 uses the map's own)
+    auto parity = [&](DevMap &dm, int b) {
+        if (!(b & 1)) return;
+        dm.touched = m->d_touched2;
+        dm.rgrid = m->d_rgrid2;
+        dm.rbox = m->d_rbox2;
+        dm.go = m->d_go2;
+        dm.marked = m->d_smarked2;
+        dm.nmarked = m->d_mk2;
     };
     while (b0 < nb) {
         const long long headroom = std::max<long long>(512, 2 * m->max_growth);
@@ -1284,9 +1323,11 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
             return rc;
         const int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
         CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
+        CK(cudaEventRecord(m->ev_seq0, s));  // the discover stream starts after the map's prior work
+        CK(cudaStreamWaitEvent(ds, m->ev_seq0, 0));
         for (int b = b0; b < nb; ++b) {
             const long long n = rays[b].count;
-            cudaEvent_t *ev = &m->mev[(size_t)6 * b];
+            cudaEvent_t *ev = &m->mev[(size_t)8 * b];
             if (n <= 0) continue;
             m->epoch += 1;
             DevMap dm = make_dm(m);
@@ -1299,24 +1340,33 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
             dm.stats = m->d_mstats + (size_t)b * MSTRIDE;
             dm.chain = m->d_chain;
             dm.batch_idx = b;
+            parity(dm, b);
             if (rays[b].on_device) srcp[b] = (const unsigned char *)rays[b].records;
             else if ((rc = upload(b, m->copy_stream))) return rc;
             const SrcOHMB1 src{srcp[b]};
             const long long l0 = m->launches;
-            k_batch_init<<<1, 32, 0, s>>>(dm, (b == b0 && keep_marks) ? 0 : 1);
-            CK(cudaEventRecord(ev[0], s));
-            if ((rc = launch_discover(m, dm, src, n, mode, 1, 1, 1, s))) return rc;
-            k_guard<<<1, 1, 0, s>>>(dm, margin);
-            k_rgrid<<<16, BLOCK, 0, s>>>(dm);
-            k_seg_scan<<<1, SEG_BUCKETS, 0, s>>>(dm);
-            k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, s>>>(dm);
+            // discover stream: batch b's preprocessing, concurrent with batch
+            // b-1's resolve and fold (it waited for b-1's walk)
+            k_batch_init<<<1, 32, 0, ds>>>(dm, (b == b0 && keep_marks) ? 0 : 1);
+            CK(cudaEventRecord(ev[0], ds));
+            if ((rc = launch_discover(m, dm, src, n, mode, 1, 1, 1, ds))) return rc;
+            k_guard<<<1, 1, 0, ds>>>(dm, margin);
+            k_rgrid<<<16, BLOCK, 0, ds>>>(dm);
+            k_seg_scan<<<1, SEG_BUCKETS, 0, ds>>>(dm);
+            k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, ds>>>(dm);
             m->launches += 5;
             if ((rc = check_launch("discover"))) return rc;
-            CK(cudaEventRecord(ev[1], s));
+            CK(cudaEventRecord(ev[1], ds));
+            // the map's stream: stamps (after b-1's fold), walk, resolve, fold
+            CK(cudaStreamWaitEvent(s, ev[1], 0));
+            k_stamp<<<m->num_sms * 2, BLOCK, 0, s>>>(dm);
+            CK(cudaEventRecord(ev[6], s));
             if ((rc = launch_walk(m, dm, src, n, mode, true, false))) return rc;
+            k_batch_regions<<<1, 1, 0, s>>>(dm);
             CK(cudaEventRecord(ev[2], s));
+            CK(cudaStreamWaitEvent(ds, ev[2], 0));  // batch b+1's discover may start
             k_resolve<false, false><<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
-            m->launches += 1;
+            m->launches += 3;
             CK(cudaEventRecord(ev[3], s));
             if ((rc = launch_bucket_fold(m, dm, src, n, maxseg, ev[4]))) return rc;
             k_batch_fin<<<1, 1, 0, s>>>(dm);
@@ -1361,10 +1411,8 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         const int cursor = (int)slot[NUM_STATS];
         DevMap dm = dms[f];
         if (slot[S_RANGE_ERR]) {
-            if (slot[S_MARKED]) {
-                const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
-                k_clear_marks<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, words);
-            }
+            const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
+            k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, words);  // the claims (never stamped)
             CK(cudaStreamSynchronize(s));
             m->nreg = cursor;
             return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range "
@@ -1403,7 +1451,7 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         dm.rec_cap = m->rec_cap;
         static const int one = 1;
         CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
-        CK(cudaMemcpyAsync(m->d_go, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dm.go, &one, sizeof(int), cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(dm.stats + S_RECORDS, 0, sizeof(unsigned long long), s));
         if (!rays[f].on_device) {
             CK(cudaMemcpyAsync(m->d_ring[f % vm_map::RING], rays[f].records,
@@ -1413,11 +1461,22 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         const SrcOHMB1 src{srcp[f]};
         const long long n = rays[f].count;
         if ((rc = launch_walk(m, dm, src, n, mode, true, true))) return rc;
-        cudaEvent_t *ev = &m->mev[(size_t)6 * f];
+        cudaEvent_t *ev = &m->mev[(size_t)8 * f];
         CK(cudaEventRecord(ev[3], s));
         if ((rc = launch_bucket_fold(m, dm, src, n, maxseg, ev[4]))) return rc;
         k_batch_fin<<<1, 1, 0, s>>>(dm);
         CK(cudaEventRecord(ev[5], s));
+        // batch f+1's discover may have run concurrently with f's (aborted)
+        // fold: drop its index claims; f+1 restarts from a clean list
+        {
+            int cur = 0;
+            CK(cudaMemcpyAsync(&cur, m->d_cursor, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            const long long words = std::min<long long>(cur, m->cap) * (long long)m->vpr;
+            k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, words);
+            CK(cudaMemsetAsync(m->d_shard_cnt, 0, 2 * sizeof(unsigned long long), s));
+            CK(cudaMemsetAsync(m->d_mk2, 0, 2 * sizeof(unsigned long long), s));
+        }
         CK(cudaMemcpyAsync(m->h_mstats + (size_t)f * MSTRIDE, dm.stats,
                            MSTRIDE * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1429,10 +1488,11 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
     }
     for (int b = 0; b < nb; ++b) {
         if (rays[b].count <= 0) continue;
-        cudaEvent_t *ev = &m->mev[(size_t)6 * b];
+        cudaEvent_t *ev = &m->mev[(size_t)8 * b];
         float t[5] = {0, 0, 0, 0, 0}, tot = 0;
         CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
         for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
+        CK(cudaEventElapsedTime(&t[1], ev[6], ev[2]));  // the walk itself (not the wait for b-1)
         out[b].gpu_ms = tot;
         out[b].discover_ms = t[0];
         out[b].walk_ms = t[1];
@@ -1497,8 +1557,7 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
     m->tsize = ts;
     for (int l = 0; l < NUM_LAYERS; ++l) {
         bool on = l == L_SCRATCH ? true
-                  : l == L_NIDX  ? ((layer_mask >> L_COV) & 1u) != 0 ||   // NDT and TSDF maps
-                                       ((layer_mask >> L_TSDF) & 1u) != 0
+                  : l == L_NIDX  ? true  // voxel index claims (every deterministic path)
                                  : ((layer_mask >> l) & 1u) != 0;
         m->bpr[l] = on ? (size_t)m->vpr * LAYER_COMP[l] * LAYER_ELEM[l] : 0;
     }
@@ -1575,6 +1634,14 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_shard_cnt);
     cudaFree(m->d_gx);
     cudaFree(m->d_ngx);
+    cudaFree(m->d_touched2);
+    cudaFree(m->d_rgrid2);
+    cudaFree(m->d_rbox2);
+    cudaFree(m->d_go2);
+    cudaFree(m->d_smarked2);
+    cudaFree(m->d_mk2);
+    if (m->disc_stream) cudaStreamDestroy(m->disc_stream);
+    if (m->ev_seq0) cudaEventDestroy(m->ev_seq0);
     cudaFree(m->d_reload);
     cudaFree(m->d_slot_last);
     cudaFree(m->d_bmask);

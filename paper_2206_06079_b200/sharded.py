@@ -192,6 +192,29 @@ def _to_device(records, dev):
 
 # ---- one process per GPU (torch.distributed) ----------------------------
 
+def _gather_batch(records, dev, group, host: bool):
+    """The whole batch on this rank's device.  Host records: every rank
+    uploads only its own slice [r*N/G, (r+1)*N/G) and the slices are
+    all-gathered device to device (NVLink with NCCL), instead of each rank
+    copying the whole batch over PCIe.  Device records are used as they are."""
+    torch = _torch()
+    import torch.distributed as dist
+    if not isinstance(records, np.ndarray):
+        return records.to(dev)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    rec = np.ascontiguousarray(records).view(np.uint8).reshape(-1, 40)
+    n = rec.shape[0]
+    per = (n + world - 1) // world
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    mine = torch.zeros((per, 40), dtype=torch.uint8)
+    mine[:hi - lo] = torch.from_numpy(rec[lo:hi])
+    mine = mine if host else mine.to(dev)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    full = torch.cat([p[:n * (q + 1) // world - n * q // world] for q, p in enumerate(parts)])
+    return full.reshape(-1).to(dev)
+
+
 def exchange_all_to_all(sends, group=None):
     """Variable-size all-to-all of 1-D/2-D tensors (same trailing shape):
     sends[d] goes to rank d; returns the tensors received from each rank.
@@ -247,7 +270,7 @@ def _submit_sharded(smap: ShardedVoxelMap, records, group=None) -> BatchStats:
     host = dist.get_backend(group) == "gloo"
     dev = smap.dev
     wire = (lambda t: t.cpu()) if host else (lambda t: t)
-    rec = _to_device(records, dev)
+    rec = _gather_batch(records, dev, group, host)
     sends, marks = smap.begin(rec)
     if smap.mode == "ndt-om":
         # requests out, Gaussian bitmaps back (in request order), then mark

@@ -1,6 +1,7 @@
 """Host side of the region-sharded mode on CPU: the variable-size
-all-to-all / all-gather used for the record exchange (gloo, world size 2)
-and the region-ownership function (vm_shard_owner, needs no device)."""
+all-to-all / all-gather used for the record exchange, the slice-upload +
+all-gather of the batch (gloo, world size 2), and the region-ownership
+function (vm_shard_owner, needs no device)."""
 import os
 import socket
 
@@ -13,7 +14,8 @@ import torch.multiprocessing as mp  # noqa: E402
 
 from paper_2206_06079_b200 import _native  # noqa: E402
 from paper_2206_06079_b200.keys import pack_region_coord  # noqa: E402
-from paper_2206_06079_b200.sharded import exchange_all_gather, exchange_all_to_all  # noqa: E402
+from paper_2206_06079_b200.sharded import (_gather_batch, exchange_all_gather,  # noqa: E402
+                                           exchange_all_to_all)
 
 
 def _free_port():
@@ -32,7 +34,12 @@ def _worker(rank, world, port, q):
         got = exchange_all_to_all(sends)
         rows = [g.tolist() for g in got]
         gathered = exchange_all_gather(torch.full((rank + 2, 2), rank, dtype=torch.int64))
-        q.put((rank, rows, gathered.tolist()))
+        # the batch: each rank contributes its slice, every rank gets it whole
+        from paper_2206_06079_b200 import scans
+        batch = scans.os64_room_scan(seed=0)[:1001]
+        full = _gather_batch(batch, "cpu", None, host=True)
+        same = bool(np.array_equal(full.numpy(), batch.view(np.uint8).reshape(-1)))
+        q.put((rank, rows, gathered.tolist(), same))
     finally:
         dist.destroy_process_group()
 
@@ -47,8 +54,9 @@ def test_variable_size_exchange_gloo():
         p.start()
     res = {}
     for _ in range(world):
-        r, rows, gathered = q.get(timeout=120)
+        r, rows, gathered, same = q.get(timeout=120)
         res[r] = (rows, gathered)
+        assert same
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
