@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(BLOCK, BK_FOLD_MINB) k_bk_fold(const __grid_co
          mi += (unsigned long long)gridDim.x * blockDim.x) {
         unsigned c;
         const unsigned s = bk_slice(b, mi, c);
+        if (c == 0u) continue;  // an index whose claim lost a race (marked (-1, -1))
         if (c > (unsigned)BK_SERIAL) {
             b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
             continue;

@@ -161,6 +161,12 @@ struct vm_map {
     int *d_touched2 = nullptr, *d_rgrid2 = nullptr, *d_rbox2 = nullptr, *d_go2 = nullptr;
     int2 *d_smarked2 = nullptr;
     size_t smarked2_cap = 0;
+    SegDesc *d_segs2 = nullptr;      // (a batch's descriptors outlive the next discover:
+    size_t segs2_cap = 0;            //  a records-overflow recovery re-walks them)
+    unsigned *d_perm2 = nullptr;
+    size_t perm2_cap = 0;
+    unsigned char *d_seg_bk2 = nullptr;
+    size_t seg_bk2_cap = 0;
     unsigned long long *d_mk2 = nullptr;  // parity-1 [nmarked, lost claims]
     static constexpr int UP_CHUNKS = 4;
     cudaEvent_t ev_up[UP_CHUNKS] = {};
@@ -1265,6 +1271,9 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
             return rc;
     }
     if ((rc = ensure_buf(&m->d_smarked2, &m->smarked2_cap, m->smarked_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_segs2, &m->segs2_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_perm2, &m->perm2_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_seg_bk2, &m->seg_bk2_cap, m->seg_cap))) return rc;
     cudaStream_t ds = m->disc_stream;
     if ((size_t)nb > m->mstats_cap) {
         cudaFree(m->d_mstats);
@@ -1315,6 +1324,10 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         dm.go = m->d_go2;
         dm.marked = m->d_smarked2;
         dm.nmarked = m->d_mk2;
+        dm.segs = m->d_segs2;
+        dm.perm = m->d_perm2;
+        dm.seg_bk = m->d_seg_bk2;
+        dm.seg_cap = std::min(m->segs2_cap, std::min(m->perm2_cap, m->seg_bk2_cap));
     };
     while (b0 < nb) {
         const long long headroom = std::max<long long>(512, 2 * m->max_growth);
@@ -1640,6 +1653,9 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_go2);
     cudaFree(m->d_smarked2);
     cudaFree(m->d_mk2);
+    cudaFree(m->d_segs2);
+    cudaFree(m->d_perm2);
+    cudaFree(m->d_seg_bk2);
     if (m->disc_stream) cudaStreamDestroy(m->disc_stream);
     if (m->ev_seq0) cudaEventDestroy(m->ev_seq0);
     cudaFree(m->d_reload);

@@ -170,8 +170,10 @@ def _batches_vs_single(batches, cfg, **kw):
     b = VoxelMap(cfg, names, **kw)
     sa = submit_batches(a, batches, "occupancy")
     sb = [submit_batch(b, x, "occupancy") for x in batches]
-    for x, y in zip(sa, sb):
-        assert [getattr(x, k) for k in STAT_FIELDS] == [getattr(y, k) for k in STAT_FIELDS]
+    for i, (x, y) in enumerate(zip(sa, sb)):
+        gx = {k: getattr(x, k) for k in STAT_FIELDS}
+        gy = {k: getattr(y, k) for k in STAT_FIELDS}
+        assert gx == gy, (i, {k: (gx[k], gy[k]) for k in STAT_FIELDS if gx[k] != gy[k]})
     _layers_equal(a, b)
     return sa, a
 
