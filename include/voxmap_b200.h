@@ -215,6 +215,11 @@ int vm_walk_voxels(double ox, double oy, double oz, double ex, double ey, double
                    double cell, int64_t cap, int64_t *coords_out, double *t0_out,
                    double *t1_out, int64_t *n_out);
 
+/* math.hypot as ndt.cholupdate3 calls it (ndt.py:37-52; CPython 3.12
+ * vector_norm): the device restatement the NDT fold runs, on n pairs
+ * ab[2n] (host buffer) into out[n] (host buffer).  A parity probe. */
+int vm_ndt_hypot(const double *ab, int64_t n, double *out);
+
 /* _kernels.hash_mix (_kernels.pyx:105-110,127-129): splitmix64 finalizer. */
 uint64_t vm_hash_mix(int64_t key);
 

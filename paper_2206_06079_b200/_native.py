@@ -26,7 +26,7 @@ EXPORTED = (
     "vm_map_set_batch_counter", "vm_map_region_last_access", "vm_map_set_spill",
     "vm_map_evict_regions", "vm_map_reload_region", "vm_map_spilled_keys",
     "vm_map_region_keys", "vm_map_ensure_regions", "vm_map_find_region", "vm_map_read_layer",
-    "vm_map_write_layer", "vm_map_layer_ptr", "vm_integrate", "vm_integrate_many", "vm_export_select", "vm_export_gather", "vm_walk_voxels", "vm_hash_mix",
+    "vm_map_write_layer", "vm_map_layer_ptr", "vm_integrate", "vm_integrate_many", "vm_export_select", "vm_export_gather", "vm_walk_voxels", "vm_ndt_hypot", "vm_hash_mix",
     "vm_kernels_integrate_occupancy", "vm_last_error", "vm_device_count", "vm_build_info",
     "vm_shard_config", "vm_shard_owner", "vm_shard_begin", "vm_shard_lists", "vm_shard_prepare",
     "vm_shard_walk", "vm_shard_ndt_bits", "vm_shard_ndt_mark",
@@ -109,6 +109,7 @@ def lib():
         "vm_export_select": ([P, P, I64, I32, D, ctypes.POINTER(I64), P, P, I64], ctypes.c_int),
         "vm_export_gather": ([P, I32, P, I64, P, P, I64, P], ctypes.c_int),
         "vm_walk_voxels": ([D] * 7 + [I64, P, P, P, ctypes.POINTER(I64)], ctypes.c_int),
+        "vm_ndt_hypot": ([P, I64, P], ctypes.c_int),
         "vm_hash_mix": ([I64], ctypes.c_uint64),
         "vm_kernels_integrate_occupancy": ([P, P, P, I64, P, P, I64, P, P, P, P, P, D, I64, D, D,
                                             D, D, I32, I32, P, P], ctypes.c_int),
@@ -406,6 +407,15 @@ def walk_voxels_native(ox, oy, oz, ex, ey, ez, cell):
     check(rc, "vm_walk_voxels")
     k = int(n.value)
     return coords[:k].copy(), t0[:k].copy(), t1[:k].copy()
+
+
+def ndt_hypot(ab) -> np.ndarray:
+    """math.hypot over the rows of ab (n x 2) with the NDT fold's device
+    restatement (ndt.py:37-52 calls it inside cholupdate3)."""
+    ab = np.ascontiguousarray(ab, dtype=np.float64).reshape(-1, 2)
+    out = np.empty(len(ab))
+    check(lib().vm_ndt_hypot(_ptr(ab), len(ab), _ptr(out)), "vm_ndt_hypot")
+    return out
 
 
 def hash_mix(key: int) -> int:

@@ -101,6 +101,8 @@ struct DevMap {
     unsigned long long *stats;
     int *go;                             // batch guard (0 = skip, replay later)
     int walk_det_launched;               // k_walk_det runs before k_walk (deterministic occupancy)
+    int ndt_segs;                        // NDT batch with segment descriptors (k_walk_ndt_det)
+    unsigned long long *nlost;           // voxel-index claims lost to a concurrent claimer (NDT / TSDF)
     int ray_order;                       // NDT walks: k_discover buckets rays by step count and
                                          // the walk takes them through perm, longest first
     // region sharding (vm_shard_*): this map owns regions with owner(key) == shard_rank

@@ -121,6 +121,17 @@ __device__ __forceinline__ int read_go(const DevMap &m) {
     return *((volatile int *)m.go);
 }
 
+constexpr int RP_BIAS = 512;  // bias of the walks' grid-relative region coordinates
+
+// The grid-relative region coordinates of the descriptor walks (k_walk_det,
+// k_walk_ndt_det) must stay inside their 10-bit fields: batches whose
+// prefetched box spans RP_BIAS - 2 regions or more on an axis (800 m at
+// 0.05 m voxels) take the generic walks (k_walk, k_walk_ndt) instead.
+__device__ __forceinline__ bool walk_det_ok(const DevMap &m) {
+    return m.rbox[3] - m.rbox[0] < RP_BIAS - 3 && m.rbox[4] - m.rbox[1] < RP_BIAS - 3 &&
+           m.rbox[5] - m.rbox[2] < RP_BIAS - 3;
+}
+
 // Global voxel coordinate of (slot, li) (keys.py:50-56).
 __device__ __forceinline__ void slot_li_to_g(const DevMap &m, int slot, int li, int g[3]) {
     int r[3];
@@ -175,6 +186,7 @@ __device__ __forceinline__ unsigned ndt_index(const DevMap &m, int slot, int li)
         return (unsigned)mi;
     }
     m.marked[mi] = make_int2(-1, -1);
+    if (m.nlost) atomicAdd(m.nlost, 1ULL);  // the batch's distinct voxels: nmarked - nlost
     return prev & ~NIDX_FLAG;
 }
 
@@ -551,6 +563,7 @@ __global__ void k_batch_init(const __grid_constant__ DevMap m, int reset_marked)
     if (t < 3) m.rbox[t] = INT_MAX;
     else if (t < 6) m.rbox[t] = INT_MIN;
     if (t < 2 && reset_marked && m.nmarked) m.nmarked[t] = 0ULL;
+    if (t == 0 && reset_marked && m.nlost) *m.nlost = 0ULL;
 }
 
 // Occupancy sample voxels: MARK_FLAG | mi into the scratch word, the brick
@@ -582,9 +595,11 @@ __global__ void k_batch_regions(const __grid_constant__ DevMap m) {
 __global__ void k_batch_fin(const __grid_constant__ DevMap m) {
     // sample voxels of the batch: the list's live length (also counts claims a
     // refused first attempt left for the replay)
-    if (m.key_mi && m.nmarked)
+    // (NDT: the claimed voxel indices)
+    if (m.nmarked)
         m.stats[S_MARKED] = *((volatile unsigned long long *)m.nmarked) -
-                            *((volatile unsigned long long *)(m.nmarked + 1));
+                            (m.key_mi ? *((volatile unsigned long long *)(m.nmarked + 1))
+                                      : (m.nlost ? *((volatile unsigned long long *)m.nlost) : 0ULL));
     // bit 0: the guard let the batch run; bit 1: neither this batch nor an
     // earlier one stopped the chain (a later batch's guard, running
     // concurrently with this fold, may already have set it)
@@ -834,6 +849,7 @@ __global__ void __launch_bounds__(BLOCK, NDT_MINB) k_walk_ndt(const __grid_const
     __shared__ int nrec;
     __shared__ unsigned long long rec_base;
     if (!read_go(m)) return;
+    if (DET && !REC_ONLY && m.walk_det_launched && walk_det_ok(m)) return;  // k_walk_ndt_det walked it
     for (int k = threadIdx.x; k < CUBE_N; k += blockDim.x) cube[k] = 0;
     for (int k = threadIdx.x; k < SLOTSET; k += blockDim.x) sset[k] = -1;
     long long first = (long long)blockIdx.x * blockDim.x;

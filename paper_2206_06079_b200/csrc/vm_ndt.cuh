@@ -83,7 +83,12 @@ __device__ __forceinline__ double py_vector_norm2(double x0, double x1, double m
     }
     const double x = csum - 1.0 + (frac1 + frac2);
     h += x / (2.0 * h);
-    return outer == 1.0 ? h / scale : outer * (h / scale);
+    // h / scale: scale = 2**-max_e, so the quotient is h * 2**max_e rounded
+    // once -- the same double as the product with the exact power of two
+    // (a multiply instead of a division on the fold's serial chain); 2**1024
+    // is not a double, that case keeps the division
+    const double hs = max_e <= 1023 ? h * ldexp(1.0, max_e) : h / scale;
+    return outer == 1.0 ? hs : outer * hs;
 }
 
 __device__ __forceinline__ double py_hypot(double a, double b) {
@@ -93,6 +98,12 @@ __device__ __forceinline__ double py_hypot(double a, double b) {
     if (x0 > mx) mx = x0;
     if (x1 > mx) mx = x1;
     return py_vector_norm2(x0, x1, mx);
+}
+
+// vm_ndt_hypot: py_hypot over pairs (parity probe against CPython's results)
+__global__ void k_py_hypot(const double *ab, double *out, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = py_hypot(ab[2 * i], ab[2 * i + 1]);
 }
 
 // ndt.cholupdate3 (ndt.py:37-52) on the lower triangle
@@ -115,9 +126,21 @@ __device__ __forceinline__ void givens_k(double &lkk, double &xk, double *li1, d
     }
 }
 
-// ndt.update_gaussian (ndt.py:55-70): fold one sample into (n, mu, S).
+// The square roots ndt.update_gaussian takes of the sample count n alone:
+// sqrt(n), sqrt(n / (n + 1)), sqrt(n + 1).  The fold computes them one
+// sample ahead, off the serial chain through S.
+struct NdtRoots {
+    double sq, f, sn;
+};
+__device__ __forceinline__ NdtRoots ndt_roots(unsigned long long n) {
+    const double dn = (double)n, dnn = (double)(n + 1);
+    return NdtRoots{sqrt(dn), sqrt(dn / dnn), sqrt(dnn)};
+}
+
+// ndt.update_gaussian (ndt.py:55-70): fold one sample into (n, mu, S);
+// rt = ndt_roots(n).
 __device__ __forceinline__ void ndt_update(unsigned long long &n, double mu[3], double S[6],
-                                           const double x[3]) {
+                                           const double x[3], const NdtRoots &rt) {
     if (n == 0) {
         n = 1;
 #pragma unroll
@@ -127,24 +150,21 @@ __device__ __forceinline__ void ndt_update(unsigned long long &n, double mu[3], 
         return;
     }
     const unsigned long long nn = n + 1;
-    const double dn = (double)n, dnn = (double)nn;
+    const double dnn = (double)nn;
     double d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) d[a] = x[a] - mu[a];
 #pragma unroll
     for (int a = 0; a < 3; ++a) mu[a] = mu[a] + d[a] / dnn;
-    const double sq = sqrt(dn);
     double L[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) L[k] = S[k] * sq;
-    const double f = sqrt(dn / dnn);
-    double xx[3] = {d[0] * f, d[1] * f, d[2] * f};
+    for (int k = 0; k < 6; ++k) L[k] = S[k] * rt.sq;
+    double xx[3] = {d[0] * rt.f, d[1] * rt.f, d[2] * rt.f};
     givens_k(L[0], xx[0], &L[1], &xx[1], &L[3], &xx[2]);
     givens_k(L[2], xx[1], &L[4], &xx[2], nullptr, nullptr);
     givens_k(L[5], xx[2], nullptr, nullptr, nullptr, nullptr);
-    const double sn = sqrt(dnn);
 #pragma unroll
-    for (int k = 0; k < 6; ++k) S[k] = L[k] / sn;
+    for (int k = 0; k < 6; ++k) S[k] = L[k] / rt.sn;
     n = nn;
 }
 
@@ -176,7 +196,11 @@ __device__ __forceinline__ bool bk_ndt_live(const DevMap &m, unsigned long long 
     if (!read_go(m)) return false;
     R = *((volatile unsigned long long *)(m.stats + S_RECORDS));
     M = *((volatile unsigned long long *)m.nmarked);
-    if (R > m.rec_cap || M > m.marked_cap) return false;
+    if (R > m.rec_cap || M > m.marked_cap) {
+        // a pipelined sequence stops here; the host re-emits this batch
+        if (m.chain) atomicCAS(m.chain, 0, m.batch_idx + 1);
+        return false;
+    }
     return true;
 }
 
@@ -508,7 +532,8 @@ __device__ __forceinline__ double4 ld_d4(const double4 *p) {  // read-only path,
     const double2 a = __ldg(q), c = __ldg(q + 1);
     return make_double4(a.x, a.y, c.x, c.y);
 }
-constexpr int NBK_PF = 4;  // phase-1 records loaded ahead
+constexpr int NBK_PF = 8;        // phase-1 records per group (the next group is in flight)
+constexpr int NBK_PF_L1 = 64;    // and the records this far ahead prefetched into L1
 
 // One lane per bucket, buckets with the most samples first, so the 32 lanes
 // of a warp hold buckets with (nearly) the same number of samples; the
@@ -516,6 +541,12 @@ constexpr int NBK_PF = 4;  // phase-1 records loaded ahead
 // lanes masked), so the lanes step through their samples together, and the
 // (sorted, read-only) records and sample end points are loaded ahead of the
 // serial chain.  Clears the index stamp and the bucket counts.
+#ifdef VM_FOLD_PROF
+// dev builds: the slowest warp task of the last fold (cycles << 24 | max
+// phase-1 records << 12 | max samples) and the sum of all tasks' cycles
+__device__ unsigned long long g_fold_prof[2];
+#endif
+
 template <bool TM>
 __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_constant__ DevMap m,
                                                                    NdtBuckets b) {
@@ -525,6 +556,9 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
     const int lane = threadIdx.x & 31;
     const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
     for (unsigned w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 32 < K; w += nwarps) {
+#ifdef VM_FOLD_PROF
+        const long long prof_t0 = clock64();
+#endif
         const unsigned t = w * 32 + lane;
         bool act = t < K;
         unsigned c = 0, ns = 0, s = 0, mi = 0;
@@ -565,11 +599,20 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
         // ---- phase 1: misses through the voxel's Gaussian, in ray order ----
         bool reset = false;
         unsigned miss_add = 0;
+        // The chain through l costs a few cycles per record, so the loads run
+        // ahead of it: the next group in registers, records NBK_PF_L1 ahead
+        // pulled into L1 (a voxel a whole scan's rays graze has thousands).
         const unsigned mp1 = __reduce_max_sync(0xffffffffu, np1);
-        for (unsigned i0 = 0; i0 < mp1; i0 += NBK_PF) {
-            unsigned wv[NBK_PF];
+        unsigned wv[NBK_PF];
 #pragma unroll
-            for (int q = 0; q < NBK_PF; ++q) wv[q] = i0 + q < np1 ? (unsigned)__ldg(v + i0 + q) : 0u;
+        for (int q = 0; q < NBK_PF; ++q) wv[q] = (unsigned)q < np1 ? (unsigned)__ldg(v + q) : 0u;
+        for (unsigned i0 = 0; i0 < mp1; i0 += NBK_PF) {
+            if (i0 + NBK_PF_L1 < np1)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(v + i0 + NBK_PF_L1));
+            unsigned nx[NBK_PF];
+#pragma unroll
+            for (int q = 0; q < NBK_PF; ++q)
+                nx[q] = i0 + NBK_PF + q < np1 ? (unsigned)__ldg(v + i0 + NBK_PF + q) : 0u;
 #pragma unroll
             for (int q = 0; q < NBK_PF; ++q) {
                 if (i0 + q < np1) {
@@ -583,6 +626,8 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
                     }
                 }
             }
+#pragma unroll
+            for (int q = 0; q < NBK_PF; ++q) wv[q] = nx[q];
         }
         if (reset) {
             n0 = 0;
@@ -619,9 +664,11 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
         const double4 *__restrict__ ps = b.pos + s + np1;
         const unsigned ms = __reduce_max_sync(0xffffffffu, ns);
         double4 cur = ns ? ld_d4(ps) : make_double4(0.0, 0.0, 0.0, 0.0);
+        NdtRoots rt = ndt_roots(n);
         for (unsigned i = 0; i < ms; ++i) {
             if (i < ns) {
                 const double4 nxt = i + 1 < ns ? ld_d4(ps + i + 1) : cur;
+                const NdtRoots rt_next = ndt_roots(n + 1);  // n grows by one per sample
                 l = clamp_add(l, m.hit32, m.cmin, m.cmax);
                 if (TM) {
                     // ndt.update_intensity (ndt.py:98-106), stored f32 per sample
@@ -633,8 +680,9 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
                     im2 = (double)(float)m2new;
                 }
                 const double e[3] = {cur.x, cur.y, cur.z};
-                ndt_update(n, mu, S, e);
+                ndt_update(n, mu, S, e, rt);
                 cur = nxt;
+                rt = rt_next;
             }
         }
         if (ns) {
@@ -663,6 +711,14 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
             occ[li] = l;
             layer_at<unsigned>(m, L_NIDX, slot)[li] = 0u;
         }
+#ifdef VM_FOLD_PROF
+        if (lane == 0) {
+            const unsigned long long dt = (unsigned long long)(clock64() - prof_t0);
+            atomicMax(&g_fold_prof[0], (dt << 24) | ((unsigned long long)min(mp1, 4095u) << 12) |
+                                           min(ms, 4095u));
+            atomicAdd(&g_fold_prof[1], dt);
+        }
+#endif
     }
 }
 

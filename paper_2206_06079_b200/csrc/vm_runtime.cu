@@ -23,6 +23,7 @@
 #include "vm_walk.cuh"
 #include "vm_compat.cuh"
 #include "vm_walk_det.cuh"
+#include "vm_walk_ndt_det.cuh"
 #include "vm_shard.cuh"
 #include "vm_bucket.cuh"
 #include "vm_ndt.cuh"
@@ -139,6 +140,8 @@ struct vm_map {
     long long rec_floor_override = 0;
     long long ndt_rec_override = 0;  // VOXMAP_B200_TEST_NDT_REC_CAP: force the NDT overflow path
     int no_ray_order = 0;  // VOXMAP_B200_NO_RAY_ORDER: NDT walk in input order (A/B runs)
+    int no_pipeline = 0;   // VOXMAP_B200_NO_PIPELINE: sequences as one vm_integrate per batch (A/B runs)
+    int ndt_generic = 0;   // VOXMAP_B200_NDT_GENERIC: NDT walks ray by ray (k_walk_ndt; A/B runs)
     int num_sms = 148;
     unsigned long long *d_stats = nullptr;
     int *d_go = nullptr;
@@ -185,6 +188,7 @@ struct vm_map {
     int2 *d_smarked = nullptr;
     size_t smarked_cap = 0;
     unsigned long long *d_shard_cnt = nullptr;  // [2 + world]: nmarked, nreq, per-dest counts
+    unsigned long long *d_nlost = nullptr;      // lost voxel-index claims of the batch (NDT / TSDF)
     ShardItemN *d_gx = nullptr;      // sharded NDT: the walk's ghost visit items
     size_t gx_cap = 0;
     unsigned long long *d_ngx = nullptr;
@@ -426,6 +430,21 @@ cudaError_t launch_wd_dim(dim3 grid, cudaStream_t s, const DevMap &dm, const Src
     return cudaSuccess;
 }
 
+template <class Src, int DIM>
+cudaError_t launch_wn_dim(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
+    const size_t smem = sizeof(WalkNdtSmem);
+    cudaError_t e = opt_in_smem<k_walk_ndt_det<Src, DIM>>(smem);
+    if (e != cudaSuccess) return e;
+    k_walk_ndt_det<Src, DIM><<<grid, BLOCK, smem, s>>>(dm, src);
+    return cudaSuccess;
+}
+
+template <class Src>
+cudaError_t launch_wn(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
+    if (dm.dim == 32 && dm.brick_shift == 3) return launch_wn_dim<Src, 32>(grid, s, dm, src);
+    return launch_wn_dim<Src, 0>(grid, s, dm, src);
+}
+
 template <bool REC_ONLY, class Src>
 cudaError_t launch_wd(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
     if (dm.dim == 32 && dm.brick_shift == 3) return launch_wd_dim<REC_ONLY, Src, 32>(grid, s, dm, src);
@@ -449,9 +468,27 @@ int launch_walk(vm_map *m, const DevMap &dm, const Src &src, long long n, int mo
     // persistent grid: 2 resident blocks per SM, never more than the work needs
     dim3 pgrid((unsigned)std::max<long long>(
         1, std::min<long long>((long long)WK_BLOCKS * m->num_sms, (n * 3 + BLOCK - 1) / BLOCK)));
-    if (mode == M_OCC || mode == M_DECAY) {
+    // NDT batches with segment descriptors (ndt_segs) take the descriptor walk
+    const bool ndt_seg = (mode == M_NDT_OM || mode == M_NDT_TM) && det && !rec_only && dm.ndt_segs;
+    if (mode == M_OCC || mode == M_DECAY || ndt_seg) {
         cudaError_t e = cudaMemsetAsync(m->d_work, 0, sizeof(unsigned long long), s);
         if (e != cudaSuccess) return fail(VM_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (ndt_seg) {
+        // the persistent descriptor walk; k_walk_ndt (input ray order) exits
+        // unless the batch's box is too large for it (walk_det_ok)
+        DevMap d2 = dm;
+        d2.walk_det_launched = 1;
+        d2.ray_order = 0;
+        const dim3 ngrid((unsigned)std::max<long long>(
+            1, std::min<long long>((long long)WN_BLOCKS * m->num_sms, (n * 3 + BLOCK - 1) / BLOCK)));
+        cudaError_t ae = launch_wn(ngrid, s, d2, src);
+        if (ae != cudaSuccess)
+            return fail(VM_ERR_CUDA, std::string("walk shared-memory opt-in: ") + cudaGetErrorString(ae));
+        if (mode == M_NDT_TM) k_walk_ndt<true, true, false><<<grid, block, 0, s>>>(d2, src, n);
+        else k_walk_ndt<false, true, false><<<grid, block, 0, s>>>(d2, src, n);
+        m->launches += 2;
+        return check_launch("walk");
     }
     const size_t smem = sizeof(WalkSmem);
     cudaError_t ae = cudaSuccess;
@@ -634,8 +671,23 @@ int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, in
     k_nbk_sort_big<<<m->num_sms, BLOCK, 0, s>>>(dm, b);
     k_nbk_gather<<<gr, BLOCK, 0, s>>>(dm, src, b);
     CK(cudaEventRecord(ev_mid, s));
+#ifdef VM_FOLD_PROF
+    {
+        unsigned long long z[2] = {0, 0};
+        cudaMemcpyToSymbolAsync(g_fold_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
+    }
+#endif
     if (tm) k_nbk_fold<true><<<gm, BLOCK, 0, s>>>(dm, b);
     else k_nbk_fold<false><<<gm, BLOCK, 0, s>>>(dm, b);
+#ifdef VM_FOLD_PROF
+    {
+        unsigned long long h[2];
+        cudaMemcpyFromSymbolAsync(h, g_fold_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        std::fprintf(stderr, "[fold] slowest task %llu cycles (phase-1 max %llu, samples max %llu); all tasks %llu cycles\n",
+                     h[0] >> 24, (h[0] >> 12) & 4095, h[0] & 4095, h[1]);
+    }
+#endif
     m->launches += 11;
     return check_launch("ndt fold");
 }
@@ -831,12 +883,14 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         return fail(VM_ERR_ARG, "batch too large for 64-bit record keys; split it");
 
     int rc;
-    const bool emit = mode == M_OCC || mode == M_DECAY;
+    // deterministic NDT on one GPU walks segment descriptors (k_walk_ndt_det)
+    const bool ndt_seg = ndt && det && m->shard_world == 1 && !m->ndt_generic;
+    const bool emit = mode == M_OCC || mode == M_DECAY || ndt_seg;
     if (emit && (rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)n * maxseg + 1))) return rc;
     if (emit && (rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
     if (emit && (rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
-    // NDT walks take their rays longest first (k_discover buckets, k_seg_scatter orders)
-    const bool ray_order = ndt && !m->no_ray_order;
+    // generic NDT walks take their rays longest first (k_discover buckets, k_seg_scatter orders)
+    const bool ray_order = ndt && !ndt_seg && !m->no_ray_order;
     if (ray_order && (rc = ensure_buf(&m->d_perm, &m->perm_cap, (size_t)n + 1))) return rc;
     if (ray_order && (rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, (size_t)n + 1))) return rc;
     // occupancy / decay records key on the index in the batch's sample-voxel list
@@ -853,6 +907,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
         if ((rc = ensure_buf(&m->d_rec_t, &m->rec_t_cap, m->rec_cap))) return rc;
         CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
+        CK(cudaMemsetAsync(m->d_nlost, 0, sizeof(unsigned long long), m->stream));
     }
     if (tsdf_det) {
         // at most one record per band visit: an upper bound, no overflow path
@@ -861,6 +916,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, need)))) return rc;
         if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
         CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
+        CK(cudaMemsetAsync(m->d_nlost, 0, sizeof(unsigned long long), m->stream));
     }
     size_t rec_need = 0;
     if (occ_det) rec_need = std::max<size_t>(m->rec_cap, rec_floor(m, n));
@@ -879,8 +935,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         DevMap dm = make_dm(m);
         dm.order_bits = order_bits;
         dm.ray_order = ray_order ? 1 : 0;
+        dm.ndt_segs = ndt_seg ? 1 : 0;
         if (key_mi || vbuck) {
             dm.key_mi = key_mi ? 1 : 0;
+            dm.nlost = vbuck && m->shard_world == 1 ? m->d_nlost : nullptr;
             dm.marked = m->d_smarked;
             dm.nmarked = m->d_shard_cnt;
             dm.marked_cap = m->smarked_cap;
@@ -986,9 +1044,12 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                                cudaMemcpyDeviceToHost, m->stream));
             CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_shard_cnt,
                                2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+            CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 3, m->d_nlost, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, m->stream));
             CK(cudaStreamSynchronize(m->stream));
             if ((rc = check_launch("batch"))) return rc;
             if (!key_mi) m->h_stats[NUM_STATS + 2] = 0;
+            if (!dm.nlost) m->h_stats[NUM_STATS + 3] = 0;
         } else {
             CK(cudaEventSynchronize(m->ev_k1));
         }
@@ -1066,6 +1127,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                 dm.ray_order = 0;
                 CK(cudaMemsetAsync(m->d_stats + S_RECORDS, 0, sizeof(unsigned long long), m->stream));
                 CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), m->stream));
+                CK(cudaMemsetAsync(m->d_nlost, 0, sizeof(unsigned long long), m->stream));
                 if ((rc = launch_discover(m, dm, src, n, mode, 1, 0, 0, m->stream))) return rc;
                 if (det && (rc = launch_walk(m, dm, src, n, mode, det, true))) return rc;
                 CK(cudaEventRecord(m->ev_res, m->stream));
@@ -1075,6 +1137,8 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                                    cudaMemcpyDeviceToHost, m->stream));
                 CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 1, m->d_shard_cnt,
                                    sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+                CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 3, m->d_nlost, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, m->stream));
                 CK(cudaStreamSynchronize(m->stream));
                 if ((rc = check_launch("batch"))) return rc;
                 if (m->h_stats[S_RECORDS] > m->rec_cap || m->h_stats[NUM_STATS + 1] > m->smarked_cap) {
@@ -1188,7 +1252,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
     out->regions_touched = (int64_t)hs[S_PREF_TOUCHED];
     out->records = (int64_t)hs[S_RECORDS];
     out->marked_voxels = key_mi   ? (int64_t)(hs[NUM_STATS + 1] - hs[NUM_STATS + 2])
-                         : vbuck ? (int64_t)hs[NUM_STATS + 1]
+                         : vbuck ? (int64_t)(hs[NUM_STATS + 1] - hs[NUM_STATS + 3])
                                  : (int64_t)hs[S_MARKED];
     out->regions_total = cursor;
     out->new_regions = cursor - nreg0;
@@ -1235,46 +1299,8 @@ void fill_stats(const unsigned long long *slot, long long n, long long regions_b
     o->touched_regions_walk = (int64_t)slot[S_WALK_TOUCHED];
 }
 
-int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_stats *out) {
-    cudaStream_t s = m->stream;
-    const int maxseg = (int)std::ceil(m->cfg.max_ray_range / m->cfg.segment_length) + 1;
-    long long nmax = 0;
-    bool any_host = false;
-    for (int b = 0; b < nb; ++b) {
-        nmax = std::max<long long>(nmax, rays[b].count);
-        if (rays[b].count > 0 && !rays[b].on_device) any_host = true;
-    }
-    for (int b = 0; b < nb; ++b) std::memset(out + b, 0, sizeof(vm_stats));
-    if (nmax <= 0) {
-        for (int b = 0; b < nb; ++b) out[b].regions_total = m->nreg;
-        return VM_OK;
-    }
-    const unsigned long long span_max = ((unsigned long long)nmax * maxseg) << 1;
-    if (span_max >= (1ULL << 32))
-        return fail(VM_ERR_ARG, "batch too large for 32-bit ray order keys; split it");
-    int rc;
-    if ((rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)nmax * maxseg + 1))) return rc;
-    if ((rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
-    if ((rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
-    if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)nmax + 1))) return rc;
-    if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, rec_floor(m, nmax)))))
-        return rc;
-    if ((rc = ensure_buckets(m, m->smarked_cap, ((unsigned long long)nmax * maxseg + 31) / 32 + 1)))
-        return rc;
-    if (!m->d_chain && (rc = dev_alloc(&m->d_chain, 1))) return rc;
-    if (!m->disc_stream) {
-        CK(cudaStreamCreateWithFlags(&m->disc_stream, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&m->ev_seq0, cudaEventDisableTiming));
-        if ((rc = dev_alloc(&m->d_touched2, m->max_slots)) || (rc = dev_alloc(&m->d_rgrid2, RG_MAX)) ||
-            (rc = dev_alloc(&m->d_rbox2, 6)) || (rc = dev_alloc(&m->d_go2, 1)) ||
-            (rc = dev_alloc(&m->d_mk2, 2)))
-            return rc;
-    }
-    if ((rc = ensure_buf(&m->d_smarked2, &m->smarked2_cap, m->smarked_cap))) return rc;
-    if ((rc = ensure_buf(&m->d_segs2, &m->segs2_cap, m->seg_cap))) return rc;
-    if ((rc = ensure_buf(&m->d_perm2, &m->perm2_cap, m->seg_cap))) return rc;
-    if ((rc = ensure_buf(&m->d_seg_bk2, &m->seg_bk2_cap, m->seg_cap))) return rc;
-    cudaStream_t ds = m->disc_stream;
+// per-batch stats slots, 8 events per batch, the host-upload ring
+int sequence_buffers(vm_map *m, int nb, long long nmax, bool any_host) {
     if ((size_t)nb > m->mstats_cap) {
         cudaFree(m->d_mstats);
         if (m->h_mstats) cudaFreeHost(m->h_mstats);
@@ -1300,6 +1326,298 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         }
         m->ring_bytes = (size_t)nmax * 40;
     }
+    return VM_OK;
+}
+
+// stage times of a finished sequence (events 0..6 of each batch)
+int sequence_times(vm_map *m, const vm_rays *rays, int nb, const std::vector<long long> &reps,
+                   const std::vector<long long> &launches, vm_stats *out) {
+    for (int b = 0; b < nb; ++b) {
+        if (rays[b].count <= 0) continue;
+        cudaEvent_t *ev = &m->mev[(size_t)8 * b];
+        float t[5] = {0, 0, 0, 0, 0}, tot = 0;
+        CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
+        for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
+        CK(cudaEventElapsedTime(&t[1], ev[6], ev[2]));  // the walk itself (not the wait for b-1)
+        out[b].gpu_ms = tot;
+        out[b].discover_ms = t[0];
+        out[b].walk_ms = t[1];
+        out[b].resolve_ms = t[2];
+        out[b].sort_ms = t[3];
+        out[b].fold_ms = t[4];
+        out[b].replays = reps[b];
+        out[b].launches = launches[b];
+    }
+    return VM_OK;
+}
+
+// Pipelined sequences of deterministic NDT-OM / NDT-TM batches: every batch is
+// integrate_impl's NDT path enqueued behind the previous one on the map's
+// stream (its counts are all read on the device), host records uploaded on
+// copy_stream into the ring.  One sync per sequence.  A guard refusal or a
+// record / voxel-index overflow stops the chain at that batch (later batches
+// are no-ops); the host recovers it exactly as integrate_impl does and
+// re-enqueues the rest.  (The discover does not overlap the previous batch's
+// fold here: both claim voxel indices in L_NIDX.)
+int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm_stats *out,
+                            int maxseg, long long nmax, bool any_host, bool ray_order) {
+    cudaStream_t s = m->stream;
+    const bool tm = mode == M_NDT_TM;
+    int rc;
+    if ((rc = sequence_buffers(m, nb, nmax, any_host))) return rc;
+    std::vector<DevMap> dms(nb);
+    std::vector<const unsigned char *> srcp(nb, nullptr);
+    std::vector<long long> reps(nb, 0), launches(nb, 0), before(nb, 0), first_before(nb, -1);
+    bool keep_claims = false;  // a replayed batch keeps its voxel-index claims (integrate_impl)
+    int b0 = 0;
+    while (b0 < nb) {
+        const long long headroom = std::max<long long>(512, 2 * m->max_growth);
+        if (m->nreg + headroom > m->cap &&
+            (rc = grow_pool(m, std::max(2 * m->cap, m->nreg + headroom))))
+            return rc;
+        const int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
+        CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
+        for (int b = b0; b < nb; ++b) {
+            const long long n = rays[b].count;
+            cudaEvent_t *ev = &m->mev[(size_t)8 * b];
+            if (n <= 0) continue;
+            m->epoch += 1;
+            DevMap dm = make_dm(m);
+            dm.batch_no = m->batch_no + (unsigned)b;
+            dm.order_bits = std::max(1, bitlen(((unsigned long long)n * maxseg) << 1));
+            dm.ray_order = ray_order ? 1 : 0;
+            dm.ndt_segs = m->ndt_generic ? 0 : 1;
+            dm.key_mi = 0;
+            dm.nlost = m->d_nlost;
+            dm.marked = m->d_smarked;
+            dm.nmarked = m->d_shard_cnt;
+            dm.marked_cap = m->smarked_cap;
+            dm.stats = m->d_mstats + (size_t)b * MSTRIDE;
+            dm.chain = m->d_chain;
+            dm.batch_idx = b;
+            if (rays[b].on_device) {
+                srcp[b] = (const unsigned char *)rays[b].records;
+            } else {
+                const int r = b % vm_map::RING;
+                CK(cudaStreamWaitEvent(m->copy_stream, m->ev_ring[r], 0));  // the slot's last batch is done
+                CK(cudaMemcpyAsync(m->d_ring[r], rays[b].records, (size_t)n * 40,
+                                   cudaMemcpyHostToDevice, m->copy_stream));
+                CK(cudaEventRecord(m->ev_ring_up[r], m->copy_stream));
+                CK(cudaStreamWaitEvent(s, m->ev_ring_up[r], 0));
+                srcp[b] = m->d_ring[r];
+            }
+            const SrcOHMB1 src{srcp[b]};
+            const long long l0 = m->launches;
+            k_batch_init<<<1, 32, 0, s>>>(dm, (b == b0 && keep_claims) ? 0 : 1);
+            CK(cudaEventRecord(ev[0], s));
+            if ((rc = launch_discover(m, dm, src, n, mode, 1, dm.ndt_segs, 1, s))) return rc;
+            k_guard<<<1, 1, 0, s>>>(dm, margin);
+            m->launches += 2;
+            if (dm.ndt_segs) {
+                k_rgrid<<<16, BLOCK, 0, s>>>(dm);
+                k_seg_scan<<<1, SEG_BUCKETS, 0, s>>>(dm);
+                k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, s>>>(dm);
+                m->launches += 3;
+            } else if (ray_order) {
+                k_seg_scan<<<1, SEG_BUCKETS, 0, s>>>(dm);
+                k_seg_scatter<<<(unsigned)((n + BLOCK - 1) / BLOCK), BLOCK, 0, s>>>(dm, n);
+                m->launches += 2;
+            }
+            if ((rc = check_launch("discover"))) return rc;
+            CK(cudaEventRecord(ev[1], s));
+            CK(cudaEventRecord(ev[6], s));
+            if ((rc = launch_walk(m, dm, src, n, mode, true, false))) return rc;
+            k_batch_regions<<<1, 1, 0, s>>>(dm);
+            CK(cudaEventRecord(ev[2], s));
+            if (tm) k_resolve<true, true><<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
+            else k_resolve<true, false><<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
+            m->launches += 2;
+            CK(cudaEventRecord(ev[3], s));
+            if ((rc = launch_ndt_fold(m, dm, src, n, maxseg, tm, ev[4]))) return rc;
+            k_batch_fin<<<1, 1, 0, s>>>(dm);
+            m->launches += 1;
+            CK(cudaEventRecord(ev[5], s));
+            if (!rays[b].on_device) CK(cudaEventRecord(m->ev_ring[b % vm_map::RING], s));
+            if ((rc = check_launch("batch"))) return rc;
+            dms[b] = dm;
+            launches[b] = m->launches - l0;
+        }
+        CK(cudaMemcpyAsync(m->h_mstats + (size_t)b0 * MSTRIDE, m->d_mstats + (size_t)b0 * MSTRIDE,
+                           (size_t)(nb - b0) * MSTRIDE * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if ((rc = check_launch("sequence"))) return rc;
+        keep_claims = false;
+        int f = nb;
+        long long regions = m->nreg;
+        for (int b = b0; b < nb; ++b) {
+            if (rays[b].count <= 0) {
+                out[b].regions_total = regions;
+                continue;
+            }
+            const unsigned long long *slot = m->h_mstats + (size_t)b * MSTRIDE;
+            if (slot[NUM_STATS + 1] != 3ULL) {
+                f = b;
+                break;
+            }
+            before[b] = first_before[b] >= 0 ? first_before[b] : regions;
+            regions = (long long)slot[NUM_STATS];
+        }
+        for (int b = b0; b < f; ++b) {
+            if (rays[b].count <= 0) continue;
+            fill_stats(m->h_mstats + (size_t)b * MSTRIDE, rays[b].count, before[b], out + b);
+            m->max_growth = std::max<long long>(m->max_growth, out[b].new_regions);
+        }
+        m->nreg = regions;
+        if (f == nb) break;
+        // ---- recover batch f (integrate_impl's NDT branches) ----
+        unsigned long long *slot = m->h_mstats + (size_t)f * MSTRIDE;
+        const int cursor = (int)slot[NUM_STATS];
+        DevMap dm = dms[f];
+        const long long words = std::min<long long>(cursor, m->cap) * (long long)m->vpr;
+        if (slot[S_RANGE_ERR]) {
+            k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, words);
+            CK(cudaStreamSynchronize(s));
+            m->nreg = cursor;
+            return fail(VM_ERR_RANGE, "ray coordinates outside the packable region range "
+                                      "(|region| < 2**20, keys.py:76-86)");
+        }
+        if (!(slot[NUM_STATS + 1] & 1ULL)) {
+            // refused: spilled regions reached (reload) or the pool is short
+            // (grow); nothing was applied, the claims stay for the replay
+            m->nreg = cursor;
+            if (slot[S_SPILLED]) {
+                if ((rc = reload_listed(m, slot[S_SPILLED]))) return rc;
+            } else {
+                m->max_growth = std::max<long long>(m->max_growth, cursor - regions);
+                if ((rc = grow_pool(m, std::max<long long>(2 * m->cap,
+                                                           cursor + 2 * margin + headroom))))
+                    return rc;
+                if (cursor + margin > m->cap)
+                    return fail(VM_ERR_OOM, "region pool exhausted (max regions reached)");
+            }
+            if (first_before[f] < 0) first_before[f] = regions;
+            reps[f] += 1;
+            b0 = f;
+            keep_claims = true;
+            continue;
+        }
+        // records or voxel indices overflowed: walk + resolve were applied,
+        // no bucket kernel ran.  Drop the claims, make room, re-emit the
+        // records only and fold them.
+        unsigned long long R = slot[S_RECORDS], M = 0;
+        CK(cudaMemcpyAsync(&M, m->d_shard_cnt, sizeof(M), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, words);
+        const size_t grow = std::max<size_t>(std::max<size_t>(R, M) + (std::max(R, M) >> 2), m->rec_cap);
+        if ((rc = ensure_records(m, grow))) return rc;
+        if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_rec_t, &m->rec_t_cap, m->rec_cap))) return rc;
+        dm.rec = m->d_rec;
+        dm.recval = m->d_val;
+        dm.rec_t = m->d_rec_t;
+        dm.rec_cap = m->rec_cap;
+        dm.marked = m->d_smarked;
+        dm.marked_cap = m->smarked_cap;
+        dm.ray_order = 0;
+        static const int one = 1;
+        CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
+        CK(cudaMemcpyAsync(dm.go, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(dm.stats + S_RECORDS, 0, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(m->d_nlost, 0, sizeof(unsigned long long), s));
+        if (!rays[f].on_device) {
+            CK(cudaMemcpyAsync(m->d_ring[f % vm_map::RING], rays[f].records,
+                               (size_t)rays[f].count * 40, cudaMemcpyHostToDevice, s));
+            srcp[f] = m->d_ring[f % vm_map::RING];
+        }
+        const SrcOHMB1 src{srcp[f]};
+        const long long n = rays[f].count;
+        cudaEvent_t *ev = &m->mev[(size_t)8 * f];
+        if ((rc = launch_discover(m, dm, src, n, mode, 1, 0, 0, s))) return rc;
+        if ((rc = launch_walk(m, dm, src, n, mode, true, true))) return rc;
+        CK(cudaEventRecord(ev[3], s));
+        if ((rc = launch_ndt_fold(m, dm, src, n, maxseg, tm, ev[4]))) return rc;
+        k_batch_fin<<<1, 1, 0, s>>>(dm);
+        CK(cudaEventRecord(ev[5], s));
+        CK(cudaMemcpyAsync(slot, dm.stats, MSTRIDE * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if ((rc = check_launch("record re-emit"))) return rc;
+        if (slot[NUM_STATS + 1] != 3ULL) {
+            m->nreg = cursor;
+            return fail(VM_ERR_CUDA, "NDT record re-emission overflowed");
+        }
+        fill_stats(slot, n, first_before[f] >= 0 ? first_before[f] : m->nreg, out + f);
+        m->max_growth = std::max<long long>(m->max_growth, out[f].new_regions);
+        m->nreg = (long long)slot[NUM_STATS];
+        b0 = f + 1;
+    }
+    return sequence_times(m, rays, nb, reps, launches, out);
+}
+
+int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_stats *out) {
+    cudaStream_t s = m->stream;
+    const int maxseg = (int)std::ceil(m->cfg.max_ray_range / m->cfg.segment_length) + 1;
+    long long nmax = 0;
+    bool any_host = false;
+    for (int b = 0; b < nb; ++b) {
+        nmax = std::max<long long>(nmax, rays[b].count);
+        if (rays[b].count > 0 && !rays[b].on_device) any_host = true;
+    }
+    for (int b = 0; b < nb; ++b) std::memset(out + b, 0, sizeof(vm_stats));
+    if (nmax <= 0) {
+        for (int b = 0; b < nb; ++b) out[b].regions_total = m->nreg;
+        return VM_OK;
+    }
+    const unsigned long long span_max = ((unsigned long long)nmax * maxseg) << 1;
+    if (span_max >= (1ULL << 32))
+        return fail(VM_ERR_ARG, "batch too large for 32-bit ray order keys; split it");
+    int rc;
+    const bool ndt = mode == M_NDT_OM || mode == M_NDT_TM;
+    const bool ray_order = ndt && m->ndt_generic && !m->no_ray_order;
+    if (ndt) {
+        // sized for the largest batch up front: nothing is reallocated while
+        // the sequence is in flight (integrate_impl's NDT bounds)
+        const size_t need = m->ndt_rec_override > 0 ? (size_t)m->ndt_rec_override
+                                                     : (size_t)nmax * 8 + 1;
+        const size_t nwork = m->ndt_generic ? (size_t)nmax + 1 : (size_t)nmax * maxseg + 1;
+        if (!m->ndt_generic && (rc = ensure_buf(&m->d_segs, &m->seg_cap, nwork))) return rc;
+        if ((rc = ensure_buf(&m->d_perm, &m->perm_cap, nwork))) return rc;
+        if ((rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, nwork))) return rc;
+        if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, need)))) return rc;
+        if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_rec_t, &m->rec_t_cap, m->rec_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_nbk_pos, &m->nbk_pos_cap, m->rec_cap))) return rc;
+        if ((rc = ensure_buckets(m, m->smarked_cap,
+                                 (2 * (unsigned long long)nmax * maxseg + 31) / 32 + 1)))
+            return rc;
+        if (!m->d_chain && (rc = dev_alloc(&m->d_chain, 1))) return rc;
+        return integrate_pipelined_ndt(m, rays, nb, mode, out, maxseg, nmax, any_host, ray_order);
+    }
+    if ((rc = ensure_buf(&m->d_segs, &m->seg_cap, (size_t)nmax * maxseg + 1))) return rc;
+    if ((rc = ensure_buf(&m->d_perm, &m->perm_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_seg_bk, &m->seg_bk_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, (size_t)nmax + 1))) return rc;
+    if ((rc = ensure_records(m, std::max<size_t>(m->rec_cap, rec_floor(m, nmax)))))
+        return rc;
+    if ((rc = ensure_buckets(m, m->smarked_cap, ((unsigned long long)nmax * maxseg + 31) / 32 + 1)))
+        return rc;
+    if (!m->d_chain && (rc = dev_alloc(&m->d_chain, 1))) return rc;
+    if (!m->disc_stream) {
+        CK(cudaStreamCreateWithFlags(&m->disc_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&m->ev_seq0, cudaEventDisableTiming));
+        if ((rc = dev_alloc(&m->d_touched2, m->max_slots)) || (rc = dev_alloc(&m->d_rgrid2, RG_MAX)) ||
+            (rc = dev_alloc(&m->d_rbox2, 6)) || (rc = dev_alloc(&m->d_go2, 1)) ||
+            (rc = dev_alloc(&m->d_mk2, 2)))
+            return rc;
+    }
+    if ((rc = ensure_buf(&m->d_smarked2, &m->smarked2_cap, m->smarked_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_segs2, &m->segs2_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_perm2, &m->perm2_cap, m->seg_cap))) return rc;
+    if ((rc = ensure_buf(&m->d_seg_bk2, &m->seg_bk2_cap, m->seg_cap))) return rc;
+    cudaStream_t ds = m->disc_stream;
+    if ((rc = sequence_buffers(m, nb, nmax, any_host))) return rc;
     std::vector<DevMap> dms(nb);
     std::vector<const unsigned char *> srcp(nb, nullptr);
     std::vector<long long> reps(nb, 0), launches(nb, 0), before(nb, 0), first_before(nb, -1);
@@ -1499,23 +1817,7 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         m->nreg = (long long)slot[NUM_STATS];
         b0 = f + 1;
     }
-    for (int b = 0; b < nb; ++b) {
-        if (rays[b].count <= 0) continue;
-        cudaEvent_t *ev = &m->mev[(size_t)8 * b];
-        float t[5] = {0, 0, 0, 0, 0}, tot = 0;
-        CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
-        for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
-        CK(cudaEventElapsedTime(&t[1], ev[6], ev[2]));  // the walk itself (not the wait for b-1)
-        out[b].gpu_ms = tot;
-        out[b].discover_ms = t[0];
-        out[b].walk_ms = t[1];
-        out[b].resolve_ms = t[2];
-        out[b].sort_ms = t[3];
-        out[b].fold_ms = t[4];
-        out[b].replays = reps[b];
-        out[b].launches = launches[b];
-    }
-    return VM_OK;
+    return sequence_times(m, rays, nb, reps, launches, out);
 }
 
 std::mutex g_walk_mu;
@@ -1595,7 +1897,7 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
         (rc = dev_alloc(&m->d_rgrid, RG_MAX)) || (rc = dev_alloc(&m->d_rbox, 6)) ||
         (rc = dev_alloc(&m->d_bmask, m->max_slots)) || (rc = dev_alloc(&m->d_gmask, m->max_slots)) ||
         (rc = dev_alloc(&m->d_seg_hist, SEG_BUCKETS)) ||
-        (rc = dev_alloc(&m->d_shard_cnt, 3)) ||
+        (rc = dev_alloc(&m->d_shard_cnt, 3)) || (rc = dev_alloc(&m->d_nlost, 1)) ||
         (rc = dev_alloc(&m->d_seg_cursor, SEG_BUCKETS)) ||
         (rc = dev_alloc(&m->d_nbig, 1)) || (rc = dev_alloc(&m->d_reload, RELOAD_CAP)) ||
         (rc = dev_alloc(&m->d_slot_last, m->max_slots)))
@@ -1617,6 +1919,8 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
     if (const char *rc_env = std::getenv("VOXMAP_B200_TEST_NDT_REC_CAP"))
         m->ndt_rec_override = std::atoll(rc_env);
     if (std::getenv("VOXMAP_B200_NO_RAY_ORDER")) m->no_ray_order = 1;
+    if (std::getenv("VOXMAP_B200_NO_PIPELINE")) m->no_pipeline = 1;
+    if (std::getenv("VOXMAP_B200_NDT_GENERIC")) m->ndt_generic = 1;
     if ((rc = grow_pool(m, std::max<long long>(64, initial_regions)))) return cleanup(rc);
     *out = m;
     return VM_OK;
@@ -1645,6 +1949,7 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_rgrid);
     cudaFree(m->d_smarked);
     cudaFree(m->d_shard_cnt);
+    cudaFree(m->d_nlost);
     cudaFree(m->d_gx);
     cudaFree(m->d_ngx);
     cudaFree(m->d_touched2);
@@ -2079,8 +2384,9 @@ int vm_integrate_many(vm_map *m, const vm_rays *rays, int32_t nbatches, int32_t 
     if (exec != VM_EXEC_CAS && exec != VM_EXEC_DETERMINISTIC) return fail(VM_ERR_ARG, "bad exec");
     if ((m->mask & MODE_MASK[mode]) != MODE_MASK[mode])
         return fail(VM_ERR_ARG, "map lacks layers required by mode");
-    bool pipelined = mode == M_OCC && exec == VM_EXEC_DETERMINISTIC && m->shard_world == 1 &&
-                     !m->sb.open;
+    bool pipelined = (mode == M_OCC || mode == M_NDT_OM || mode == M_NDT_TM) &&
+                     exec == VM_EXEC_DETERMINISTIC && m->shard_world == 1 && !m->sb.open &&
+                     !m->no_pipeline;
     for (int b = 0; b < nbatches && pipelined; ++b) {
         if (rays[b].count > 0 && (rays[b].format != VM_RAYS_OHMB1 || !rays[b].records))
             pipelined = false;
@@ -2279,6 +2585,26 @@ int vm_walk_voxels(double ox, double oy, double oz, double ex, double ey, double
         CK(cudaMemcpy(t0_out, d_t0, n * sizeof(double), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(t1_out, d_t1, n * sizeof(double), cudaMemcpyDeviceToHost));
     }
+    return VM_OK;
+}
+
+int vm_ndt_hypot(const double *ab, int64_t n, double *out) {
+    if (n < 0 || (n > 0 && (!ab || !out))) return fail(VM_ERR_ARG, "bad hypot arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(VM_ERR_NODEV, "no CUDA device available");
+    if (n == 0) return VM_OK;
+    double *d = nullptr;
+    CK(cudaMalloc(&d, (size_t)n * 3 * sizeof(double)));
+    cudaError_t e = cudaMemcpy(d, ab, (size_t)n * 2 * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        k_py_hypot<<<(unsigned)((n + BLOCK - 1) / BLOCK), BLOCK>>>(d, d + 2 * n, n);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpy(out, d + 2 * n, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(VM_ERR_CUDA, cudaGetErrorString(e));
     return VM_OK;
 }
 

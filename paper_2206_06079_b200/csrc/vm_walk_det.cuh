@@ -42,7 +42,6 @@ constexpr unsigned long long WD_CUBE_TAG = 1ULL << 40;  // key = cube cell, not 
 #define VM_WD_BLOCKS 3
 #endif
 constexpr int WD_BLOCKS = VM_WD_BLOCKS;  // resident blocks per SM
-constexpr int RP_BIAS = 512;  // bias of the grid-relative region coordinates
 
 struct WalkDetSmem {
     unsigned cube[WCUBE_N];          // miss counts around the sensor
@@ -83,9 +82,13 @@ __device__ __noinline__ int wd_slow_region(const DevMap &m, const WalkDetSmem &s
     return slot;
 }
 
+template <int DIM>
 __device__ __noinline__ unsigned wd_vid_of(const DevMap &m, const WalkDetSmem &sm, int gx, int gy,
                                            int gz, bool insert) {
-    const int rx = floordiv(gx, m.dim), ry = floordiv(gy, m.dim), rz = floordiv(gz, m.dim);
+    // DIM = 32: floor division by the region edge is an arithmetic shift
+    const int rx = DIM == 32 ? gx >> 5 : floordiv(gx, m.dim);
+    const int ry = DIM == 32 ? gy >> 5 : floordiv(gy, m.dim);
+    const int rz = DIM == 32 ? gz >> 5 : floordiv(gz, m.dim);
     int s;
     const unsigned ux = (unsigned)(rx - sm.gb[0]), uy = (unsigned)(ry - sm.gb[1]),
                    uz = (unsigned)(rz - sm.gb[2]);
@@ -104,14 +107,6 @@ __device__ __noinline__ unsigned wd_vid_of(const DevMap &m, const WalkDetSmem &s
     if (s < 0 || s >= m.cap) return 0xFFFFFFFFu;
     return (unsigned)s * (unsigned)m.vpr +
            (unsigned)((gx - rx * m.dim) + m.dim * ((gy - ry * m.dim) + m.dim * (gz - rz * m.dim)));
-}
-
-// The grid-relative region coordinates must stay inside their 10-bit fields:
-// batches whose prefetched box spans RP_BIAS - 2 regions or more on an axis
-// (800 m at 0.05 m voxels) take the generic walk (k_walk) instead.
-__device__ __forceinline__ bool walk_det_ok(const DevMap &m) {
-    return m.rbox[3] - m.rbox[0] < RP_BIAS - 3 && m.rbox[4] - m.rbox[1] < RP_BIAS - 3 &&
-           m.rbox[5] - m.rbox[2] < RP_BIAS - 3;
 }
 
 // brick bit of local index li; DIM = 32 (the default region) folds the shifts
@@ -163,15 +158,26 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
     }
     __syncthreads();
     unsigned *const scr = reinterpret_cast<unsigned *>(m.slab[L_SCRATCH]);
-    for (int k = threadIdx.x; k < WCUBE_N / 32; k += blockDim.x) sm.cmark[k] = 0u;
-    __syncthreads();
-    for (int k = threadIdx.x; k < WCUBE_N; k += blockDim.x) {
-        const unsigned vid = wd_vid_of(m, sm, sm.anchor[0] + k % WCUBE,
-                                       sm.anchor[1] + (k / WCUBE) % WCUBE,
-                                       sm.anchor[2] + k / (WCUBE * WCUBE), false);
-        sm.cube[k] = 0u;
-        if (vid != 0xFFFFFFFFu && (__ldcg(scr + vid) & MARK_FLAG))
-            atomicOr(sm.cmark + (k >> 5), 1u << (k & 31));
+    {
+        // the cube's sample-voxel bitmap: every voxel id first, then all the
+        // scratch loads in flight together, one ballot per 32 cells
+        static_assert(WCUBE_N % BLOCK == 0, "cube cells per thread");
+        constexpr int PER = WCUBE_N / BLOCK;
+        unsigned vid[PER], c[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int k = threadIdx.x + j * BLOCK;
+            vid[j] = wd_vid_of<DIM>(m, sm, sm.anchor[0] + k % WCUBE, sm.anchor[1] + (k / WCUBE) % WCUBE,
+                                    sm.anchor[2] + k / (WCUBE * WCUBE), false);
+            sm.cube[k] = 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) c[j] = vid[j] != 0xFFFFFFFFu ? __ldcg(scr + vid[j]) : 0u;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const unsigned word = __ballot_sync(0xffffffffu, (c[j] & MARK_FLAG) != 0u);
+            if ((threadIdx.x & 31) == 0) sm.cmark[(threadIdx.x + j * BLOCK) >> 5] = word;
+        }
     }
     __syncthreads();
 
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
             const int s = wd_slow_region(m, sm, rp, &b);
             set_region(s, b);
         } else if (parked == 2) {
-            const unsigned vid = wd_vid_of(m, sm, sm.endc[threadIdx.x][0], sm.endc[threadIdx.x][1],
+            const unsigned vid = wd_vid_of<DIM>(m, sm, sm.endc[threadIdx.x][0], sm.endc[threadIdx.x][1],
                                            sm.endc[threadIdx.x][2], true);
             vbase = vid == 0xFFFFFFFFu ? vid : vid - vid % vpr;
             li = vid == 0xFFFFFFFFu ? 0 : (int)(vid % vpr);
@@ -412,16 +418,28 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
 #pragma unroll
             for (int q = 0; q < WD_STEPS; ++q) {
                 w[q] = 0u;
-                v[q] = sm.vids[q][threadIdx.x];
+                v[q] = 0u;
+                if ((live >> q) & 1u) v[q] = sm.vids[q][threadIdx.x];
                 if ((need >> q) & 1u) w[q] = __ldcg(scr + v[q]);
             }
+            // candidates that are not records: the delayed miss count
+            unsigned recm = 0u;
 #pragma unroll
             for (int q = 0; q < WD_STEPS; ++q) {
                 const bool cand = (live >> q) & 1u;
                 const bool rec = cand && (((sure >> q) & 1u) || (w[q] & MARK_FLAG));
                 if (cand && !rec && !REC_ONLY) red_add(scr + v[q], 1u);
-                const unsigned long long kf = m.key_mi ? (w[q] & ~MARK_FLAG) : v[q];
-                push_records(rec, (kf << ob) | (okey & ~1u) | ((hits >> q) & 1u));
+                recm |= (unsigned)rec << q;
+            }
+            // records (a few per window at most): only the steps some lane holds one
+            const unsigned wrec = __reduce_or_sync(0xffffffffu, recm);
+            if (wrec) {
+#pragma unroll
+                for (int q = 0; q < WD_STEPS; ++q) {
+                    if (!((wrec >> q) & 1u)) continue;  // warp-uniform
+                    const unsigned long long kf = m.key_mi ? (w[q] & ~MARK_FLAG) : v[q];
+                    push_records((recm >> q) & 1u, (kf << ob) | (okey & ~1u) | ((hits >> q) & 1u));
+                }
             }
             live = 0u;
             hits = 0u;
@@ -500,7 +518,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
             const unsigned c = sm.cube[k];
             if (!c) continue;
             ++flushed;
-            const unsigned vid = wd_vid_of(m, sm, sm.anchor[0] + k % WCUBE,
+            const unsigned vid = wd_vid_of<DIM>(m, sm, sm.anchor[0] + k % WCUBE,
                                            sm.anchor[1] + (k / WCUBE) % WCUBE,
                                            sm.anchor[2] + k / (WCUBE * WCUBE), true);
             if (vid != 0xFFFFFFFFu) red_add(scr + vid, c);

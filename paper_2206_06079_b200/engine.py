@@ -157,7 +157,7 @@ def submit_batches(vmap: VoxelMap, batches, mode: str, opts: ExecutorOptions | N
     """Integrate a sequence of batches in order: the same map state and the
     same per-batch stats as calling `submit_batch` once per batch (the
     reference CLI's offline replay loop, cli.py:122-127).  Deterministic
-    occupancy over OHMB1 record arrays runs as one pipelined device sequence
+    occupancy and NDT over OHMB1 record arrays run as one pipelined device sequence
     (vm_integrate_many: host uploads overlap earlier batches' compute, one
     sync at the end); `wall_time` of each batch is its share of the call."""
     if opts is None:

@@ -134,3 +134,76 @@ def test_ndt_record_overflow_replay(monkeypatch):
     s2 = submit_batch(small, more[0], "ndt-om")
     assert s1.voxel_visits == s2.voxel_visits and s1.records == s2.records
     assert os.environ.get("VOXMAP_B200_TEST_NDT_REC_CAP") == "4096"
+
+
+NDT_STAT_FIELDS = ("rays_in", "rays_processed", "segments", "voxel_visits", "region_misses",
+                   "regions_touched", "records", "marked_voxels", "new_regions")
+
+
+def _sequence_vs_single(batches, mode, cfg, **kw):
+    """submit_batches (one pipelined device sequence, vm_integrate_many) against
+    one submit_batch per batch: the same stats and the same bits."""
+    from paper_2206_06079_b200 import submit_batches
+    a = VoxelMap(cfg, MODE_LAYERS[mode], **kw)
+    b = VoxelMap(cfg, MODE_LAYERS[mode], **kw)
+    sa = submit_batches(a, batches, mode)
+    sb = [submit_batch(b, x, mode) for x in batches]
+    for i, (x, y) in enumerate(zip(sa, sb)):
+        gx = {k: getattr(x, k) for k in NDT_STAT_FIELDS}
+        gy = {k: getattr(y, k) for k in NDT_STAT_FIELDS}
+        assert gx == gy, (i, {k: (gx[k], gy[k]) for k in NDT_STAT_FIELDS if gx[k] != gy[k]})
+    assert set(a.regions) == set(b.regions)
+    for rk, region in a.regions.items():
+        for name in MODE_LAYERS[mode]:
+            assert np.array_equal(region.buffers[name].view(np.uint8),
+                                  b.regions[rk].buffers[name].view(np.uint8)), (rk, name)
+    return sa, a
+
+
+@pytest.mark.parametrize("mode", ["ndt-om", "ndt-tm"])
+def test_ndt_pipelined_sequence_matches_per_batch(mode):
+    """NDT sequences run as one pipelined device sequence; a tiny initial
+    region pool forces mid-sequence refusals (grow + replay from that batch,
+    its voxel-index claims kept) and an empty batch sits in the middle.
+    (0.04 m voxels: 1.28 m regions, about a thousand per scan.)"""
+    data = scans.os64_tunnel_scans(5)
+    seq = [data[0], data[1][:0], data[1], data[2], data[3], data[4]]
+    sa, _ = _sequence_vs_single(seq, mode, MapConfig(voxel_size=0.04), initial_regions=64)
+    assert any(s.replays for s in sa)
+    assert sum(s.records for s in sa) > 0
+
+
+@pytest.mark.slow
+def test_ndt_pipelined_sequence_record_overflow(monkeypatch):
+    """Records / voxel indices overflowing mid-sequence stop the chain at that
+    batch; it is re-emitted into grown buffers and folded, the rest
+    re-enqueued -- the bits of an unconstrained per-batch run."""
+    from paper_2206_06079_b200 import submit_batches
+    data = scans.os64_tunnel_scans(4)
+    ref = VoxelMap(MapConfig(), MODE_LAYERS["ndt-om"])
+    want = [submit_batch(ref, x, "ndt-om") for x in data]
+    monkeypatch.setenv("VOXMAP_B200_TEST_NDT_REC_CAP", "4096")
+    vm = VoxelMap(MapConfig(), MODE_LAYERS["ndt-om"])
+    got = submit_batches(vm, data, "ndt-om")
+    assert max(s.records for s in got) > 4096
+    for x, y in zip(got, want):
+        assert (x.voxel_visits, x.records, x.marked_voxels) == (y.voxel_visits, y.records, y.marked_voxels)
+    assert set(vm.regions) == set(ref.regions)
+    for rk, region in ref.regions.items():
+        for name in MODE_LAYERS["ndt-om"]:
+            assert np.array_equal(region.buffers[name].view(np.uint8),
+                                  vm.regions[rk].buffers[name].view(np.uint8)), (rk, name)
+
+
+@pytest.mark.slow
+def test_ndt_pipelined_c3_against_oracle():
+    """Eight C3 scans through submit_batches against the C oracle, bit for bit."""
+    from paper_2206_06079_b200 import submit_batches
+    data = scans.os64_tunnel_scans(8)
+    vm = VoxelMap(MapConfig(), MODE_LAYERS["ndt-om"])
+    stats = submit_batches(vm, data, "ndt-om")
+    om, ostats = _oracle(data, MapConfig(), "ndt-om")
+    for s, o in zip(stats, ostats):
+        assert (s.voxel_visits, s.segments, s.rays_processed) == \
+            (o["voxel_visits"], o["segments"], o["rays_processed"])
+    _assert_layers_equal(vm, om, MODE_LAYERS["ndt-om"])

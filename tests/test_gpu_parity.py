@@ -45,6 +45,20 @@ def test_walk_random_vs_oracle():
         assert np.array_equal(t1.view(np.uint64), ot1.view(np.uint64))
 
 
+def test_ndt_hypot_matches_cpython_on_gpu():
+    """The NDT fold's math.hypot (CPython 3.12 vector_norm, incl. the
+    power-of-two rescale done as a multiply) against CPython's own results on
+    8000 pairs spanning subnormal to near-overflow exponents."""
+    z = np.load(GOLDEN / "arith.npz")
+    got = _native.ndt_hypot(z["hy"])
+    assert np.array_equal(got.view(np.uint64), z["hyp"].view(np.uint64))
+    edge = np.array([[0.0, 0.0], [-0.0, 5e-324], [1.7e308, 1.7e308], [np.inf, 1.0],
+                     [3.0, 4.0], [2.0 ** 1023, 2.0 ** 1023], [2.2250738585072014e-308, 1e-310]])
+    import math
+    want = np.array([math.hypot(a, b) for a, b in edge])
+    assert np.array_equal(_native.ndt_hypot(edge).view(np.uint64), want.view(np.uint64))
+
+
 def test_hash_mix_matches_reference():
     for k in (0, 1, 12345, 2 ** 40 + 17, -1 % (2 ** 63)):
         assert _native.hash_mix(k) == orc.hash_mix(k)

@@ -155,3 +155,28 @@ def test_last_access_follows_prefetch():
     rk = tuple(int(c) for c in np.floor(o / cfg.region_size))
     assert vm.regions[rk].last_access == 3
     assert pack_region_coord(rk) >= 0
+
+
+def test_pipelined_ndt_sequence_reloads_spilled_regions(tmp_path):
+    """An NDT-OM sequence reaching regions spilled to disk: the guard refuses
+    the batch, the runtime reloads them and replays -- the never-evicted bits."""
+    from paper_2206_06079_b200 import submit_batches
+    cfg = MapConfig()
+    data = scans.os64_tunnel_scans(6)
+    names = MODE_LAYERS["ndt-om"]
+    a = VoxelMap(cfg, names)
+    b = VoxelMap(cfg, names, spill_dir=tmp_path / "spill")
+    submit_batches(a, data[:2], "ndt-om")
+    submit_batches(b, data[:2], "ndt-om")
+    b.batch_counter += 5
+    assert b.evict_stale_regions(age=1) > 0
+    sa = submit_batches(a, data[2:], "ndt-om")
+    sb = submit_batches(b, data[2:], "ndt-om")
+    assert [s.voxel_visits for s in sa] == [s.voxel_visits for s in sb]
+    assert any(s.replays for s in sb)
+    b._reload_all_spilled()
+    assert set(a.regions) == set(b.regions)
+    for rk, region in a.regions.items():
+        for name in names:
+            assert np.array_equal(region.buffers[name].view(np.uint8),
+                                  b.regions[rk].buffers[name].view(np.uint8)), (rk, name)
