@@ -42,13 +42,19 @@ constexpr unsigned long long WD_CUBE_TAG = 1ULL << 40;  // key = cube cell, not 
 #define VM_WD_BLOCKS 3
 #endif
 constexpr int WD_BLOCKS = VM_WD_BLOCKS;  // resident blocks per SM
+#ifndef VM_WD_DEFER
+#define VM_WD_DEFER 0
+#endif
+// 1: a window's candidate counter loads are consumed one window later (the
+// L2 round trip overlaps the next eight steps instead of stalling the warp)
+constexpr int WD_DEFER = VM_WD_DEFER;
 
 struct WalkDetSmem {
     unsigned cube[WCUBE_N];          // miss counts around the sensor
     unsigned cmark[WCUBE_N / 32];    // sample-voxel bitmap of the cube
     int2 grid[RG_SMEM_DET];          // (slot, brick summary of sample voxels)
     unsigned long long wbuf[BLOCK / 32][WK_WBUF];
-    unsigned vids[WD_STEPS][BLOCK];  // voxel id of each in-flight visit
+    unsigned vids[1 + WD_DEFER][WD_STEPS][BLOCK];  // voxel id of each in-flight visit
     SegDesc pf[BLOCK];
     int endc[BLOCK][3];
     int gb[3], gn[3], gs[3];  // grid origin, extents, strides (1, nx, nx*ny)
@@ -69,7 +75,7 @@ __device__ __noinline__ int wd_slow_region(const DevMap &m, const WalkDetSmem &s
         const int gi = ux + sm.gs[1] * uy + sm.gs[2] * uz;
         const int s = sm.gmode == 1 ? sm.grid[gi].x : __ldg(m.rgrid + gi);
         if (s >= 0 && s < m.cap) {
-            *bm = sm.gmode == 1 ? (unsigned)sm.grid[gi].y : __ldcg(m.bmask + s);
+            *bm = sm.gmode == 1 ? (unsigned)sm.grid[gi].y : __ldg(m.bmask + s);
             return s;
         }
     }
@@ -208,6 +214,13 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
     // candidates of the window: bit q of `live` -- slot q holds a candidate
     // (voxel id in sm.vids); `sure` -- known record (cube sample voxel / forced)
     unsigned live = 0, hits = 0, sure = 0;
+    // WD_DEFER: the previous window's candidates (vids[par ^ 1]), their
+    // counter words in flight, and its segment's order key
+    unsigned par = 0;
+    unsigned plive = 0, phits = 0, psure = 0, pokey = 0;
+    unsigned pw[WD_STEPS];
+#pragma unroll
+    for (int q = 0; q < WD_STEPS; ++q) pw[q] = 0u;
     // WD_AGG (off): the step's miss count applied after the step by the warp
     // as a whole -- lanes counting the same voxel at the same step merge into
     // one atomic (~46% of C2's per-step counts outside the sensor cube share
@@ -278,7 +291,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
                     b = (unsigned)ge.y;
                 } else {
                     s = __ldg(m.rgrid + gi);
-                    if (s >= 0 && s < m.cap) b = __ldcg(m.bmask + s);
+                    if (s >= 0 && s < m.cap) b = __ldg(m.bmask + s);
                 }
             }
             if (s < 0) s = wd_slow_region(m, sm, rp, &b);
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
             if (in_cube) {
                 const unsigned ck = cube_cell(cp);
                 if (((sm.cmark[ck >> 5] >> (ck & 31)) & 1u) || forced) {
-                    sm.vids[Q][threadIdx.x] = vid;
+                    sm.vids[par][Q][threadIdx.x] = vid;
                     live |= 1u << Q;
                     sure |= 1u << Q;
                 } else if (!REC_ONLY) {
@@ -333,7 +346,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
                     else atomicAdd(sm.cube + ck, 1u);
                 }
             } else if (((bm >> wd_brick<DIM>(li, m.bsh)) & 1u) || forced) {
-                sm.vids[Q][threadIdx.x] = vid;
+                sm.vids[par][Q][threadIdx.x] = vid;
                 live |= 1u << Q;
                 if (forced) sure |= 1u << Q;
             } else if (!REC_ONLY) {
@@ -376,7 +389,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
                     b = (unsigned)ge.y;
                 } else {
                     s = __ldg(m.rgrid + gi);
-                    if (s >= 0 && s < m.cap) b = __ldcg(m.bmask + s);
+                    if (s >= 0 && s < m.cap) b = __ldg(m.bmask + s);
                 }
             }
             if (s >= 0) {
@@ -408,38 +421,57 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         active = true;
     };
 
+    // candidates of one window (bit q of lv: slot q of vids[pp] holds one;
+    // w: their counter words): records or the delayed miss count
+    auto retire = [&](unsigned lv, unsigned sr, unsigned ht, unsigned ok, const unsigned(&w)[WD_STEPS],
+                      unsigned pp) {
+        unsigned v[WD_STEPS];
+        // key_mi: the counter of a sample voxel holds MARK_FLAG | its index in
+        // the batch's sample-voxel list, which then keys the record
+#pragma unroll
+        for (int q = 0; q < WD_STEPS; ++q) v[q] = ((lv >> q) & 1u) ? sm.vids[pp][q][threadIdx.x] : 0u;
+        unsigned recm = 0u;
+#pragma unroll
+        for (int q = 0; q < WD_STEPS; ++q) {
+            const bool cand = (lv >> q) & 1u;
+            const bool rec = cand && (((sr >> q) & 1u) || (w[q] & MARK_FLAG));
+            if (cand && !rec && !REC_ONLY) red_add(scr + v[q], 1u);
+            recm |= (unsigned)rec << q;
+        }
+        // records (a few per window at most): only the steps some lane holds one
+        const unsigned wrec = __reduce_or_sync(0xffffffffu, recm);
+        if (wrec) {
+#pragma unroll
+            for (int q = 0; q < WD_STEPS; ++q) {
+                if (!((wrec >> q) & 1u)) continue;  // warp-uniform
+                const unsigned long long kf = m.key_mi ? (w[q] & ~MARK_FLAG) : v[q];
+                push_records((recm >> q) & 1u, (kf << ob) | (ok & ~1u) | ((ht >> q) & 1u));
+            }
+        }
+    };
+
     for (;;) {
         // ---- retire the window: candidates become records or miss counts ----
-        if (__any_sync(0xffffffffu, live != 0u)) {
-            unsigned w[WD_STEPS], v[WD_STEPS];
-            // key_mi: the counter of a sample voxel holds MARK_FLAG | its index in
-            // the batch's sample-voxel list, which then keys the record
-            const unsigned need = m.key_mi ? live : (live & ~sure);
+        if (__any_sync(0xffffffffu, (live | plive) != 0u)) {
+            if (WD_DEFER) {
+                retire(plive, psure, phits, pokey, pw, par ^ 1u);
+                // issue this window's loads; they are read at the next retire
+                const unsigned need = m.key_mi ? live : (live & ~sure);
 #pragma unroll
-            for (int q = 0; q < WD_STEPS; ++q) {
-                w[q] = 0u;
-                v[q] = 0u;
-                if ((live >> q) & 1u) v[q] = sm.vids[q][threadIdx.x];
-                if ((need >> q) & 1u) w[q] = __ldcg(scr + v[q]);
-            }
-            // candidates that are not records: the delayed miss count
-            unsigned recm = 0u;
+                for (int q = 0; q < WD_STEPS; ++q)
+                    pw[q] = ((need >> q) & 1u) ? __ldcg(scr + sm.vids[par][q][threadIdx.x]) : 0u;
+                plive = live;
+                psure = sure;
+                phits = hits;
+                pokey = okey;
+                par ^= 1u;
+            } else {
+                unsigned w[WD_STEPS];
+                const unsigned need = m.key_mi ? live : (live & ~sure);
 #pragma unroll
-            for (int q = 0; q < WD_STEPS; ++q) {
-                const bool cand = (live >> q) & 1u;
-                const bool rec = cand && (((sure >> q) & 1u) || (w[q] & MARK_FLAG));
-                if (cand && !rec && !REC_ONLY) red_add(scr + v[q], 1u);
-                recm |= (unsigned)rec << q;
-            }
-            // records (a few per window at most): only the steps some lane holds one
-            const unsigned wrec = __reduce_or_sync(0xffffffffu, recm);
-            if (wrec) {
-#pragma unroll
-                for (int q = 0; q < WD_STEPS; ++q) {
-                    if (!((wrec >> q) & 1u)) continue;  // warp-uniform
-                    const unsigned long long kf = m.key_mi ? (w[q] & ~MARK_FLAG) : v[q];
-                    push_records((recm >> q) & 1u, (kf << ob) | (okey & ~1u) | ((hits >> q) & 1u));
-                }
+                for (int q = 0; q < WD_STEPS; ++q)
+                    w[q] = ((need >> q) & 1u) ? __ldcg(scr + sm.vids[0][q][threadIdx.x]) : 0u;
+                retire(live, sure, hits, okey, w, 0u);
             }
             live = 0u;
             hits = 0u;
@@ -499,6 +531,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
             }
         }
     }
+    if (WD_DEFER && __any_sync(0xffffffffu, plive != 0u)) retire(plive, psure, phits, pokey, pw, par ^ 1u);
     // flush the warp's remaining records
     __syncwarp();
     {

@@ -100,7 +100,7 @@ __device__ __noinline__ int wn_slow_region(const DevMap &m, const WalkNdtSmem &s
         const int gi = ux + sm.gs[1] * uy + sm.gs[2] * uz;
         const int s = sm.gmode == 1 ? sm.grid[gi].x : __ldg(m.rgrid + gi);
         if (s >= 0 && s < m.cap) {
-            *gm = sm.gmode == 1 ? (unsigned)sm.grid[gi].y : __ldcg(m.gmask + s);
+            *gm = sm.gmode == 1 ? (unsigned)sm.grid[gi].y : __ldg(m.gmask + s);
             return s;
         }
     }
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
                     g = (unsigned)ge.y;
                 } else {
                     s = __ldg(m.rgrid + gi);
-                    if (s >= 0 && s < m.cap) g = __ldcg(m.gmask + s);
+                    if (s >= 0 && s < m.cap) g = __ldg(m.gmask + s);
                 }
             }
             if (s < 0) s = wn_slow_region(m, sm, rp, &g);
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
                     g = (unsigned)ge.y;
                 } else {
                     s = __ldg(m.rgrid + gi);
-                    if (s >= 0 && s < m.cap) g = __ldcg(m.gmask + s);
+                    if (s >= 0 && s < m.cap) g = __ldg(m.gmask + s);
                 }
             }
             if (s >= 0) {
