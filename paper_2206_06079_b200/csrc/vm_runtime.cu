@@ -160,6 +160,7 @@ struct vm_map {
     // pipelined sequences: batch b+1's discover runs on disc_stream while batch
     // b resolves and folds; batch-scoped buffers alternate by batch parity
     cudaStream_t disc_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;  // NDT: bucket kernels next to k_resolve
     cudaEvent_t ev_seq0 = nullptr;
     int *d_touched2 = nullptr, *d_rgrid2 = nullptr, *d_rbox2 = nullptr, *d_go2 = nullptr;
     int2 *d_smarked2 = nullptr;
@@ -625,11 +626,14 @@ int launch_bucket_fold(vm_map *m, const DevMap &dm, const Src &src, long long n,
 }
 
 // NDT records: bucketed by voxel index, sorted per bucket, folded in order
-// (vm_ndt.cuh).  Every count is read on the device.
+// (vm_ndt.cuh).  Every count is read on the device.  launch_ndt_prep runs the
+// phase-1 weights and the bucket kernels on `s`; they touch the records and
+// the Gaussians of voxels holding one (count >= 3), never a voxel k_resolve
+// updates (those got only order-free misses), so the pipelined paths run
+// them on a second stream next to k_resolve.  launch_ndt_fold_only folds.
 template <class Src>
-int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, int maxseg, bool tm,
-                    cudaEvent_t ev_mid) {
-    cudaStream_t s = m->stream;
+int launch_ndt_prep(vm_map *m, const DevMap &dm, const Src &src, long long n, int maxseg,
+                    cudaStream_t s, NdtBuckets *out) {
     const unsigned long long span = (unsigned long long)n * maxseg;
     const unsigned long long bwords = (2 * span + 31) / 32 + 1;
     int rc;
@@ -655,8 +659,8 @@ int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, in
         unsigned h[NBK_BINS];
         unsigned long long st[NUM_STATS], nm = 0;
         CK(cudaMemcpyAsync(h, b.hist, sizeof(h), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(st, m->d_stats, sizeof(st), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(&nm, m->d_shard_cnt, sizeof(nm), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(st, dm.stats, sizeof(st), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&nm, dm.nmarked, sizeof(nm), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         std::fprintf(stderr, "[ndt] R=%llu M=%llu buckets by size:", st[S_RECORDS], nm);
         for (int i = 0; i < NBK_BINS; ++i)
@@ -670,7 +674,15 @@ int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, in
     k_nbk_sort_mid<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, b);
     k_nbk_sort_big<<<m->num_sms, BLOCK, 0, s>>>(dm, b);
     k_nbk_gather<<<gr, BLOCK, 0, s>>>(dm, src, b);
-    CK(cudaEventRecord(ev_mid, s));
+    m->launches += 10;
+    *out = b;
+    return check_launch("ndt buckets");
+}
+
+int launch_ndt_fold_only(vm_map *m, const DevMap &dm, const NdtBuckets &b, bool tm) {
+    cudaStream_t s = m->stream;
+    const unsigned gm = (unsigned)std::max<long long>(
+        1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
 #ifdef VM_FOLD_PROF
     {
         unsigned long long z[2] = {0, 0};
@@ -688,8 +700,42 @@ int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, in
                      h[0] >> 24, (h[0] >> 12) & 4095, h[0] & 4095, h[1]);
     }
 #endif
-    m->launches += 11;
+    m->launches += 1;
     return check_launch("ndt fold");
+}
+
+// prep + fold on the map's stream (after k_resolve)
+template <class Src>
+int launch_ndt_fold(vm_map *m, const DevMap &dm, const Src &src, long long n, int maxseg, bool tm,
+                    cudaEvent_t ev_mid) {
+    NdtBuckets b;
+    int rc = launch_ndt_prep(m, dm, src, n, maxseg, m->stream, &b);
+    if (rc) return rc;
+    CK(cudaEventRecord(ev_mid, m->stream));
+    return launch_ndt_fold_only(m, dm, b, tm);
+}
+
+// The NDT batch tail with the bucket kernels next to k_resolve: the aux
+// stream waits for `walked` (recorded after the walk on the map's stream),
+// prepares the buckets; the map's stream resolves, waits for them (ev_mid,
+// recorded on the aux stream), folds.
+template <class Src>
+int launch_ndt_tail(vm_map *m, const DevMap &dm, const Src &src, long long n, int maxseg, bool tm,
+                    cudaEvent_t walked, cudaEvent_t resolved, cudaEvent_t ev_mid) {
+    if (!m->aux_stream) CK(cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking));
+    cudaStream_t s = m->stream;
+    CK(cudaStreamWaitEvent(m->aux_stream, walked, 0));
+    NdtBuckets b;
+    int rc = launch_ndt_prep(m, dm, src, n, maxseg, m->aux_stream, &b);
+    if (rc) return rc;
+    CK(cudaEventRecord(ev_mid, m->aux_stream));
+    if (tm) k_resolve<true, true><<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
+    else k_resolve<true, false><<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
+    m->launches += 1;
+    if ((rc = check_launch("resolve"))) return rc;
+    CK(cudaEventRecord(resolved, s));
+    CK(cudaStreamWaitEvent(s, ev_mid, 0));
+    return launch_ndt_fold_only(m, dm, b, tm);
 }
 
 // Deterministic TSDF: the band visits bucketed by voxel (the NDT bucket
@@ -1021,17 +1067,22 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
                                sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
             CK(cudaEventRecord(m->ev_k2, m->stream));
         }
-        if (resolve) {
+        // deterministic NDT on one GPU: k_resolve runs inside launch_ndt_tail
+        const bool ndt_tail = ndt && det && m->shard_world == 1;
+        if (resolve && !ndt_tail) {
             if (ndt && mode == M_NDT_TM) k_resolve<true, true><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
             else if (ndt) k_resolve<true, false><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
             else k_resolve<false, false><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
             m->launches += 1;
             if ((rc = check_launch("resolve"))) return rc;
         }
-        CK(cudaEventRecord(m->ev_res, m->stream));
+        if (!ndt_tail) CK(cudaEventRecord(m->ev_res, m->stream));
         if (key_mi || vbuck) {
             // the whole batch is enqueued; one sync at its end
-            if (ndt) rc = launch_ndt_fold(m, dm, src, n, maxseg, mode == M_NDT_TM, m->ev_sort);
+            if (ndt_tail)
+                rc = launch_ndt_tail(m, dm, src, n, maxseg, mode == M_NDT_TM, m->ev_w1, m->ev_res,
+                                     m->ev_sort);
+            else if (ndt) rc = launch_ndt_fold(m, dm, src, n, maxseg, mode == M_NDT_TM, m->ev_sort);
             else if (tsdf_det) rc = launch_tsdf_fold(m, dm, src, n, m->ev_sort);
             else rc = launch_bucket_fold(m, dm, src, n, maxseg, m->ev_sort);
             if (rc) return rc;
@@ -1152,6 +1203,10 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
             CK(cudaEventElapsedTime(&ms_res, m->ev_w1, m->ev_res));
             CK(cudaEventElapsedTime(&ms_sort, m->ev_res, m->ev_sort));
             CK(cudaEventElapsedTime(&ms_fold, m->ev_sort, m->ev_end));
+            if (ms_sort < 0.f) {  // the buckets were ready before k_resolve ended
+                ms_fold += ms_sort;
+                ms_sort = 0.f;
+            }
             break;
         }
         if (key_mi) {
@@ -1339,6 +1394,10 @@ int sequence_times(vm_map *m, const vm_rays *rays, int nb, const std::vector<lon
         CK(cudaEventElapsedTime(&tot, ev[0], ev[5]));
         for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
         CK(cudaEventElapsedTime(&t[1], ev[6], ev[2]));  // the walk itself (not the wait for b-1)
+        if (t[3] < 0.f) {  // NDT: the buckets were ready before k_resolve ended
+            t[4] += t[3];
+            t[3] = 0.f;
+        }
         out[b].gpu_ms = tot;
         out[b].discover_ms = t[0];
         out[b].walk_ms = t[1];
@@ -1429,11 +1488,8 @@ int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm
             if ((rc = launch_walk(m, dm, src, n, mode, true, false))) return rc;
             k_batch_regions<<<1, 1, 0, s>>>(dm);
             CK(cudaEventRecord(ev[2], s));
-            if (tm) k_resolve<true, true><<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
-            else k_resolve<true, false><<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
-            m->launches += 2;
-            CK(cudaEventRecord(ev[3], s));
-            if ((rc = launch_ndt_fold(m, dm, src, n, maxseg, tm, ev[4]))) return rc;
+            m->launches += 1;
+            if ((rc = launch_ndt_tail(m, dm, src, n, maxseg, tm, ev[2], ev[3], ev[4]))) return rc;
             k_batch_fin<<<1, 1, 0, s>>>(dm);
             m->launches += 1;
             CK(cudaEventRecord(ev[5], s));
@@ -1962,6 +2018,7 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_perm2);
     cudaFree(m->d_seg_bk2);
     if (m->disc_stream) cudaStreamDestroy(m->disc_stream);
+    if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
     if (m->ev_seq0) cudaEventDestroy(m->ev_seq0);
     cudaFree(m->d_reload);
     cudaFree(m->d_slot_last);

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 python bench.py --workload c3 --steps 3 --warmup 3 --no-cpu > gpurun_out/r3f_c3.txt 2>&1
+grep -h -o '"value": [0-9.]*\|"e2e": {"value": [0-9.]*\|stages_ms_per_step[^}]*' gpurun_out/r3f_c3.txt > gpurun_out/r3f_summary.txt
+timeout 1200 python -m pytest tests/test_gpu_ndt.py tests/test_gpu_store.py tests/test_gpu_sharded.py tests/test_gpu_edges.py -q -m gpu -x > gpurun_out/r3f_t.txt 2>&1; echo rc=$? >> gpurun_out/r3f_t.txt
