@@ -432,7 +432,7 @@ def main():
     else:
         wb, _ = ndt_bytes(s0["S"], s0["V"], r["H"], s0["records"] - r["H"], r["U"])
         bytes_launch = wb / max(1, s0["batches"])
-        kernel = "k_walk_ndt"
+        kernel = "k_walk_ndt_det" if det else "k_walk_ndt"
     achieved = bytes_launch / (walk_ms * 1e-3) / 1e9 if walk_ms > 0 else 0.0
     visits_launch = s0["V"] / max(1, s0["batches"])
     line = None
@@ -483,11 +483,12 @@ def main():
                 "workload": n["desc"]["workload"], "config": n["desc"], "value": n["value"],
                 "unit": UNIT, "ms_per_step": n["ms"] / n["steps"], "steps": n["steps"],
                 "e2e": n["e2e"], "clocks": n["clocks"], "gpu_launches": n["launches"],
-                "roofline": {"bound": "hbm", "kernel": "k_walk_ndt", "unit": "GB/s",
+                "roofline": {"bound": "hbm", "kernel": "k_walk_ndt_det", "unit": "GB/s",
                              "achieved": wb / nb / (nwalk * 1e-3) / 1e9 if nwalk else 0.0,
                              "peak": peak, "peak_kind": peak_kind,
                              "frac": (wb / nb / (nwalk * 1e-3) / 1e9) / peak if nwalk else None,
                              "bytes_per_launch": wb / nb, "avg_launch_ms": nwalk,
+                             "traffic": load_traffic("c3", "det"),
                              "step_bytes": wb + fb,
                              "step_frac": (wb + fb) / (ns["gpu_ms"] * 1e-3) / 1e9 / peak},
                 "stats": {"segments": ns["S"], "visits": ns["V"], "hits": n["H"],
@@ -681,7 +682,7 @@ def run_sharded(args, world, rank, dev, dist):
             "voxel_updates_per_s": s0["V"] * args.steps / (ms * 1e-3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_walk_det" if mode == "occupancy" else "k_walk_ndt",
+                         "kernel": "k_walk_det" if mode == "occupancy" else "k_walk_ndt (sharded)",
                          "peak_kind": peak_kind, "bytes_per_launch": bytes_gpu,
                          "avg_launch_ms": walk_ms},
             "e2e": e2e, "cpu_baseline": None,

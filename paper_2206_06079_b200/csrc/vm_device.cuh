@@ -19,8 +19,9 @@ enum Layer {
     L_SCRATCH = 0,  // private: per-voxel miss counter (deterministic resolve)
     L_OCC = 1, L_MEAN = 2, L_COUNT = 3, L_COV = 4, L_HIT = 5, L_MISS = 6,
     L_INTENS = 7, L_DHITS = 8, L_DDIST = 9, L_TSDF = 10,
-    L_NIDX = 11,    // private (NDT maps): per-voxel bucket index of the batch's ordered records
-    NUM_LAYERS = 12
+    L_NIDX = 11,    // private: per-voxel bucket index of the batch's ordered records
+    L_NIDX2 = 12,   // private (NDT maps): the same for odd batches of a pipelined sequence
+    NUM_LAYERS = 13
 };
 
 enum Mode { M_OCC = 0, M_DECAY = 1, M_NDT_OM = 2, M_NDT_TM = 3, M_TSDF = 4 };
@@ -102,6 +103,7 @@ struct DevMap {
     int *go;                             // batch guard (0 = skip, replay later)
     int walk_det_launched;               // k_walk_det runs before k_walk (deterministic occupancy)
     int ndt_segs;                        // NDT batch with segment descriptors (k_walk_ndt_det)
+    int nidx;                            // the batch's index-claim layer (L_NIDX / L_NIDX2)
     unsigned long long *nlost;           // voxel-index claims lost to a concurrent claimer (NDT / TSDF)
     int ray_order;                       // NDT walks: k_discover buckets rays by step count and
                                          // the walk takes them through perm, longest first

@@ -175,7 +175,7 @@ constexpr unsigned NIDX_FLAG = 0x80000000u;  // index-layer stamp (vm_ndt.cuh)
 // marked (-1, -1)).  Returns 0xFFFFFFFF when the index list is full (the
 // batch then re-runs with room for every index, see bk_ndt_live).
 __device__ __forceinline__ unsigned ndt_index(const DevMap &m, int slot, int li) {
-    unsigned *w = layer_at<unsigned>(m, L_NIDX, slot) + li;
+    unsigned *w = layer_at<unsigned>(m, m.nidx, slot) + li;
     unsigned cur = *((volatile unsigned *)w);
     if (cur & NIDX_FLAG) return cur & ~NIDX_FLAG;
     const unsigned long long mi = atomicAdd(m.nmarked, 1ULL);
@@ -193,7 +193,7 @@ __device__ __forceinline__ unsigned ndt_index(const DevMap &m, int slot, int li)
 // ndt_index for the occupancy sample-voxel list: counts the lost races in
 // nmarked[1], so the list's live length is nmarked[0] - nmarked[1]
 __device__ __forceinline__ unsigned claim_sample_voxel(const DevMap &m, int slot, int li) {
-    unsigned *w = layer_at<unsigned>(m, L_NIDX, slot) + li;
+    unsigned *w = layer_at<unsigned>(m, m.nidx, slot) + li;
     const unsigned cur = *((volatile unsigned *)w);
     if (cur & NIDX_FLAG) return cur & ~NIDX_FLAG;
     const unsigned long long mi = atomicAdd(m.nmarked, 1ULL);
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(BLOCK) k_stamp(const __grid_constant__ DevMap 
         if (sl.x < 0 || sl.x >= m.cap) continue;
         const unsigned long long vid = (unsigned long long)sl.x * m.vpr + sl.y;
         reinterpret_cast<unsigned *>(m.slab[L_SCRATCH])[vid] = MARK_FLAG | (unsigned)mi;
-        reinterpret_cast<unsigned *>(m.slab[L_NIDX])[vid] = 0u;
+        reinterpret_cast<unsigned *>(m.slab[m.nidx])[vid] = 0u;
         const unsigned bit = bsh >= 0 ? 1u << brick_of(sl.y, m.bsh) : 0xFFFFFFFFu;
         if (!(__ldcg(m.bmask + sl.x) & bit)) atomicOr(m.bmask + sl.x, bit);
     }

@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
         }
         if (act) {
             occ[li] = l;
-            layer_at<unsigned>(m, L_NIDX, slot)[li] = 0u;
+            layer_at<unsigned>(m, m.nidx, slot)[li] = 0u;
         }
 #ifdef VM_FOLD_PROF
         if (lane == 0) {
@@ -765,14 +765,14 @@ __global__ void __launch_bounds__(BLOCK) k_tsdf_fold(const __grid_constant__ Dev
         }
         buf[2 * li] = fd;
         buf[2 * li + 1] = fw;
-        layer_at<unsigned>(m, L_NIDX, slot)[li] = 0u;
+        layer_at<unsigned>(m, m.nidx, slot)[li] = 0u;
     }
 }
 
 // Refused / failed batches leave index stamps behind: clear every stamped
 // word of the first `words` voxels (the list of indices is not trusted).
 __global__ void k_nbk_clear(const __grid_constant__ DevMap m, long long words) {
-    unsigned *w = reinterpret_cast<unsigned *>(m.slab[L_NIDX]);
+    unsigned *w = reinterpret_cast<unsigned *>(m.slab[m.nidx]);
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < words;
          k += (long long)gridDim.x * blockDim.x)
         if (w[k]) w[k] = 0u;

@@ -51,8 +51,8 @@ int fail(int code, const std::string &msg) {
 
 constexpr int RELOAD_CAP = 4096;  // spilled regions one refused attempt can list
 
-const int LAYER_ELEM[NUM_LAYERS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 8, 4, 4};
-const int LAYER_COMP[NUM_LAYERS] = {1, 1, 1, 1, 6, 1, 1, 2, 1, 1, 2, 1};
+const int LAYER_ELEM[NUM_LAYERS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 8, 4, 4, 4};
+const int LAYER_COMP[NUM_LAYERS] = {1, 1, 1, 1, 6, 1, 1, 2, 1, 1, 2, 1, 1};
 
 int bitlen(unsigned long long x) {
     int b = 0;
@@ -190,6 +190,7 @@ struct vm_map {
     size_t smarked_cap = 0;
     unsigned long long *d_shard_cnt = nullptr;  // [2 + world]: nmarked, nreq, per-dest counts
     unsigned long long *d_nlost = nullptr;      // lost voxel-index claims of the batch (NDT / TSDF)
+    unsigned long long *d_nlost2 = nullptr;     // ... of odd batches in a pipelined NDT sequence
     ShardItemN *d_gx = nullptr;      // sharded NDT: the walk's ghost visit items
     size_t gx_cap = 0;
     unsigned long long *d_ngx = nullptr;
@@ -295,6 +296,7 @@ DevMap make_dm(const vm_map *m) {
     d.rec_invalid = ~0ULL;
     d.walk_slot0 = 1 << 30;
     d.key_mi = 0;
+    d.nidx = L_NIDX;
     d.reload = m->d_reload;
     d.reload_cap = RELOAD_CAP;
     d.batch_no = m->batch_no;
@@ -1410,20 +1412,50 @@ int sequence_times(vm_map *m, const vm_rays *rays, int nb, const std::vector<lon
     return VM_OK;
 }
 
+// the discover stream and the batch-scoped buffers of parity 1
+int ensure_disc_stream(vm_map *m) {
+    int rc;
+    if (!m->disc_stream) {
+        CK(cudaStreamCreateWithFlags(&m->disc_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&m->ev_seq0, cudaEventDisableTiming));
+        if ((rc = dev_alloc(&m->d_touched2, m->max_slots)) || (rc = dev_alloc(&m->d_rgrid2, RG_MAX)) ||
+            (rc = dev_alloc(&m->d_rbox2, 6)) || (rc = dev_alloc(&m->d_go2, 1)) ||
+            (rc = dev_alloc(&m->d_mk2, 2)) || (rc = dev_alloc(&m->d_nlost2, 1)))
+            return rc;
+    }
+    return VM_OK;
+}
+
 // Pipelined sequences of deterministic NDT-OM / NDT-TM batches: every batch is
-// integrate_impl's NDT path enqueued behind the previous one on the map's
-// stream (its counts are all read on the device), host records uploaded on
-// copy_stream into the ring.  One sync per sequence.  A guard refusal or a
-// record / voxel-index overflow stops the chain at that batch (later batches
-// are no-ops); the host recovers it exactly as integrate_impl does and
-// re-enqueues the rest.  (The discover does not overlap the previous batch's
-// fold here: both claim voxel indices in L_NIDX.)
+// integrate_impl's NDT path enqueued behind the previous one (its counts are
+// all read on the device), host records uploaded on copy_stream into the
+// ring.  One sync per sequence.  Batch b+1's discover runs on disc_stream
+// while batch b folds (the fold's long serial tail leaves most SMs idle): it
+// starts once b's k_resolve and bucket kernels are done, claims its voxel
+// indices in the other index layer (L_NIDX2 for odd batches) with its own
+// index list, counters and guard flag; b+1's walk follows b's fold on the
+// map's stream.  A guard refusal or a record / voxel-index overflow stops
+// the chain at that batch (later batches are no-ops); the host recovers it
+// exactly as integrate_impl does and re-enqueues the rest.
 int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm_stats *out,
                             int maxseg, long long nmax, bool any_host, bool ray_order) {
     cudaStream_t s = m->stream;
     const bool tm = mode == M_NDT_TM;
     int rc;
     if ((rc = sequence_buffers(m, nb, nmax, any_host))) return rc;
+    if ((rc = ensure_disc_stream(m))) return rc;
+    if ((rc = ensure_buf(&m->d_smarked2, &m->smarked2_cap, m->smarked_cap))) return rc;
+    cudaStream_t ds = m->disc_stream;
+    // batch-scoped state of odd batches
+    auto parity = [&](DevMap &dm, int b) {
+        if (!(b & 1)) return;
+        dm.nidx = L_NIDX2;
+        dm.go = m->d_go2;
+        dm.marked = m->d_smarked2;
+        dm.nmarked = m->d_mk2;
+        dm.marked_cap = m->smarked2_cap;
+        dm.nlost = m->d_nlost2;
+    };
     std::vector<DevMap> dms(nb);
     std::vector<const unsigned char *> srcp(nb, nullptr);
     std::vector<long long> reps(nb, 0), launches(nb, 0), before(nb, 0), first_before(nb, -1);
@@ -1436,6 +1468,8 @@ int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm
             return rc;
         const int margin = 64 + (int)std::min<long long>(1 << 20, headroom / 4);
         CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
+        CK(cudaEventRecord(m->ev_seq0, s));  // the discover stream starts after the map's prior work
+        CK(cudaStreamWaitEvent(ds, m->ev_seq0, 0));
         for (int b = b0; b < nb; ++b) {
             const long long n = rays[b].count;
             cudaEvent_t *ev = &m->mev[(size_t)8 * b];
@@ -1454,6 +1488,7 @@ int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm
             dm.stats = m->d_mstats + (size_t)b * MSTRIDE;
             dm.chain = m->d_chain;
             dm.batch_idx = b;
+            parity(dm, b);
             if (rays[b].on_device) {
                 srcp[b] = (const unsigned char *)rays[b].records;
             } else {
@@ -1462,34 +1497,43 @@ int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm
                 CK(cudaMemcpyAsync(m->d_ring[r], rays[b].records, (size_t)n * 40,
                                    cudaMemcpyHostToDevice, m->copy_stream));
                 CK(cudaEventRecord(m->ev_ring_up[r], m->copy_stream));
-                CK(cudaStreamWaitEvent(s, m->ev_ring_up[r], 0));
+                CK(cudaStreamWaitEvent(ds, m->ev_ring_up[r], 0));
                 srcp[b] = m->d_ring[r];
             }
             const SrcOHMB1 src{srcp[b]};
             const long long l0 = m->launches;
-            k_batch_init<<<1, 32, 0, s>>>(dm, (b == b0 && keep_claims) ? 0 : 1);
-            CK(cudaEventRecord(ev[0], s));
-            if ((rc = launch_discover(m, dm, src, n, mode, 1, dm.ndt_segs, 1, s))) return rc;
-            k_guard<<<1, 1, 0, s>>>(dm, margin);
+            // discover stream (after the previous batch's resolve + buckets, queued
+            // below): the batch's preprocessing, next to the previous fold
+            k_batch_init<<<1, 32, 0, ds>>>(dm, (b == b0 && keep_claims) ? 0 : 1);
+            CK(cudaEventRecord(ev[0], ds));
+            if ((rc = launch_discover(m, dm, src, n, mode, 1, dm.ndt_segs, 1, ds))) return rc;
+            k_guard<<<1, 1, 0, ds>>>(dm, margin);
             m->launches += 2;
             if (dm.ndt_segs) {
-                k_rgrid<<<16, BLOCK, 0, s>>>(dm);
-                k_seg_scan<<<1, SEG_BUCKETS, 0, s>>>(dm);
-                k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, s>>>(dm);
+                k_rgrid<<<16, BLOCK, 0, ds>>>(dm);
+                k_seg_scan<<<1, SEG_BUCKETS, 0, ds>>>(dm);
+                k_seg_scatter<<<(unsigned)((n * maxseg + BLOCK - 1) / BLOCK), BLOCK, 0, ds>>>(dm);
                 m->launches += 3;
             } else if (ray_order) {
-                k_seg_scan<<<1, SEG_BUCKETS, 0, s>>>(dm);
-                k_seg_scatter<<<(unsigned)((n + BLOCK - 1) / BLOCK), BLOCK, 0, s>>>(dm, n);
+                k_seg_scan<<<1, SEG_BUCKETS, 0, ds>>>(dm);
+                k_seg_scatter<<<(unsigned)((n + BLOCK - 1) / BLOCK), BLOCK, 0, ds>>>(dm, n);
                 m->launches += 2;
             }
             if ((rc = check_launch("discover"))) return rc;
-            CK(cudaEventRecord(ev[1], s));
+            CK(cudaEventRecord(ev[1], ds));
+            // the map's stream: walk (after the previous fold), resolve, fold
+            CK(cudaStreamWaitEvent(s, ev[1], 0));
             CK(cudaEventRecord(ev[6], s));
             if ((rc = launch_walk(m, dm, src, n, mode, true, false))) return rc;
             k_batch_regions<<<1, 1, 0, s>>>(dm);
             CK(cudaEventRecord(ev[2], s));
             m->launches += 1;
             if ((rc = launch_ndt_tail(m, dm, src, n, maxseg, tm, ev[2], ev[3], ev[4]))) return rc;
+            // batch b+1's discover may start: b's k_resolve (ev[3]) and bucket
+            // kernels (ev[4]) are done with the region box, grid, touched list
+            // and record buffer
+            CK(cudaStreamWaitEvent(ds, ev[3], 0));
+            CK(cudaStreamWaitEvent(ds, ev[4], 0));
             k_batch_fin<<<1, 1, 0, s>>>(dm);
             m->launches += 1;
             CK(cudaEventRecord(ev[5], s));
@@ -1562,26 +1606,37 @@ int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm
         // no bucket kernel ran.  Drop the claims, make room, re-emit the
         // records only and fold them.
         unsigned long long R = slot[S_RECORDS], M = 0;
-        CK(cudaMemcpyAsync(&M, m->d_shard_cnt, sizeof(M), cudaMemcpyDeviceToHost, s));
+        int cur = 0;
+        CK(cudaMemcpyAsync(&M, dm.nmarked, sizeof(M), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&cur, m->d_cursor, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, words);
+        {
+            // batch f+1's discover may have run next to f's (aborted) fold:
+            // drop its claims in the other index layer; f+1 restarts clean
+            DevMap d2 = dm;
+            d2.nidx = dm.nidx == L_NIDX ? L_NIDX2 : L_NIDX;
+            const long long w2 = std::min<long long>(cur, m->cap) * (long long)m->vpr;
+            k_nbk_clear<<<m->num_sms * 4, BLOCK, 0, s>>>(d2, w2);
+        }
         const size_t grow = std::max<size_t>(std::max<size_t>(R, M) + (std::max(R, M) >> 2), m->rec_cap);
         if ((rc = ensure_records(m, grow))) return rc;
         if ((rc = ensure_buf(&m->d_smarked, &m->smarked_cap, m->rec_cap))) return rc;
+        if ((rc = ensure_buf(&m->d_smarked2, &m->smarked2_cap, m->rec_cap))) return rc;
         if ((rc = ensure_buf(&m->d_rec_t, &m->rec_t_cap, m->rec_cap))) return rc;
         dm.rec = m->d_rec;
         dm.recval = m->d_val;
         dm.rec_t = m->d_rec_t;
         dm.rec_cap = m->rec_cap;
-        dm.marked = m->d_smarked;
-        dm.marked_cap = m->smarked_cap;
+        dm.marked = (f & 1) ? m->d_smarked2 : m->d_smarked;
+        dm.marked_cap = (f & 1) ? m->smarked2_cap : m->smarked_cap;
         dm.ray_order = 0;
         static const int one = 1;
         CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
         CK(cudaMemcpyAsync(dm.go, &one, sizeof(int), cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(dm.stats + S_RECORDS, 0, sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(m->d_shard_cnt, 0, sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(m->d_nlost, 0, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(dm.nmarked, 0, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(dm.nlost, 0, sizeof(unsigned long long), s));
         if (!rays[f].on_device) {
             CK(cudaMemcpyAsync(m->d_ring[f % vm_map::RING], rays[f].records,
                                (size_t)rays[f].count * 40, cudaMemcpyHostToDevice, s));
@@ -1660,14 +1715,7 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
     if ((rc = ensure_buckets(m, m->smarked_cap, ((unsigned long long)nmax * maxseg + 31) / 32 + 1)))
         return rc;
     if (!m->d_chain && (rc = dev_alloc(&m->d_chain, 1))) return rc;
-    if (!m->disc_stream) {
-        CK(cudaStreamCreateWithFlags(&m->disc_stream, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&m->ev_seq0, cudaEventDisableTiming));
-        if ((rc = dev_alloc(&m->d_touched2, m->max_slots)) || (rc = dev_alloc(&m->d_rgrid2, RG_MAX)) ||
-            (rc = dev_alloc(&m->d_rbox2, 6)) || (rc = dev_alloc(&m->d_go2, 1)) ||
-            (rc = dev_alloc(&m->d_mk2, 2)))
-            return rc;
-    }
+    if ((rc = ensure_disc_stream(m))) return rc;
     if ((rc = ensure_buf(&m->d_smarked2, &m->smarked2_cap, m->smarked_cap))) return rc;
     if ((rc = ensure_buf(&m->d_segs2, &m->segs2_cap, m->seg_cap))) return rc;
     if ((rc = ensure_buf(&m->d_perm2, &m->perm2_cap, m->seg_cap))) return rc;
@@ -1929,6 +1977,7 @@ int vm_map_create(const vm_config *cfg, uint32_t layer_mask, int32_t device,
     for (int l = 0; l < NUM_LAYERS; ++l) {
         bool on = l == L_SCRATCH ? true
                   : l == L_NIDX  ? true  // voxel index claims (every deterministic path)
+                  : l == L_NIDX2 ? ((layer_mask >> L_COV) & 1u) != 0  // NDT: odd batches' claims
                                  : ((layer_mask >> l) & 1u) != 0;
         m->bpr[l] = on ? (size_t)m->vpr * LAYER_COMP[l] * LAYER_ELEM[l] : 0;
     }
@@ -2006,6 +2055,7 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_smarked);
     cudaFree(m->d_shard_cnt);
     cudaFree(m->d_nlost);
+    cudaFree(m->d_nlost2);
     cudaFree(m->d_gx);
     cudaFree(m->d_ngx);
     cudaFree(m->d_touched2);

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(BLOCK) k_shard_ndt_clear(const __grid_constant
          mi += (unsigned long long)gridDim.x * blockDim.x) {
         const int2 sl = m.marked[mi];
         if (sl.x < 0 || !is_ghost(m, sl.x)) continue;
-        layer_at<unsigned>(m, L_NIDX, sl.x)[sl.y] = 0u;
+        layer_at<unsigned>(m, m.nidx, sl.x)[sl.y] = 0u;
         m.marked[mi] = make_int2(-1, -1);  // the fold skips the bucket
     }
     unsigned *scr0 = reinterpret_cast<unsigned *>(m.slab[L_SCRATCH]);
