@@ -1446,9 +1446,13 @@ int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm
     if ((rc = ensure_disc_stream(m))) return rc;
     if ((rc = ensure_buf(&m->d_smarked2, &m->smarked2_cap, m->smarked_cap))) return rc;
     cudaStream_t ds = m->disc_stream;
-    // batch-scoped state of odd batches
+    // batch-scoped state of odd batches; parity = position among the
+    // non-empty batches (consecutive batches alternate, an empty one between or not)
+    std::vector<int> par(nb, 0);
+    for (int b = 0, k = 0; b < nb; ++b)
+        if (rays[b].count > 0) par[b] = (k++) & 1;
     auto parity = [&](DevMap &dm, int b) {
-        if (!(b & 1)) return;
+        if (!par[b]) return;
         dm.nidx = L_NIDX2;
         dm.go = m->d_go2;
         dm.marked = m->d_smarked2;
@@ -1628,8 +1632,8 @@ int integrate_pipelined_ndt(vm_map *m, const vm_rays *rays, int nb, int mode, vm
         dm.recval = m->d_val;
         dm.rec_t = m->d_rec_t;
         dm.rec_cap = m->rec_cap;
-        dm.marked = (f & 1) ? m->d_smarked2 : m->d_smarked;
-        dm.marked_cap = (f & 1) ? m->smarked2_cap : m->smarked_cap;
+        dm.marked = par[f] ? m->d_smarked2 : m->d_smarked;
+        dm.marked_cap = par[f] ? m->smarked2_cap : m->smarked_cap;
         dm.ray_order = 0;
         static const int one = 1;
         CK(cudaMemsetAsync(m->d_chain, 0, sizeof(int), s));
@@ -1737,9 +1741,14 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
         srcp[b] = m->d_ring[r];
         return VM_OK;
     };
-    // batch-scoped buffers of parity 1 (parity 0 uses the map's own)
+    // batch-scoped buffers of parity 1 (parity 0 uses the map's own); parity =
+    // position among the non-empty batches, so consecutive batches of the
+    // pipeline alternate with an empty batch in between too
+    std::vector<int> par(nb, 0);
+    for (int b = 0, k = 0; b < nb; ++b)
+        if (rays[b].count > 0) par[b] = (k++) & 1;
     auto parity = [&](DevMap &dm, int b) {
-        if (!(b & 1)) return;
+        if (!par[b]) return;
         dm.touched = m->d_touched2;
         dm.rgrid = m->d_rgrid2;
         dm.rbox = m->d_rbox2;
