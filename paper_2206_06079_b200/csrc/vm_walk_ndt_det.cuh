@@ -40,11 +40,23 @@ constexpr int WN_STEPS = VM_WN_STEPS;  // steps per window (in-flight candidates
 constexpr int WN_BLOCKS = VM_WN_BLOCKS;  // resident blocks per SM
 constexpr int WN_WBUF = 64;              // per-warp record ring (flushed 32 at a time)
 
-static_assert(WCUBE_N % BLOCK == 0, "cube cells per thread");
+// the sensor cube of this walk (log2 edge; 4 = k_walk_det's 16^3)
+#ifndef VM_WN_CB
+#define VM_WN_CB 4
+#endif
+constexpr int NCB = VM_WN_CB;
+constexpr int NCUBE = 1 << NCB;
+constexpr int NCUBE_N = NCUBE * NCUBE * NCUBE;
+__device__ __forceinline__ unsigned ncube_cell(unsigned cp) {
+    return (cp & (NCUBE - 1u)) | ((cp >> (8 - NCB)) & ((NCUBE - 1u) << NCB)) |
+           ((cp >> (16 - 2 * NCB)) & ((NCUBE - 1u) << (2 * NCB)));
+}
+constexpr unsigned NCUBE_OUT = (0xFFu & ~(NCUBE - 1u)) * 0x010101u;
+static_assert(NCUBE_N % BLOCK == 0, "cube cells per thread");
 
 struct WalkNdtSmem {
-    unsigned cube[WCUBE_N];            // order-free miss counts around the sensor
-    unsigned cgauss[WCUBE_N / 32];     // cube voxels holding a Gaussian
+    unsigned cube[NCUBE_N];            // order-free miss counts around the sensor
+    unsigned cgauss[NCUBE_N / 32];     // cube voxels holding a Gaussian
     int2 grid[RG_SMEM_DET];            // (slot, Gaussian brick summary)
     unsigned long long wkey[BLOCK / 32][WN_WBUF];
     double2 wt[BLOCK / 32][WN_WBUF];
@@ -166,7 +178,7 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
             int r0[3];
             unpack_region(d0.rkey, r0);
             for (int a = 0; a < 3; ++a)
-                sm.anchor[a] = r0[a] * m.dim + (int)((d0.lp0 >> (10 * a)) & 1023u) - 1 - WCUBE / 2;
+                sm.anchor[a] = r0[a] * m.dim + (int)((d0.lp0 >> (10 * a)) & 1023u) - 1 - NCUBE / 2;
         } else {
             sm.anchor[0] = sm.anchor[1] = sm.anchor[2] = 1 << 29;
         }
@@ -185,13 +197,13 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
     {
         // the cube's Gaussian bitmap: every voxel id first, then all count
         // loads in flight together, one ballot per 32 cells
-        constexpr int PER = WCUBE_N / BLOCK;
+        constexpr int PER = NCUBE_N / BLOCK;
         unsigned vid[PER], c[PER];
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int k = threadIdx.x + j * BLOCK;
-            vid[j] = wn_vid_of<DIM>(m, sm, sm.anchor[0] + k % WCUBE, sm.anchor[1] + (k / WCUBE) % WCUBE,
-                               sm.anchor[2] + k / (WCUBE * WCUBE), false);
+            vid[j] = wn_vid_of<DIM>(m, sm, sm.anchor[0] + k % NCUBE, sm.anchor[1] + (k / NCUBE) % NCUBE,
+                               sm.anchor[2] + k / (NCUBE * NCUBE), false);
             sm.cube[k] = 0u;
         }
 #pragma unroll
@@ -309,7 +321,7 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
         const unsigned ux = (unsigned)(r0[0] * dim + (int)(lp & 1023u) - 1 - sm.anchor[0]);
         const unsigned uy = (unsigned)(r0[1] * dim + (int)((lp >> 10) & 1023u) - 1 - sm.anchor[1]);
         const unsigned uz = (unsigned)(r0[2] * dim + (int)(lp >> 20) - 1 - sm.anchor[2]);
-        in_cube = (ux | uy | uz) < (unsigned)WCUBE;
+        in_cube = (ux | uy | uz) < (unsigned)NCUBE;
         cp = ux | (uy << 8) | (uz << 16);
         pf_valid = false;
         active = true;
@@ -349,7 +361,7 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
             const unsigned vid = vbase + (unsigned)li;
             if (vbase != 0xFFFFFFFFu) {
                 if (in_cube) {
-                    const unsigned ck = cube_cell(cp);
+                    const unsigned ck = ncube_cell(cp);
                     if ((sm.cgauss[ck >> 5] >> (ck & 31)) & 1u) {
                         sm.vids[Q][threadIdx.x] = vid;
                         sm.tv[Q][threadIdx.x] = make_double2(tprev, tn);
@@ -382,7 +394,7 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
         li += dl;
         if (in_cube) {
             cp += (unsigned)((int)dp >> sh) << (8 * ax);
-            in_cube = (cp & CUBE_OUT) == 0;
+            in_cube = (cp & NCUBE_OUT) == 0;
         }
         if (((lp >> sh) & 1023u) - 1u >= (unsigned)dim) {
             // region crossing: wrap the local coordinate, step the grid index
@@ -531,13 +543,13 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
     }
     __syncthreads();
     unsigned long long flushed = 0;
-    for (int k = threadIdx.x; k < WCUBE_N; k += blockDim.x) {
+    for (int k = threadIdx.x; k < NCUBE_N; k += blockDim.x) {
         const unsigned c = sm.cube[k];
         if (!c) continue;
         ++flushed;
-        const unsigned vid = wn_vid_of<DIM>(m, sm, sm.anchor[0] + k % WCUBE,
-                                       sm.anchor[1] + (k / WCUBE) % WCUBE,
-                                       sm.anchor[2] + k / (WCUBE * WCUBE), true);
+        const unsigned vid = wn_vid_of<DIM>(m, sm, sm.anchor[0] + k % NCUBE,
+                                       sm.anchor[1] + (k / NCUBE) % NCUBE,
+                                       sm.anchor[2] + k / (NCUBE * NCUBE), true);
         if (vid != 0xFFFFFFFFu) red_add(scr + vid, c);
     }
     unsigned long long st[3] = {visits, rmiss, flushed};
