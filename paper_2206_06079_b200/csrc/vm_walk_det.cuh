@@ -31,6 +31,10 @@ namespace vm {
 #define VM_WD_STEPS 8
 #endif
 constexpr int WD_STEPS = VM_WD_STEPS;  // steps per window (in-flight visits per lane)
+#ifndef VM_WD_UNROLL
+#define VM_WD_UNROLL 1  // steps of the window loop unrolled
+#endif
+constexpr int WD_UNROLL = VM_WD_UNROLL;
 #ifndef VM_WD_AGG
 #define VM_WD_AGG 0  // measured: 31% fewer REDs but +16% instructions and MATCH latency
                      // (short-scoreboard stalls): C2 walk 60.9 -> 94.2 ms per step
@@ -516,7 +520,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         }
         if (!__any_sync(0xffffffffu, active || pf_valid || !exhausted || parked)) break;
         if (!__any_sync(0xffffffffu, active)) continue;
-#pragma unroll 1
+#pragma unroll WD_UNROLL
         for (int q = 0; q < WD_STEPS; ++q) {
             step(q);
             if (WD_AGG && !REC_ONLY) {
