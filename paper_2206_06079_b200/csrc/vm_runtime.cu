@@ -424,13 +424,19 @@ cudaError_t opt_in_smem(size_t smem) {
     return e;
 }
 
+template <bool REC_ONLY, class Src, int DIM, bool SHARD>
+cudaError_t launch_wd_sh(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
+    const size_t smem = sizeof(WalkDetSmem);
+    cudaError_t e = opt_in_smem<k_walk_det<REC_ONLY, Src, DIM, SHARD>>(smem);
+    if (e != cudaSuccess) return e;
+    k_walk_det<REC_ONLY, Src, DIM, SHARD><<<grid, BLOCK, smem, s>>>(dm, src);
+    return cudaSuccess;
+}
+
 template <bool REC_ONLY, class Src, int DIM>
 cudaError_t launch_wd_dim(dim3 grid, cudaStream_t s, const DevMap &dm, const Src &src) {
-    const size_t smem = sizeof(WalkDetSmem);
-    cudaError_t e = opt_in_smem<k_walk_det<REC_ONLY, Src, DIM>>(smem);
-    if (e != cudaSuccess) return e;
-    k_walk_det<REC_ONLY, Src, DIM><<<grid, BLOCK, smem, s>>>(dm, src);
-    return cudaSuccess;
+    if (dm.shard_world > 1) return launch_wd_sh<REC_ONLY, Src, DIM, true>(grid, s, dm, src);
+    return launch_wd_sh<REC_ONLY, Src, DIM, false>(grid, s, dm, src);
 }
 
 template <class Src, int DIM>

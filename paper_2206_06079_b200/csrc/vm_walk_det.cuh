@@ -128,8 +128,10 @@ __device__ __forceinline__ unsigned wd_brick(int li, const int bsh[3]) {
     return brick_of(li, bsh);
 }
 
-// DIM: compile-time region edge (32), or 0 for any other region_dim
-template <bool REC_ONLY, class Src, int DIM = 0>
+// DIM: compile-time region edge (32), or 0 for any other region_dim.
+// SHARD: a region-sharded map (walk-created regions force records); single
+// GPU maps compile that bookkeeping out.
+template <bool REC_ONLY, class Src, int DIM = 0, bool SHARD = true>
 __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_constant__ DevMap m,
                                                                Src src) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -205,8 +207,9 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
     unsigned lp = 0, rp = 0, vbase = 0xFFFFFFFFu, okey = 0, cp = 0, bm = 0;
     const bool bricks = m.brick_shift >= 0;
     int li = 0, gi = 0, rem = 0;
-    int dli0 = 0, dli1 = 0, dli2 = 0;       // local-index step per axis
-    unsigned dlp0 = 0, dlp1 = 0, dlp2 = 0;  // packed-coordinate step per axis
+    int dli0 = 0, dli1 = 0, dli2 = 0;       // local-index step per axis (DIM != 32)
+    unsigned dlp0 = 0, dlp1 = 0, dlp2 = 0;  // packed-coordinate step per axis (DIM != 32)
+    unsigned sg3 = 0;  // DIM 32: the step direction codes, 2 bits per axis (step + 1)
     bool active = false, in_cube = false, ingrid = false;
     // rare events park the lane until the window boundary, where they are
     // resolved outside the unrolled steps (no call inside them)
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
     auto set_region = [&](int s, unsigned b) {
         vbase = s >= 0 && s < m.cap ? (unsigned)s * vpr : 0xFFFFFFFFu;
         bm = bricks ? b : 0xFFFFFFFFu;
-        forced = m.shard_world > 1 && s >= m.walk_slot0;
+        if (SHARD) forced = m.shard_world > 1 && s >= m.walk_slot0;
     };
 
     auto start = [&]() {
@@ -271,12 +274,16 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
              dim * ((int)((lp >> 10) & 1023u) - 1 + dim * ((int)(lp >> 20) - 1));
         const int sx = (int)((codes >> 1) & 3u) - 1, sy = (int)((codes >> 3) & 3u) - 1,
                   sz = (int)((codes >> 5) & 3u) - 1;
-        dli0 = sx;
-        dli1 = sy * dim;
-        dli2 = sz * dim * dim;
-        dlp0 = (unsigned)sx;
-        dlp1 = (unsigned)sy << 10;
-        dlp2 = (unsigned)sz << 20;
+        if (DIM == 32) {
+            sg3 = (codes >> 1) & 63u;
+        } else {
+            dli0 = sx;
+            dli1 = sy * dim;
+            dli2 = sz * dim * dim;
+            dlp0 = (unsigned)sx;
+            dlp1 = (unsigned)sy << 10;
+            dlp2 = (unsigned)sz << 20;
+        }
         int r0[3];
         unpack_region(d.rkey, r0);
         const int u0 = r0[0] - sm.gb[0], u1 = r0[1] - sm.gb[1], u2 = r0[2] - sm.gb[2];
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         if (vbase != 0xFFFFFFFFu) {
             if (in_cube) {
                 const unsigned ck = cube_cell(cp);
-                if (((sm.cmark[ck >> 5] >> (ck & 31)) & 1u) || forced) {
+                if (((sm.cmark[ck >> 5] >> (ck & 31)) & 1u) || (SHARD && forced)) {
                     sm.vids[par][Q][threadIdx.x] = vid;
                     live |= 1u << Q;
                     sure |= 1u << Q;
@@ -349,10 +356,10 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
                     if (WD_AGG) pend = WD_CUBE_TAG | ck;
                     else atomicAdd(sm.cube + ck, 1u);
                 }
-            } else if (((bm >> wd_brick<DIM>(li, m.bsh)) & 1u) || forced) {
+            } else if (((bm >> wd_brick<DIM>(li, m.bsh)) & 1u) || (SHARD && forced)) {
                 sm.vids[par][Q][threadIdx.x] = vid;
                 live |= 1u << Q;
-                if (forced) sure |= 1u << Q;
+                if (SHARD && forced) sure |= 1u << Q;
             } else if (!REC_ONLY) {
                 if (WD_AGG) pend = vid;
                 else red_add(scr + vid, 1u);
@@ -367,13 +374,23 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
         // ---- advance (t_max[axis] += t_delta[axis]) ----
         --rem;
         const int ax = dda_advance(tx, ty, tz, dx, dy, dz);
-        const int dl = ax == 2 ? dli2 : (ax == 1 ? dli1 : dli0);
-        const unsigned dp = ax == 2 ? dlp2 : (ax == 1 ? dlp1 : dlp0);
         const int sh = 10 * ax;
+        int dl, sgn;
+        unsigned dp;
+        if (DIM == 32) {
+            // branch-free: the axis' step from its 2-bit code; strides 1, 32, 1024
+            sgn = (int)((sg3 >> (2 * ax)) & 3u) - 1;
+            dl = (int)((unsigned)sgn << (5 * ax));
+            dp = (unsigned)sgn << sh;
+        } else {
+            dl = ax == 2 ? dli2 : (ax == 1 ? dli1 : dli0);
+            dp = ax == 2 ? dlp2 : (ax == 1 ? dlp1 : dlp0);
+            sgn = (int)dp >> sh;
+        }
         lp += dp;
         li += dl;
         if (in_cube) {
-            cp += (unsigned)((int)dp >> sh) << (8 * ax);  // the step (+-1) into the cube field
+            cp += (unsigned)sgn << (8 * ax);  // the step (+-1) into the cube field
             in_cube = (cp & CUBE_OUT) == 0;
         }
         if (((lp >> sh) & 1023u) - 1u >= (unsigned)dim) {
@@ -382,7 +399,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
             li -= dim * dl;
             rp += dp;
             const unsigned f = ((rp >> sh) & 1023u) - RP_BIAS;
-            gi += ((int)dp >> sh) * sm.gs[ax];
+            gi += sgn * sm.gs[ax];
             ingrid = ingrid && f < (unsigned)sm.gn[ax];
             int s = -1;
             unsigned b = 0xFFFFFFFFu;
@@ -416,7 +433,7 @@ __global__ void __launch_bounds__(BLOCK, WD_BLOCKS) k_walk_det(const __grid_cons
                                            sm.endc[threadIdx.x][2], true);
             vbase = vid == 0xFFFFFFFFu ? vid : vid - vid % vpr;
             li = vid == 0xFFFFFFFFu ? 0 : (int)(vid % vpr);
-            forced = m.shard_world > 1 && vid != 0xFFFFFFFFu && (int)(vid / vpr) >= m.walk_slot0;
+            if (SHARD) forced = m.shard_world > 1 && vid != 0xFFFFFFFFu && (int)(vid / vpr) >= m.walk_slot0;
             bm = 0xFFFFFFFFu;  // the end voxel is a candidate
             in_cube = false;
             jumped = true;

@@ -230,8 +230,9 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
     unsigned lp = 0, rp = 0, vbase = 0xFFFFFFFFu, oi = 0, cp = 0, gm = 0;
     bool sample = false;
     int li = 0, gi = 0, rem = 0;
-    int dli0 = 0, dli1 = 0, dli2 = 0;
-    unsigned dlp0 = 0, dlp1 = 0, dlp2 = 0;
+    int dli0 = 0, dli1 = 0, dli2 = 0;       // DIM != 32
+    unsigned dlp0 = 0, dlp1 = 0, dlp2 = 0;  // DIM != 32
+    unsigned sg3 = 0;  // DIM 32: the step direction codes, 2 bits per axis (step + 1)
     bool active = false, in_cube = false, ingrid = false;
     int parked = 0;  // 1: region lookup after a crossing, 2: fallback jump to the end cell
     bool jumped = false;
@@ -285,12 +286,16 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
              dim * ((int)((lp >> 10) & 1023u) - 1 + dim * ((int)(lp >> 20) - 1));
         const int sx = (int)((codes >> 1) & 3u) - 1, sy = (int)((codes >> 3) & 3u) - 1,
                   sz = (int)((codes >> 5) & 3u) - 1;
-        dli0 = sx;
-        dli1 = sy * dim;
-        dli2 = sz * dim * dim;
-        dlp0 = (unsigned)sx;
-        dlp1 = (unsigned)sy << 10;
-        dlp2 = (unsigned)sz << 20;
+        if (DIM == 32) {
+            sg3 = (codes >> 1) & 63u;
+        } else {
+            dli0 = sx;
+            dli1 = sy * dim;
+            dli2 = sz * dim * dim;
+            dlp0 = (unsigned)sx;
+            dlp1 = (unsigned)sy << 10;
+            dlp2 = (unsigned)sz << 20;
+        }
         int r0[3];
         unpack_region(d.rkey, r0);
         const int u0 = r0[0] - sm.gb[0], u1 = r0[1] - sm.gb[1], u2 = r0[2] - sm.gb[2];
@@ -387,13 +392,23 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
         }
         tprev = tn;
         --rem;
-        const int dl = ax == 2 ? dli2 : (ax == 1 ? dli1 : dli0);
-        const unsigned dp = ax == 2 ? dlp2 : (ax == 1 ? dlp1 : dlp0);
         const int sh = 10 * ax;
+        int dl, sgn;
+        unsigned dp;
+        if (DIM == 32) {
+            // branch-free: the axis' step from its 2-bit code; strides 1, 32, 1024
+            sgn = (int)((sg3 >> (2 * ax)) & 3u) - 1;
+            dl = (int)((unsigned)sgn << (5 * ax));
+            dp = (unsigned)sgn << sh;
+        } else {
+            dl = ax == 2 ? dli2 : (ax == 1 ? dli1 : dli0);
+            dp = ax == 2 ? dlp2 : (ax == 1 ? dlp1 : dlp0);
+            sgn = (int)dp >> sh;
+        }
         lp += dp;
         li += dl;
         if (in_cube) {
-            cp += (unsigned)((int)dp >> sh) << (8 * ax);
+            cp += (unsigned)sgn << (8 * ax);
             in_cube = (cp & NCUBE_OUT) == 0;
         }
         if (((lp >> sh) & 1023u) - 1u >= (unsigned)dim) {
@@ -402,7 +417,7 @@ __global__ void __launch_bounds__(BLOCK, WN_BLOCKS) k_walk_ndt_det(const __grid_
             li -= dim * dl;
             rp += dp;
             const unsigned f = ((rp >> sh) & 1023u) - RP_BIAS;
-            gi += ((int)dp >> sh) * sm.gs[ax];
+            gi += sgn * sm.gs[ax];
             ingrid = ingrid && f < (unsigned)sm.gn[ax];
             int s = -1;
             unsigned g = 0xFFFFFFFFu;
