@@ -368,6 +368,9 @@ __global__ void __launch_bounds__(DISC_BT, DISC_MINB) k_discover(const __grid_co
     const int s = blockIdx.y;
     const bool mine = ok && s < r.nseg;
     if (s != 0) st[0] = st[1] = st[2] = 0;  // ray statistics are counted once
+    // a later-segment block none of whose rays reach that segment (most of the
+    // third, degenerate-segment row) has nothing to count, record or stamp
+    if (s != 0 && !__syncthreads_or(mine)) return;
     // warp-aggregated allocation of segment descriptors
     unsigned long long dbase = 0;
     if (emit) {
@@ -1047,6 +1050,9 @@ __global__ void __launch_bounds__(BLOCK) k_walk_tsdf(const __grid_constant__ Dev
 #ifndef RES_U
 #define RES_U 2     // scratch quads in flight per thread
 #endif
+#ifndef RES_PIPE
+#define RES_PIPE 0  // software-pipelined scratch loads (experiment knob)
+#endif
 #ifndef RES_MINB
 #define RES_MINB 8  // k_resolve resident blocks per SM: 8 x 2 quads in flight beat
                     // 4 x 4 and 2 x 8 (C2 resolve 10.0 / 10.5 / 11.6 ms per step)
@@ -1061,15 +1067,34 @@ __device__ __forceinline__ void resolve_range(const DevMap &m, int slot, int v0,
         // occupancy quads of the non-zero ones, also all in flight
         const uint4 *s4 = reinterpret_cast<const uint4 *>(scr);
         float4 *o4 = reinterpret_cast<float4 *>(occ);
+#if RES_PIPE
+        // the next chunk's scratch loads are issued before this chunk's
+        // occupancy round trip (two dependent loads per chunk otherwise)
+        uint4 wn[RES_U];
+#pragma unroll
+        for (int u = 0; u < RES_U; ++u) {
+            const int q = (v0 >> 2) + threadIdx.x + u * blockDim.x;
+            wn[u] = q < (v1 >> 2) ? __ldcs(s4 + q) : make_uint4(0, 0, 0, 0);
+        }
+#endif
         for (int q0 = (v0 >> 2) + threadIdx.x; q0 < (v1 >> 2); q0 += RES_U * blockDim.x) {
             uint4 w[RES_U];
             float4 l[RES_U];
             unsigned nz = 0;
+#if RES_PIPE
+#pragma unroll
+            for (int u = 0; u < RES_U; ++u) {
+                w[u] = wn[u];
+                const int q = q0 + RES_U * blockDim.x + u * blockDim.x;
+                wn[u] = q < (v1 >> 2) ? __ldcs(s4 + q) : make_uint4(0, 0, 0, 0);
+            }
+#else
 #pragma unroll
             for (int u = 0; u < RES_U; ++u) {
                 const int q = q0 + u * blockDim.x;
                 w[u] = q < (v1 >> 2) ? __ldcs(s4 + q) : make_uint4(0, 0, 0, 0);
             }
+#endif
 #pragma unroll
             for (int u = 0; u < RES_U; ++u) {
                 // counted voxels (MARK'ed words -- sample voxels -- are the fold's)

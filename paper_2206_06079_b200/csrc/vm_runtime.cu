@@ -1048,7 +1048,7 @@ int integrate_impl(vm_map *m, const Src &src, long long n, int mode, int exec, v
         k_guard<<<1, 1, 0, m->stream>>>(dm, margin);
         if (emit) {
             if (key_mi) {
-                k_stamp<<<m->num_sms * 2, BLOCK, 0, m->stream>>>(dm);
+                k_stamp<<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
                 m->launches += 1;
             }
             k_rgrid<<<16, BLOCK, 0, m->stream>>>(dm);
@@ -1809,7 +1809,7 @@ int integrate_pipelined(vm_map *m, const vm_rays *rays, int nb, int mode, vm_sta
             CK(cudaEventRecord(ev[1], ds));
             // the map's stream: stamps (after b-1's fold), walk, resolve, fold
             CK(cudaStreamWaitEvent(s, ev[1], 0));
-            k_stamp<<<m->num_sms * 2, BLOCK, 0, s>>>(dm);
+            k_stamp<<<m->num_sms * 8, BLOCK, 0, s>>>(dm);
             CK(cudaEventRecord(ev[6], s));
             if ((rc = launch_walk(m, dm, src, n, mode, true, false))) return rc;
             k_batch_regions<<<1, 1, 0, s>>>(dm);
