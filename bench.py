@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=("c2", "c1", "c3", "c4", "c5"), default="c2")
+    ap.add_argument("--workload", choices=("c2", "c2_01", "c1", "c3", "c4", "c5"), default="c2")
     ap.add_argument("--exec", dest="exec_", choices=("det", "cas"), default="det")
     ap.add_argument("--batches", type=int, default=1000, help="C2 batches per step")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -74,6 +74,17 @@ def workload(name: str, batches: int):
                     rays_per_scan=int(len(scan_list[0])), batches=len(data),
                     batch_period_s=scans.BATCH_PERIOD, rays_per_batch=int(len(data[0])),
                     voxel_size=0.05, region_dim=32, mode="occupancy")
+        mode = "occupancy"
+    elif name == "c2_01":
+        # the north_star target's case: sustained 0.1 m occupancy integration
+        # (C2's OS1-128 sequence and batching, at 0.1 m voxels)
+        cfg = MapConfig(voxel_size=0.1)
+        scan_list = scans.os128_canyon_batches(batches)
+        data = scans.batch_by_period(np.concatenate(scan_list))
+        desc = dict(workload="C2 sequence at 0.1 m: synthetic OS1-128 street canyon",
+                    scans=len(scan_list), rays_per_scan=int(len(scan_list[0])), batches=len(data),
+                    batch_period_s=scans.BATCH_PERIOD, rays_per_batch=int(len(data[0])),
+                    voxel_size=0.1, region_dim=32, mode="occupancy")
         mode = "occupancy"
     elif name == "c1":
         cfg = MapConfig(voxel_size=0.1)
@@ -478,7 +489,23 @@ def main():
         nb = max(1, ns["batches"])
         nwalk = ns["walk_ms"] / nb
         c1 = run_gpu_workload("c1", args, dev, torch, steps=50, e2e_steps=20)
+        o1 = run_gpu_workload("c2_01", args, dev, torch, steps=min(args.steps, 5), e2e_steps=3)
         if rank == 0:
+            o1s = o1["s0"]
+            o1_walk = o1s["walk_ms"] / max(1, o1s["batches"])
+            o1_bytes = algorithmic_bytes(o1s["S"], o1s["V"], o1["H"]) / max(1, o1s["batches"])
+            line["occ_0p1m"] = {
+                "workload": o1["desc"]["workload"], "config": o1["desc"], "value": o1["value"],
+                "unit": UNIT, "ms_per_step": o1["ms"] / o1["steps"], "steps": o1["steps"],
+                "e2e": o1["e2e"], "clocks": o1["clocks"], "gpu_launches": o1["launches"],
+                "target_rays_per_s": 260e6,
+                "roofline": {"bound": "hbm", "kernel": "k_walk_det", "unit": "GB/s",
+                             "achieved": o1_bytes / (o1_walk * 1e-3) / 1e9 if o1_walk else 0.0,
+                             "peak": peak, "peak_kind": peak_kind,
+                             "frac": (o1_bytes / (o1_walk * 1e-3) / 1e9) / peak if o1_walk else None,
+                             "bytes_per_launch": o1_bytes, "avg_launch_ms": o1_walk},
+                "stages_ms_per_step": {k: round(o1s[k], 4) for k in (
+                    "discover_ms", "walk_ms", "resolve_ms", "sort_ms", "fold_ms", "gpu_ms")}}
             line["ndt_om"] = {
                 "workload": n["desc"]["workload"], "config": n["desc"], "value": n["value"],
                 "unit": UNIT, "ms_per_step": n["ms"] / n["steps"], "steps": n["steps"],

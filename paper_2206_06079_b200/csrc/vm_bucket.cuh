@@ -29,6 +29,12 @@ namespace vm {
 #define BK_FOLD_MINB 1  // k_bk_fold resident blocks per SM (register budget)
 #endif
 
+#ifndef VM_BK_BIG_BPS
+#define VM_BK_BIG_BPS 4
+#endif
+// k_bk_fold_big blocks per SM: one bucket per block at a time, whose serial
+// fold keeps one warp busy while the others wait -- several buckets per SM
+constexpr int BK_BIG_BPS = VM_BK_BIG_BPS;
 constexpr int BK_SERIAL = 16;
 constexpr int BK_SMEM = 4096;
 
@@ -131,21 +137,40 @@ __device__ __forceinline__ void vf_begin(const DevMap &m, VoxFold &f, unsigned v
     slot_li_to_g(m, (int)(vid / (unsigned)m.vpr), (int)(vid % (unsigned)m.vpr), f.g);
 }
 
-// one hit of segment order index `oi` (= ray * maxseg + seg), after the
-// misses counted so far (reference.py:43-57)
-template <class Src>
-__device__ __forceinline__ void vf_hit(const DevMap &m, const Src &src, VoxFold &f, unsigned oi) {
+// one hit with sample end point ep, after the misses counted so far
+// (reference.py:43-57)
+__device__ __forceinline__ void vf_hit_ep(const DevMap &m, VoxFold &f, const double ep[3]) {
     f.l = miss_k(f.l, f.misses, m.miss32, m.cmin, m.cmax);
     f.misses = 0;
     f.l = clamp_add(f.l, m.hit32, m.cmin, m.cmax);
     if (m.slab[L_MEAN]) {
-        const long long ray = (long long)(oi / (unsigned)m.maxseg);
-        double ep[3];
-        float it;
-        src.load_end(ray, ep, it);
         const double off[3] = {ep[0] / m.vox - (double)f.g[0], ep[1] / m.vox - (double)f.g[1],
                                ep[2] / m.vox - (double)f.g[2]};
         fold_mean(f.packed, f.count, off);
+    }
+}
+
+// ... of segment order index `oi` (= ray * maxseg + seg)
+template <class Src>
+__device__ __forceinline__ void vf_hit(const DevMap &m, const Src &src, VoxFold &f, unsigned oi) {
+    double ep[3] = {0.0, 0.0, 0.0};
+    if (m.slab[L_MEAN]) {
+        float it;
+        src.load_end((long long)(oi / (unsigned)m.maxseg), ep, it);
+    }
+    vf_hit_ep(m, f, ep);
+}
+
+// The end point of a lane's hit record, loaded by every lane at once before
+// a warp folds a run serially (the loads leave the serial chain; the fold
+// then takes each hit's point from its lane)
+template <class Src>
+__device__ __forceinline__ void vf_lane_end(const DevMap &m, const Src &src, bool hit, unsigned oi,
+                                            double e[3]) {
+    e[0] = e[1] = e[2] = 0.0;
+    if (hit && m.slab[L_MEAN]) {
+        float it;
+        src.load_end((long long)(oi / (unsigned)m.maxseg), e, it);
     }
 }
 
@@ -207,15 +232,19 @@ template <class Src>
 __device__ __forceinline__ void vf_warp_chunk(const DevMap &m, const Src &src, VoxFold &f,
                                               unsigned x, int n) {
     const int lane = threadIdx.x & 31;
-    const unsigned hmask = __ballot_sync(0xffffffffu, lane < n && (x & 1u));
+    const bool hit = lane < n && (x & 1u);
+    const unsigned hmask = __ballot_sync(0xffffffffu, hit);
+    double e[3];
+    vf_lane_end(m, src, hit, x >> 1, e);  // all the chunk's end points in flight at once
     int cur = 0;
     unsigned hm = hmask;
     while (hm) {
         const int h = __ffs(hm) - 1;
         hm &= hm - 1;
         f.misses += (unsigned)(h - cur);
-        const unsigned hx = __shfl_sync(0xffffffffu, x, h);
-        vf_hit(m, src, f, hx >> 1);
+        const double ep[3] = {__shfl_sync(0xffffffffu, e[0], h), __shfl_sync(0xffffffffu, e[1], h),
+                              __shfl_sync(0xffffffffu, e[2], h)};
+        vf_hit_ep(m, f, ep);
         cur = h + 1;
     }
     f.misses += (unsigned)(n - cur);
@@ -302,14 +331,21 @@ __global__ void __launch_bounds__(BLOCK) k_bk_fold_big(const __grid_constant__ D
                         f.misses += before;
                         const unsigned pL = __shfl_sync(0xffffffffu, p, L);
                         const unsigned hL = __shfl_sync(0xffffffffu, h, L);
+                        // lane j loads the end point of order (w0 + L) * 32 + j if it hit
+                        double e[3];
+                        vf_lane_end(m, src, (hL >> lane) & 1u, (unsigned)((w0 + L) * 32 + lane), e);
                         unsigned bits = pL;
                         while (bits) {
                             const int bi = __ffs(bits) - 1;
                             bits &= bits - 1;
-                            if ((hL >> bi) & 1u)
-                                vf_hit(m, src, f, (unsigned)((w0 + L) * 32 + bi));
-                            else
+                            if ((hL >> bi) & 1u) {
+                                const double ep[3] = {__shfl_sync(0xffffffffu, e[0], bi),
+                                                      __shfl_sync(0xffffffffu, e[1], bi),
+                                                      __shfl_sync(0xffffffffu, e[2], bi)};
+                                vf_hit_ep(m, f, ep);
+                            } else {
                                 ++f.misses;
+                            }
                         }
                         prev = L + 1;
                     }

@@ -592,7 +592,7 @@ int ensure_buckets(vm_map *m, size_t nmarked_cap, size_t bwords) {
         CK(cudaMalloc((void **)&m->d_bk_perm, nc * sizeof(unsigned)));
         m->bk_cap = nc;
     }
-    const size_t need = (size_t)m->num_sms * 2 * bwords;
+    const size_t need = (size_t)m->num_sms * BK_BIG_BPS * 2 * bwords;
     if (need > m->bk_bits_cap || !m->d_bk_bits) {
         cudaFree(m->d_bk_bits);
         m->d_bk_bits = nullptr;
@@ -628,7 +628,7 @@ int launch_bucket_fold(vm_map *m, const DevMap &dm, const Src &src, long long n,
     const unsigned gf = (unsigned)std::max<long long>(
         1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
     k_bk_fold<<<gf, BLOCK, 0, s>>>(dm, src, b);
-    k_bk_fold_big<<<m->num_sms, BLOCK, 0, s>>>(dm, src, b);
+    k_bk_fold_big<<<m->num_sms * BK_BIG_BPS, BLOCK, 0, s>>>(dm, src, b);
     m->launches += 6;
     return check_launch("bucket fold");
 }

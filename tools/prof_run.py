@@ -23,8 +23,8 @@ ap.add_argument("--device", action="store_true")
 a = ap.parse_args()
 if a.workload == "c1":
     cfg, mode, data = MapConfig(), "occupancy", [scans.os64_room_scan()] * a.batches
-elif a.workload == "c2":
-    cfg, mode = MapConfig(voxel_size=0.05), "occupancy"
+elif a.workload in ("c2", "c2_01"):
+    cfg, mode = MapConfig(voxel_size=0.05 if a.workload == "c2" else 0.1), "occupancy"
     data = scans.batch_by_period(np.concatenate(scans.os128_canyon_batches(a.batches)))
 else:
     cfg, mode, data = MapConfig(), "ndt-om", scans.os64_tunnel_scans(a.batches)
