@@ -36,6 +36,7 @@ namespace vm {
 // fold keeps one warp busy while the others wait -- several buckets per SM
 constexpr int BK_BIG_BPS = VM_BK_BIG_BPS;
 constexpr int BK_SERIAL = 16;
+constexpr int BK_WARP = 1024;  // one warp sorts (bitonic, shared memory) and folds up to this
 constexpr int BK_SMEM = 4096;
 
 struct BucketState {
@@ -43,8 +44,10 @@ struct BucketState {
     unsigned *off;               // [M + 1] slice offset (k_bk_alloc), bumped by the scatter
     unsigned *cursor;            // slice allocation cursor (zeroed per batch)
     unsigned *val;               // [R] bucketed (order << 1 | hit) payloads
-    int *big;                    // buckets for the block kernels
+    int *big;                    // buckets for the block kernel (> BK_WARP records)
     unsigned long long *nbig;
+    int *mid;                    // buckets for the warp kernel (BK_SERIAL < records <= BK_WARP)
+    unsigned long long *nmid;
     unsigned *bits;              // huge buckets: per block 2 * bwords words
     unsigned long long bwords;   // words of one bitmap (order space / 32)
 };
@@ -202,7 +205,8 @@ __global__ void __launch_bounds__(BLOCK, BK_FOLD_MINB) k_bk_fold(const __grid_co
         const unsigned s = bk_slice(b, mi, c);
         if (c == 0u) continue;  // an index whose claim lost a race (marked (-1, -1))
         if (c > (unsigned)BK_SERIAL) {
-            b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
+            if (c <= (unsigned)BK_WARP) b.mid[atomicAdd(b.nmid, 1ULL)] = (int)mi;
+            else b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
             continue;
         }
         b.cnt[mi] = 0u;
@@ -248,6 +252,57 @@ __device__ __forceinline__ void vf_warp_chunk(const DevMap &m, const Src &src, V
         cur = h + 1;
     }
     f.misses += (unsigned)(n - cur);
+}
+
+// One warp per medium bucket: bitonic sort of the padded slice in the warp's
+// shared-memory window (warp-synchronous), then the chunked fold -- no block
+// barrier, so every warp of the block folds its own bucket.
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_bk_fold_mid(const __grid_constant__ DevMap m, Src src,
+                                                       BucketState b) {
+    __shared__ unsigned sv[BLOCK / 32][BK_WARP];
+    unsigned long long R, M;
+    if (!bk_live(m, R, M)) return;
+    const unsigned long long nm = *((volatile unsigned long long *)b.nmid);
+    const int lane = threadIdx.x & 31;
+    unsigned *const w = sv[threadIdx.x >> 5];
+    const unsigned long long nw = (unsigned long long)gridDim.x * (BLOCK / 32);
+    for (unsigned long long t = (unsigned long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+         t < nm; t += nw) {
+        const unsigned long long mi = (unsigned long long)b.mid[t];
+        unsigned c;
+        const unsigned s = bk_slice(b, mi, c);
+        __syncwarp();
+        if (lane == 0) b.cnt[mi] = 0u;
+        unsigned P = 32;
+        while (P < c) P <<= 1;
+        for (unsigned i = lane; i < P; i += 32) w[i] = i < c ? b.val[s + i] : 0xFFFFFFFFu;
+        __syncwarp();
+        for (unsigned k = 2; k <= P; k <<= 1) {
+            for (unsigned j = k >> 1; j > 0; j >>= 1) {
+                for (unsigned i = lane; i < P; i += 32) {
+                    const unsigned p = i ^ j;
+                    if (p > i) {
+                        const unsigned a = w[i], bb = w[p];
+                        if ((a > bb) == ((i & k) == 0)) {
+                            w[i] = bb;
+                            w[p] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        VoxFold f;
+        vf_begin(m, f, marked_vid(m, mi));
+        for (unsigned base = 0; base < c; base += 32) {
+            const int n = (int)min(32u, c - base);
+            const unsigned x = lane < n ? w[base + lane] : 0u;
+            vf_warp_chunk(m, src, f, x, n);
+        }
+        if (lane == 0) vf_end(m, f);
+        __syncwarp();
+    }
 }
 
 // One block per large bucket.

@@ -106,6 +106,7 @@ struct vm_map {
     long long *d_big = nullptr;
     size_t big_cap = 0;
     unsigned long long *d_nbig = nullptr;
+    unsigned long long *d_nmid = nullptr;  // occupancy bucket fold: medium buckets
     // bucketed fold of the deterministic occupancy records (vm_bucket.cuh)
     unsigned *d_bk_cnt = nullptr, *d_bk_off = nullptr;
     size_t bk_cap = 0;
@@ -614,9 +615,11 @@ int launch_bucket_fold(vm_map *m, const DevMap &dm, const Src &src, long long n,
         CK(cudaMemset(m->d_nbk_small, 0, (2 * NBK_BINS + 4) * sizeof(unsigned)));
     }
     unsigned *cursor = m->d_nbk_small + 2 * NBK_BINS + 2;
+    if (!m->d_nmid && (rc = dev_alloc(&m->d_nmid, 1))) return rc;
     BucketState b{m->d_bk_cnt, m->d_bk_off, cursor, reinterpret_cast<unsigned *>(m->d_rec2),
-                  m->d_bk_big, m->d_nbig, m->d_bk_bits, bwords};
+                  m->d_bk_big, m->d_nbig, m->d_bk_big2, m->d_nmid, m->d_bk_bits, bwords};
     CK(cudaMemsetAsync(m->d_nbig, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(m->d_nmid, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(cursor, 0, sizeof(unsigned), s));
     const unsigned g = (unsigned)m->num_sms * 8;
     const unsigned ga = (unsigned)std::max<long long>(
@@ -628,8 +631,9 @@ int launch_bucket_fold(vm_map *m, const DevMap &dm, const Src &src, long long n,
     const unsigned gf = (unsigned)std::max<long long>(
         1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
     k_bk_fold<<<gf, BLOCK, 0, s>>>(dm, src, b);
+    k_bk_fold_mid<<<m->num_sms * 4, BLOCK, 0, s>>>(dm, src, b);
     k_bk_fold_big<<<m->num_sms * BK_BIG_BPS, BLOCK, 0, s>>>(dm, src, b);
-    m->launches += 6;
+    m->launches += 7;
     return check_launch("bucket fold");
 }
 
@@ -2091,6 +2095,7 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_gmask);
     cudaFree(m->d_big);
     cudaFree(m->d_nbig);
+    cudaFree(m->d_nmid);
     cudaFree(m->d_bk_cnt);
     cudaFree(m->d_bk_off);
     cudaFree(m->d_bk_big);

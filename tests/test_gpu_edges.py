@@ -151,6 +151,31 @@ def test_c2_twenty_batches_pipelined_bit_exact():
                                   om.layer(rk, name).view(np.uint8)), (rk, name)
 
 
+@pytest.mark.slow
+def test_c2_sequence_at_0p1m_pipelined_bit_exact():
+    """The north_star target's case -- C2's OS1-128 sequence at 0.1 m voxels,
+    where sample voxels collect hundreds to thousands of records per batch
+    (the warp and block bucket folds) -- 10 batches through submit_batches
+    against the C oracle, bit for bit."""
+    from paper_2206_06079_b200 import submit_batches
+    cfg = MapConfig(voxel_size=0.1)
+    data = scans.batch_by_period(np.concatenate(scans.os128_canyon_batches(100)))[:10]
+    names = MODE_LAYERS["occupancy"]
+    vm = VoxelMap(cfg, names)
+    om = orc.OracleMap(cfg, names)
+    sts = submit_batches(vm, data, "occupancy")
+    for st, rec in zip(sts, data):
+        ost = om.integrate_records(rec, "occupancy")
+        assert (st.voxel_visits, st.segments, st.region_misses) == \
+            (ost["voxel_visits"], ost["segments"], 0)
+    assert max(s.records for s in sts) > 0
+    assert set(vm.regions) == set(om.region_keys())
+    for rk, region in vm.regions.items():
+        for name in names:
+            assert np.array_equal(region.buffers[name].view(np.uint8),
+                                  om.layer(rk, name).view(np.uint8)), (rk, name)
+
+
 def _layers_equal(a, b):
     assert set(a.regions) == set(b.regions)
     for rk, region in a.regions.items():
