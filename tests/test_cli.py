@@ -70,7 +70,9 @@ def test_online_replay_keeps_up_at_sensor_rate():
     rec = np.concatenate(scans.os128_canyon_batches(100))  # 1 s of sensor time
     batches = cli._batches(rec)
     vm = VoxelMap(MapConfig(voxel_size=0.05), MODE_LAYERS["occupancy"])
-    cli._run_offline(vm, batches[:1], "occupancy", ExecutorOptions())  # device warm-up
+    # device warm-up through the online path itself (a consumer thread and
+    # per-batch submit_batch: its kernels load lazily on their first launch)
+    cli._run_online(vm, batches[:2], "occupancy", ExecutorOptions())
     vm.clear()
     rows, dropped = cli._run_online(vm, batches, "occupancy", ExecutorOptions())
     assert dropped == 0 and len(rows) == len(batches) == 10
