@@ -524,6 +524,296 @@ __global__ void __launch_bounds__(BLOCK) k_nbk_gather(const __grid_constant__ De
     }
 }
 
+// ---- the same bucket preparation in four launches (NDT-OM / NDT-TM) ----
+// The ten kernels above (weigh, count, alloc, order, perm, scatter, three
+// sorts, gather) are each a few microseconds of work behind a launch and a
+// tail; on the NDT batch tail they sit on the critical path next to
+// k_resolve.  Fused by dependency: weigh + count (both per record), alloc +
+// order (the last block to finish turns the class histogram into cursors),
+// perm + scatter (both need only the slices and cursors), the three sorts +
+// gather (block roles by bucket size; each bucket gathers its sample end
+// points once sorted).  Same results: a bucket's order comes from its sort,
+// not from the scatter.
+
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_nbk_weigh_count(const __grid_constant__ DevMap m, Src src,
+                                                           NdtBuckets b) {
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = m.rec[i];
+        const unsigned mi = (unsigned)(k >> 32);
+        if (mi >= M) continue;
+        atomicAdd(b.cnt + mi, 1u);
+        if ((k >> 31) & 1ULL) {
+            atomicAdd(b.cnt2 + mi, 1u);
+            continue;  // a sample (phase 2): no weight
+        }
+        const int2 sl = m.marked[mi];
+        if (sl.x < 0) continue;
+        const int s = sl.x, li = sl.y;
+        const unsigned oi = (unsigned)k & 0x7FFFFFFFu;
+        Ray r;
+        src.load((long long)(oi / (unsigned)m.maxseg), r.o, r.e, r.has, r.inten);
+        prep_ray(m, r, true);
+        double so[3], se[3];
+        int sh;
+        segment_of(m, r, (int)(oi % (unsigned)m.maxseg), so, se, sh);
+        const double v[3] = {se[0] - so[0], se[1] - so[1], se[2] - so[2]};
+        int g[3];
+        slot_li_to_g(m, s, li, g);
+        double off[3], mu[3];
+        unpack_mean(layer_at<unsigned>(m, L_MEAN, s)[li], off);
+        for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
+        float c6[6];
+        const float *cov = layer_at<float>(m, L_COV, s) + li * 6;
+        for (int j = 0; j < 6; ++j) c6[j] = cov[j];
+        const double2 t = m.rec_t[i];
+        const double gw = gaussian_weight(mu, c6, m.sigma2, so, v, t.x, t.y);
+        const float d32 = (float)(gw * m.miss_delta);
+        m.recval[i] = (__float_as_uint(d32) & 0x7FFFFFFFu) | (gw >= m.miss_check ? 0x80000000u : 0u);
+    }
+}
+
+// k_nbk_alloc, then the last block to finish runs k_nbk_order
+// (cursor[NBK_BINS + 2] counts finished blocks; the last one resets it).
+__global__ void __launch_bounds__(BLOCK) k_nbk_alloc_order(const __grid_constant__ DevMap m, NdtBuckets b) {
+    __shared__ unsigned h[NBK_BINS];
+    __shared__ bool last;
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x) h[i] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < M; base += stride) {
+        const unsigned long long mi = base + threadIdx.x;
+        const unsigned c = mi < M ? b.cnt[mi] : 0u;
+        unsigned incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned wb = 0;
+        if (lane == 31 && tot) wb = atomicAdd(b.cursor + NBK_BINS + 1, tot);
+        wb = __shfl_sync(0xffffffffu, wb, 31);
+        if (c) {
+            b.off[mi] = wb + incl - c;
+            atomicAdd(h + nbk_class(b.cnt2[mi]), 1u);
+            if (c > (unsigned)NBK_WARP_MAX) b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
+            else if (c > (unsigned)NBK_SERIAL) b.mid[atomicAdd(b.nmid, 1ULL)] = (int)mi;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x)
+        if (h[i]) atomicAdd(b.hist + i, h[i]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(b.cursor + NBK_BINS + 2, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x) h[i] = atomicExch(b.hist + i, 0u);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    unsigned run = 0;
+    for (int i = NBK_BINS - 1; i >= 0; --i) {
+        b.cursor[i] = run;
+        run += h[i];
+    }
+    b.cursor[NBK_BINS] = run;
+    b.cursor[NBK_BINS + 2] = 0u;
+}
+
+// k_nbk_perm's loop, then k_nbk_scatter's
+__global__ void __launch_bounds__(BLOCK) k_nbk_perm_scatter(const __grid_constant__ DevMap m, NdtBuckets b) {
+    __shared__ unsigned cnt[NBK_BINS], base[NBK_BINS];
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    for (unsigned long long b0 = (unsigned long long)blockIdx.x * blockDim.x; b0 < M;
+         b0 += (unsigned long long)gridDim.x * blockDim.x) {
+        for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x) cnt[i] = 0u;
+        __syncthreads();
+        const unsigned long long mi = b0 + threadIdx.x;
+        const unsigned c = mi < M ? b.cnt[mi] : 0u;
+        const int bin = c ? nbk_class(b.cnt2[mi]) : -1;
+        unsigned r = 0;
+        if (bin >= 0) r = atomicAdd(cnt + bin, 1u);
+        __syncthreads();
+        for (int i = threadIdx.x; i < NBK_BINS; i += blockDim.x)
+            if (cnt[i]) base[i] = atomicAdd(b.cursor + i, cnt[i]);
+        __syncthreads();
+        if (bin >= 0) b.perm[base[bin] + r] = (unsigned)mi;
+        __syncthreads();
+    }
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < R;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = m.rec[i];
+        const unsigned mi = (unsigned)(k >> 32);
+        if (mi >= M) continue;
+        const unsigned pos = atomicAdd(b.off + mi, 1u);
+        b.val[pos] = (k << 32) | (m.recval ? (unsigned long long)m.recval[i] : 0ULL);
+    }
+}
+
+// a sorted slot: its value, and for a sample its end point next to it
+template <class Src>
+__device__ __forceinline__ void nbk_put(const DevMap &m, const Src &src, const NdtBuckets &b,
+                                        unsigned p, unsigned long long v) {
+    b.val[p] = v;
+    if (!(v >> 63)) return;
+    const unsigned oi = (unsigned)(v >> 32) & 0x7FFFFFFFu;
+    double e[3];
+    float it;
+    src.load_end((long long)(oi / (unsigned)m.maxseg), e, it);
+    b.pos[p] = make_double4(e[0], e[1], e[2], (double)it);
+}
+
+// Block roles: [0, nbig_blocks) the block sorts of k_nbk_sort_big, then
+// nmid_blocks of k_nbk_sort_mid's warp sorts, the rest k_nbk_sort_small's
+// thread sorts (and single-record buckets); every sorted slot is written
+// with nbk_put (k_nbk_gather's end points).
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_nbk_sort_gather(const __grid_constant__ DevMap m, Src src,
+                                                           NdtBuckets b, int nbig_blocks,
+                                                           int nmid_blocks) {
+    __shared__ union {
+        unsigned long long mid[NBK_MID_WARPS][NBK_WARP_MAX];
+        struct {
+            unsigned long long sv[NBK_SMEM];
+            unsigned wsum[BLOCK];
+        } big;
+    } sh;
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    const int bid = (int)blockIdx.x;
+    if (bid < nbig_blocks) {
+        unsigned long long *sv = sh.big.sv;
+        unsigned *wsum = sh.big.wsum;
+        const unsigned long long nb = *((volatile unsigned long long *)b.nbig);
+        unsigned *pres = b.bits + (size_t)bid * 2 * b.bwords;
+        unsigned *pref = pres + b.bwords;
+        for (unsigned long long w = bid; w < nb; w += nbig_blocks) {
+            const unsigned mi = (unsigned)b.big[w];
+            unsigned c;
+            const unsigned s = nbk_start(b, mi, c);
+            if (c <= (unsigned)NBK_SMEM) {
+                unsigned P = 32;
+                while (P < c) P <<= 1;
+                for (unsigned i = threadIdx.x; i < P; i += blockDim.x) sv[i] = i < c ? b.val[s + i] : ~0ULL;
+                __syncthreads();
+                for (unsigned k = 2; k <= P; k <<= 1) {
+                    for (unsigned j = k >> 1; j > 0; j >>= 1) {
+                        for (unsigned i = threadIdx.x; i < P; i += blockDim.x) {
+                            const unsigned p = i ^ j;
+                            if (p > i) {
+                                const unsigned long long x = sv[i], y = sv[p];
+                                if ((x > y) == ((i & k) == 0)) {
+                                    sv[i] = y;
+                                    sv[p] = x;
+                                }
+                            }
+                        }
+                        __syncthreads();
+                    }
+                }
+                for (unsigned i = threadIdx.x; i < c; i += blockDim.x) nbk_put(m, src, b, s + i, sv[i]);
+                __syncthreads();
+                continue;
+            }
+            for (unsigned long long i = threadIdx.x; i < b.bwords; i += blockDim.x) pres[i] = 0u;
+            __syncthreads();
+            for (unsigned i = threadIdx.x; i < c; i += blockDim.x) {
+                const unsigned sk = (unsigned)(b.val[s + i] >> 32);
+                const unsigned long long bit = (unsigned long long)(sk >> 31) * b.span + (sk & 0x7FFFFFFFu);
+                atomicOr(pres + (bit >> 5), 1u << (bit & 31));
+            }
+            __syncthreads();
+            const unsigned long long per = (b.bwords + blockDim.x - 1) / blockDim.x;
+            const unsigned long long w0 = per * threadIdx.x, w1 = min(b.bwords, w0 + per);
+            unsigned loc = 0;
+            for (unsigned long long i = w0; i < w1; ++i) loc += __popc(pres[i]);
+            wsum[threadIdx.x] = loc;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned run = 0;
+                for (int t = 0; t < (int)blockDim.x; ++t) {
+                    const unsigned v = wsum[t];
+                    wsum[t] = run;
+                    run += v;
+                }
+            }
+            __syncthreads();
+            unsigned run = wsum[threadIdx.x];
+            for (unsigned long long i = w0; i < w1; ++i) {
+                pref[i] = run;
+                run += __popc(pres[i]);
+            }
+            __syncthreads();
+            for (unsigned i = threadIdx.x; i < c; i += blockDim.x) {
+                const unsigned long long v = b.val[s + i];
+                const unsigned sk = (unsigned)(v >> 32);
+                const unsigned long long bit = (unsigned long long)(sk >> 31) * b.span + (sk & 0x7FFFFFFFu);
+                const unsigned rank = pref[bit >> 5] + __popc(pres[bit >> 5] & ((1u << (bit & 31)) - 1u));
+                b.tmp[s + rank] = v;
+            }
+            __syncthreads();
+            for (unsigned i = threadIdx.x; i < c; i += blockDim.x) nbk_put(m, src, b, s + i, b.tmp[s + i]);
+            __syncthreads();
+        }
+        return;
+    }
+    if (bid < nbig_blocks + nmid_blocks) {
+        const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+        unsigned long long *my = sh.mid[wi];
+        const unsigned long long nm = *((volatile unsigned long long *)b.nmid);
+        for (unsigned long long w = (unsigned long long)(bid - nbig_blocks) * NBK_MID_WARPS + wi; w < nm;
+             w += (unsigned long long)nmid_blocks * NBK_MID_WARPS) {
+            const unsigned mi = (unsigned)b.mid[w];
+            unsigned c;
+            const unsigned s = nbk_start(b, mi, c);
+            for (unsigned i = lane; i < c; i += 32) my[i] = b.val[s + i];
+            __syncwarp();
+            for (unsigned i = lane; i < c; i += 32) {
+                const unsigned long long x = my[i];
+                unsigned rank = 0;
+                for (unsigned j = 0; j < c; ++j) rank += my[j] < x ? 1u : 0u;
+                nbk_put(m, src, b, s + rank, x);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+    const unsigned K = *((volatile unsigned *)(b.cursor + NBK_BINS));
+    const unsigned nsmall = (gridDim.x - (unsigned)(nbig_blocks + nmid_blocks)) * blockDim.x;
+    for (unsigned t = (unsigned)(bid - nbig_blocks - nmid_blocks) * blockDim.x + threadIdx.x; t < K;
+         t += nsmall) {
+        unsigned c;
+        const unsigned s = nbk_start(b, b.perm[t], c);
+        if (c > (unsigned)NBK_SERIAL) continue;
+        if (c == 1) {
+            nbk_put(m, src, b, s, b.val[s]);
+            continue;
+        }
+        unsigned long long r[NBK_SERIAL];
+#pragma unroll
+        for (int i = 0; i < NBK_SERIAL; ++i) r[i] = (unsigned)i < c ? b.val[s + i] : ~0ULL;
+#pragma unroll
+        for (int k = 2; k <= NBK_SERIAL; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+                for (int i = 0; i < NBK_SERIAL; ++i)
+                    if ((i ^ j) > i) cswap(r[i], r[i ^ j], (i & k) == 0);
+#pragma unroll
+        for (int i = 0; i < NBK_SERIAL; ++i)
+            if ((unsigned)i < c) nbk_put(m, src, b, s + i, r[i]);
+    }
+}
+
 #ifndef NBK_FOLD_MINB
 #define NBK_FOLD_MINB 2
 #endif

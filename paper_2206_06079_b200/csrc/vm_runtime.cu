@@ -660,10 +660,21 @@ int launch_ndt_prep(vm_map *m, const DevMap &dm, const Src &src, long long n, in
                  m->d_nbk_small + NBK_BINS, m->d_rec2, m->d_rec, m->d_nbk_pos, m->d_bk_big,
                  m->d_bk_big2, m->d_nbk_ctr, m->d_nbk_ctr + 1, m->d_bk_bits, bwords, span};
     CK(cudaMemsetAsync(m->d_nbk_ctr, 0, 2 * sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(b.cursor + NBK_BINS, 0, 2 * sizeof(unsigned), s));
+    CK(cudaMemsetAsync(b.cursor + NBK_BINS, 0, 3 * sizeof(unsigned), s));
     const unsigned gr = (unsigned)m->num_sms * 8;
     const unsigned gm = (unsigned)std::max<long long>(
         1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
+    static const bool split = std::getenv("VOXMAP_B200_NBK_SPLIT") != nullptr;  // A/B knob
+    if (!split) {
+        // four launches (vm_ndt.cuh: fused bucket preparation)
+        k_nbk_weigh_count<<<gr, BLOCK, 0, s>>>(dm, src, b);
+        k_nbk_alloc_order<<<gm, BLOCK, 0, s>>>(dm, b);
+        k_nbk_perm_scatter<<<gr, BLOCK, 0, s>>>(dm, b);
+        k_nbk_sort_gather<<<gr, BLOCK, 0, s>>>(dm, src, b, m->num_sms, m->num_sms * 4);
+        m->launches += 4;
+        *out = b;
+        return check_launch("ndt buckets");
+    }
     k_ndt_weigh<<<gr, BLOCK, 0, s>>>(dm, src);
     k_nbk_count<<<gr, BLOCK, 0, s>>>(dm, b);
     k_nbk_alloc<<<gm, BLOCK, 0, s>>>(dm, b);
