@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(BLOCK) k_bk_count(const __grid_constant__ DevM
 
 // Each bucket's slice: one atomic per warp on a slice cursor (the slices need
 // not follow the sample-voxel order, so no scan)
-__global__ void __launch_bounds__(BLOCK) k_bk_alloc(const __grid_constant__ DevMap m, BucketState b) {
+__global__ void __launch_bounds__(BLOCK) k_bk_alloc(const __grid_constant__ DevMap m, BucketState b,
+                                                    bool classify) {
     unsigned long long R, M;
     if (!bk_live(m, R, M)) return;
     const int lane = threadIdx.x & 31;
@@ -97,6 +98,11 @@ __global__ void __launch_bounds__(BLOCK) k_bk_alloc(const __grid_constant__ DevM
         if (lane == 31 && tot) wb = atomicAdd(b.cursor, tot);
         wb = __shfl_sync(0xffffffffu, wb, 31);
         if (mi < M) b.off[mi] = wb + incl - c;
+        // classify: the fused fold (k_bk_fold_all) reads the warp / block lists
+        if (classify && c > (unsigned)BK_SERIAL) {
+            if (c <= (unsigned)BK_WARP) b.mid[atomicAdd(b.nmid, 1ULL)] = (int)mi;
+            else b.big[atomicAdd(b.nbig, 1ULL)] = (int)mi;
+        }
     }
 }
 
@@ -258,16 +264,13 @@ __device__ __forceinline__ void vf_warp_chunk(const DevMap &m, const Src &src, V
 // shared-memory window (warp-synchronous), then the chunked fold -- no block
 // barrier, so every warp of the block folds its own bucket.
 template <class Src>
-__global__ void __launch_bounds__(BLOCK) k_bk_fold_mid(const __grid_constant__ DevMap m, Src src,
-                                                       BucketState b) {
-    __shared__ unsigned sv[BLOCK / 32][BK_WARP];
-    unsigned long long R, M;
-    if (!bk_live(m, R, M)) return;
+__device__ __forceinline__ void bk_fold_mid_body(const DevMap &m, const Src &src, const BucketState &b,
+                                                 unsigned (*sv)[BK_WARP], unsigned bid, unsigned nblk) {
     const unsigned long long nm = *((volatile unsigned long long *)b.nmid);
     const int lane = threadIdx.x & 31;
     unsigned *const w = sv[threadIdx.x >> 5];
-    const unsigned long long nw = (unsigned long long)gridDim.x * (BLOCK / 32);
-    for (unsigned long long t = (unsigned long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+    const unsigned long long nw = (unsigned long long)nblk * (BLOCK / 32);
+    for (unsigned long long t = (unsigned long long)bid * (BLOCK / 32) + (threadIdx.x >> 5);
          t < nm; t += nw) {
         const unsigned long long mi = (unsigned long long)b.mid[t];
         unsigned c;
@@ -305,18 +308,24 @@ __global__ void __launch_bounds__(BLOCK) k_bk_fold_mid(const __grid_constant__ D
     }
 }
 
-// One block per large bucket.
 template <class Src>
-__global__ void __launch_bounds__(BLOCK) k_bk_fold_big(const __grid_constant__ DevMap m, Src src,
+__global__ void __launch_bounds__(BLOCK) k_bk_fold_mid(const __grid_constant__ DevMap m, Src src,
                                                        BucketState b) {
-    __shared__ unsigned sv[BK_SMEM];
+    __shared__ unsigned sv[BLOCK / 32][BK_WARP];
     unsigned long long R, M;
     if (!bk_live(m, R, M)) return;
+    bk_fold_mid_body(m, src, b, sv, blockIdx.x, gridDim.x);
+}
+
+// One block per large bucket.
+template <class Src>
+__device__ __forceinline__ void bk_fold_big_body(const DevMap &m, const Src &src, const BucketState &b,
+                                                 unsigned *sv, unsigned bid, unsigned nblk) {
     const unsigned long long nb = *((volatile unsigned long long *)b.nbig);
     const int lane = threadIdx.x & 31;
-    unsigned *pres = b.bits + (size_t)blockIdx.x * 2 * b.bwords;
+    unsigned *pres = b.bits + (size_t)bid * 2 * b.bwords;
     unsigned *hitb = pres + b.bwords;
-    for (unsigned long long w = blockIdx.x; w < nb; w += gridDim.x) {
+    for (unsigned long long w = bid; w < nb; w += nblk) {
         const unsigned long long mi = (unsigned long long)b.big[w];
         unsigned c;
         const unsigned s = bk_slice(b, mi, c);
@@ -410,6 +419,68 @@ __global__ void __launch_bounds__(BLOCK) k_bk_fold_big(const __grid_constant__ D
             }
             __syncthreads();
         }
+    }
+}
+
+template <class Src>
+__global__ void __launch_bounds__(BLOCK) k_bk_fold_big(const __grid_constant__ DevMap m, Src src,
+                                                       BucketState b) {
+    __shared__ unsigned sv[BK_SMEM];
+    unsigned long long R, M;
+    if (!bk_live(m, R, M)) return;
+    bk_fold_big_body(m, src, b, sv, blockIdx.x, gridDim.x);
+}
+
+// The three folds in one launch, by block roles: [0, nbig_blocks) the block
+// buckets, then nmid_blocks of warp buckets, the rest one thread per small
+// bucket (k_bk_alloc classified them with classify = true).  A bucket's
+// fold does not depend on another's, so the long serial chains of the
+// largest buckets (dispatched first) run beside the rest instead of after it.
+template <class Src>
+__global__ void __launch_bounds__(BLOCK, 4) k_bk_fold_all(const __grid_constant__ DevMap m, Src src,
+                                                          BucketState b, int nbig_blocks,
+                                                          int nmid_blocks) {
+    __shared__ union {
+        unsigned mid[BLOCK / 32][BK_WARP];
+        unsigned big[BK_SMEM];
+    } sh;
+    unsigned long long R, M;
+    if (!bk_live(m, R, M)) return;
+    const int bid = (int)blockIdx.x;
+    if (bid < nbig_blocks) {
+        bk_fold_big_body(m, src, b, sh.big, (unsigned)bid, (unsigned)nbig_blocks);
+        return;
+    }
+    if (bid < nbig_blocks + nmid_blocks) {
+        bk_fold_mid_body(m, src, b, sh.mid, (unsigned)(bid - nbig_blocks), (unsigned)nmid_blocks);
+        return;
+    }
+    const unsigned long long nsmall =
+        (unsigned long long)(gridDim.x - (unsigned)(nbig_blocks + nmid_blocks)) * blockDim.x;
+    for (unsigned long long mi = (unsigned long long)(bid - nbig_blocks - nmid_blocks) * blockDim.x +
+                                 threadIdx.x;
+         mi < M; mi += nsmall) {
+        unsigned c;
+        const unsigned s = bk_slice(b, mi, c);
+        if (c == 0u || c > (unsigned)BK_SERIAL) continue;
+        b.cnt[mi] = 0u;
+        unsigned v[BK_SERIAL];
+        for (unsigned i = 0; i < c; ++i) {
+            const unsigned x = b.val[s + i];
+            int j = (int)i - 1;
+            while (j >= 0 && v[j] > x) {
+                v[j + 1] = v[j];
+                --j;
+            }
+            v[j + 1] = x;
+        }
+        VoxFold f;
+        vf_begin(m, f, marked_vid(m, mi));
+        for (unsigned i = 0; i < c; ++i) {
+            if (v[i] & 1u) vf_hit(m, src, f, v[i] >> 1);
+            else ++f.misses;
+        }
+        vf_end(m, f);
     }
 }
 

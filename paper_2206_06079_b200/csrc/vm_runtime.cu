@@ -624,10 +624,18 @@ int launch_bucket_fold(vm_map *m, const DevMap &dm, const Src &src, long long n,
     const unsigned g = (unsigned)m->num_sms * 8;
     const unsigned ga = (unsigned)std::max<long long>(
         1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
+    static const bool split = std::getenv("VOXMAP_B200_BK_SPLIT") != nullptr;  // A/B knob
     k_bk_count<<<g, BLOCK, 0, s>>>(dm, b);
-    k_bk_alloc<<<ga, BLOCK, 0, s>>>(dm, b);
+    k_bk_alloc<<<ga, BLOCK, 0, s>>>(dm, b, !split);
     k_bk_scatter<<<g, BLOCK, 0, s>>>(dm, b);
     CK(cudaEventRecord(ev_mid, s));
+    if (!split) {
+        // one fold launch, block roles by bucket size (vm_bucket.cuh: k_bk_fold_all)
+        const int nbig = m->num_sms * BK_BIG_BPS, nmid = m->num_sms * 4;
+        k_bk_fold_all<<<(unsigned)(nbig + nmid + m->num_sms * 8), BLOCK, 0, s>>>(dm, src, b, nbig, nmid);
+        m->launches += 4;
+        return check_launch("bucket fold");
+    }
     const unsigned gf = (unsigned)std::max<long long>(
         1, std::min<long long>((long long)m->num_sms * 8, ((long long)m->smarked_cap + BLOCK - 1) / BLOCK));
     k_bk_fold<<<gf, BLOCK, 0, s>>>(dm, src, b);
