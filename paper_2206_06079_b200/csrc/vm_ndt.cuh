@@ -1012,6 +1012,253 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
     }
 }
 
+// ---- the same fold with the Givens rotations pipelined over three lanes ----
+// ndt_update's serial chain is three rotations per sample (cholupdate3), but
+// rotation k only reads column k of the factor and the rotated vector left by
+// rotation k - 1 of the SAME sample.  So three lanes hold one bucket: lane
+// k of the triple owns column k (diagonal Ld, entries below it La, Lb) and
+// applies rotation k to sample t - k in step t, taking the vector from lane
+// k - 1 (one shuffle per step).  Every lane's loop-carried chain is then one
+// rotation (scale, hypot, divisions, rescale) instead of three: the same
+// operations in the same order per value, so the factor is bit-identical to
+// ndt_update's.  Lane 0 of a triple also carries the mean (Welford), the
+// occupancy hit and the TM intensity, like the one-lane fold.  Ten buckets
+// per warp (lanes 30, 31 idle); phase 1 runs on all three lanes alike.
+constexpr int NBK3_PER_WARP = 10;
+
+// rotation of column (Ld; La, Lb) by the vector (xd; xa, xb) after the
+// count's scale sq, then the rescale by sn (ndt_update / givens_k, one column)
+__device__ __forceinline__ void ndt_rot_column(double &Ld, double &La, double &Lb, double xd,
+                                               double &xa, double &xb, double sq, double sn) {
+    Ld = Ld * sq;
+    La = La * sq;
+    Lb = Lb * sq;
+    const double r = py_hypot(Ld, xd);
+    if (r != 0.0) {
+        const double c = Ld / r, s = xd / r;
+        Ld = r;
+        const double la = La, lb = Lb;
+        La = c * la + s * xa;
+        xa = c * xa - s * la;
+        Lb = c * lb + s * xb;
+        xb = c * xb - s * lb;
+    }
+    Ld = Ld / sn;
+    La = La / sn;
+    Lb = Lb / sn;
+}
+
+template <bool TM>
+__global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid_constant__ DevMap m,
+                                                                    NdtBuckets b) {
+    unsigned long long R, M;
+    if (!bk_ndt_live(m, R, M)) return;
+    const unsigned K = *((volatile unsigned *)(b.cursor + NBK_BINS));
+    const int lane = threadIdx.x & 31;
+    const int k = lane % 3;                   // the column this lane rotates
+    const int tri = lane / 3;                 // the bucket of the warp (10 = idle)
+    const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+    for (unsigned w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * NBK3_PER_WARP < K;
+         w += nwarps) {
+        const unsigned t = w * NBK3_PER_WARP + tri;
+        bool act = tri < NBK3_PER_WARP && t < K;
+        unsigned c = 0, ns = 0, s = 0, mi = 0;
+        int slot = 0, li = 0;
+        if (act) {
+            mi = b.perm[t];
+            s = nbk_start(b, mi, c);
+            ns = b.cnt2[mi];
+            const int2 sl = m.marked[mi];
+            slot = sl.x;
+            li = sl.y;
+            act = slot >= 0;
+        }
+        __syncwarp();
+        if (k == 0 && tri < NBK3_PER_WARP && t < K) {
+            b.cnt[mi] = 0u;
+            b.cnt2[mi] = 0u;
+        }
+        if (!act) c = ns = 0;
+        const unsigned long long *__restrict__ v = b.val + s;
+        const unsigned np1 = c - ns;  // phase-1 records sort first
+        float *occ = nullptr, *cov = nullptr, *ib = nullptr;
+        unsigned *mb = nullptr, *cb = nullptr, *hb = nullptr, *missb = nullptr;
+        int g[3] = {0, 0, 0};
+        float l = 0.0f;
+        unsigned n0 = 0;
+        if (act) {
+            slot_li_to_g(m, slot, li, g);
+            occ = layer_at<float>(m, L_OCC, slot);
+            mb = layer_at<unsigned>(m, L_MEAN, slot);
+            cb = layer_at<unsigned>(m, L_COUNT, slot);
+            cov = layer_at<float>(m, L_COV, slot);
+            if (TM) {
+                ib = layer_at<float>(m, L_INTENS, slot);
+                hb = layer_at<unsigned>(m, L_HIT, slot);
+                missb = layer_at<unsigned>(m, L_MISS, slot);
+            }
+            l = occ[li];
+            n0 = cb[li];
+        }
+        const bool writer = act && k == 0;
+        // ---- phase 1 (k_nbk_fold's loop; the three lanes of a bucket alike) ----
+        bool reset = false;
+        unsigned miss_add = 0;
+        const unsigned mp1 = __reduce_max_sync(0xffffffffu, np1);
+        unsigned wv[NBK_PF];
+#pragma unroll
+        for (int q = 0; q < NBK_PF; ++q) wv[q] = (unsigned)q < np1 ? (unsigned)__ldg(v + q) : 0u;
+        for (unsigned i0 = 0; i0 < mp1; i0 += NBK_PF) {
+            if (i0 + NBK_PF_L1 < np1 && k == 0)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(v + i0 + NBK_PF_L1));
+            unsigned nx[NBK_PF];
+#pragma unroll
+            for (int q = 0; q < NBK_PF; ++q)
+                nx[q] = i0 + NBK_PF + q < np1 ? (unsigned)__ldg(v + i0 + NBK_PF + q) : 0u;
+#pragma unroll
+            for (int q = 0; q < NBK_PF; ++q) {
+                if (i0 + q < np1) {
+                    const float d = reset ? m.miss32 : -__uint_as_float(wv[q] & 0x7FFFFFFFu);
+                    l = clamp_add(l, d, m.cmin, m.cmax);
+                    if (TM && (reset || (wv[q] >> 31))) ++miss_add;
+                    if (!reset && l < m.fthresh && n0 > 0) {
+                        reset = true;
+                        miss_add = 0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NBK_PF; ++q) wv[q] = nx[q];
+        }
+        if (reset) {
+            n0 = 0;
+            if (writer) {
+                cb[li] = 0;
+                mb[li] = 0;
+#pragma unroll
+                for (int q = 0; q < 6; ++q) cov[li * 6 + q] = 0.0f;
+                if (TM) {
+                    hb[li] = 0;
+                    missb[li] = 0;
+                    ib[li * 2] = 0.0f;
+                    ib[li * 2 + 1] = 0.0f;
+                }
+            }
+        }
+        if (TM && writer && miss_add) missb[li] += miss_add;
+        // ---- phase 2: lane k applies rotation k to sample (step - k) ----
+        // column k of the lower triangle (l00, l10, l11, l20, l21, l22)
+        const int cd = k == 0 ? 0 : (k == 1 ? 2 : 5);
+        const int ca = k == 0 ? 1 : 4, cbi = 3;
+        double Ld = 0.0, La = 0.0, Lb = 0.0;
+        double mu[3] = {0.0, 0.0, 0.0};
+        double imean = 0.0, im2 = 0.0;
+        if (ns) {
+            if (!reset) {  // a reset zeroed the stored factor (and n0)
+                Ld = (double)cov[li * 6 + cd];
+                if (k < 2) La = (double)cov[li * 6 + ca];
+                if (k == 0) Lb = (double)cov[li * 6 + cbi];
+            }
+            if (k == 0 && n0 > 0) {
+                double off[3];
+                unpack_mean(mb[li], off);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) mu[a] = ((double)g[a] + off[a]) * m.vox;
+            }
+            if (TM && k == 0) {
+                imean = ib[li * 2];
+                im2 = ib[li * 2 + 1];
+            }
+        }
+        const double4 *__restrict__ ps = b.pos + s + np1;
+        const unsigned ms = __reduce_max_sync(0xffffffffu, ns);
+        double oa = 0.0, ob = 0.0;  // this lane's rotated vector entries, for lane k + 1
+        // lane 0: the next sample's end point is loaded a step ahead of its use
+        double4 curp = (k == 0 && ns) ? ld_d4(ps) : make_double4(0.0, 0.0, 0.0, 0.0);
+        for (unsigned step = 0; step < ms + 2; ++step) {
+            const double ind = __shfl_up_sync(0xffffffffu, oa, 1);
+            const double ina = __shfl_up_sync(0xffffffffu, ob, 1);
+            const unsigned j = step - (unsigned)k;  // this lane's sample (wraps when step < k)
+            if (j < ns) {
+                const unsigned long long nj = (unsigned long long)n0 + j;
+                double xd, xa, xb;
+                if (k == 0) {
+                    const double4 cur = curp;
+                    if (j + 1 < ns) curp = ld_d4(ps + j + 1);
+                    l = clamp_add(l, m.hit32, m.cmin, m.cmax);
+                    if (TM) {
+                        const double val = cur.w, nn = (double)(nj + 1);
+                        const double d = val - imean;
+                        const double mnew = imean + d / nn;
+                        const double m2new = im2 + d * (val - mnew);
+                        imean = (double)(float)mnew;
+                        im2 = (double)(float)m2new;
+                    }
+                    const double e[3] = {cur.x, cur.y, cur.z};
+                    if (nj == 0) {
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) mu[a] = e[a];
+                        xd = xa = xb = 0.0;
+                    } else {
+                        const double dnn = (double)(nj + 1);
+                        double d[3];
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) d[a] = e[a] - mu[a];
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) mu[a] = mu[a] + d[a] / dnn;
+                        const double f = sqrt((double)nj / dnn);
+                        xd = d[0] * f;
+                        xa = d[1] * f;
+                        xb = d[2] * f;
+                    }
+                } else {
+                    xd = ind;
+                    xa = ina;
+                    xb = 0.0;
+                }
+                if (nj == 0) {
+                    // ndt_update's first sample: the factor is zero
+                    Ld = La = Lb = 0.0;
+                } else {
+                    ndt_rot_column(Ld, La, Lb, xd, xa, xb, sqrt((double)nj), sqrt((double)(nj + 1)));
+                }
+                oa = xa;
+                ob = xb;
+            }
+        }
+        const unsigned long long n = (unsigned long long)n0 + ns;
+        if (ns && act) {
+            cov[li * 6 + cd] = (float)Ld;
+            if (k < 2) cov[li * 6 + ca] = (float)La;
+            if (k == 0) cov[li * 6 + cbi] = (float)Lb;
+        }
+        if (ns && writer) {
+            if (TM) {
+                ib[li * 2] = (float)imean;
+                ib[li * 2 + 1] = (float)im2;
+                hb[li] += ns;
+            }
+            cb[li] = n > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned)n;
+            if (n >= 3 && m.gmask)
+                atomicOr(m.gmask + slot, m.brick_shift >= 0 ? 1u << brick_of(li, m.bsh) : 0xFFFFFFFFu);
+            double frac[3];
+            const double hi = 1.0 - 1.0 / 2048.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                double f = mu[a] / m.vox - (double)g[a];
+                if (f < 0.0) f = 0.0;
+                if (f > hi) f = hi;
+                frac[a] = f;
+            }
+            mb[li] = pack_mean(frac);
+        }
+        if (writer) {
+            occ[li] = l;
+            layer_at<unsigned>(m, m.nidx, slot)[li] = 0u;
+        }
+    }
+}
+
 // Deterministic TSDF (reference.py:153-175): one thread per voxel bucket
 // merges the voxel's band visits in ray order; clears the index stamp and
 // the bucket count.

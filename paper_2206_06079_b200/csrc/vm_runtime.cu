@@ -720,8 +720,19 @@ int launch_ndt_fold_only(vm_map *m, const DevMap &dm, const NdtBuckets &b, bool 
         cudaMemcpyToSymbolAsync(g_fold_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
     }
 #endif
-    if (tm) k_nbk_fold<true><<<gm, BLOCK, 0, s>>>(dm, b);
-    else k_nbk_fold<false><<<gm, BLOCK, 0, s>>>(dm, b);
+    static const bool fold1 = std::getenv("VOXMAP_B200_FOLD1") != nullptr;  // A/B knob
+    if (fold1) {
+        if (tm) k_nbk_fold<true><<<gm, BLOCK, 0, s>>>(dm, b);
+        else k_nbk_fold<false><<<gm, BLOCK, 0, s>>>(dm, b);
+    } else {
+        // three lanes per bucket, the rotations pipelined (vm_ndt.cuh: k_nbk_fold3)
+        const unsigned g3 = (unsigned)std::max<long long>(
+            1, std::min<long long>((long long)m->num_sms * 8,
+                                   ((long long)m->smarked_cap + NBK3_PER_WARP * (BLOCK / 32) - 1) /
+                                       (NBK3_PER_WARP * (BLOCK / 32))));
+        if (tm) k_nbk_fold3<true><<<g3, BLOCK, 0, s>>>(dm, b);
+        else k_nbk_fold3<false><<<g3, BLOCK, 0, s>>>(dm, b);
+    }
 #ifdef VM_FOLD_PROF
     {
         unsigned long long h[2];
@@ -2970,6 +2981,9 @@ int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, i
                            m->stream));
         CK(cudaMemcpyAsync((int *)(m->h_stats + NUM_STATS) + 1, m->d_go, sizeof(int),
                            cudaMemcpyDeviceToHost, m->stream));
+        // the slice's new sample voxels, read with the guard's verdict (one sync)
+        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_shard_cnt, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, m->stream));
         CK(cudaStreamSynchronize(m->stream));
         const int cursor = *(const int *)(m->h_stats + NUM_STATS);
         const int go = *((const int *)(m->h_stats + NUM_STATS) + 1);
@@ -2987,15 +3001,10 @@ int vm_shard_begin(vm_map *m, const vm_rays *rays, int32_t mode, int32_t exec, i
         m->nreg = cursor;
         break;
     }
-    CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_shard_cnt, sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, m->stream));
-    CK(cudaStreamSynchronize(m->stream));
     if (sb.ndt) {
-        // requests: every ghost region of the slice's prefetch set (touched list)
-        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_stats + S_WALK_TOUCHED,
-                           sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
-        CK(cudaStreamSynchronize(m->stream));
-        counts_out[0] = (int64_t)m->h_stats[NUM_STATS + 2];
+        // requests: every ghost region of the slice's prefetch set (touched
+        // list; its length came back with the guard's stats)
+        counts_out[0] = (int64_t)m->h_stats[S_WALK_TOUCHED];
         counts_out[1] = 0;
         sb.nmarks = 0;
         sb.open = true;
@@ -3158,6 +3167,9 @@ int vm_shard_export(vm_map *m, void *out, int64_t cap_per_dest, int64_t *per_des
     const int W = m->shard_world;
     CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_stats + S_RECORDS, sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, m->stream));
+    if (m->sb.ndt)  // the ghost-visit count, in the same round trip
+        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 3, m->d_ngx, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
     const unsigned long long R = m->h_stats[NUM_STATS + 2];
     if (R > m->rec_cap) return fail(VM_ERR_OOM, "record buffer overflow in a sharded batch");
@@ -3166,8 +3178,7 @@ int vm_shard_export(vm_map *m, void *out, int64_t cap_per_dest, int64_t *per_des
     CK(cudaMemsetAsync(m->d_shard_cnt + 2, 0, (size_t)W * sizeof(unsigned long long), m->stream));
     const unsigned long long cap = (unsigned long long)std::max<int64_t>(cap_per_dest, 0);
     if (m->sb.ndt) {
-        unsigned long long ng = 0;
-        CK(cudaMemcpy(&ng, m->d_ngx, sizeof(ng), cudaMemcpyDeviceToHost));
+        const unsigned long long ng = m->h_stats[NUM_STATS + 3];
         if (ng > m->gx_cap) return fail(VM_ERR_OOM, "ghost visit buffer overflow in a sharded batch");
         k_shard_ndt_export<<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm, R, (ShardItemN *)out,
                                                                     m->d_shard_cnt + 2, cap);
@@ -3226,10 +3237,7 @@ int vm_shard_import(vm_map *m, const void *in, int64_t n) {
         m->launches += 2;
         if ((rc = check_launch("shard import"))) return rc;
     }
-    int cursor;
-    if ((rc = read_cursor(m, &cursor))) return rc;
-    m->nreg = cursor;
-    return VM_OK;
+    return VM_OK;  // vm_shard_finish reads the region cursor
 }
 
 int vm_shard_finish(vm_map *m, vm_stats *out) {
@@ -3237,12 +3245,17 @@ int vm_shard_finish(vm_map *m, vm_stats *out) {
     CK(cudaSetDevice(m->device));
     auto &sb = m->sb;
     int rc;
-    int cursor;
-    if ((rc = read_cursor(m, &cursor))) return rc;
-    m->nreg = cursor;
+    // region cursor, stats and (NDT) the voxel-index count in one round trip
+    CK(cudaMemcpyAsync(m->h_stats + NUM_STATS, m->d_cursor, sizeof(int), cudaMemcpyDeviceToHost,
+                       m->stream));
     CK(cudaMemcpyAsync(m->h_stats, m->d_stats, NUM_STATS * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, m->stream));
+    if (sb.ndt)
+        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_shard_cnt, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
+    const int cursor = *(const int *)(m->h_stats + NUM_STATS);
+    m->nreg = cursor;
     const unsigned long long Rtot = std::min<unsigned long long>(m->h_stats[S_RECORDS], m->rec_cap);
     if (m->h_stats[S_RECORDS] > m->rec_cap) return fail(VM_ERR_OOM, "record buffer overflow on import");
     if (sb.ndt) {
@@ -3252,9 +3265,6 @@ int vm_shard_finish(vm_map *m, vm_stats *out) {
         CK(cudaEventRecord(m->ev_k1, m->stream));
         k_resolve<true, false><<<m->num_sms * 8, BLOCK, 0, m->stream>>>(dm);
         CK(cudaEventRecord(m->ev_res, m->stream));
-        CK(cudaMemcpyAsync(m->h_stats + NUM_STATS + 2, m->d_shard_cnt, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, m->stream));
-        CK(cudaStreamSynchronize(m->stream));
         if (m->h_stats[NUM_STATS + 2] > m->smarked_cap)
             return fail(VM_ERR_OOM, "voxel index overflow in a sharded NDT batch");
         rc = with_src(m, [&](auto src) {
