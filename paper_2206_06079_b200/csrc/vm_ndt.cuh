@@ -91,13 +91,52 @@ __device__ __forceinline__ double py_vector_norm2(double x0, double x1, double m
     return outer == 1.0 ? hs : outer * hs;
 }
 
-__device__ __forceinline__ double py_hypot(double a, double b) {
+__device__ __noinline__ double py_hypot_slow(double a, double b) {
     if (isnan(a) || isnan(b)) return __longlong_as_double(0x7ff8000000000000LL);
     const double x0 = fabs(a), x1 = fabs(b);
     double mx = 0.0;
     if (x0 > mx) mx = x0;
     if (x1 > mx) mx = x1;
     return py_vector_norm2(x0, x1, mx);
+}
+
+// py_vector_norm2's arithmetic for the common case -- max(|a|, |b|) a normal
+// double below 2**1022, no NaN -- with frexp / ldexp as exponent-field
+// arithmetic (exact: the scale factors are powers of two), straight-line
+// code on the fold's serial chain.  Zero, subnormal, huge, infinite and NaN
+// operands take the general routine.
+__device__ __forceinline__ double py_hypot(double a, double b) {
+    const double x0 = fabs(a), x1 = fabs(b);
+    const double mx = x0 > x1 ? x0 : x1;
+    const int ex = (int)(__double_as_longlong(mx) >> 52);  // biased exponent (mx >= 0)
+    if (isnan(a) || isnan(b) || ex < 1 || ex > 2044) return py_hypot_slow(a, b);
+    // frexp: mx = f * 2**max_e, f in [0.5, 1), max_e = ex - 1022
+    const double scale = __longlong_as_double((long long)(2045 - ex) << 52);   // 2**-max_e
+    const double unscale = __longlong_as_double((long long)(ex + 1) << 52);    // 2**max_e
+    double csum = 1.0, frac1 = 0.0, frac2 = 0.0;
+    const double v[2] = {x0, x1};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double x = v[i] * scale;
+        const double hi = x * x, lo = fma(x, x, -hi);
+        const double s = csum + hi;
+        const double sl = (csum - s) + hi;
+        csum = s;
+        frac1 += lo;
+        frac2 += sl;
+    }
+    double h = sqrt(csum - 1.0 + (frac1 + frac2));
+    {
+        const double hi = -h * h, lo = fma(-h, h, -hi);
+        const double s = csum + hi;
+        const double sl = (csum - s) + hi;
+        csum = s;
+        frac1 += lo;
+        frac2 += sl;
+    }
+    const double x = csum - 1.0 + (frac1 + frac2);
+    h += x / (2.0 * h);
+    return h * unscale;
 }
 
 // vm_ndt_hypot: py_hypot over pairs (parity probe against CPython's results)
@@ -1060,6 +1099,9 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid
     const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
     for (unsigned w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * NBK3_PER_WARP < K;
          w += nwarps) {
+#ifdef VM_FOLD_PROF
+        const long long prof_t0 = clock64();
+#endif
         const unsigned t = w * NBK3_PER_WARP + tri;
         bool act = tri < NBK3_PER_WARP && t < K;
         unsigned c = 0, ns = 0, s = 0, mi = 0;
@@ -1256,6 +1298,14 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid
             occ[li] = l;
             layer_at<unsigned>(m, m.nidx, slot)[li] = 0u;
         }
+#ifdef VM_FOLD_PROF
+        if (lane == 0) {
+            const unsigned long long dt = (unsigned long long)(clock64() - prof_t0);
+            atomicMax(&g_fold_prof[0], (dt << 24) | ((unsigned long long)min(mp1, 4095u) << 12) |
+                                           min(ms, 4095u));
+            atomicAdd(&g_fold_prof[1], dt);
+        }
+#endif
     }
 }
 

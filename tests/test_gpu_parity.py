@@ -59,6 +59,20 @@ def test_ndt_hypot_matches_cpython_on_gpu():
     assert np.array_equal(_native.ndt_hypot(edge).view(np.uint64), want.view(np.uint64))
 
 
+def test_ndt_hypot_fast_path_matches_cpython_on_random_pairs():
+    """The straight-line common case of the fold's hypot (exponent-field
+    scaling instead of frexp / ldexp) on 200 k pairs of the magnitudes the
+    Cholesky factors and rotated deviations take (1e-9 .. 1e3, mixed signs,
+    a share of exact ties and zeros), bit for bit against math.hypot."""
+    import math
+    rng = np.random.default_rng(7)
+    ab = rng.standard_normal((200_000, 2)) * 10.0 ** rng.uniform(-9, 3, (200_000, 2))
+    ab[:500, 1] = ab[:500, 0]
+    ab[500:1000, 0] = 0.0
+    want = np.array([math.hypot(a, b) for a, b in ab])
+    assert np.array_equal(_native.ndt_hypot(ab).view(np.uint64), want.view(np.uint64))
+
+
 def test_hash_mix_matches_reference():
     for k in (0, 1, 12345, 2 ** 40 + 17, -1 % (2 ** 63)):
         assert _native.hash_mix(k) == orc.hash_mix(k)
