@@ -148,14 +148,38 @@ __device__ __forceinline__ void vf_begin(const DevMap &m, VoxFold &f, unsigned v
 
 // one hit with sample end point ep, after the misses counted so far
 // (reference.py:43-57)
+#ifndef BK_FAST
+#define BK_FAST 0  // 1: verified fast divisions in the hit step (measured slower, DESIGN)
+#endif
+template <bool FAST>
+__device__ __forceinline__ void vf_mean_hit(const DevMap &m, const int g[3], const double ep[3],
+                                            unsigned &packed, unsigned &count, bool &ok) {
+    const double off[3] = {vdiv<FAST>(ep[0], m.vox, ok) - (double)g[0],
+                           vdiv<FAST>(ep[1], m.vox, ok) - (double)g[1],
+                           vdiv<FAST>(ep[2], m.vox, ok) - (double)g[2]};
+    fold_mean_v<FAST>(packed, count, off, ok);
+}
+
+// The six divisions of a hit (the end point's voxel fraction, the running
+// mean) are independent; BK_FAST issues them as the verified branch-free
+// operators (vm_device.cuh: xdiv; a hit whose check fails is redone with
+// IEEE division).  Measured slower than IEEE division (C2@0.1 m fold 9.2 ->
+// 10.7 ms per step), so off.
 __device__ __forceinline__ void vf_hit_ep(const DevMap &m, VoxFold &f, const double ep[3]) {
     f.l = miss_k(f.l, f.misses, m.miss32, m.cmin, m.cmax);
     f.misses = 0;
     f.l = clamp_add(f.l, m.hit32, m.cmin, m.cmax);
     if (m.slab[L_MEAN]) {
-        const double off[3] = {ep[0] / m.vox - (double)f.g[0], ep[1] / m.vox - (double)f.g[1],
-                               ep[2] / m.vox - (double)f.g[2]};
-        fold_mean(f.packed, f.count, off);
+        bool ok = true;
+        if (BK_FAST) {
+            unsigned p2 = f.packed, c2 = f.count;
+            vf_mean_hit<true>(m, f.g, ep, p2, c2, ok);
+            if (ok) {
+                f.packed = p2;
+                f.count = c2;
+            }
+        }
+        if (!BK_FAST || !ok) vf_mean_hit<false>(m, f.g, ep, f.packed, f.count, ok);
     }
 }
 

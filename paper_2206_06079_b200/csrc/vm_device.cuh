@@ -210,6 +210,69 @@ __device__ __forceinline__ float miss_k(float l, unsigned k, float d, float cmin
     return l;
 }
 
+// ---- verified fast division / square root (the serial folds' steps) ----
+// IEEE `a / b` and `sqrt(x)` compile to an approximation, Newton steps and a
+// branch to a slow path that needs the result first, so a thread's
+// independent divisions run one after another.  These variants are
+// branch-free: the Newton result q is checked to be THE correctly rounded
+// value (the exact residual a - b*q, one FMA, is below half an ulp of q
+// times |b|; operands and result well inside the normal range), and `ok`
+// turns false otherwise -- the caller then redoes the step with the IEEE
+// operators, so the values are always the IEEE ones.
+__device__ __forceinline__ int xexp(double v) {
+    return (int)((unsigned long long)__double_as_longlong(v) >> 52) & 0x7FF;
+}
+__device__ __forceinline__ bool xmid(double v) {
+    const int e = xexp(v);
+    return e > 200 && e < 1800;
+}
+__device__ __forceinline__ double xpow2(int biased) { return __longlong_as_double((long long)biased << 52); }
+__device__ __forceinline__ double xrcp(double b) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+    double e = fma(-b, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-b, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double xdiv(double a, double b, bool &ok) {
+    const double y = xrcp(b);
+    double q = a * y;
+    q = fma(fma(-b, q, a), y, q);
+    const double r = fma(-b, q, a);
+    const double e = ((b < 0.0) != (q < 0.0)) ? -r : r;
+    const double hb = fabs(b) * xpow2(xexp(q) - 53);
+    const bool p2 = (__double_as_longlong(q) & 0xFFFFFFFFFFFFFLL) == 0;
+    const bool good = xmid(q) && xmid(a) && xmid(b) && e < hb && -e < (p2 ? 0.5 * hb : hb);
+    ok = ok && (good || (a == 0.0 && xmid(b)));
+    return a == 0.0 ? a * y : q;
+}
+__device__ __forceinline__ double xsqrt(double x, bool &ok) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = fma(y, fma(-hx * y, y, 0.5), y);
+    y = fma(y, fma(-hx * y, y, 0.5), y);
+    double s = x * y;
+    s = fma(fma(-s, s, x), 0.5 * y, s);
+    const double r = fma(-s, s, x);
+    const double su = s * xpow2(xexp(s) - 52);
+    const bool p2 = (__double_as_longlong(s) & 0xFFFFFFFFFFFFFLL) == 0;
+    const bool good = x > 0.0 && xmid(x) && xmid(s) && r <= su && -r < (p2 ? 0.5 * su : su);
+    ok = ok && (good || x == 0.0);
+    return x == 0.0 ? x : s;
+}
+// FAST: the verified operators (ok false = redo with IEEE); else IEEE
+template <bool FAST>
+__device__ __forceinline__ double vdiv(double a, double b, bool &ok) {
+    if (FAST) return xdiv(a, b, ok);
+    return a / b;
+}
+template <bool FAST>
+__device__ __forceinline__ double vsqrt(double x, bool &ok) {
+    if (FAST) return xsqrt(x, ok);
+    return sqrt(x);
+}
 // subvoxel.py:16-23
 __device__ __forceinline__ unsigned pack_mean(const double off[3]) {
     unsigned packed = 0;
@@ -227,6 +290,25 @@ __device__ __forceinline__ void unpack_mean(unsigned packed, double out[3]) {
     for (int a = 0; a < 3; ++a) out[a] = ((double)((packed >> (10 * a)) & 1023u) + 0.5) / 1024.0;
 }
 // subvoxel.py:34-49 (the oracle's `/ (count + 1)` form, not the native `* w`)
+// fold_mean with the division selectable (FAST: verified, `ok` false = redo)
+template <bool FAST>
+__device__ __forceinline__ void fold_mean_v(unsigned &packed, unsigned &count, const double s[3],
+                                            bool &ok) {
+    if (count >= 0xFFFFFFFFu) return;
+    if (count == 0) {
+        packed = pack_mean(s);
+        count = 1;
+        return;
+    }
+    double m[3];
+    unpack_mean(packed, m);
+    double div = (double)count + 1.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) m[a] = m[a] + vdiv<FAST>(s[a] - m[a], div, ok);
+    packed = pack_mean(m);
+    count += 1;
+}
+
 __device__ __forceinline__ void fold_mean(unsigned &packed, unsigned &count, const double s[3]) {
     if (count >= 0xFFFFFFFFu) return;
     if (count == 0) {

@@ -1051,6 +1051,47 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold(const __grid_
     }
 }
 
+// py_hypot's common case with the verified operators
+__device__ __forceinline__ double xhypot(double a, double b, bool &ok) {
+    const double x0 = fabs(a), x1 = fabs(b);
+    const double mx = x0 > x1 ? x0 : x1;
+    if (isnan(x0) || isnan(x1) || !(mx > 0.0) || !xmid(mx)) {
+        ok = ok && mx == 0.0 && !isnan(x0) && !isnan(x1);
+        return 0.0;
+    }
+    const int ex = xexp(mx);
+    const double scale = xpow2(2045 - ex), unscale = xpow2(ex + 1);
+    double csum = 1.0, frac1 = 0.0, frac2 = 0.0;
+    const double v[2] = {x0, x1};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double x = v[i] * scale;
+        const double hi = x * x, lo = fma(x, x, -hi);
+        const double s = csum + hi;
+        const double sl = (csum - s) + hi;
+        csum = s;
+        frac1 += lo;
+        frac2 += sl;
+    }
+    double h = xsqrt(csum - 1.0 + (frac1 + frac2), ok);
+    {
+        const double hi = -h * h, lo = fma(-h, h, -hi);
+        const double s = csum + hi;
+        const double sl = (csum - s) + hi;
+        csum = s;
+        frac1 += lo;
+        frac2 += sl;
+    }
+    const double x = csum - 1.0 + (frac1 + frac2);
+    h += xdiv(x, 2.0 * h, ok);
+    return h * unscale;
+}
+template <bool FAST>
+__device__ __forceinline__ double vhypot(double a, double b, bool &ok) {
+    if (FAST) return xhypot(a, b, ok);
+    return py_hypot(a, b);
+}
+
 // ---- the same fold with the Givens rotations pipelined over three lanes ----
 // ndt_update's serial chain is three rotations per sample (cholupdate3), but
 // rotation k only reads column k of the factor and the rotated vector left by
@@ -1067,14 +1108,16 @@ constexpr int NBK3_PER_WARP = 10;
 
 // rotation of column (Ld; La, Lb) by the vector (xd; xa, xb) after the
 // count's scale sq, then the rescale by sn (ndt_update / givens_k, one column)
+template <bool FAST>
 __device__ __forceinline__ void ndt_rot_column(double &Ld, double &La, double &Lb, double xd,
-                                               double &xa, double &xb, double sq, double sn) {
+                                               double &xa, double &xb, double sq, double sn,
+                                               bool &ok) {
     Ld = Ld * sq;
     La = La * sq;
     Lb = Lb * sq;
-    const double r = py_hypot(Ld, xd);
+    const double r = vhypot<FAST>(Ld, xd, ok);
     if (r != 0.0) {
-        const double c = Ld / r, s = xd / r;
+        const double c = vdiv<FAST>(Ld, r, ok), s = vdiv<FAST>(xd, r, ok);
         Ld = r;
         const double la = La, lb = Lb;
         La = c * la + s * xa;
@@ -1082,10 +1125,55 @@ __device__ __forceinline__ void ndt_rot_column(double &Ld, double &La, double &L
         Lb = c * lb + s * xb;
         xb = c * xb - s * lb;
     }
-    Ld = Ld / sn;
-    La = La / sn;
-    Lb = Lb / sn;
+    Ld = vdiv<FAST>(Ld, sn, ok);
+    La = vdiv<FAST>(La, sn, ok);
+    Lb = vdiv<FAST>(Lb, sn, ok);
 }
+
+// One step of lane k (sample nj = n0 + j): lane 0 folds the sample into the
+// Welford mean and forms the vector, every lane rotates its column.
+template <bool FAST>
+__device__ __forceinline__ void ndt_fold3_step(int k, unsigned long long nj, const double e[3],
+                                               double mu[3], double ind, double ina, double &Ld,
+                                               double &La, double &Lb, double &oa, double &ob,
+                                               bool &ok) {
+    double xd, xa, xb;
+    if (k == 0) {
+        if (nj == 0) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) mu[a] = e[a];
+            xd = xa = xb = 0.0;
+        } else {
+            const double dnn = (double)(nj + 1);
+            double d[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) d[a] = e[a] - mu[a];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) mu[a] = mu[a] + vdiv<FAST>(d[a], dnn, ok);
+            const double f = vsqrt<FAST>(vdiv<FAST>((double)nj, dnn, ok), ok);
+            xd = d[0] * f;
+            xa = d[1] * f;
+            xb = d[2] * f;
+        }
+    } else {
+        xd = ind;
+        xa = ina;
+        xb = 0.0;
+    }
+    if (nj == 0) {
+        // ndt_update's first sample: the factor is zero
+        Ld = La = Lb = 0.0;
+    } else {
+        ndt_rot_column<FAST>(Ld, La, Lb, xd, xa, xb, vsqrt<FAST>((double)nj, ok),
+                             vsqrt<FAST>((double)(nj + 1), ok), ok);
+    }
+    oa = xa;
+    ob = xb;
+}
+
+#ifndef NBK3_FAST
+#define NBK3_FAST 0  // 1: verified fast operators in k_nbk_fold3 (measured slower, DESIGN)
+#endif
 
 template <bool TM>
 __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid_constant__ DevMap m,
@@ -1223,7 +1311,7 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid
             const unsigned j = step - (unsigned)k;  // this lane's sample (wraps when step < k)
             if (j < ns) {
                 const unsigned long long nj = (unsigned long long)n0 + j;
-                double xd, xa, xb;
+                double e[3] = {0.0, 0.0, 0.0};
                 if (k == 0) {
                     const double4 cur = curp;
                     if (j + 1 < ns) curp = ld_d4(ps + j + 1);
@@ -1236,36 +1324,27 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid
                         imean = (double)(float)mnew;
                         im2 = (double)(float)m2new;
                     }
-                    const double e[3] = {cur.x, cur.y, cur.z};
-                    if (nj == 0) {
-#pragma unroll
-                        for (int a = 0; a < 3; ++a) mu[a] = e[a];
-                        xd = xa = xb = 0.0;
-                    } else {
-                        const double dnn = (double)(nj + 1);
-                        double d[3];
-#pragma unroll
-                        for (int a = 0; a < 3; ++a) d[a] = e[a] - mu[a];
-#pragma unroll
-                        for (int a = 0; a < 3; ++a) mu[a] = mu[a] + d[a] / dnn;
-                        const double f = sqrt((double)nj / dnn);
-                        xd = d[0] * f;
-                        xa = d[1] * f;
-                        xb = d[2] * f;
+                    e[0] = cur.x;
+                    e[1] = cur.y;
+                    e[2] = cur.z;
+                }
+                bool ok = true;
+                if (NBK3_FAST) {
+                    double mu2[3] = {mu[0], mu[1], mu[2]};
+                    double Ld2 = Ld, La2 = La, Lb2 = Lb, oa2, ob2;
+                    ndt_fold3_step<true>(k, nj, e, mu2, ind, ina, Ld2, La2, Lb2, oa2, ob2, ok);
+                    if (ok) {
+                        mu[0] = mu2[0];
+                        mu[1] = mu2[1];
+                        mu[2] = mu2[2];
+                        Ld = Ld2;
+                        La = La2;
+                        Lb = Lb2;
+                        oa = oa2;
+                        ob = ob2;
                     }
-                } else {
-                    xd = ind;
-                    xa = ina;
-                    xb = 0.0;
                 }
-                if (nj == 0) {
-                    // ndt_update's first sample: the factor is zero
-                    Ld = La = Lb = 0.0;
-                } else {
-                    ndt_rot_column(Ld, La, Lb, xd, xa, xb, sqrt((double)nj), sqrt((double)(nj + 1)));
-                }
-                oa = xa;
-                ob = xb;
+                if (!NBK3_FAST || !ok) ndt_fold3_step<false>(k, nj, e, mu, ind, ina, Ld, La, Lb, oa, ob, ok);
             }
         }
         const unsigned long long n = (unsigned long long)n0 + ns;
