@@ -2,6 +2,7 @@
 #include <cstdio>
 #include "ndt_fast.cuh"
 using namespace vm;
+using namespace vm::micro;
 __global__ void k(double *out, long long *cyc, double seed, int iters, int fast) {
     unsigned long long n = 5;
     double mu[3] = {seed, seed + 0.1, seed + 0.2};

@@ -3,6 +3,7 @@
 #pragma once
 #include "../../paper_2206_06079_b200/csrc/vm_ndt.cuh"
 namespace vm {
+namespace micro {  // the product's xdiv / xsqrt (vm_device.cuh) have other signatures
 __device__ __forceinline__ int xexp(double v) { return (int)((unsigned long long)__double_as_longlong(v) >> 52) & 0x7FF; }
 __device__ __forceinline__ bool xmid(double v) { const int e = xexp(v); return e > 200 && e < 1800; }
 __device__ __forceinline__ double xpow2(int biased) { return __longlong_as_double((long long)biased << 52); }
@@ -102,4 +103,5 @@ __device__ __forceinline__ bool ndt_update_fast(unsigned long long n, const doub
     for (int k = 0; k < 6; ++k) S_o[k] = xdiv(L[k], rt.sn, ysn, ok);
     return ok;
 }
+}  // namespace micro
 }  // namespace vm
