@@ -2,7 +2,6 @@
 #include <cstdio>
 #include "ndt_fast.cuh"
 using namespace vm;
-using namespace vm::micro;
 __global__ void k(double *out, long long *cyc, double seed, int iters, int fast) {
     unsigned long long n = 5;
     double mu[3] = {seed, seed + 0.1, seed + 0.2};
@@ -14,7 +13,7 @@ __global__ void k(double *out, long long *cyc, double seed, int iters, int fast)
         const double x[3] = {seed + 0.01 * (i & 7), seed + 0.1 + 0.013 * (i & 3), seed + 0.2 - 0.007 * (i & 5)};
         const NdtRoots rn = ndt_roots(n + 1);
         double mo[3], so[6];
-        if (fast && ndt_update_fast(n, mu, S, x, rt, xrcp((double)(n + 1)), xrcp(rt.sn), mo, so)) {
+        if (fast && micro::ndt_update_fast(n, mu, S, x, rt, micro::xrcp((double)(n + 1)), micro::xrcp(rt.sn), mo, so)) {
             for (int a = 0; a < 3; ++a) mu[a] = mo[a];
             for (int q = 0; q < 6; ++q) S[q] = so[q];
             ++n;
