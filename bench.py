@@ -482,7 +482,7 @@ def main():
     if default_run and not args.no_extra:
         # the NDT-OM half of the metric (configs[2], C3) and the 0.1 m
         # occupancy scan (configs[0], C1), measured in the same run
-        n = run_gpu_workload("c3", args, dev, torch, steps=min(args.steps, 3), e2e_steps=1)
+        n = run_gpu_workload("c3", args, dev, torch, steps=min(args.steps, 3), e2e_steps=3)
         ns = n["s0"]
         V3 = ns["records"] - n["H"]
         wb, fb = ndt_bytes(ns["S"], ns["V"], n["H"], V3, n["U"])
