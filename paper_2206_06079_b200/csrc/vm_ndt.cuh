@@ -224,7 +224,29 @@ struct NdtBuckets {
     unsigned *bits;                  // huge buckets: per block 2 * bwords words
     unsigned long long bwords;       // words of one (phase, order) bitmap
     unsigned long long span;         // n * maxseg (orders per phase)
+    const double4 *roots = nullptr;  // [nroots] (sqrt(n), sqrt(n / (n + 1)), sqrt(n + 1)), k_nbk_fold3
+    unsigned nroots = 0;
 };
+
+// The square roots of the sample count each Welford / Givens step needs,
+// tabulated once per map (the same IEEE operations as ndt_roots / the fold
+// step), so the fold's steps load them instead of computing them.
+constexpr unsigned NDT_ROOTS_N = 1u << 16;
+__global__ void k_ndt_roots(double4 *out, unsigned n) {
+    const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double dn = (double)i, dnn = (double)(i + 1);
+    out[i] = make_double4(sqrt(dn), sqrt(dn / dnn), sqrt(dnn), 0.0);
+}
+__device__ __forceinline__ double4 ndt_roots_of(const NdtBuckets &b, unsigned long long n) {
+    if (n < b.nroots) {
+        const double2 *q = reinterpret_cast<const double2 *>(b.roots + n);
+        const double2 lo = __ldg(q), hi = __ldg(q + 1);
+        return make_double4(lo.x, lo.y, hi.x, hi.y);
+    }
+    const double dn = (double)n, dnn = (double)(n + 1);
+    return make_double4(sqrt(dn), sqrt(dn / dnn), sqrt(dnn), 0.0);
+}
 
 constexpr int NBK_WARP_MAX = 512;  // warp rank sort (shared-memory staging: 4 KiB per warp)
 
@@ -1134,9 +1156,9 @@ __device__ __forceinline__ void ndt_rot_column(double &Ld, double &La, double &L
 // Welford mean and forms the vector, every lane rotates its column.
 template <bool FAST>
 __device__ __forceinline__ void ndt_fold3_step(int k, unsigned long long nj, const double e[3],
-                                               double mu[3], double ind, double ina, double &Ld,
-                                               double &La, double &Lb, double &oa, double &ob,
-                                               bool &ok) {
+                                               const double4 &rt, double mu[3], double ind,
+                                               double ina, double &Ld, double &La, double &Lb,
+                                               double &oa, double &ob, bool &ok) {
     double xd, xa, xb;
     if (k == 0) {
         if (nj == 0) {
@@ -1150,7 +1172,7 @@ __device__ __forceinline__ void ndt_fold3_step(int k, unsigned long long nj, con
             for (int a = 0; a < 3; ++a) d[a] = e[a] - mu[a];
 #pragma unroll
             for (int a = 0; a < 3; ++a) mu[a] = mu[a] + vdiv<FAST>(d[a], dnn, ok);
-            const double f = vsqrt<FAST>(vdiv<FAST>((double)nj, dnn, ok), ok);
+            const double f = rt.y;  // sqrt(nj / (nj + 1))
             xd = d[0] * f;
             xa = d[1] * f;
             xb = d[2] * f;
@@ -1164,8 +1186,7 @@ __device__ __forceinline__ void ndt_fold3_step(int k, unsigned long long nj, con
         // ndt_update's first sample: the factor is zero
         Ld = La = Lb = 0.0;
     } else {
-        ndt_rot_column<FAST>(Ld, La, Lb, xd, xa, xb, vsqrt<FAST>((double)nj, ok),
-                             vsqrt<FAST>((double)(nj + 1), ok), ok);
+        ndt_rot_column<FAST>(Ld, La, Lb, xd, xa, xb, rt.x, rt.z, ok);
     }
     oa = xa;
     ob = xb;
@@ -1305,12 +1326,16 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid
         double oa = 0.0, ob = 0.0;  // this lane's rotated vector entries, for lane k + 1
         // lane 0: the next sample's end point is loaded a step ahead of its use
         double4 curp = (k == 0 && ns) ? ld_d4(ps) : make_double4(0.0, 0.0, 0.0, 0.0);
+        // this lane's first sample's roots; the next sample's are loaded a step ahead
+        double4 rtp = ns ? ndt_roots_of(b, n0) : make_double4(0.0, 0.0, 0.0, 0.0);
         for (unsigned step = 0; step < ms + 2; ++step) {
             const double ind = __shfl_up_sync(0xffffffffu, oa, 1);
             const double ina = __shfl_up_sync(0xffffffffu, ob, 1);
             const unsigned j = step - (unsigned)k;  // this lane's sample (wraps when step < k)
             if (j < ns) {
                 const unsigned long long nj = (unsigned long long)n0 + j;
+                const double4 rtc = rtp;
+                if (j + 1 < ns) rtp = ndt_roots_of(b, nj + 1);
                 double e[3] = {0.0, 0.0, 0.0};
                 if (k == 0) {
                     const double4 cur = curp;
@@ -1332,7 +1357,7 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid
                 if (NBK3_FAST) {
                     double mu2[3] = {mu[0], mu[1], mu[2]};
                     double Ld2 = Ld, La2 = La, Lb2 = Lb, oa2, ob2;
-                    ndt_fold3_step<true>(k, nj, e, mu2, ind, ina, Ld2, La2, Lb2, oa2, ob2, ok);
+                    ndt_fold3_step<true>(k, nj, e, rtc, mu2, ind, ina, Ld2, La2, Lb2, oa2, ob2, ok);
                     if (ok) {
                         mu[0] = mu2[0];
                         mu[1] = mu2[1];
@@ -1344,7 +1369,7 @@ __global__ void __launch_bounds__(BLOCK, NBK_FOLD_MINB) k_nbk_fold3(const __grid
                         ob = ob2;
                     }
                 }
-                if (!NBK3_FAST || !ok) ndt_fold3_step<false>(k, nj, e, mu, ind, ina, Ld, La, Lb, oa, ob, ok);
+                if (!NBK3_FAST || !ok) ndt_fold3_step<false>(k, nj, e, rtc, mu, ind, ina, Ld, La, Lb, oa, ob, ok);
             }
         }
         const unsigned long long n = (unsigned long long)n0 + ns;

@@ -120,6 +120,7 @@ struct vm_map {
     double2 *d_rec_t = nullptr;      // NDT: chords of the phase-1 records (k_ndt_weigh)
     size_t rec_t_cap = 0;
     unsigned *d_nbk_small = nullptr; // NDT: size histogram, cursors, live count, slice cursor
+    double4 *d_ndt_roots = nullptr;  // NDT: tabulated count roots (k_ndt_roots)
     unsigned *d_bk_bits = nullptr;
     size_t bk_bits_cap = 0;
     // pipelined sequences (vm_integrate_many)
@@ -726,12 +727,20 @@ int launch_ndt_fold_only(vm_map *m, const DevMap &dm, const NdtBuckets &b, bool 
         else k_nbk_fold<false><<<gm, BLOCK, 0, s>>>(dm, b);
     } else {
         // three lanes per bucket, the rotations pipelined (vm_ndt.cuh: k_nbk_fold3)
+        if (!m->d_ndt_roots) {
+            CK(cudaMalloc((void **)&m->d_ndt_roots, NDT_ROOTS_N * sizeof(double4)));
+            k_ndt_roots<<<NDT_ROOTS_N / BLOCK, BLOCK, 0, s>>>(m->d_ndt_roots, NDT_ROOTS_N);
+            m->launches += 1;
+        }
+        NdtBuckets b3 = b;
+        b3.roots = m->d_ndt_roots;
+        b3.nroots = NDT_ROOTS_N;
         const unsigned g3 = (unsigned)std::max<long long>(
             1, std::min<long long>((long long)m->num_sms * 8,
                                    ((long long)m->smarked_cap + NBK3_PER_WARP * (BLOCK / 32) - 1) /
                                        (NBK3_PER_WARP * (BLOCK / 32))));
-        if (tm) k_nbk_fold3<true><<<g3, BLOCK, 0, s>>>(dm, b);
-        else k_nbk_fold3<false><<<g3, BLOCK, 0, s>>>(dm, b);
+        if (tm) k_nbk_fold3<true><<<g3, BLOCK, 0, s>>>(dm, b3);
+        else k_nbk_fold3<false><<<g3, BLOCK, 0, s>>>(dm, b3);
     }
 #ifdef VM_FOLD_PROF
     {
@@ -2136,6 +2145,7 @@ int vm_map_destroy(vm_map *m) {
     cudaFree(m->d_nbk_pos);
     cudaFree(m->d_rec_t);
     cudaFree(m->d_nbk_small);
+    cudaFree(m->d_ndt_roots);
     cudaFree(m->d_bk_bits);
     cudaFree(m->d_chain);
     cudaFree(m->d_mstats);
