@@ -183,6 +183,23 @@ __device__ __forceinline__ void vf_hit_ep(const DevMap &m, VoxFold &f, const dou
     }
 }
 
+// The same hit with the end point's voxel fraction ep / vox - g already
+// computed (by the lane that loaded the end point, off the serial chain:
+// the divisions are the same operations, only issued earlier).
+__device__ __forceinline__ void vf_hit_off(const DevMap &m, VoxFold &f, const double off[3]) {
+    f.l = miss_k(f.l, f.misses, m.miss32, m.cmin, m.cmax);
+    f.misses = 0;
+    f.l = clamp_add(f.l, m.hit32, m.cmin, m.cmax);
+    if (m.slab[L_MEAN]) fold_mean(f.packed, f.count, off);
+}
+
+// every lane: the voxel fraction of the end point it loaded (vf_lane_end)
+__device__ __forceinline__ void vf_lane_off(const DevMap &m, const VoxFold &f, double e[3]) {
+    if (!m.slab[L_MEAN]) return;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) e[a] = e[a] / m.vox - (double)f.g[a];
+}
+
 // ... of segment order index `oi` (= ray * maxseg + seg)
 template <class Src>
 __device__ __forceinline__ void vf_hit(const DevMap &m, const Src &src, VoxFold &f, unsigned oi) {
@@ -270,15 +287,16 @@ __device__ __forceinline__ void vf_warp_chunk(const DevMap &m, const Src &src, V
     const unsigned hmask = __ballot_sync(0xffffffffu, hit);
     double e[3];
     vf_lane_end(m, src, hit, x >> 1, e);  // all the chunk's end points in flight at once
+    vf_lane_off(m, f, e);                 // and their voxel fractions, all lanes at once
     int cur = 0;
     unsigned hm = hmask;
     while (hm) {
         const int h = __ffs(hm) - 1;
         hm &= hm - 1;
         f.misses += (unsigned)(h - cur);
-        const double ep[3] = {__shfl_sync(0xffffffffu, e[0], h), __shfl_sync(0xffffffffu, e[1], h),
-                              __shfl_sync(0xffffffffu, e[2], h)};
-        vf_hit_ep(m, f, ep);
+        const double off[3] = {__shfl_sync(0xffffffffu, e[0], h), __shfl_sync(0xffffffffu, e[1], h),
+                               __shfl_sync(0xffffffffu, e[2], h)};
+        vf_hit_off(m, f, off);
         cur = h + 1;
     }
     f.misses += (unsigned)(n - cur);
@@ -422,15 +440,16 @@ __device__ __forceinline__ void bk_fold_big_body(const DevMap &m, const Src &src
                         // lane j loads the end point of order (w0 + L) * 32 + j if it hit
                         double e[3];
                         vf_lane_end(m, src, (hL >> lane) & 1u, (unsigned)((w0 + L) * 32 + lane), e);
+                        vf_lane_off(m, f, e);
                         unsigned bits = pL;
                         while (bits) {
                             const int bi = __ffs(bits) - 1;
                             bits &= bits - 1;
                             if ((hL >> bi) & 1u) {
-                                const double ep[3] = {__shfl_sync(0xffffffffu, e[0], bi),
-                                                      __shfl_sync(0xffffffffu, e[1], bi),
-                                                      __shfl_sync(0xffffffffu, e[2], bi)};
-                                vf_hit_ep(m, f, ep);
+                                const double off[3] = {__shfl_sync(0xffffffffu, e[0], bi),
+                                                       __shfl_sync(0xffffffffu, e[1], bi),
+                                                       __shfl_sync(0xffffffffu, e[2], bi)};
+                                vf_hit_off(m, f, off);
                             } else {
                                 ++f.misses;
                             }
