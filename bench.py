@@ -366,6 +366,9 @@ def run_gpu_workload(name, args, dev, torch, world=1, dist=None, steps=None, e2e
         f1.record(stream)
         torch.cuda.synchronize()
         ems = max(f0.elapsed_time(f1), (time.perf_counter() - t0) * 1e3)
+        if os.environ.get("VOXMAP_B200_E2E_DEBUG"):
+            print(f"[e2e] {name}: device {f0.elapsed_time(f1):.2f} ms, wall "
+                  f"{(time.perf_counter() - t0) * 1e3:.2f} ms for {e2e_steps} steps", file=sys.stderr)
         if dist:
             t = torch.tensor([ems], device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
